@@ -1,0 +1,70 @@
+"""Seeded layer inputs (features, weights, upstream gradient).
+
+Distributions: X ~ U(-1,1); typed weight matrices
+Glorot-uniform +-sqrt(6/(fan_in+fan_out)); RGAT attention vectors ~ U(-1,1)/sqrt(d);
+HGT relation prior mu_r = 1 (reading g7, not trained); upstream gradient
+G = dL/dout ~ U(-1,1) (reading g12: loss L = sum(out * G)).
+
+Seeds: graph 1, X 2, W 3, G 4 (D1).  Everything is float64 on the host; the
+bf16 path receives `round_bf16` copies (round-to-nearest-even), and the oracle
+evaluates the same rounded values.
+"""
+from __future__ import annotations
+
+from typing import Dict
+
+import numpy as np
+
+from .graphs import HeteroGraph
+
+
+def _glorot(rng, shape, fan_in, fan_out):
+    lim = np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-lim, lim, size=shape)
+
+
+def layer_inputs(model: str, g: HeteroGraph, d_in: int, d_out: int,
+                 seed_x: int = 2, seed_w: int = 3) -> Dict[str, np.ndarray]:
+    """Features and weights for one layer of `model` in {'rgcn','rgat','hgt'}."""
+    n, r, t = g.num_nodes, g.num_rels, g.num_node_types
+    rx = np.random.default_rng(seed_x)
+    rw = np.random.default_rng(seed_w)
+    out: Dict[str, np.ndarray] = {"X": rx.uniform(-1.0, 1.0, size=(n, d_in))}
+    if model == "rgcn":
+        out["W"] = _glorot(rw, (r, d_in, d_out), d_in, d_out)
+        out["W0"] = _glorot(rw, (d_in, d_out), d_in, d_out)
+    elif model == "rgat":
+        out["W"] = _glorot(rw, (r, d_in, d_out), d_in, d_out)
+        out["a"] = rw.uniform(-1.0, 1.0, size=(r, d_out)) / np.sqrt(d_out)
+        out["b"] = rw.uniform(-1.0, 1.0, size=(r, d_out)) / np.sqrt(d_out)
+    elif model == "hgt":
+        out["Wk"] = _glorot(rw, (t, d_in, d_out), d_in, d_out)
+        out["Wq"] = _glorot(rw, (t, d_in, d_out), d_in, d_out)
+        out["Wv"] = _glorot(rw, (t, d_in, d_out), d_in, d_out)
+        out["Watt"] = _glorot(rw, (r, d_out, d_out), d_out, d_out)
+        out["Wmsg"] = _glorot(rw, (r, d_out, d_out), d_out, d_out)
+        out["mu"] = np.ones(r)
+    else:
+        raise ValueError(f"unknown model {model!r}")
+    return out
+
+
+def upstream_grad(n: int, d_out: int, seed: int = 4) -> np.ndarray:
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, d_out))
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round float64 values to the nearest bf16 value (ties to even), returned as float64.
+    Goes through float32 first (exact for these magnitudes), then rounds the
+    float32 bit pattern to its upper 16 bits."""
+    f = np.ascontiguousarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = (u + 0x7FFF + lsb) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """uint16 bf16 bit patterns of round_bf16(x) (for uploading to the device)."""
+    f = round_bf16(x).astype(np.float32)
+    return (f.view(np.uint32) >> 16).astype(np.uint16)

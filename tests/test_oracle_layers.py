@@ -1,0 +1,221 @@
+"""Pins of the layer oracle (oracle/layers.py) against things other than itself.
+
+Forward:
+  * RGCN identity weights, c = 1, sigma = id on G7: out[q] = h_q+h_a+h_b+h_c+h_p
+  * RGCN, one relation, no self-loop, c = 1/sqrt(d_out d_in) == dense GCN A* X W
+  * RGCN multi-relation == dense aggregate-then-transform sum_r (C_r o A_r) X W_r
+  * RGAT == dense multi-relation GAT in matrix form; HGT == dense masked scaled
+    dot-product attention (P:578-588 g-SDDMM + masked row softmax)
+  * edge softmax sums to 1 per destination with >= 1 in-edge
+  * uniform X and identical relation weights => alpha = 1/in-degree
+  * empty rows give zero aggregation
+Backward:
+  * central finite differences, h = 1e-6, fp64
+  * softmax-Jacobian rows sum to zero for any upstream gradient
+  * chunked-destination decomposition (oracle/sample.py) reproduces the full gradients
+"""
+import numpy as np
+import pytest
+
+from oracle import layers as L
+from oracle import dense as D
+from oracle import fd
+from oracle import sample as S
+from synth import g7, random_small_graph, layer_inputs, upstream_grad, config_graph
+from synth.graphs import HeteroGraph
+
+
+def _rel_err(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def test_rgcn_identity_g7():
+    g = g7()
+    X = np.random.default_rng(0).normal(size=(5, 4))
+    I = np.eye(4)
+    out, _ = L.rgcn_forward(g, X, np.stack([I, I]), I, np.ones(g.num_edges))
+    q, a, b, c, p = 4, 0, 1, 2, 3
+    assert np.allclose(out[q], X[q] + X[a] + X[b] + X[c] + X[p], atol=1e-14)
+    # p receives writes from a, b and cites from q
+    assert np.allclose(out[p], X[p] + X[a] + X[b] + X[q], atol=1e-14)
+    # authors have no in-edges: self-loop only
+    assert np.allclose(out[a], X[a], atol=0)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gcn_reduction(seed):
+    g = random_small_graph(seed, max_rels=1)
+    g = HeteroGraph(g.node_type_ptr, 1, g.src, g.dst, np.zeros_like(g.rel))
+    rng = np.random.default_rng(seed)
+    X = rng.normal(size=(g.num_nodes, 5))
+    W = rng.normal(size=(1, 5, 3))
+    norm = L.rgcn_edge_norm(g, "sym")
+    out, _ = L.rgcn_forward(g, X, W, np.zeros((5, 3)), norm, self_loop=False)
+    ref = D.gcn_dense(g, X, W[0])
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_rgcn_dense(seed):
+    g = random_small_graph(seed)
+    inp = layer_inputs("rgcn", g, 6, 5, seed_x=seed, seed_w=seed + 1)
+    norm = L.rgcn_edge_norm(g, "mean")
+    out, _ = L.rgcn_forward(g, inp["X"], inp["W"], inp["W0"], norm)
+    ref = D.rgcn_dense(g, inp["X"], inp["W"], inp["W0"], norm)
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
+def _in_degree(g):
+    return np.bincount(g.dst, minlength=g.num_nodes)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_rgat_dense(seed):
+    g = random_small_graph(seed)
+    inp = layer_inputs("rgat", g, 6, 5, seed_x=seed, seed_w=seed + 1)
+    out, c = L.rgat_forward(g, inp["X"], inp["W"], inp["a"], inp["b"])
+    ref, alpha_cat = D.rgat_dense(g, inp["X"], inp["W"], inp["a"], inp["b"])
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+    assert np.allclose(c["alpha"], D.edge_alpha_from_dense(g, alpha_cat), atol=1e-13)
+    # logits as a g-SDDMM: z_e = (X W_r)[src].a_r + (X W_r)[dst].b_r
+    for r in range(g.num_rels):
+        m = g.rel == r
+        if not m.any():
+            continue
+        sub = HeteroGraph(g.node_type_ptr, g.num_rels, g.src[m], g.dst[m], g.rel[m])
+        H = inp["X"] @ inp["W"][r]
+        ones = np.ones((g.num_nodes, 1))
+        z = D.gsddmm_dense(sub, ones, (H @ inp["a"][r])[:, None]) + D.gsddmm_dense(sub, (H @ inp["b"][r])[:, None], ones)
+        assert np.allclose(c["z"][m], z, atol=1e-13)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_hgt_dense(seed):
+    g = random_small_graph(seed)
+    inp = layer_inputs("hgt", g, 6, 4, seed_x=seed, seed_w=seed + 1)
+    inp["mu"] = np.random.default_rng(seed).uniform(0.5, 1.5, size=g.num_rels)
+    args = [inp[k] for k in ("X", "Wk", "Wq", "Wv", "Watt", "Wmsg", "mu")]
+    out, c = L.hgt_forward(g, *args)
+    ref, alpha_cat = D.hgt_dense(g, *args)
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+    assert np.allclose(c["alpha"], D.edge_alpha_from_dense(g, alpha_cat), atol=1e-13)
+
+
+def test_hgt_one_relation_is_masked_attention():
+    """R = 1, T = 1, Watt = Wmsg = I: out = softmax_mask(Q K^T / sqrt(d)) V (textbook attention)."""
+    g = random_small_graph(7, max_rels=1, max_types=1)
+    g = HeteroGraph(np.array([0, g.num_nodes]), 1, g.src, g.dst, np.zeros_like(g.rel))
+    rng = np.random.default_rng(3)
+    d = 4
+    X = rng.normal(size=(g.num_nodes, d))
+    Wk, Wq, Wv = (rng.normal(size=(1, d, d)) for _ in range(3))
+    I = np.eye(d)[None]
+    out, _ = L.hgt_forward(g, X, Wk, Wq, Wv, I, I, np.ones(1))
+    Q, K, V = X @ Wq[0], X @ Wk[0], X @ Wv[0]
+    A = np.zeros((g.num_nodes, g.num_nodes), bool)
+    A[g.dst, g.src] = True
+    Lg = np.where(A, Q @ K.T / np.sqrt(d), -np.inf)
+    ref = np.zeros_like(out)
+    for i in range(g.num_nodes):
+        if A[i].any():
+            w = np.exp(Lg[i] - Lg[i][A[i]].max())
+            w[~A[i]] = 0
+            ref[i] = (w / w.sum()) @ V
+    assert np.allclose(out, ref, atol=1e-12)
+
+
+@pytest.mark.parametrize("model", ["rgat", "hgt"])
+def test_softmax_sums_to_one_and_uniform(model):
+    g = config_graph("tiny", seed=1, scale=0.2)
+    inp = layer_inputs(model, g, 8, 8)
+    out, c = L.forward(model, g, inp)
+    s = np.zeros(g.num_nodes)
+    np.add.at(s, g.dst, c["alpha"])
+    deg = _in_degree(g)
+    assert np.allclose(s[deg > 0], 1.0, atol=1e-12)
+    assert np.all(out[deg == 0] == 0.0)           # empty rows: zero aggregation
+    # uniform features and identical relation weights -> alpha = 1/in-degree
+    u = {k: v.copy() for k, v in inp.items()}
+    u["X"][:] = 0.3
+    for k in ("W", "a", "b", "Watt", "Wmsg"):
+        if k in u:
+            u[k][:] = u[k][0]
+    for k in ("Wk", "Wq", "Wv"):
+        if k in u:
+            u[k][:] = u[k][0]
+    _, cu = L.forward(model, g, u)
+    assert np.allclose(cu["alpha"], 1.0 / deg[g.dst], atol=1e-12)
+
+
+def test_softmax_backward_rows_sum_to_zero():
+    g = config_graph("tiny", seed=2, scale=0.2)
+    rng = np.random.default_rng(5)
+    l = rng.normal(size=g.num_edges)
+    alpha, _, _ = L.edge_softmax(l, g.dst, g.num_nodes)
+    dl = L.edge_softmax_backward(alpha, rng.normal(size=g.num_edges), g.dst, g.num_nodes)
+    rows = np.zeros(g.num_nodes)
+    np.add.at(rows, g.dst, dl)
+    assert np.max(np.abs(rows)) < 1e-13
+
+
+def _fd_check(model, g, d_in, d_out, seed, n_probe=6, opts=None):
+    opts = opts or {}
+    inp = layer_inputs(model, g, d_in, d_out, seed_x=seed, seed_w=seed + 1)
+    G = upstream_grad(g.num_nodes, d_out, seed=seed + 2)
+    if model == "rgcn":
+        opts.setdefault("norm", L.rgcn_edge_norm(g, "mean"))
+    grads = L.backward(model, g, inp, G, **opts)
+
+    def fwd(p):
+        return L.forward(model, g, p, **opts)[0]
+
+    rng = np.random.default_rng(seed)
+    for name in ("X",) + L.PARAMS[model]:
+        if "d" + name not in grads:
+            continue
+        arr = inp[name]
+        idx = [tuple(int(rng.integers(0, s)) for s in arr.shape) for _ in range(n_probe)]
+        num = fd.fd_entries(fwd, inp, G, name, idx)
+        ana = np.array([grads["d" + name][i] for i in idx])
+        err = np.abs(ana - num) / np.maximum(1.0, np.abs(num))
+        assert np.max(err) <= 1e-6, (model, name, err)
+
+
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+def test_fd_g7(model):
+    _fd_check(model, g7(), 3, 4, seed=11, n_probe=12)
+
+
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+@pytest.mark.parametrize("seed", range(8))
+def test_fd_random(model, seed):
+    g = random_small_graph(100 + seed, allow_multi=(seed % 2 == 1))
+    _fd_check(model, g, 5, 4, seed=seed)
+
+
+def test_fd_rgcn_without_self_loop():
+    g = random_small_graph(3)
+    _fd_check("rgcn", g, 4, 4, seed=3, opts={"self_loop": False, "norm": L.rgcn_edge_norm(g, "sym")})
+
+
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+def test_destination_decomposition(model):
+    """Sum over destination chunks of (in-edge subgraph, masked G) == full gradients."""
+    g = config_graph("tiny", seed=3, scale=0.3)
+    inp = layer_inputs(model, g, 8, 8)
+    G = upstream_grad(g.num_nodes, 8)
+    norm = L.rgcn_edge_norm(g, "mean") if model == "rgcn" else None
+    full = L.backward(model, g, inp, G, norm=norm)
+    out_full, _ = L.forward(model, g, inp, norm=norm)
+    chunks = np.array_split(np.random.default_rng(0).permutation(g.num_nodes), 3)
+    acc = {k: np.zeros_like(v) for k, v in full.items()}
+    for ch in chunks:
+        sub, eids = S.in_edge_subgraph(g, ch)
+        kw = {"norm": norm[eids]} if model == "rgcn" else {}
+        part = L.backward(model, sub, inp, S.masked_grad(G, ch), **kw)
+        for k in acc:
+            acc[k] += part[k]
+        out_sub, _ = L.forward(model, sub, inp, **kw)
+        assert np.allclose(out_sub[ch], out_full[ch], atol=1e-12)
+    for k in full:
+        assert _rel_err(acc[k], full[k]) < 1e-12, k
