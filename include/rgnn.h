@@ -1,0 +1,226 @@
+/*
+ * rgnn.h — C-ABI of librgnn: one relational-GNN layer (RGCN / RGAT / HGT),
+ * forward and backward, on a typed heterograph, for NVIDIA B200 (sm_100a).
+ *
+ * The operations are those of the Hector hot path of arxiv 2412.04747 Ch. 3
+ * (PAPER.md = P:line, SPEC.md = S:line; SURVEY.md §8(b) lists this boundary):
+ *   - graph build: type sort, dst-CSR, src-CSC, compact (relation, source) pair
+ *     index ("precompute this mapping and store it in a CSR-like format",
+ *     P:774 §3.3.2; emitted preprocessing "converting COO to CSR", §3.3.6)
+ *   - layer forward: typed segment GEMM Y[S] = X[G] x W[T] over compact pairs
+ *     (§3.3.3, algo:gemm_template P:901-918; compact materialization
+ *     P:764-776; linear-operator reordering P:820-823), edge logits (g-SDDMM,
+ *     P:578-588; lst:ir_example P:739-745), edge softmax (lst:ir_example P:730-738),
+ *     aggregation by destination (g-SpMM; Eq. 3.1)
+ *   - layer backward (§3.3.5) over the dst-CSR and the src-CSC.
+ * The model readings (HGT formula, RGAT message, norms, slope ...) are listed in
+ * DESIGN.md "Readings".
+ *
+ * Conventions
+ *   - Every pointer argument documented "device" must point to device memory
+ *     of the current CUDA device; "host" pointers are ordinary host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All device work is enqueued on it.  Only rgnn_graph_build synchronises the
+ *     stream (once, to read back the pair count and the validation flag).
+ *   - Calls never abort and never throw across the ABI.  They return an
+ *     rgnn_status; on failure a thread-local message is available from
+ *     rgnn_last_error().  Output buffers are unspecified after a failure.
+ *   - Node ids are global; node type t owns ids [node_type_ptr[t], node_type_ptr[t+1])
+ *     ("nodes are presorted", §3.4.1).  Edge e = (src[e], dst[e], rel[e]);
+ *     edge ids are positions in the COO arrays.
+ *   - Feature/weight matrices are dense row-major.  dtype RGNN_F32 = float,
+ *     RGNN_BF16 = bfloat16 (uint16 bit patterns).  Gradients are always float.
+ */
+#ifndef RGNN_H_
+#define RGNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RGNN_API __attribute__((visibility("default")))
+#else
+#define RGNN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RGNN_OK = 0,
+  RGNN_ERR_INVALID_ARG = 1,   /* NULL/inconsistent sizes/unknown enum */
+  RGNN_ERR_OUT_OF_RANGE = 2,  /* node or relation id out of range (message names the first bad edge) */
+  RGNN_ERR_UNSUPPORTED = 3,   /* shape not supported (e.g. d_out not in {16,32,64,128}) */
+  RGNN_ERR_OOM = 4,           /* the allocator callback returned NULL */
+  RGNN_ERR_CUDA = 5,          /* a CUDA runtime error (message has the CUDA error string) */
+  RGNN_ERR_NCCL = 6           /* reserved for library-owned collectives */
+} rgnn_status;
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+RGNN_API const char* rgnn_last_error(void);
+/* Library version and build string (static storage). */
+RGNN_API const char* rgnn_version(void);
+
+/* Device allocator callbacks.  Every device buffer the library owns (graph
+ * index arrays, sort temporaries) is obtained through them, so the caller's
+ * allocator (e.g. PyTorch's caching allocator) owns all device memory.
+ * alloc must return a 256-byte aligned device pointer or NULL.  If both are
+ * NULL the library uses cudaMallocAsync / cudaFreeAsync on the build stream. */
+typedef void* (*rgnn_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*rgnn_free_fn)(void* ptr, void* stream, void* ctx);
+
+/* ------------------------------------------------------------------ graph */
+typedef struct rgnn_graph_s* rgnn_graph_t;
+
+/* Build the typed graph (C1 of SURVEY.md §8(c)).
+ *   num_nodes, num_node_types, node_type_ptr (host, int64[T+1], ptr[0]=0, ptr[T]=num_nodes)
+ *   num_rels R >= 1; num_edges E >= 0 (E = 0 is valid, compaction ratio 1.0)
+ *   src, dst, rel: device int32[E] COO arrays (read only; not retained)
+ *   dst_lo, dst_hi: the owned destination range; edges whose dst lies outside are
+ *     dropped (destination partitioning for multi-GPU runs); pass 0, num_nodes on 1 GPU.
+ *   On success *out receives a handle owning all index arrays.
+ * Bit-exact contract: every exported array equals the oracle's C1 definition:
+ *   CSR order = stable sort of edge ids by (dst, rel, src, eid); CSC order by
+ *   (src, rel, dst, eid); pairs = distinct (rel, src) ascending; edge_pair[e] = rank
+ *   of (rel_e, src_e).
+ * Errors: INVALID_ARG (bad counts/pointers), OUT_OF_RANGE (an id outside
+ *   [0,N) or [0,R); message names the first offending edge index),
+ *   UNSUPPORTED (E >= 2^31 or key width 2*ceil(log2 N)+ceil(log2 R) > 64),
+ *   OOM, CUDA.  Synchronises `stream` once. */
+RGNN_API rgnn_status rgnn_graph_build(int64_t num_nodes, int32_t num_node_types, const int64_t* node_type_ptr,
+                             int32_t num_rels, int64_t num_edges, const int32_t* src, const int32_t* dst,
+                             const int32_t* rel, int64_t dst_lo, int64_t dst_hi, rgnn_alloc_fn alloc,
+                             rgnn_free_fn free_fn, void* alloc_ctx, void* stream, rgnn_graph_t* out);
+
+typedef struct {
+  int64_t num_nodes;
+  int64_t num_edges;        /* edges kept (dst in [dst_lo, dst_hi)) */
+  int64_t num_pairs;        /* U = distinct (rel, src) pairs among kept edges */
+  int64_t max_in_degree;
+  int64_t max_pair_degree;  /* largest number of edges sharing one pair */
+  int64_t dst_lo, dst_hi;
+  int32_t num_node_types;
+  int32_t num_rels;
+  double compaction_ratio;  /* U / E (1.0 if E == 0), §3.4.3 */
+} rgnn_graph_info;
+
+RGNN_API rgnn_status rgnn_graph_get_info(rgnn_graph_t g, rgnn_graph_info* out_host);
+
+typedef enum {
+  RGNN_ARR_ETYPE_PTR = 0,    /* int32[R+1]  edges per relation prefix (etype_ptr) */
+  RGNN_ARR_ROW_PTR = 1,      /* int32[N+1]  dst-CSR row pointer */
+  RGNN_ARR_CSR_SRC = 2,      /* int32[E]    source of each CSR entry */
+  RGNN_ARR_CSR_REL = 3,      /* int32[E]    relation of each CSR entry */
+  RGNN_ARR_CSR_EID = 4,      /* int32[E]    edge id of each CSR entry */
+  RGNN_ARR_COL_PTR = 5,      /* int32[N+1]  src-CSC column pointer */
+  RGNN_ARR_CSC_DST = 6,      /* int32[E] */
+  RGNN_ARR_CSC_REL = 7,      /* int32[E] */
+  RGNN_ARR_CSC_EID = 8,      /* int32[E] */
+  RGNN_ARR_PAIR_REL_PTR = 9, /* int32[R+1]  unique_etype_ptr */
+  RGNN_ARR_PAIR_SRC = 10,    /* int32[U]    unique_row_idx */
+  RGNN_ARR_EDGE_PAIR = 11,   /* int32[E]    pair of each edge id */
+  RGNN_ARR_CSR_PAIR = 12,    /* int32[E]    pair of each CSR entry */
+  RGNN_ARR_CSC_PAIR = 13,    /* int32[E]    pair of each CSC entry */
+  RGNN_ARR_COUNT = 14
+} rgnn_array;
+
+/* Copy one index array (as typed above) into caller memory.
+ * dst_device: device buffer of `bytes` >= count*4.  Enqueued on `stream`.
+ * Errors: INVALID_ARG (unknown array, buffer too small). */
+RGNN_API rgnn_status rgnn_graph_export(rgnn_graph_t g, rgnn_array which, void* dst_device, size_t bytes, void* stream);
+/* Element count of an index array. */
+RGNN_API rgnn_status rgnn_graph_array_size(rgnn_graph_t g, rgnn_array which, int64_t* count);
+/* Free the handle and all its arrays (through the free callback).  NULL is a no-op. */
+RGNN_API rgnn_status rgnn_graph_destroy(rgnn_graph_t g);
+
+/* ------------------------------------------------------------------ layer */
+typedef enum { RGNN_RGCN = 0, RGNN_RGAT = 1, RGNN_HGT = 2 } rgnn_model;
+typedef enum { RGNN_F32 = 0, RGNN_BF16 = 1 } rgnn_dtype;
+/* RGCN per-edge multiplier 1/c_{v,r} of Eq. 3.1 (reading g1):
+ *   MEAN 1/|{e' in in(v): rel e' = rel e}|, SYM 1/sqrt(outdeg(src) indeg(dst)) (GCN A*),
+ *   NONE 1, CUSTOM the caller's float[E] array indexed by edge id. */
+typedef enum { RGNN_NORM_MEAN = 0, RGNN_NORM_SYM = 1, RGNN_NORM_NONE = 2, RGNN_NORM_CUSTOM = 3 } rgnn_norm_kind;
+
+typedef struct {
+  int32_t model;       /* rgnn_model */
+  int32_t dtype;       /* rgnn_dtype of X, the weights and the projected tables */
+  int32_t d_in;        /* input feature width, multiple of 16, <= 256 */
+  int32_t d_out;       /* output width, one of 16, 32, 64, 128 */
+  int32_t self_loop;   /* RGCN: add X W_0 (virtual self-loop); ignored otherwise */
+  int32_t norm_kind;   /* RGCN: rgnn_norm_kind */
+  float leaky_slope;   /* RGAT LeakyReLU slope (reading g6: 0.2) */
+  int32_t gemm_impl;   /* 0 auto (bf16 -> tcgen05 when d_in % 64 == 0), 1 force SIMT, 2 force tcgen05 */
+} rgnn_layer_desc;
+
+/* Layer weights, device pointers in the layer dtype (mu and edge_norm: float).
+ * Unused fields may be NULL. */
+typedef struct {
+  const void* W;           /* RGCN, RGAT: [R][d_in][d_out]  relation weights W_r */
+  const void* W0;          /* RGCN: [d_in][d_out]           self-loop weight W_0 (self_loop=1) */
+  const void* a;           /* RGAT: [R][d_out]  source attention vector w_s[r] (lst:ir_example) */
+  const void* b;           /* RGAT: [R][d_out]  destination attention vector w_t[r] */
+  const void* Wk;          /* HGT: [T][d_in][d_out] key projection per node type */
+  const void* Wq;          /* HGT: [T][d_in][d_out] query projection per node type */
+  const void* Wv;          /* HGT: [T][d_in][d_out] value projection per node type */
+  const void* Watt;        /* HGT: [R][d_out][d_out] relation attention matrix */
+  const void* Wmsg;        /* HGT: [R][d_out][d_out] relation message matrix */
+  const float* mu;         /* HGT: [R] relation prior (not trained) */
+  const float* edge_norm;  /* RGCN, norm_kind CUSTOM: [E] by edge id */
+} rgnn_weights;
+
+/* Weight gradients, device float pointers, same shapes as rgnn_weights.
+ * A NULL field is not computed (gradient pruning). */
+typedef struct {
+  float* dW;
+  float* dW0;
+  float* da;
+  float* db;
+  float* dWk;
+  float* dWq;
+  float* dWv;
+  float* dWatt;
+  float* dWmsg;
+} rgnn_weight_grads;
+
+/* Bytes of the `saved` buffer (forward -> backward activations) and of the
+ * `scratch` buffer (temporaries of one forward or backward call).  Both are
+ * caller-owned device memory, 256-byte aligned.
+ * Errors: INVALID_ARG / UNSUPPORTED for a bad descriptor. */
+RGNN_API rgnn_status rgnn_layer_workspace(rgnn_graph_t g, const rgnn_layer_desc* desc, size_t* saved_bytes,
+                                 size_t* scratch_bytes);
+
+/* Forward: out[N][d_out] (float, device) = the layer output for every node
+ * (rows of destinations outside [dst_lo, dst_hi) and zero in-degree rows hold
+ * only the self-loop term for RGCN, zero otherwise; reading g10).
+ * X: device [N][d_in] in the layer dtype.  saved: written, needed by backward.
+ * Errors: INVALID_ARG (NULL pointers for the model, bad desc), UNSUPPORTED, CUDA. */
+RGNN_API rgnn_status rgnn_layer_forward(rgnn_graph_t g, const rgnn_layer_desc* desc, const void* X, const rgnn_weights* w,
+                               float* out, void* saved, void* scratch, void* stream);
+
+/* Backward of L = sum(out * dout) (reading g12).  `out` is the forward output
+ * (read by RGAT/HGT for the softmax backward row term G_v . out_v), `saved` the
+ * buffer written by the matching forward.  dX: device float [N][d_in] (NULL = not
+ * computed), dW: per-field device float (NULL = pruned).  Every requested output
+ * is fully overwritten (no accumulation into caller data).
+ * Errors: as for forward. */
+RGNN_API rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* desc, const void* X, const rgnn_weights* w,
+                                const float* out, const void* saved, const float* dout, float* dX,
+                                const rgnn_weight_grads* dW, void* scratch, void* stream);
+
+/* ------------------------------------------------------------------ profiling
+ * When enabled, every kernel the library launches is bracketed by CUDA events
+ * on its launch stream.  rgnn_profile_read synchronises those events and
+ * writes a JSON object {"kernel": {"launches": n, "ms": total}, ...} into buf. */
+RGNN_API rgnn_status rgnn_profile_enable(int32_t on);
+RGNN_API rgnn_status rgnn_profile_reset(void);
+RGNN_API rgnn_status rgnn_profile_read(char* buf, size_t len);
+
+/* Number of kernels launched by the library since load (all threads). */
+RGNN_API int64_t rgnn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RGNN_H_ */

@@ -1,0 +1,433 @@
+// SIMT dense kernels: typed segment GEMM (fp32 path; bf16 fallback shapes),
+// segmented weight gradients, per-node row reduction, and the small
+// weight-weight products of linear-operator reordering (A2).
+//
+// The fp32 path must match the fp64 oracle to 1e-4 with TF32 off, and tcgen05
+// has no fp32 kind (SURVEY.md §0 finding 8), so fp32 GEMMs run on FFMA.  At
+// d = 64 these GEMMs are HBM-bound (arithmetic intensity 16 flop/B fp32), so
+// the kernel is organised for coalesced gathers and stores, not for FLOPs.
+#include "ops.cuh"
+
+namespace rgnn {
+namespace {
+
+constexpr int BM = 64;  // rows per tile
+constexpr int KC = 16;  // k chunk
+
+template <class T> __device__ __forceinline__ float ldf(const T* p) { return to_f(*p); }
+
+// 256 threads: tx = tid % 16 owns columns tx + 16 j, ty = tid / 16 owns rows 4 ty .. 4 ty + 3.
+template <class TA, class TB, class TY, int N>
+__global__ void __launch_bounds__(256) k_gemm_simt(const Tile* __restrict__ tiles, const TA* __restrict__ A, int K,
+                                                   const int32_t* __restrict__ gather, const TB* __restrict__ B,
+                                                   bool transB, TY* __restrict__ Y, const float* __restrict__ dotvec,
+                                                   float* __restrict__ dotout) {
+  constexpr int NJ = N / 16;
+  __shared__ __align__(16) float As[KC][BM + 4];
+  __shared__ __align__(16) float Bs[KC][N];
+  const Tile t = tiles[blockIdx.x];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int nrows = t.row1 - t.row0;
+  const TB* Bw = B + (size_t)t.w * K * N;
+
+  // loader mapping for A: row lr = tid / 4 (0..63), 4 consecutive k at (tid % 4) * 4
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  int64_t arow = -1;
+  if (lr < nrows) {
+    int64_t r = t.row0 + lr;
+    arow = gather ? (int64_t)gather[r] : r;
+  }
+  float acc[4][NJ];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += KC) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) As[lk + i][lr] = arow >= 0 ? ldf(A + arow * K + k0 + lk + i) : 0.f;
+    for (int idx = tid; idx < KC * N; idx += 256) {
+      int kk = idx / N, n = idx % N;
+      Bs[kk][n] = transB ? ldf(Bw + (size_t)n * K + k0 + kk) : ldf(Bw + (size_t)(k0 + kk) * N + n);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      float a[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        float b = Bs[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(a[i], b, acc[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int lrow = ty * 4 + i;
+    int64_t row = t.row0 + lrow;
+    if (dotvec) {  // per-row scalar epilogue: dot of the fp32 row with a per-weight vector
+      float d = 0.f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) d = fmaf(acc[i][j], dotvec[(size_t)t.w * N + tx + 16 * j], d);
+      d = group_sum<16>(d);
+      if (tx == 0 && lrow < nrows) dotout[row] = d;
+    }
+    if (lrow < nrows) {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) Y[row * N + tx + 16 * j] = from_f<TY>(acc[i][j]);
+    }
+  }
+}
+
+template <class TA, class TB, class TY>
+void gemm_dispatch(const GemmArgs& a, cudaStream_t s) {
+  const TA* A = static_cast<const TA*>(a.A);
+  const TB* B = static_cast<const TB*>(a.B);
+  TY* Y = static_cast<TY*>(a.Y);
+  dim3 g(a.ntiles), b(256);
+#define RGNN_GEMM_CASE(NN)                                                                                  \
+  case NN:                                                                                                  \
+    launch("gemm_simt", k_gemm_simt<TA, TB, TY, NN>, g, b, 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, \
+           a.dotvec, a.dotout);                                                                             \
+    break;
+  switch (a.N) {
+    RGNN_GEMM_CASE(16)
+    RGNN_GEMM_CASE(32)
+    RGNN_GEMM_CASE(64)
+    RGNN_GEMM_CASE(128)
+    RGNN_GEMM_CASE(256)
+    default:
+      RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "gemm: N must be one of 16,32,64,128,256");
+  }
+#undef RGNN_GEMM_CASE
+}
+
+// ---------------------------------------------------------------- weight gradient
+// grid (tiles, ceil(K1/64), ceil(K2/64)); 256 threads own a 4x4 block of a 64x64 output tile.
+template <class TA>
+__global__ void __launch_bounds__(256) k_wgrad(const Tile* __restrict__ tiles, const TA* __restrict__ A, int K1,
+                                               const int32_t* __restrict__ gather, const float* __restrict__ Bm,
+                                               int K2, float* __restrict__ partial) {
+  __shared__ __align__(16) float As[32][64 + 4];
+  __shared__ __align__(16) float Bs[32][64 + 4];
+  const Tile t = tiles[blockIdx.x];
+  const int k1_0 = blockIdx.y * 64, k2_0 = blockIdx.z * 64;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[4][4] = {};
+  const int lrow = tid >> 3, lcol = (tid & 7) * 8;  // loader: 32 rows x 64 cols, 8 per thread
+  for (int r0 = t.row0; r0 < t.row1; r0 += 32) {
+    int r = r0 + lrow;
+    bool ok = r < t.row1;
+    int64_t ar = ok ? (gather ? (int64_t)gather[r] : (int64_t)r) : 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      int k1 = k1_0 + lcol + c, k2 = k2_0 + lcol + c;
+      As[lrow][lcol + c] = (ok && k1 < K1) ? to_f(A[ar * K1 + k1]) : 0.f;
+      Bs[lrow][lcol + c] = (ok && k2 < K2) ? Bm[(int64_t)r * K2 + k2] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      float4 a4 = *reinterpret_cast<const float4*>(&As[rr][ty * 4]);
+      float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      float b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[rr][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* out = partial + (size_t)blockIdx.x * K1 * K2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int k1 = k1_0 + ty * 4 + i;
+    if (k1 >= K1) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int k2 = k2_0 + tx + 16 * j;
+      if (k2 < K2) out[(size_t)k1 * K2 + k2] = acc[i][j];
+    }
+  }
+}
+
+// out[seg_w[s]][i] = sum over tiles of segment s (in order) of partial[tile][i]
+__global__ void k_seg_partial_reduce(int nseg, const int32_t* __restrict__ seg_tile_ptr, const int32_t* __restrict__ seg_w,
+                                     const float* __restrict__ partial, int64_t width, float* __restrict__ out) {
+  int sidx = blockIdx.y;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (sidx >= nseg || i >= width) return;
+  float acc = 0.f;
+  for (int t = seg_tile_ptr[sidx]; t < seg_tile_ptr[sidx + 1]; ++t) acc += partial[(size_t)t * width + i];
+  out[(size_t)seg_w[sidx] * width + i] = acc;
+}
+
+// per tile: partial[tile][k] = sum_rows wt[row] * A[gather(row)][k]; threads over k
+template <class TA>
+__global__ void k_seg_wsum(const Tile* __restrict__ tiles, const float* __restrict__ wt, const TA* __restrict__ A,
+                           int K, const int32_t* __restrict__ gather, float* __restrict__ partial) {
+  const Tile t = tiles[blockIdx.x];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    float acc = 0.f;
+    for (int r = t.row0; r < t.row1; ++r) {
+      int64_t ar = gather ? (int64_t)gather[r] : (int64_t)r;
+      acc = fmaf(wt[r], to_f(A[ar * K + k]), acc);
+    }
+    partial[(size_t)blockIdx.x * K + k] = acc;
+  }
+}
+
+// warp per node u: out[u] (+)= sum of rows Y[list[i]]
+__global__ void k_seg_reduce_rows(int64_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                                  const float* __restrict__ Y, int K, float* __restrict__ out, bool accumulate) {
+  int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (u >= n) return;
+  int b = ptr[u], e = ptr[u + 1];
+  for (int c = lane * 4; c < K; c += 128) {
+    float4 acc = accumulate ? *reinterpret_cast<const float4*>(out + u * K + c) : make_float4(0, 0, 0, 0);
+    int i = b;
+    for (; i + 1 < e; i += 2) {
+      float4 v0 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i] * K + c));
+      float4 v1 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i + 1] * K + c));
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+    }
+    if (i < e) {
+      float4 v0 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i] * K + c));
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+    }
+    *reinterpret_cast<float4*>(out + u * K + c) = acc;
+  }
+}
+
+// ---------------------------------------------------------------- A2 weight products
+// y_r = W_r b_r  (t-path of RGAT after reordering: attt = (h_d W_r) . b_r = h_d . (W_r b_r))
+template <class TW>
+__global__ void k_rgat_y(int d_in, int d_out, const TW* W, const TW* b, float* y) {
+  int r = blockIdx.x;
+  for (int k = threadIdx.x; k < d_in; k += blockDim.x) {
+    float acc = 0.f;
+    for (int n = 0; n < d_out; ++n)
+      acc = fmaf(to_f(W[((size_t)r * d_in + k) * d_out + n]), to_f(b[(size_t)r * d_out + n]), acc);
+    y[(size_t)r * d_in + k] = acc;
+  }
+}
+
+// F[r*T+t] = [ (mu_r/sqrt(d)) Wk_t Watt_r | Wv_t Wmsg_r ]   (d_in x 2d)
+template <class TW>
+__global__ void k_hgt_fold(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt, const TW* Wmsg,
+                           const float* mu, float* F, TW* Fdt) {
+  int rt = blockIdx.x, r = rt / T, t = rt % T;
+  float c = mu[r] * rsqrtf((float)d);
+  for (int idx = threadIdx.x; idx < d_in * 2 * d; idx += blockDim.x) {
+    int k = idx / (2 * d), n2 = idx % (2 * d);
+    bool key = n2 < d;
+    int n = key ? n2 : n2 - d;
+    const TW* L = key ? Wk : Wv;
+    const TW* Rm = key ? Watt : Wmsg;
+    float acc = 0.f;
+    for (int j = 0; j < d; ++j)
+      acc = fmaf(to_f(L[((size_t)t * d_in + k) * d + j]), to_f(Rm[((size_t)r * d + j) * d + n]), acc);
+    if (key) acc *= c;
+    F[(size_t)rt * d_in * 2 * d + idx] = acc;
+    if (Fdt) Fdt[(size_t)rt * d_in * 2 * d + idx] = from_f<TW>(acc);
+  }
+}
+
+// Unfold dF[r*T+t] (d_in x 2d) into the four HGT weight gradients (fixed summation order).
+template <class TW>
+__global__ void k_hgt_unfold_node(int R, int T, int d_in, int d, const TW* Watt, const TW* Wmsg, const float* mu,
+                                  const float* dF, float* dWk, float* dWv) {
+  // one thread per (t, k, j) of dWk / dWv
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)T * d_in * d) return;
+  int t = idx / (d_in * d), k = (idx / d) % d_in, j = idx % d;
+  float ak = 0.f, av = 0.f;
+  for (int r = 0; r < R; ++r) {
+    const float* f = dF + ((size_t)(r * T + t) * d_in + k) * 2 * d;
+    float c = mu[r] * rsqrtf((float)d);
+    float sk = 0.f, sv = 0.f;
+    for (int n = 0; n < d; ++n) {
+      sk = fmaf(f[n], to_f(Watt[((size_t)r * d + j) * d + n]), sk);
+      sv = fmaf(f[d + n], to_f(Wmsg[((size_t)r * d + j) * d + n]), sv);
+    }
+    ak = fmaf(c, sk, ak);
+    av += sv;
+  }
+  if (dWk) dWk[idx] = ak;
+  if (dWv) dWv[idx] = av;
+}
+
+template <class TW>
+__global__ void k_hgt_unfold_rel(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const float* mu,
+                                 const float* dF, float* dWatt, float* dWmsg) {
+  // one thread per (r, j, n)
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)R * d * d) return;
+  int r = idx / (d * d), j = (idx / d) % d, n = idx % d;
+  float c = mu[r] * rsqrtf((float)d);
+  float ak = 0.f, av = 0.f;
+  for (int t = 0; t < T; ++t) {
+    const float* f = dF + (size_t)(r * T + t) * d_in * 2 * d;
+    for (int k = 0; k < d_in; ++k) {
+      ak = fmaf(to_f(Wk[((size_t)t * d_in + k) * d + j]), f[(size_t)k * 2 * d + n], ak);
+      av = fmaf(to_f(Wv[((size_t)t * d_in + k) * d + j]), f[(size_t)k * 2 * d + d + n], av);
+    }
+  }
+  if (dWatt) dWatt[idx] = c * ak;
+  if (dWmsg) dWmsg[idx] = av;
+}
+
+// dW_r += Bsum_r^T b_r (outer product, destination side of the t-path); db_r = Bsum_r W_r
+template <class TW>
+__global__ void k_rgat_tpath_grads(int R, int d_in, int d_out, const TW* W, const TW* b, const float* Bsum, float* dW,
+                                   float* db) {
+  int r = blockIdx.x;
+  if (dW)
+    for (int idx = threadIdx.x; idx < d_in * d_out; idx += blockDim.x) {
+      int k = idx / d_out, n = idx % d_out;
+      dW[(size_t)r * d_in * d_out + idx] += Bsum[(size_t)r * d_in + k] * to_f(b[(size_t)r * d_out + n]);
+    }
+  if (db)
+    for (int n = threadIdx.x; n < d_out; n += blockDim.x) {
+      float acc = 0.f;
+      for (int k = 0; k < d_in; ++k)
+        acc = fmaf(Bsum[(size_t)r * d_in + k], to_f(W[((size_t)r * d_in + k) * d_out + n]), acc);
+      db[(size_t)r * d_out + n] = acc;
+    }
+}
+
+template <class TI>
+__global__ void k_to_f32(int64_t n, const TI* in, float* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = to_f(in[i]);
+}
+template <class TO>
+__global__ void k_from_f32(int64_t n, const float* in, TO* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = from_f<TO>(in[i]);
+}
+
+}  // namespace
+
+void gemm_simt(const GemmArgs& a, cudaStream_t s) {
+  RGNN_CHECK(a.K % KC == 0 && a.K > 0, RGNN_ERR_UNSUPPORTED, "gemm: K must be a positive multiple of 16");
+  if (a.a_dtype == F32 && a.b_dtype == F32 && a.y_dtype == F32) gemm_dispatch<float, float, float>(a, s);
+  else if (a.a_dtype == BF16 && a.b_dtype == BF16 && a.y_dtype == BF16) gemm_dispatch<bf16, bf16, bf16>(a, s);
+  else if (a.a_dtype == BF16 && a.b_dtype == BF16 && a.y_dtype == F32) gemm_dispatch<bf16, bf16, float>(a, s);
+  else if (a.a_dtype == F32 && a.b_dtype == BF16 && a.y_dtype == F32) gemm_dispatch<float, bf16, float>(a, s);
+  else RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "gemm: unsupported dtype combination");
+}
+
+void wgrad(const WgradArgs& a, cudaStream_t s) {
+  const Plan& p = *a.plan;
+  RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));
+  if (p.count == 0) return;
+  dim3 g(p.count, ceil_div(a.K1, 64), ceil_div(a.K2, 64));
+  if (a.a_dtype == F32)
+    launch("wgrad", k_wgrad<float>, g, dim3(256), 0, s, p.tiles, static_cast<const float*>(a.A), a.K1, a.gather, a.Bm,
+           a.K2, a.partial);
+  else
+    launch("wgrad", k_wgrad<bf16>, g, dim3(256), 0, s, p.tiles, static_cast<const bf16*>(a.A), a.K1, a.gather, a.Bm,
+           a.K2, a.partial);
+  int64_t width = (int64_t)a.K1 * a.K2;
+  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,
+         p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
+}
+
+void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather, float* out,
+              int num_w, float* partial, cudaStream_t s) {
+  const Plan& p = *plan;
+  RGNN_CUDA(cudaMemsetAsync(out, 0, (size_t)num_w * K * sizeof(float), s));
+  if (p.count == 0) return;
+  if (a_dtype == F32)
+    launch("seg_wsum", k_seg_wsum<float>, dim3(p.count), dim3(std::min(K, 256)), 0, s, p.tiles, wt,
+           static_cast<const float*>(A), K, gather, partial);
+  else
+    launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(std::min(K, 256)), 0, s, p.tiles, wt,
+           static_cast<const bf16*>(A), K, gather, partial);
+  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(K, 256), p.nseg), dim3(256), 0, s, p.nseg,
+         p.seg_tile_ptr, p.seg_w, partial, (int64_t)K, out);
+}
+
+void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const float* Y, int K, float* out,
+                     bool accumulate, cudaStream_t s) {
+  RGNN_CHECK(K % 4 == 0, RGNN_ERR_UNSUPPORTED, "row width must be a multiple of 4");
+  launch("seg_reduce_rows", k_seg_reduce_rows, dim3(ceil_div(n * 32, 256)), dim3(256), 0, s, n, ptr, list, Y, K, out,
+         accumulate);
+}
+
+void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b, int dtype, float* y,
+                        cudaStream_t s) {
+  if (dtype == F32)
+    launch("rgat_y", k_rgat_y<float>, dim3(R), dim3(std::min(d_in, 256)), 0, s, d_in, d_out,
+           static_cast<const float*>(W), static_cast<const float*>(b), y);
+  else
+    launch("rgat_y", k_rgat_y<bf16>, dim3(R), dim3(std::min(d_in, 256)), 0, s, d_in, d_out,
+           static_cast<const bf16*>(W), static_cast<const bf16*>(b), y);
+}
+
+void hgt_fold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+              const float* mu, int dtype, float* F, void* Fdt, cudaStream_t s) {
+  if (dtype == F32)
+    launch("hgt_fold", k_hgt_fold<float>, dim3(R * T), dim3(256), 0, s, R, T, d_in, d, static_cast<const float*>(Wk),
+           static_cast<const float*>(Wv), static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, F,
+           static_cast<float*>(nullptr));
+  else
+    launch("hgt_fold", k_hgt_fold<bf16>, dim3(R * T), dim3(256), 0, s, R, T, d_in, d, static_cast<const bf16*>(Wk),
+           static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, F,
+           static_cast<bf16*>(Fdt));
+}
+
+void hgt_unfold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+                const float* mu, int dtype, const float* dF, float* dWk, float* dWv, float* dWatt, float* dWmsg,
+                cudaStream_t s) {
+  int64_t nn = (int64_t)T * d_in * d, nr = (int64_t)R * d * d;
+  if (dtype == F32) {
+    if (dWk || dWv)
+      launch("hgt_unfold_node", k_hgt_unfold_node<float>, dim3(ceil_div(nn, 128)), dim3(128), 0, s, R, T, d_in, d,
+             static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, dF, dWk, dWv);
+    if (dWatt || dWmsg)
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<float>, dim3(ceil_div(nr, 128)), dim3(128), 0, s, R, T, d_in, d,
+             static_cast<const float*>(Wk), static_cast<const float*>(Wv), mu, dF, dWatt, dWmsg);
+  } else {
+    if (dWk || dWv)
+      launch("hgt_unfold_node", k_hgt_unfold_node<bf16>, dim3(ceil_div(nn, 128)), dim3(128), 0, s, R, T, d_in, d,
+             static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, dF, dWk, dWv);
+    if (dWatt || dWmsg)
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<bf16>, dim3(ceil_div(nr, 128)), dim3(128), 0, s, R, T, d_in, d,
+             static_cast<const bf16*>(Wk), static_cast<const bf16*>(Wv), mu, dF, dWatt, dWmsg);
+  }
+}
+
+void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, int dtype, const float* Bsum,
+                      float* dW, float* db, cudaStream_t s) {
+  if (dtype == F32)
+    launch("rgat_tpath_grads", k_rgat_tpath_grads<float>, dim3(R), dim3(256), 0, s, R, d_in, d_out,
+           static_cast<const float*>(W), static_cast<const float*>(b), Bsum, dW, db);
+  else
+    launch("rgat_tpath_grads", k_rgat_tpath_grads<bf16>, dim3(R), dim3(256), 0, s, R, d_in, d_out,
+           static_cast<const bf16*>(W), static_cast<const bf16*>(b), Bsum, dW, db);
+}
+
+void convert_f32(int64_t n, const void* in, int dtype, float* out, cudaStream_t s) {
+  if (dtype == F32)
+    RGNN_CUDA(cudaMemcpyAsync(out, in, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  else
+    launch("to_f32", k_to_f32<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, n, static_cast<const bf16*>(in), out);
+}
+
+void convert_dt(int64_t n, const float* in, void* out, int dtype, cudaStream_t s) {
+  if (dtype == F32)
+    RGNN_CUDA(cudaMemcpyAsync(out, in, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  else
+    launch("from_f32", k_from_f32<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, n, in, static_cast<bf16*>(out));
+}
+
+}  // namespace rgnn

@@ -1,0 +1,398 @@
+// A0 — graph build (C1 of §8(c)).
+//
+// From device COO (src, dst, rel) it builds, all on the GPU with stable radix
+// sorts (CUB, CUDA toolkit) and flag/scan compaction:
+//   etype_ptr, dst-CSR (key (dst, rel, src, eid)), src-CSC (key (src, rel, dst, eid)),
+//   compact pairs = runs of (src, rel) in CSC order re-ranked by (rel, src)
+//   ("one row per unique (edge type, source node) pair", §3.3.2),
+//   edge_pair / csr_pair / csc_pair, the per-source pair list, the CSC->CSR map,
+//   (rel, dst) runs for the RGAT destination-side gradient, and the (rel, src type)
+//   sub-segments used by HGT's folded weights.
+// Stability of the LSD radix sort makes the eid tie-break implicit: equal keys keep
+// ascending edge order.  Host syncs: twice (after counting, after building).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "graph.cuh"
+
+namespace rgnn {
+namespace {
+
+__global__ void k_validate(int64_t E, const int32_t* src, const int32_t* dst, const int32_t* rel, int64_t N,
+                           int32_t R, int64_t dst_lo, int64_t dst_hi, unsigned long long* first_bad,
+                           int32_t* keep_flag) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int32_t s = src[e], d = dst[e], r = rel[e];
+  bool ok = s >= 0 && s < N && d >= 0 && d < N && r >= 0 && r < R;
+  if (!ok) atomicMin(first_bad, (unsigned long long)e);
+  keep_flag[e] = ok && d >= dst_lo && d < dst_hi;
+}
+
+__global__ void k_gather3(int64_t E, const int32_t* idx, const int32_t* a, const int32_t* b, const int32_t* c,
+                          int32_t* oa, int32_t* ob, int32_t* oc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  int32_t j = idx[i];
+  oa[i] = a[j]; ob[i] = b[j]; oc[i] = c[j];
+}
+
+__global__ void k_iota(int64_t n, int32_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)i;
+}
+
+// key = (a << (wb + wc)) | (b << wc) | c
+__global__ void k_make_key(int64_t E, const int32_t* a, const int32_t* b, const int32_t* c, int wb, int wc,
+                           uint64_t* key) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  key[i] = ((uint64_t)(uint32_t)a[i] << (wb + wc)) | ((uint64_t)(uint32_t)b[i] << wc) | (uint64_t)(uint32_t)c[i];
+}
+
+__global__ void k_decode_key(int64_t E, const uint64_t* key, int wb, int wc, int32_t* a, int32_t* b, int32_t* c) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  uint64_t k = key[i];
+  a[i] = (int32_t)(k >> (wb + wc));
+  b[i] = (int32_t)((k >> wc) & ((1ull << wb) - 1));
+  c[i] = (int32_t)(k & ((1ull << wc) - 1));
+}
+
+__global__ void k_histogram(int64_t E, const int32_t* v, int32_t* count) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) atomicAdd(&count[v[i]], 1);  // integer: order-independent result
+}
+
+// heads of runs of equal (a, b) in a sorted sequence
+__global__ void k_run_heads(int64_t E, const int32_t* a, const int32_t* b, int32_t* flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  flag[i] = (i == 0) || a[i] != a[i - 1] || b[i] != b[i - 1];
+}
+
+__global__ void k_run_info(int64_t nruns, int64_t E, const int32_t* head_pos, const int32_t* a, const int32_t* b,
+                           int nb_b, uint64_t* run_key, int32_t* run_len) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nruns) return;
+  int32_t h = head_pos[j];
+  int32_t nx = (j + 1 < nruns) ? head_pos[j + 1] : (int32_t)E;
+  run_len[j] = nx - h;
+  // run key sorted by (b, a): relation-major
+  run_key[j] = ((uint64_t)(uint32_t)b[h] << nb_b) | (uint64_t)(uint32_t)a[h];
+}
+
+__global__ void k_scatter_rank(int64_t n, const int32_t* order, int32_t* rank_of) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) rank_of[order[p]] = (int32_t)p;
+}
+
+__global__ void k_pair_fields(int64_t n, const int32_t* order, const uint64_t* sorted_key, int nb,
+                              const int32_t* head_pos, const int32_t* run_len, int32_t* node_of, int32_t* rel_of,
+                              int32_t* beg, int32_t* deg) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint64_t k = sorted_key[p];
+  node_of[p] = (int32_t)(k & ((1ull << nb) - 1));
+  rel_of[p] = (int32_t)(k >> nb);
+  int32_t j = order[p];
+  beg[p] = head_pos[j];
+  deg[p] = run_len[j];
+}
+
+// position -> run index (inclusive scan of heads - 1) -> pair rank
+__global__ void k_pos_pair(int64_t E, const int32_t* run_incl, const int32_t* rank_of_run, int32_t* pos_pair) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) pos_pair[i] = rank_of_run[run_incl[i] - 1];
+}
+
+__global__ void k_scatter(int64_t E, const int32_t* idx, const int32_t* val, int32_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) out[idx[i]] = val[i];
+}
+__global__ void k_scatter_iota(int64_t E, const int32_t* idx, int32_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) out[idx[i]] = (int32_t)i;
+}
+__global__ void k_gather(int64_t E, const int32_t* idx, const int32_t* val, int32_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) out[i] = val[idx[i]];
+}
+
+__global__ void k_max_diff(int64_t n, const int32_t* ptr, unsigned long long* mx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) atomicMax(mx, (unsigned long long)(ptr[i + 1] - ptr[i]));
+}
+__global__ void k_max_val(int64_t n, const int32_t* v, unsigned long long* mx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) atomicMax(mx, (unsigned long long)v[i]);
+}
+
+// first pair index whose (rel, src) >= (r, node_type_ptr[t]) for every (r, t) and the end
+__global__ void k_rt_bounds(int32_t R, int32_t T, const int64_t* ntp, int nb, const uint64_t* sorted_key, int64_t U,
+                            int32_t* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > R * T) return;
+  if (i == R * T) { out[i] = (int32_t)U; return; }
+  int r = i / T, t = i % T;
+  uint64_t target = ((uint64_t)r << nb) | (uint64_t)ntp[t];
+  int64_t lo = 0, hi = U;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) / 2;
+    if (sorted_key[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  out[i] = (int32_t)lo;
+}
+
+int bits_for(int64_t n) {
+  int b = 0;
+  while ((int64_t(1) << b) < n) ++b;
+  return std::max(b, 1);
+}
+
+const int TB = 256;
+
+struct Tmp {  // temporaries freed at the end of the build
+  const Allocator& a;
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  Tmp(const Allocator& al, cudaStream_t st) : a(al), s(st) {}
+  template <class T>
+  T* get(size_t n) {
+    void* p = a.get((n ? n : 1) * sizeof(T), s);
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Tmp() {
+    for (void* p : ptrs) a.put(p, s);
+  }
+};
+
+void radix_pairs(Tmp& tmp, const uint64_t* kin, uint64_t* kout, const int32_t* vin, int32_t* vout, int64_t n,
+                 int end_bit, cudaStream_t s) {
+  if (n == 0) return;
+  size_t bytes = 0;
+  RGNN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, s));
+  void* t = tmp.get<char>(bytes);
+  RGNN_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, s));
+  count_launch();
+}
+
+void excl_scan_counts(Tmp& tmp, int32_t* counts, int32_t* out, int64_t n, cudaStream_t s) {
+  // out[0..n] = exclusive scan of counts[0..n-1] with out[n] = total
+  size_t bytes = 0;
+  RGNN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, out, (int)(n + 1), s));
+  void* t = tmp.get<char>(bytes);
+  RGNN_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, counts, out, (int)(n + 1), s));
+  count_launch();
+}
+
+void incl_scan(Tmp& tmp, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  size_t bytes = 0;
+  RGNN_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int)n, s));
+  void* t = tmp.get<char>(bytes);
+  RGNN_CUDA(cub::DeviceScan::InclusiveSum(t, bytes, in, out, (int)n, s));
+  count_launch();
+}
+
+// compact positions i with flag[i] != 0 (in order); returns count through d_num
+void select_flagged(Tmp& tmp, const int32_t* flags, int32_t* out, int32_t* d_num, int64_t n, cudaStream_t s) {
+  if (n == 0) {
+    RGNN_CUDA(cudaMemsetAsync(d_num, 0, sizeof(int32_t), s));
+    return;
+  }
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t bytes = 0;
+  RGNN_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_num, (int)n, s));
+  void* t = tmp.get<char>(bytes);
+  RGNN_CUDA(cub::DeviceSelect::Flagged(t, bytes, it, flags, out, d_num, (int)n, s));
+  count_launch();
+}
+
+// histogram of v[0..n) into [0, nbins) and exclusive prefix (nbins+1 entries)
+void hist_prefix(Tmp& tmp, const int32_t* v, int64_t n, int64_t nbins, int32_t* ptr_out, cudaStream_t s) {
+  int32_t* cnt = tmp.get<int32_t>(nbins + 1);
+  RGNN_CUDA(cudaMemsetAsync(cnt, 0, (nbins + 1) * sizeof(int32_t), s));
+  launch("graph_histogram", k_histogram, dim3(ceil_div(n, TB)), dim3(TB), 0, s, n, v, cnt);
+  excl_scan_counts(tmp, cnt, ptr_out, nbins, s);
+}
+
+}  // namespace
+
+void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, const int32_t* rel_in,
+                 int64_t E_in, cudaStream_t s) {
+  const int64_t N = g->N;
+  const int32_t R = g->R, T = g->T;
+  Tmp tmp(g->alloc, s);
+
+  // ---- validate + filter to the owned destination range
+  unsigned long long* d_stats = tmp.get<unsigned long long>(4);
+  unsigned long long init[4] = {~0ull, 0, 0, 0};
+  RGNN_CUDA(cudaMemcpyAsync(d_stats, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  int32_t* keep = tmp.get<int32_t>(E_in);
+  launch("graph_validate", k_validate, dim3(ceil_div(E_in, TB)), dim3(TB), 0, s, E_in, src_in, dst_in, rel_in, N, R,
+         g->dst_lo, g->dst_hi, d_stats, keep);
+  int32_t* kept = tmp.get<int32_t>(E_in);
+  int32_t* d_num = tmp.get<int32_t>(4);
+  select_flagged(tmp, keep, kept, d_num, E_in, s);
+  unsigned long long h_bad = 0;
+  int32_t h_kept = 0;
+  RGNN_CUDA(cudaMemcpyAsync(&h_bad, d_stats, sizeof(h_bad), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaMemcpyAsync(&h_kept, d_num, sizeof(h_kept), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  if (h_bad != ~0ull)
+    RGNN_FAIL(RGNN_ERR_OUT_OF_RANGE, "node or relation id out of range at edge " + std::to_string(h_bad));
+  const int64_t E = h_kept;
+  g->E = E;
+
+  int32_t* src = tmp.get<int32_t>(E);
+  int32_t* dst = tmp.get<int32_t>(E);
+  int32_t* rel = tmp.get<int32_t>(E);
+  g->kept_eid = g->dev_i32(E, s);
+  RGNN_CUDA(cudaMemcpyAsync(g->kept_eid, kept, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  launch("graph_gather", k_gather3, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, kept, src_in, dst_in, rel_in, src, dst,
+         rel);
+
+  const int nb = bits_for(N), rb = bits_for(R);
+  g->nb = nb;
+  g->rb = rb;
+  RGNN_CHECK(2 * nb + rb <= 64, RGNN_ERR_UNSUPPORTED, "sort key wider than 64 bits (N or R too large)");
+
+  int32_t* eid = tmp.get<int32_t>(E);
+  launch("graph_iota", k_iota, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, eid);
+  uint64_t* key = tmp.get<uint64_t>(E);
+  uint64_t* key_sorted = tmp.get<uint64_t>(E);
+
+  // ---- etype_ptr
+  g->etype_ptr = g->dev_i32(R + 1, s);
+  hist_prefix(tmp, rel, E, R, g->etype_ptr, s);
+
+  // ---- dst-CSR: key (dst, rel, src), stable => eid ascending among equals
+  g->csr_src = g->dev_i32(E, s);
+  g->csr_rel = g->dev_i32(E, s);
+  g->csr_eid = g->dev_i32(E, s);
+  g->row_ptr = g->dev_i32(N + 1, s);
+  int32_t* csr_dst = tmp.get<int32_t>(E);
+  launch("graph_key", k_make_key, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, dst, rel, src, rb, nb, key);
+  radix_pairs(tmp, key, key_sorted, eid, g->csr_eid, E, 2 * nb + rb, s);
+  launch("graph_decode", k_decode_key, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, key_sorted, rb, nb, csr_dst,
+         g->csr_rel, g->csr_src);
+  hist_prefix(tmp, dst, E, N, g->row_ptr, s);
+
+  // ---- src-CSC: key (src, rel, dst)
+  g->csc_dst = g->dev_i32(E, s);
+  g->csc_rel = g->dev_i32(E, s);
+  g->csc_eid = g->dev_i32(E, s);
+  g->col_ptr = g->dev_i32(N + 1, s);
+  int32_t* csc_src = tmp.get<int32_t>(E);
+  launch("graph_key", k_make_key, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, src, rel, dst, rb, nb, key);
+  radix_pairs(tmp, key, key_sorted, eid, g->csc_eid, E, 2 * nb + rb, s);
+  launch("graph_decode", k_decode_key, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, key_sorted, rb, nb, csc_src,
+         g->csc_rel, g->csc_dst);
+  hist_prefix(tmp, src, E, N, g->col_ptr, s);
+
+  // ---- runs of (src, rel) in CSC order = compact pairs; runs of (dst, rel) in CSR order = dst pairs
+  int32_t* flag = tmp.get<int32_t>(E);
+  int32_t* head_pos = tmp.get<int32_t>(E);
+  int32_t* dflag = tmp.get<int32_t>(E);
+  int32_t* dhead_pos = tmp.get<int32_t>(E);
+  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csc_src, g->csc_rel, flag);
+  select_flagged(tmp, flag, head_pos, d_num, E, s);
+  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csr_dst, g->csr_rel, dflag);
+  select_flagged(tmp, dflag, dhead_pos, d_num + 1, E, s);
+  int32_t h_counts[2] = {0, 0};
+  RGNN_CUDA(cudaMemcpyAsync(h_counts, d_num, sizeof(h_counts), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  const int64_t U = h_counts[0], UD = h_counts[1];
+  g->U = U;
+  g->UD = UD;
+
+  // pairs: sort runs by (rel, src)
+  uint64_t* rkey = tmp.get<uint64_t>(U);
+  uint64_t* rkey_sorted = tmp.get<uint64_t>(U);
+  int32_t* rlen = tmp.get<int32_t>(U);
+  int32_t* ridx = tmp.get<int32_t>(U);
+  int32_t* order = tmp.get<int32_t>(U);
+  int32_t* rank_of_run = tmp.get<int32_t>(U);
+  int32_t* pair_rel = tmp.get<int32_t>(U);
+  launch("graph_runs", k_run_info, dim3(ceil_div(U, TB)), dim3(TB), 0, s, U, E, head_pos, csc_src, g->csc_rel, nb,
+         rkey, rlen);
+  launch("graph_iota", k_iota, dim3(ceil_div(U, TB)), dim3(TB), 0, s, U, ridx);
+  radix_pairs(tmp, rkey, rkey_sorted, ridx, order, U, nb + rb, s);
+  launch("graph_rank", k_scatter_rank, dim3(ceil_div(U, TB)), dim3(TB), 0, s, U, order, rank_of_run);
+  g->pair_src = g->dev_i32(U, s);
+  g->pair_csc_beg = g->dev_i32(U, s);
+  g->pair_deg = g->dev_i32(U, s);
+  launch("graph_pairs", k_pair_fields, dim3(ceil_div(U, TB)), dim3(TB), 0, s, U, order, rkey_sorted, nb, head_pos,
+         rlen, g->pair_src, pair_rel, g->pair_csc_beg, g->pair_deg);
+  g->pair_rel_ptr = g->dev_i32(R + 1, s);
+  hist_prefix(tmp, pair_rel, U, R, g->pair_rel_ptr, s);
+  // per-source pair list: heads in CSC order are the pairs ordered by (src, rel)
+  g->src_pairs = g->dev_i32(U, s);
+  RGNN_CUDA(cudaMemcpyAsync(g->src_pairs, rank_of_run, U * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  g->src_pair_ptr = g->dev_i32(N + 1, s);
+  hist_prefix(tmp, g->pair_src, U, N, g->src_pair_ptr, s);
+  // csc_pair, edge_pair, csr_pair
+  int32_t* run_incl = tmp.get<int32_t>(E);
+  incl_scan(tmp, flag, run_incl, E, s);
+  g->csc_pair = g->dev_i32(E, s);
+  g->edge_pair = g->dev_i32(E, s);
+  g->csr_pair = g->dev_i32(E, s);
+  launch("graph_pos_pair", k_pos_pair, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, run_incl, rank_of_run, g->csc_pair);
+  launch("graph_scatter", k_scatter, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csc_eid, g->csc_pair, g->edge_pair);
+  launch("graph_gather1", k_gather, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csr_eid, g->edge_pair, g->csr_pair);
+  // csc2csr
+  int32_t* csr_pos_of_eid = tmp.get<int32_t>(E);
+  g->csc2csr = g->dev_i32(E, s);
+  launch("graph_scatter_iota", k_scatter_iota, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csr_eid, csr_pos_of_eid);
+  launch("graph_gather1", k_gather, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csc_eid, csr_pos_of_eid, g->csc2csr);
+
+  // (rel, dst) pairs from CSR runs
+  uint64_t* dkey = tmp.get<uint64_t>(UD);
+  uint64_t* dkey_sorted = tmp.get<uint64_t>(UD);
+  int32_t* dlen = tmp.get<int32_t>(UD);
+  int32_t* didx = tmp.get<int32_t>(UD);
+  int32_t* dorder = tmp.get<int32_t>(UD);
+  int32_t* dpair_rel = tmp.get<int32_t>(UD);
+  launch("graph_runs", k_run_info, dim3(ceil_div(UD, TB)), dim3(TB), 0, s, UD, E, dhead_pos, csr_dst, g->csr_rel, nb,
+         dkey, dlen);
+  launch("graph_iota", k_iota, dim3(ceil_div(UD, TB)), dim3(TB), 0, s, UD, didx);
+  radix_pairs(tmp, dkey, dkey_sorted, didx, dorder, UD, nb + rb, s);
+  g->dpair_dst = g->dev_i32(UD, s);
+  g->dpair_csr_beg = g->dev_i32(UD, s);
+  g->dpair_cnt = g->dev_i32(UD, s);
+  launch("graph_pairs", k_pair_fields, dim3(ceil_div(UD, TB)), dim3(TB), 0, s, UD, dorder, dkey_sorted, nb, dhead_pos,
+         dlen, g->dpair_dst, dpair_rel, g->dpair_csr_beg, g->dpair_cnt);
+  int32_t* dpair_rel_ptr = tmp.get<int32_t>(R + 1);
+  hist_prefix(tmp, dpair_rel, UD, R, dpair_rel_ptr, s);
+
+  // (rel, src type) sub-segments of the pairs
+  int64_t* d_ntp = tmp.get<int64_t>(T + 1);
+  RGNN_CUDA(cudaMemcpyAsync(d_ntp, g->node_type_ptr.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  int32_t* rt = tmp.get<int32_t>((int64_t)R * T + 1);
+  launch("graph_rt_bounds", k_rt_bounds, dim3(ceil_div((int64_t)R * T + 1, TB)), dim3(TB), 0, s, R, T, d_ntp, nb,
+         rkey_sorted, U, rt);
+
+  // stats
+  launch("graph_maxdeg", k_max_diff, dim3(ceil_div(N, TB)), dim3(TB), 0, s, N, g->row_ptr, d_stats + 1);
+  launch("graph_maxdeg", k_max_val, dim3(ceil_div(U, TB)), dim3(TB), 0, s, U, g->pair_deg, d_stats + 2);
+  unsigned long long h_stats[4];
+  g->pair_rel_ptr_h.resize(R + 1);
+  g->dpair_rel_ptr_h.resize(R + 1);
+  g->pair_rt_ptr_h.resize((size_t)R * T + 1);
+  RGNN_CUDA(cudaMemcpyAsync(h_stats, d_stats, sizeof(h_stats), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaMemcpyAsync(g->pair_rel_ptr_h.data(), g->pair_rel_ptr, (R + 1) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaMemcpyAsync(g->dpair_rel_ptr_h.data(), dpair_rel_ptr, (R + 1) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaMemcpyAsync(g->pair_rt_ptr_h.data(), rt, ((size_t)R * T + 1) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  g->max_in_deg = (int64_t)h_stats[1];
+  g->max_pair_deg = (int64_t)h_stats[2];
+}
+
+}  // namespace rgnn

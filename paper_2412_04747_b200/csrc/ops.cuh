@@ -1,0 +1,69 @@
+// Host-side entry points of the kernels (internal).
+#pragma once
+
+#include "graph.cuh"
+
+namespace rgnn {
+
+enum DType { F32 = 0, BF16 = 1 };
+
+// Typed segment GEMM  Y[row] = A[gather(row)] x B_w  for every tile (row0,row1,w)
+// (the GEMM template Y[S] = X[G] x W[T], §3.3.3; segment MM P:634).
+struct GemmArgs {
+  const Tile* tiles = nullptr;
+  int ntiles = 0;
+  const void* A = nullptr;
+  int a_dtype = F32;
+  int K = 0;                        // A width
+  const int32_t* gather = nullptr;  // NULL: identity
+  const void* B = nullptr;          // weights: [w][K][N] or (transB) [w][N][K]
+  int b_dtype = F32;
+  bool transB = false;
+  void* Y = nullptr;
+  int y_dtype = F32;
+  int N = 0;          // Y width (ldy = N)
+  const float* dotvec = nullptr;  // optional epilogue: dotout[row] = sum_n Y_fp32[row][n] * dotvec[w][n]
+  float* dotout = nullptr;
+};
+void gemm_simt(const GemmArgs& a, cudaStream_t s);
+bool gemm_tc_supported(const GemmArgs& a);
+void gemm_tc(const GemmArgs& a, cudaStream_t s);
+
+// Segmented weight gradient  out[w] = sum_{rows of w} A[gather(row)]^T Bm[row]   (fp32 out)
+// Deterministic two-level reduction: per-tile partials, then per-segment sums in tile order.
+struct WgradArgs {
+  const Plan* plan = nullptr;  // tiles with pad = segment id, w = weight index
+  const void* A = nullptr;
+  int a_dtype = F32;
+  int K1 = 0;
+  const int32_t* gather = nullptr;
+  const float* Bm = nullptr;
+  int K2 = 0;
+  float* out = nullptr;  // [num_w][K1][K2]
+  int num_w = 0;
+  float* partial = nullptr;  // scratch [ntiles][K1][K2]
+};
+void wgrad(const WgradArgs& a, cudaStream_t s);
+
+// out[w][k] = sum_{rows of w} wt[row] * A[gather(row)][k]  (fp32 out; same two-level scheme)
+void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather,
+              float* out, int num_w, float* partial, cudaStream_t s);
+
+// out[u][:] (+)= sum_{i in [ptr[u], ptr[u+1])} Y[list[i]][:]   (fp32 rows of width K)
+void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const float* Y, int K, float* out,
+                     bool accumulate, cudaStream_t s);
+
+// A2 (linear-operator reordering): weight-weight products.
+void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b, int dtype, float* y,
+                        cudaStream_t s);
+void hgt_fold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+              const float* mu, int dtype, float* F32out, void* Fdt, cudaStream_t s);
+void hgt_unfold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+                const float* mu, int dtype, const float* dF, float* dWk, float* dWv, float* dWatt, float* dWmsg,
+                cudaStream_t s);
+void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, int dtype, const float* Bsum,
+                      float* dW, float* db, cudaStream_t s);
+void convert_f32(int64_t n, const void* in, int dtype, float* out, cudaStream_t s);
+void convert_dt(int64_t n, const float* in, void* out, int dtype, cudaStream_t s);
+
+}  // namespace rgnn

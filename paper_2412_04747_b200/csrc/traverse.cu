@@ -1,0 +1,721 @@
+// Edge-traversal kernels.
+//
+// Forward, destination-major over the dst-CSR (one warp per destination row v):
+//   A3 edge logits (g-SDDMM; RGAT: LeakyReLU(s_p + x_v . y_r), lst:ir_example
+//      P:739-745 after reordering; HGT: K~_p . q_v with K~ pre-scaled by mu_r/sqrt(d)),
+//   A4 edge softmax (lst:ir_example P:730-738) as an online max/sum rescale,
+//   A5 attention- or norm-weighted aggregation of the compact pair rows (g-SpMM),
+// all fused, so logits and attention never touch HBM; only (m_v, sum_v) are saved.
+// The warp is split into EG = 32 / LPR edge groups of LPR lanes; a group owns one
+// edge at a time and each lane moves one 16-byte vector of the gathered row, so a
+// warp has EG rows in flight per step and UNR steps are unrolled.  Each group keeps
+// its own online-softmax state; the states are merged with shuffles at the end.
+//
+// Backward, destination-major (A6): recompute logits/alpha from (m_v, sum_v), the
+// softmax backward row term sum_e alpha_e dalpha_e = G_v . out_v, per-edge
+// (alpha_e, dl_e or dz_e) to a CSR-ordered buffer, dQ_v (HGT) or the t-path dX_v (RGAT).
+// Backward, pair-major over the src-CSC (A7): one group per compact pair p, summing
+// over its edges (contiguous in the CSC) -> dP_p / [dK~_p | dM_p].  No atomics.
+#include <math_constants.h>
+
+#include "ops.cuh"
+#include "traverse.cuh"
+
+namespace rgnn {
+namespace {
+
+constexpr int UNR = 4;
+
+template <class TP, int D>
+struct Geo {
+  static constexpr int V = Vec<TP>::N;  // elements per lane-vector
+  static constexpr int LPR = D / V;     // lanes per row
+  static constexpr int EG = 32 / LPR;   // edge groups per warp
+  static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "unsupported row width");
+};
+
+template <int V>
+__device__ __forceinline__ void ld_f32(const float* p, float* o) {
+#pragma unroll
+  for (int i = 0; i < V; i += 4) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(p + i));
+    o[i] = x.x; o[i + 1] = x.y; o[i + 2] = x.z; o[i + 3] = x.w;
+  }
+}
+template <int V>
+__device__ __forceinline__ void st_f32(float* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < V; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+}
+// 4 consecutive elements of a table row as floats (8 B for bf16, 16 B for fp32)
+__device__ __forceinline__ void ld4(const float* p, float* o) {
+  float4 x = __ldg(reinterpret_cast<const float4*>(p));
+  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
+}
+__device__ __forceinline__ void ld4(const bf16* p, float* o) {
+  uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+  o[0] = __uint_as_float(x.x << 16); o[1] = __uint_as_float(x.x & 0xffff0000u);
+  o[2] = __uint_as_float(x.y << 16); o[3] = __uint_as_float(x.y & 0xffff0000u);
+}
+
+// sum over the LPR lanes of one group
+template <int LPR>
+__device__ __forceinline__ float gsum(float x) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ float safe_exp_diff(float a, float b) {  // exp(a - b), 0 when a = -inf
+  return a == -CUDART_INF_F ? 0.f : __expf(a - b);
+}
+
+// Merge the online-softmax states of the EG groups (lanes with equal lane % LPR).
+template <int LPR, int V>
+__device__ __forceinline__ void merge_groups(float& m, float& s, float* acc) {
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+    float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    float mn = fmaxf(m, m2);
+    float a = safe_exp_diff(m, mn), b = safe_exp_diff(m2, mn);
+    s = s * a + s2 * b;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float x2 = __shfl_xor_sync(0xffffffffu, acc[k], o);
+      acc[k] = acc[k] * a + x2 * b;
+    }
+    m = mn;
+  }
+}
+
+template <int LPR, int V>
+__device__ __forceinline__ void sum_groups(float* acc) {
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+}
+
+// ------------------------------------------------------------------ RGCN forward (A5)
+// out_v (+)= sum_e norm_e P[pair_e]     (Eq. 3.1; self-loop X W_0 already in out when accumulate)
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+                                                  const int32_t* __restrict__ csr_pair,
+                                                  const float* __restrict__ norm, const TP* __restrict__ P,
+                                                  float* __restrict__ out, bool accumulate) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= N) return;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int b = row_ptr[v], e = row_ptr[v + 1];
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
+    const int i0 = base + g;
+    uint4 raw[UNR];
+    float w[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * EG;
+      w[u] = 0.f;
+      raw[u] = make_uint4(0, 0, 0, 0);
+      if (i < e) {
+        int p = csr_pair[i];
+        w[u] = norm[i];
+        raw[u] = ldg16(P + (int64_t)p * D + c * V);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float x[V];
+      cvt16<TP>(raw[u], x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(w[u], x[k], acc[k]);
+    }
+  }
+  sum_groups<LPR, V>(acc);
+  if (g == 0) {
+    float* o = out + v * D + c * V;
+    if (accumulate) {
+      float prev[V];
+      ld_f32<V>(o, prev);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += prev[k];
+    }
+    st_f32<V>(o, acc);
+  }
+}
+
+// ------------------------------------------------------------------ HGT forward (A3+A4+A5)
+// KM row of pair p = [K~_p | M_p] (2D wide);  l_e = K~_p . q_v;  out_v = sum softmax(l)_e M_p
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+                                                 const int32_t* __restrict__ csr_pair, const TP* __restrict__ KM,
+                                                 const TP* __restrict__ Q, float* __restrict__ out,
+                                                 float2* __restrict__ stats) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= N) return;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int b = row_ptr[v], e = row_ptr[v + 1];
+  float q[V];
+  cvt16<TP>(ldg16(Q + v * D + c * V), q);
+  float m = -CUDART_INF_F, s = 0.f, acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
+    const int i0 = base + g;
+    uint4 rk[UNR], rm[UNR];
+    bool ok[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * EG;
+      ok[u] = i < e;
+      rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
+      if (ok[u]) {
+        int64_t p = csr_pair[i];
+        rk[u] = ldg16(KM + p * 2 * D + c * V);
+        rm[u] = ldg16(KM + p * 2 * D + D + c * V);
+      }
+    }
+    float l[UNR], mx = m;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float kx[V];
+      cvt16<TP>(rk[u], kx);
+      float d = 0.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) d = fmaf(kx[k], q[k], d);
+      d = gsum<LPR>(d);
+      l[u] = ok[u] ? d : -CUDART_INF_F;
+      mx = fmaxf(mx, l[u]);
+    }
+    float sc = safe_exp_diff(m, mx);
+    s *= sc;
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] *= sc;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float w = safe_exp_diff(l[u], mx);
+      s += w;
+      float mv[V];
+      cvt16<TP>(rm[u], mv);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(w, mv[k], acc[k]);
+    }
+    m = mx;
+  }
+  merge_groups<LPR, V>(m, s, acc);
+  float inv = s > 0.f ? 1.f / s : 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] *= inv;
+  if (g == 0) st_f32<V>(out + v * D + c * V, acc);
+  if (lane == 0) stats[v] = make_float2(m, s);
+}
+
+// ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
+// z_e = s_p + x_v . y_r (reordered t-path), l = LeakyReLU(z), out_v = sum softmax(l)_e P_p.
+// Requires d_in == d_out == D (x_v chunk in registers).
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+                                                  const int32_t* __restrict__ csr_pair,
+                                                  const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+                                                  const float* __restrict__ spair, const TP* __restrict__ X,
+                                                  const float* __restrict__ y, float slope, float* __restrict__ out,
+                                                  float2* __restrict__ stats) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= N) return;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int b = row_ptr[v], e = row_ptr[v + 1];
+  float x[V];
+  cvt16<TP>(ldg16(X + v * D + c * V), x);
+  float m = -CUDART_INF_F, s = 0.f, acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
+    const int i0 = base + g;
+    uint4 rp[UNR];
+    float sp[UNR], yv[UNR][V];
+    bool ok[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * EG;
+      ok[u] = i < e;
+      rp[u] = make_uint4(0, 0, 0, 0);
+      sp[u] = 0.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
+      if (ok[u]) {
+        int64_t p = csr_pair[i];
+        int r = csr_rel[i];
+        rp[u] = ldg16(P + p * D + c * V);
+        sp[u] = spair[p];
+        ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+      }
+    }
+    float l[UNR], mx = m;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) t = fmaf(x[k], yv[u][k], t);
+      t = gsum<LPR>(t);
+      float z = sp[u] + t;
+      float lz = z > 0.f ? z : slope * z;
+      l[u] = ok[u] ? lz : -CUDART_INF_F;
+      mx = fmaxf(mx, l[u]);
+    }
+    float sc = safe_exp_diff(m, mx);
+    s *= sc;
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] *= sc;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float w = safe_exp_diff(l[u], mx);
+      s += w;
+      float pv[V];
+      cvt16<TP>(rp[u], pv);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(w, pv[k], acc[k]);
+    }
+    m = mx;
+  }
+  merge_groups<LPR, V>(m, s, acc);
+  float inv = s > 0.f ? 1.f / s : 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] *= inv;
+  if (g == 0) st_f32<V>(out + v * D + c * V, acc);
+  if (lane == 0) stats[v] = make_float2(m, s);
+}
+
+// ------------------------------------------------------------------ HGT backward, dst-major (A6)
+// alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
+// dQ_v = sum_e dl_e K~_p ; ebuf[csr pos] = (alpha_e, dl_e)
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t N, const int32_t* __restrict__ row_ptr,
+                                                     const int32_t* __restrict__ csr_pair,
+                                                     const TP* __restrict__ KM, const TP* __restrict__ Q,
+                                                     const float2* __restrict__ stats, const float* __restrict__ Gr,
+                                                     const float* __restrict__ out, float2* __restrict__ ebuf,
+                                                     float* __restrict__ dQ) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= N) return;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int b = row_ptr[v], e = row_ptr[v + 1];
+  float dq[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) dq[k] = 0.f;
+  if (e > b) {
+    float q[V], gv[V], ov[V];
+    cvt16<TP>(ldg16(Q + v * D + c * V), q);
+    ld_f32<V>(Gr + v * D + c * V, gv);
+    ld_f32<V>(out + v * D + c * V, ov);
+    float go = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
+    go = gsum<LPR>(go);
+    const float2 st = stats[v];
+    const float inv = 1.f / st.y;
+    for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
+    const int i0 = base + g;
+      uint4 rk[UNR], rm[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        int i = i0 + u * EG;
+        rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
+        if (i < e) {
+          int64_t p = csr_pair[i];
+          rk[u] = ldg16(KM + p * 2 * D + c * V);
+          rm[u] = ldg16(KM + p * 2 * D + D + c * V);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        int i = i0 + u * EG;
+        float kx[V], mv[V];
+        cvt16<TP>(rk[u], kx);
+        cvt16<TP>(rm[u], mv);
+        float l = 0.f, da = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          l = fmaf(kx[k], q[k], l);
+          da = fmaf(gv[k], mv[k], da);
+        }
+        l = gsum<LPR>(l);
+        da = gsum<LPR>(da);
+        float alpha = __expf(l - st.x) * inv;
+        float dl = alpha * (da - go);
+        if (i < e) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
+          if (c == 0) ebuf[i] = make_float2(alpha, dl);
+        }
+      }
+    }
+  }
+  sum_groups<LPR, V>(dq);
+  if (g == 0) st_f32<V>(dQ + v * D + c * V, dq);
+}
+
+// ------------------------------------------------------------------ RGAT backward, dst-major (A6)
+// dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
+// dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path) ; ebuf[i] = (alpha_e, dz_e)
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t N, const int32_t* __restrict__ row_ptr,
+                                                      const int32_t* __restrict__ csr_pair,
+                                                      const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+                                                      const float* __restrict__ spair, const TP* __restrict__ X,
+                                                      const float* __restrict__ y, float slope,
+                                                      const float2* __restrict__ stats,
+                                                      const float* __restrict__ Gr, const float* __restrict__ out,
+                                                      float2* __restrict__ ebuf, float* __restrict__ dX) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= N) return;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int b = row_ptr[v], e = row_ptr[v + 1];
+  float dx[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) dx[k] = 0.f;
+  if (e > b) {
+    float x[V], gv[V], ov[V];
+    cvt16<TP>(ldg16(X + v * D + c * V), x);
+    ld_f32<V>(Gr + v * D + c * V, gv);
+    ld_f32<V>(out + v * D + c * V, ov);
+    float go = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
+    go = gsum<LPR>(go);
+    const float2 st = stats[v];
+    const float inv = 1.f / st.y;
+    for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
+    const int i0 = base + g;
+      uint4 rp[UNR];
+      float sp[UNR], yv[UNR][V];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        int i = i0 + u * EG;
+        rp[u] = make_uint4(0, 0, 0, 0);
+        sp[u] = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
+        if (i < e) {
+          int64_t p = csr_pair[i];
+          int r = csr_rel[i];
+          rp[u] = ldg16(P + p * D + c * V);
+          sp[u] = spair[p];
+          ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        int i = i0 + u * EG;
+        float pv[V];
+        cvt16<TP>(rp[u], pv);
+        float t = 0.f, da = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          t = fmaf(x[k], yv[u][k], t);
+          da = fmaf(gv[k], pv[k], da);
+        }
+        t = gsum<LPR>(t);
+        da = gsum<LPR>(da);
+        float z = sp[u] + t;
+        float l = z > 0.f ? z : slope * z;
+        float alpha = __expf(l - st.x) * inv;
+        float dz = alpha * (da - go) * (z > 0.f ? 1.f : slope);
+        if (i < e) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
+          if (c == 0) ebuf[i] = make_float2(alpha, dz);
+        }
+      }
+    }
+  }
+  sum_groups<LPR, V>(dx);
+  if (g == 0) st_f32<V>(dX + v * D + c * V, dx);
+}
+
+// ------------------------------------------------------------------ pair-major backward (A7)
+// One group of D/4 lanes per compact pair p; each lane owns 4 fp32 columns.
+template <int D>
+struct PGeo {
+  static constexpr int LPR = D / 4;
+  static constexpr int EG = 32 / LPR;
+};
+
+// RGCN: dP_p = sum_{e in p} norm_e G[d_e]
+template <int D>
+__global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
+                                                       const int32_t* __restrict__ pair_deg,
+                                                       const int32_t* __restrict__ csc_dst,
+                                                       const float* __restrict__ csc_norm,
+                                                       const float* __restrict__ Gr, float* __restrict__ dP) {
+  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (p >= U) return;
+  const int b = pair_beg[p], n = pair_deg[p];
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j0 = 0; j0 < n; j0 += UNR) {
+    float4 gr[UNR];
+    float w[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      gr[u] = make_float4(0, 0, 0, 0);
+      w[u] = 0.f;
+      if (j0 + u < n) {
+        int i = b + j0 + u;
+        w[u] = csc_norm[i];
+        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      acc[0] = fmaf(w[u], gr[u].x, acc[0]); acc[1] = fmaf(w[u], gr[u].y, acc[1]);
+      acc[2] = fmaf(w[u], gr[u].z, acc[2]); acc[3] = fmaf(w[u], gr[u].w, acc[3]);
+    }
+  }
+  *reinterpret_cast<float4*>(dP + p * D + c * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
+// RGAT: dP_p = sum alpha_e G[d_e] + (sum dz_e) a_r ; wsum_p = sum dz_e
+template <class TW, int D>
+__global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
+                                                       const int32_t* __restrict__ pair_deg,
+                                                       const int32_t* __restrict__ csc_dst,
+                                                       const int32_t* __restrict__ csc_rel,
+                                                       const int32_t* __restrict__ csc2csr,
+                                                       const float2* __restrict__ ebuf, const float* __restrict__ Gr,
+                                                       const TW* __restrict__ avec, float* __restrict__ dP,
+                                                       float* __restrict__ wsum) {
+  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (p >= U) return;
+  const int b = pair_beg[p], n = pair_deg[p];
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, zs = 0.f;
+  for (int j0 = 0; j0 < n; j0 += UNR) {
+    float4 gr[UNR];
+    float2 ab[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      gr[u] = make_float4(0, 0, 0, 0);
+      ab[u] = make_float2(0.f, 0.f);
+      if (j0 + u < n) {
+        int i = b + j0 + u;
+        ab[u] = ebuf[csc2csr[i]];
+        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      acc[0] = fmaf(ab[u].x, gr[u].x, acc[0]); acc[1] = fmaf(ab[u].x, gr[u].y, acc[1]);
+      acc[2] = fmaf(ab[u].x, gr[u].z, acc[2]); acc[3] = fmaf(ab[u].x, gr[u].w, acc[3]);
+      zs += ab[u].y;
+    }
+  }
+  const int r = csc_rel[b];
+  float a4[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a4[k] = to_f(avec[(int64_t)r * D + c * 4 + k]);
+  *reinterpret_cast<float4*>(dP + p * D + c * 4) =
+      make_float4(fmaf(zs, a4[0], acc[0]), fmaf(zs, a4[1], acc[1]), fmaf(zs, a4[2], acc[2]), fmaf(zs, a4[3], acc[3]));
+  if (c == 0) wsum[p] = zs;
+}
+
+// HGT: dM_p = sum alpha_e G[d_e] ; dK~_p = sum dl_e q_{d_e} ; dKM_p = [dK~_p | dM_p]
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
+                                                      const int32_t* __restrict__ pair_deg,
+                                                      const int32_t* __restrict__ csc_dst,
+                                                      const int32_t* __restrict__ csc2csr,
+                                                      const float2* __restrict__ ebuf, const float* __restrict__ Gr,
+                                                      const TP* __restrict__ Q, float* __restrict__ dKM) {
+  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (p >= U) return;
+  const int b = pair_beg[p], n = pair_deg[p];
+  float am[4] = {0.f, 0.f, 0.f, 0.f}, ak[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j0 = 0; j0 < n; j0 += UNR) {
+    float4 gr[UNR];
+    float qv[UNR][4];
+    float2 ab[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      gr[u] = make_float4(0, 0, 0, 0);
+      ab[u] = make_float2(0.f, 0.f);
+      qv[u][0] = qv[u][1] = qv[u][2] = qv[u][3] = 0.f;
+      if (j0 + u < n) {
+        int i = b + j0 + u;
+        int64_t d = csc_dst[i];
+        ab[u] = ebuf[csc2csr[i]];
+        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + d * D + c * 4));
+        ld4(Q + d * D + c * 4, qv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      am[0] = fmaf(ab[u].x, gr[u].x, am[0]); am[1] = fmaf(ab[u].x, gr[u].y, am[1]);
+      am[2] = fmaf(ab[u].x, gr[u].z, am[2]); am[3] = fmaf(ab[u].x, gr[u].w, am[3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ak[k] = fmaf(ab[u].y, qv[u][k], ak[k]);
+    }
+  }
+  float* o = dKM + p * 2 * D;
+  *reinterpret_cast<float4*>(o + c * 4) = make_float4(ak[0], ak[1], ak[2], ak[3]);
+  *reinterpret_cast<float4*>(o + D + c * 4) = make_float4(am[0], am[1], am[2], am[3]);
+}
+
+// c_{v,r} = sum of dz over the CSR run of (dst v, rel r)   (RGAT destination-side weight terms)
+__global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
+                            const float2* __restrict__ ebuf, float* __restrict__ csum) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= UD) return;
+  float acc = 0.f;
+  for (int i = beg[j], e = beg[j] + cnt[j]; i < e; ++i) acc += ebuf[i].y;
+  csum[j] = acc;
+}
+
+template <class F>
+void by_width(int D, F&& f) {
+  switch (D) {
+    case 16: f(std::integral_constant<int, 16>()); break;
+    case 32: f(std::integral_constant<int, 32>()); break;
+    case 64: f(std::integral_constant<int, 64>()); break;
+    case 128: f(std::integral_constant<int, 128>()); break;
+    default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "d_out must be one of 16, 32, 64, 128");
+  }
+}
+
+inline dim3 warp_grid(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
+
+}  // namespace
+
+void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* norm, const void* P, float* out,
+                       bool accumulate, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("rgcn_fwd_traverse", k_rgcn_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, norm, static_cast<const float*>(P), out, accumulate);
+    else
+      launch("rgcn_fwd_traverse", k_rgcn_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, norm, static_cast<const bf16*>(P), out, accumulate);
+  });
+}
+
+void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
+                      float2* stats, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("hgt_fwd_traverse", k_hgt_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q), out, stats);
+    else
+      launch("hgt_fwd_traverse", k_hgt_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q), out, stats);
+  });
+}
+
+void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
+                       const float* y, float slope, float* out, float2* stats, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("rgat_fwd_traverse", k_rgat_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair, static_cast<const float*>(X), y, slope,
+             out, stats);
+    else
+      launch("rgat_fwd_traverse", k_rgat_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair, static_cast<const bf16*>(X), y, slope,
+             out, stats);
+  });
+}
+
+void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                 const float* G, const float* out, float2* ebuf, float* dQ, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("hgt_bwd_dst", k_hgt_bwd_dst<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q), stats, G, out, ebuf, dQ);
+    else
+      launch("hgt_bwd_dst", k_hgt_bwd_dst<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q), stats, G, out, ebuf, dQ);
+  });
+}
+
+void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
+                  const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
+                  float* dX, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("rgat_bwd_dst", k_rgat_bwd_dst<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair, static_cast<const float*>(X), y, slope,
+             stats, G, out, ebuf, dX);
+    else
+      launch("rgat_bwd_dst", k_rgat_bwd_dst<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
+             g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair, static_cast<const bf16*>(X), y, slope,
+             stats, G, out, ebuf, dX);
+  });
+}
+
+static dim3 pair_grid(int64_t U, int D) {
+  int eg = 32 / (D / 4);
+  return dim3(ceil_div(ceil_div(U, eg) * (int64_t)32, 256));
+}
+
+void rgcn_bwd_pair(const rgnn_graph_s* g, int D, const float* csc_norm, const float* G, float* dP, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    launch("rgcn_bwd_pair", k_rgcn_bwd_pair<DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
+           g->pair_deg, g->csc_dst, csc_norm, G, dP);
+  });
+}
+
+void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
+                   float* dP, float* wsum, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("rgat_bwd_pair", k_rgat_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
+             g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const float*>(a),
+             dP, wsum);
+    else
+      launch("rgat_bwd_pair", k_rgat_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
+             g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const bf16*>(a),
+             dP, wsum);
+  });
+}
+
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
+                  float* dKM, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32)
+      launch("hgt_bwd_pair", k_hgt_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
+             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const float*>(Q), dKM);
+    else
+      launch("hgt_bwd_pair", k_hgt_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
+             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const bf16*>(Q), dKM);
+  });
+}
+
+void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s) {
+  launch("rgat_dpair_sum", k_dpair_sum, dim3(ceil_div(g->UD, 256)), dim3(256), 0, s, g->UD, g->dpair_csr_beg,
+         g->dpair_cnt, ebuf, csum);
+}
+
+}  // namespace rgnn

@@ -1,0 +1,23 @@
+// Host wrappers of the traversal kernels (traverse.cu).
+#pragma once
+#include "graph.cuh"
+
+namespace rgnn {
+void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* norm, const void* P, float* out,
+                       bool accumulate, cudaStream_t s);
+void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
+                      float2* stats, cudaStream_t s);
+void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
+                       const float* y, float slope, float* out, float2* stats, cudaStream_t s);
+void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                 const float* G, const float* out, float2* ebuf, float* dQ, cudaStream_t s);
+void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
+                  const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
+                  float* dX, cudaStream_t s);
+void rgcn_bwd_pair(const rgnn_graph_s* g, int D, const float* csc_norm, const float* G, float* dP, cudaStream_t s);
+void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
+                   float* dP, float* wsum, cudaStream_t s);
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
+                  float* dKM, cudaStream_t s);
+void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
+}  // namespace rgnn

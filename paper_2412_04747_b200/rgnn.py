@@ -1,0 +1,283 @@
+"""Thin ctypes binding over librgnn.so (include/rgnn.h).
+
+Argument marshalling only: every step of the layer runs in the library's CUDA
+kernels.  PyTorch supplies device memory (the allocator callbacks and the
+workspace tensors), the stream, and the dtype bookkeeping.  There is no CPU
+fallback: importing works without a GPU, but every call needs the built
+library and a CUDA device, and fails loudly otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from typing import Dict, Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librgnn.so")
+
+RGCN, RGAT, HGT = 0, 1, 2
+MODELS = {"rgcn": RGCN, "rgat": RGAT, "hgt": HGT}
+F32, BF16 = 0, 1
+DTYPES = {"f32": F32, "bf16": BF16}
+NORMS = {"mean": 0, "sym": 1, "none": 2, "custom": 3}
+ARRAYS = ["etype_ptr", "row_ptr", "csr_src", "csr_rel", "csr_eid", "col_ptr", "csc_dst", "csc_rel", "csc_eid",
+          "pair_rel_ptr", "pair_src", "edge_pair", "csr_pair", "csc_pair"]
+EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_get_info", "rgnn_graph_export",
+            "rgnn_graph_array_size", "rgnn_graph_destroy", "rgnn_layer_workspace", "rgnn_layer_forward",
+            "rgnn_layer_backward", "rgnn_profile_enable", "rgnn_profile_reset", "rgnn_profile_read",
+            "rgnn_launch_count"]
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class GraphInfo(C.Structure):
+    _fields_ = [("num_nodes", C.c_int64), ("num_edges", C.c_int64), ("num_pairs", C.c_int64),
+                ("max_in_degree", C.c_int64), ("max_pair_degree", C.c_int64), ("dst_lo", C.c_int64),
+                ("dst_hi", C.c_int64), ("num_node_types", C.c_int32), ("num_rels", C.c_int32),
+                ("compaction_ratio", C.c_double)]
+
+
+class LayerDescC(C.Structure):
+    _fields_ = [("model", C.c_int32), ("dtype", C.c_int32), ("d_in", C.c_int32), ("d_out", C.c_int32),
+                ("self_loop", C.c_int32), ("norm_kind", C.c_int32), ("leaky_slope", C.c_float),
+                ("gemm_impl", C.c_int32)]
+
+
+WEIGHT_FIELDS = ["W", "W0", "a", "b", "Wk", "Wq", "Wv", "Watt", "Wmsg", "mu", "edge_norm"]
+GRAD_FIELDS = ["dW", "dW0", "da", "db", "dWk", "dWq", "dWv", "dWatt", "dWmsg"]
+
+
+class WeightsC(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in WEIGHT_FIELDS]
+
+
+class GradsC(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in GRAD_FIELDS]
+
+
+class RGNNError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"rgnn status {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load librgnn.so (built by paper_2412_04747_b200.build).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2412_04747_b200.build` "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.rgnn_last_error.restype = C.c_char_p
+        L.rgnn_version.restype = C.c_char_p
+        L.rgnn_launch_count.restype = C.c_int64
+        for name in EXPORTED:
+            if name not in ("rgnn_last_error", "rgnn_version", "rgnn_launch_count"):
+                getattr(L, name).restype = C.c_int
+        L.rgnn_graph_build.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, ALLOC_FN, FREE_FN,
+                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.rgnn_graph_get_info.argtypes = [C.c_void_p, C.POINTER(GraphInfo)]
+        L.rgnn_graph_export.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.rgnn_graph_array_size.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64)]
+        L.rgnn_graph_destroy.argtypes = [C.c_void_p]
+        L.rgnn_layer_workspace.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.POINTER(C.c_size_t),
+                                           C.POINTER(C.c_size_t)]
+        L.rgnn_layer_forward.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.c_void_p, C.POINTER(WeightsC),
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.rgnn_layer_backward.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.c_void_p, C.POINTER(WeightsC),
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GradsC),
+                                          C.c_void_p, C.c_void_p]
+        L.rgnn_profile_enable.argtypes = [C.c_int32]
+        L.rgnn_profile_read.argtypes = [C.c_char_p, C.c_size_t]
+        _lib = L
+    return _lib
+
+
+def _check(st: int) -> None:
+    if st != 0:
+        raise RGNNError(st, lib().rgnn_last_error().decode())
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def version() -> str:
+    return lib().rgnn_version().decode()
+
+
+def launch_count() -> int:
+    return int(lib().rgnn_launch_count())
+
+
+class _TorchAllocator:
+    """Allocator callbacks backed by torch's caching allocator; keeps tensors alive by pointer."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.live: Dict[int, torch.Tensor] = {}
+
+        def _alloc(nbytes, stream, ctx):
+            try:
+                t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+            except RuntimeError:
+                return None
+            self.live[t.data_ptr()] = t
+            return t.data_ptr()
+
+        def _free(ptr, stream, ctx):
+            self.live.pop(int(ptr), None)
+
+        self.alloc_cb = ALLOC_FN(_alloc)
+        self.free_cb = FREE_FN(_free)
+
+
+class Graph:
+    """A built typed graph (rgnn_graph_build).  src/dst/rel: int32 tensors (moved to the device)."""
+
+    def __init__(self, num_nodes: int, node_type_ptr, num_rels: int, src: torch.Tensor, dst: torch.Tensor,
+                 rel: torch.Tensor, dst_range=None, device="cuda"):
+        self.device = torch.device(device)
+        self._alloc = _TorchAllocator(self.device)
+        ntp = (C.c_int64 * len(node_type_ptr))(*[int(x) for x in node_type_ptr])
+        src = torch.as_tensor(src, dtype=torch.int32).to(self.device).contiguous()
+        dst = torch.as_tensor(dst, dtype=torch.int32).to(self.device).contiguous()
+        rel = torch.as_tensor(rel, dtype=torch.int32).to(self.device).contiguous()
+        lo, hi = (0, int(num_nodes)) if dst_range is None else (int(dst_range[0]), int(dst_range[1]))
+        h = C.c_void_p()
+        e = int(src.numel())
+        _check(lib().rgnn_graph_build(int(num_nodes), len(node_type_ptr) - 1, ntp, int(num_rels), e,
+                                      src.data_ptr() if e else None, dst.data_ptr() if e else None,
+                                      rel.data_ptr() if e else None, lo, hi, self._alloc.alloc_cb,
+                                      self._alloc.free_cb, None, _stream(), C.byref(h)))
+        self.handle = h
+        self.node_type_ptr = [int(x) for x in node_type_ptr]
+
+    @classmethod
+    def from_hetero(cls, g, dst_range=None, device="cuda") -> "Graph":
+        """From a synth.HeteroGraph-like object (node_type_ptr, num_rels, src, dst, rel)."""
+        return cls(int(g.node_type_ptr[-1]), list(g.node_type_ptr), int(g.num_rels), torch.from_numpy(g.src),
+                   torch.from_numpy(g.dst), torch.from_numpy(g.rel), dst_range=dst_range, device=device)
+
+    def info(self) -> Dict[str, float]:
+        i = GraphInfo()
+        _check(lib().rgnn_graph_get_info(self.handle, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in GraphInfo._fields_}
+
+    def export(self, name: str) -> torch.Tensor:
+        which = ARRAYS.index(name)
+        n = C.c_int64()
+        _check(lib().rgnn_graph_array_size(self.handle, which, C.byref(n)))
+        out = torch.empty(max(n.value, 1), dtype=torch.int32, device=self.device)
+        _check(lib().rgnn_graph_export(self.handle, which, out.data_ptr(), out.numel() * 4, _stream()))
+        return out[:n.value]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().rgnn_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Layer:
+    """One RGNN layer bound to a graph: rgnn_layer_forward / rgnn_layer_backward.
+
+    weights: dict with the rgnn_weights fields in the layer dtype (mu / edge_norm float32).
+    """
+
+    def __init__(self, graph: Graph, model: str, d_in: int, d_out: int, dtype: str = "f32", self_loop: bool = True,
+                 norm: str = "mean", leaky_slope: float = 0.2, gemm_impl: int = 0):
+        self.graph = graph
+        self.desc = LayerDescC(MODELS[model], DTYPES[dtype], d_in, d_out, int(self_loop), NORMS[norm],
+                               float(leaky_slope), int(gemm_impl))
+        self.model, self.dtype_name = model, dtype
+        self.torch_dtype = torch.float32 if dtype == "f32" else torch.bfloat16
+        sb, xb = C.c_size_t(), C.c_size_t()
+        _check(lib().rgnn_layer_workspace(graph.handle, C.byref(self.desc), C.byref(sb), C.byref(xb)))
+        self.saved = torch.empty(sb.value, dtype=torch.uint8, device=graph.device)
+        self.scratch = torch.empty(xb.value, dtype=torch.uint8, device=graph.device)
+        self.n = graph.info()["num_nodes"]
+        self.d_in, self.d_out = d_in, d_out
+
+    def _weights(self, w: Dict[str, torch.Tensor]) -> WeightsC:
+        wc = WeightsC()
+        for f in WEIGHT_FIELDS:
+            t = w.get(f)
+            if t is not None:
+                want = torch.float32 if f in ("mu", "edge_norm") else self.torch_dtype
+                if t.dtype != want:
+                    raise TypeError(f"weight {f} must be {want}, got {t.dtype}")
+                setattr(wc, f, _ptr(t))
+        return wc
+
+    def forward(self, X: torch.Tensor, w: Dict[str, torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if X.dtype != self.torch_dtype:
+            raise TypeError(f"X must be {self.torch_dtype}")
+        if out is None:
+            out = torch.empty(self.n, self.d_out, dtype=torch.float32, device=X.device)
+        self._wc = self._weights(w)
+        _check(lib().rgnn_layer_forward(self.graph.handle, C.byref(self.desc), _ptr(X), C.byref(self._wc), _ptr(out),
+                                        _ptr(self.saved), _ptr(self.scratch), _stream()))
+        return out
+
+    def backward(self, X: torch.Tensor, w: Dict[str, torch.Tensor], out: torch.Tensor, dout: torch.Tensor,
+                 need_dX: bool = True, grads: Optional[Dict[str, torch.Tensor]] = None,
+                 need: Optional[list] = None) -> Dict[str, torch.Tensor]:
+        """Gradients of sum(out * dout).  `need` lists weight-gradient names to compute
+        (default: all for the model); missing ones are pruned."""
+        wc = self._weights(w)
+        shapes = {k: tuple(v.shape) for k, v in w.items() if v is not None and k not in ("mu", "edge_norm")}
+        default = {"rgcn": ["dW", "dW0"] if self.desc.self_loop else ["dW"], "rgat": ["dW", "da", "db"],
+                   "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[self.model]
+        need = default if need is None else need
+        grads = dict(grads or {})
+        gc = GradsC()
+        for name in need:
+            if name not in grads:
+                grads[name] = torch.empty(shapes[name[1:]], dtype=torch.float32, device=X.device)
+            setattr(gc, name, _ptr(grads[name]))
+        if need_dX and "dX" not in grads:
+            grads["dX"] = torch.empty(self.n, self.d_in, dtype=torch.float32, device=X.device)
+        _check(lib().rgnn_layer_backward(self.graph.handle, C.byref(self.desc), _ptr(X), C.byref(wc), _ptr(out),
+                                         _ptr(self.saved), _ptr(dout), _ptr(grads.get("dX")) if need_dX else None,
+                                         C.byref(gc), _ptr(self.scratch), _stream()))
+        return grads
+
+
+def profile_enable(on: bool = True) -> None:
+    _check(lib().rgnn_profile_enable(int(on)))
+
+
+def profile_reset() -> None:
+    _check(lib().rgnn_profile_reset())
+
+
+def profile_read() -> Dict[str, Dict[str, float]]:
+    buf = C.create_string_buffer(1 << 16)
+    _check(lib().rgnn_profile_read(buf, len(buf)))
+    return json.loads(buf.value.decode())
