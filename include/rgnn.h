@@ -145,7 +145,7 @@ typedef enum { RGNN_NORM_MEAN = 0, RGNN_NORM_SYM = 1, RGNN_NORM_NONE = 2, RGNN_N
 typedef struct {
   int32_t model;       /* rgnn_model */
   int32_t dtype;       /* rgnn_dtype of X, the weights and the projected tables */
-  int32_t d_in;        /* input feature width, multiple of 16, <= 256 */
+  int32_t d_in;        /* input feature width, one of 16, 32, 64, 128, 256 */
   int32_t d_out;       /* output width, one of 16, 32, 64, 128 */
   int32_t self_loop;   /* RGCN: add X W_0 (virtual self-loop); ignored otherwise */
   int32_t norm_kind;   /* RGCN: rgnn_norm_kind */

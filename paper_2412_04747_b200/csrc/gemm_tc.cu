@@ -1,7 +1,279 @@
-// tcgen05 typed segment GEMM (placeholder until the sm_100a kernel lands).
+// A1 on the 5th-generation tensor cores: typed segment GEMM  Y[row] = X[gather(row)] x W_w
+// for the bf16 path (GEMM template Y[S] = X[G] x W[T], §3.3.3; compact rows P:764-776).
+//
+// One CTA per 128-row tile of one segment (tiles never cross a weight segment):
+//   * 128 threads gather the tile's A rows (X[pair_src[row]], bf16, K-major) and the
+//     segment's B = W_w^T (pre-transposed to K-major by k_transpose_kmajor) into shared
+//     memory with cp.async, already in the 128-byte-swizzled canonical UMMA layout
+//     (8-row x 128 B atoms, 16-byte chunk c of row r stored at chunk c ^ (r % 8));
+//   * one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=n_out,
+//     K=16 per instruction) accumulating fp32 in TMEM, then tcgen05.commit -> mbarrier;
+//   * the 4 warps read their 32 TMEM lanes (= tile rows) with tcgen05.ld.32x32b and
+//     run the fused epilogue: optional per-row dot with a per-weight vector (RGAT
+//     s_p = P_p . a_r, "per-row scalar"), conversion, and the row store.
+// Several CTAs per SM (TMEM 512 columns / n_out columns each) overlap one tile's
+// gather with another's MMA and epilogue.  At d = 64 the GEMM is HBM-bound
+// (32 flop/B vs a ~213 flop/B ridge), so the design goal is bytes in flight.
+#include <cuda.h>
+
 #include "ops.cuh"
 
 namespace rgnn {
-bool gemm_tc_supported(const GemmArgs&) { return false; }
-void gemm_tc(const GemmArgs&, cudaStream_t) { RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "tcgen05 GEMM not built"); }
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+
+// K-major, 128B-swizzle UMMA shared-memory descriptor (sm_100 format: version 1,
+// LBO = 1 (unused for swizzled K-major), SBO = 1024 B between 8-row atoms).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t umma_idesc_bf16(int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                       // c_format = F32
+  d |= 1u << 7;                       // a_format = BF16
+  d |= 1u << 10;                      // b_format = BF16
+  d |= (uint32_t)(n >> 3) << 17;      // N >> 3
+  d |= (uint32_t)(128 >> 4) << 24;    // M >> 4
+  return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void store_row32(float* y, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(y + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+}
+__device__ __forceinline__ void store_row32(bf16* y, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 8) store16(y + i, v + i);
+}
+
+// K-major bf16 copy of the weights: Wt[w][n][k] = W[w][k][n] (or of W^T when transB: Wt[w][n][k] = W[w][n][k]).
+template <class TW>
+__global__ void k_transpose_kmajor(int64_t nw, int K, int N, const TW* __restrict__ W, bool transB,
+                                   bf16* __restrict__ Wt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t per = (int64_t)K * N;
+  if (i >= nw * per) return;
+  int64_t w = i / per, r = i % per;
+  int n = r / K, k = r % K;
+  float v = transB ? to_f(W[w * per + (int64_t)n * K + k]) : to_f(W[w * per + (int64_t)k * N + n]);
+  Wt[i] = __float2bfloat16_rn(v);
+}
+
+// N = n_out (multiple of 16, <= 256); KB = K / 64 (1..4).
+template <class TY, int N, int KB>
+__global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles, const bf16* __restrict__ A,
+                                                 const int32_t* __restrict__ gather, const bf16* __restrict__ Bt,
+                                                 TY* __restrict__ Y, const float* __restrict__ dotvec,
+                                                 float* __restrict__ dotout) {
+  constexpr int K = KB * 64;
+  constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  constexpr uint32_t A_BYTES = 128 * 128;  // per K block
+  constexpr uint32_t B_BYTES = N * 128;    // per K block
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + KB * A_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + KB * B_BYTES);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Tile t = tiles[blockIdx.x];
+  const int nrows = t.row1 - t.row0;
+
+  if (warp == 0) tmem_alloc<NCOLS>(tslot);
+  if (tid == 32) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+
+  // ---- gather A rows and B rows into swizzled smem (8 lanes per 128-byte row: coalesced)
+  const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      int idx = it * 128 + tid;
+      int r = idx >> 3, c = idx & 7;
+      int rr = r < nrows ? r : nrows - 1;
+      int64_t src_row = gather ? (int64_t)gather[t.row0 + rr] : (int64_t)(t.row0 + rr);
+      cp_async16(sA_u + kb * A_BYTES + r * 128 + ((c ^ (r & 7)) << 4), A + src_row * K + kb * 64 + c * 8);
+    }
+    const bf16* Bw = Bt + (size_t)t.w * N * K;
+    for (int idx = tid; idx < N * 8; idx += 128) {
+      int r = idx >> 3, c = idx & 7;
+      cp_async16(sB_u + kb * B_BYTES + r * 128 + ((c ^ (r & 7)) << 4), Bw + (int64_t)r * K + kb * 64 + c * 8);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  // generic-proxy smem writes -> visible to the tensor core (async proxy)
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (tid == 0) {
+    const uint32_t idesc = umma_idesc_bf16(N);
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint64_t da = umma_desc_sw128(sA_u + kb * A_BYTES + k * 32);
+        uint64_t db = umma_desc_sw128(sB_u + kb * B_BYTES + k * 32);
+        umma_bf16(tmem, da, db, idesc, (kb | k) ? 1u : 0u);
+      }
+    umma_commit(bar);
+  }
+  mbar_wait(bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+
+  // ---- epilogue: thread = tile row (TMEM lane 32*warp + lane)
+  const int r = warp * 32 + lane;
+  const bool valid = r < nrows;
+  const int64_t row = t.row0 + r;
+  float dot = 0.f;
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+    if (dotvec) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
+    }
+    if (valid) store_row32(Y + row * N + c0, v);
+  }
+  if (dotvec && valid) dotout[row] = dot;
+
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<NCOLS>(tmem);
+}
+
+template <class TY, int N, int KB>
+void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  size_t smem = 1024 + KB * (128 * 128 + N * 128) + 64;
+  // keep concurrent CTAs per SM within the 512 TMEM columns (alloc never waits)
+  size_t floor_smem = (size_t)(232448 / (512 / NCOLS + 1)) + 1;
+  smem = std::max(smem, floor_smem);
+  auto k = k_gemm_tc<TY, N, KB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  launch("gemm_tc", k, dim3(a.ntiles), dim3(128), smem, s, a.tiles, static_cast<const bf16*>(a.A), a.gather, Bt,
+         static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+}
+
+template <class TY, int KB>
+void by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  switch (a.N) {
+    case 16: launch_tc<TY, 16, KB>(a, Bt, s); break;
+    case 32: launch_tc<TY, 32, KB>(a, Bt, s); break;
+    case 64: launch_tc<TY, 64, KB>(a, Bt, s); break;
+    case 128: launch_tc<TY, 128, KB>(a, Bt, s); break;
+    case 256: launch_tc<TY, 256, KB>(a, Bt, s); break;
+    default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "tcgen05 gemm: N");
+  }
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& a) {
+  if (a.a_dtype != BF16 || a.b_dtype != BF16) return false;
+  if (a.K % 64 != 0 || a.K > 128) return false;
+  if (!(a.N == 16 || a.N == 32 || a.N == 64 || a.N == 128 || a.N == 256)) return false;
+  if (a.K / 64 == 2 && a.N == 256) return false;  // smem budget
+  return a.bt_scratch != nullptr;
+}
+
+void gemm_tc(const GemmArgs& a, cudaStream_t s) {
+  // K-major bf16 image of the weights for the B operand
+  int64_t total = (int64_t)a.num_w * a.K * a.N;
+  bf16* Bt = static_cast<bf16*>(a.bt_scratch);
+  launch("gemm_tc_prep_b", k_transpose_kmajor<bf16>, dim3(ceil_div(total, 256)), dim3(256), 0, s, (int64_t)a.num_w,
+         a.K, a.N, static_cast<const bf16*>(a.B), a.transB, Bt);
+  const int KB = a.K / 64;
+  if (a.y_dtype == BF16) {
+    if (KB == 1) by_n<bf16, 1>(a, Bt, s); else by_n<bf16, 2>(a, Bt, s);
+  } else {
+    if (KB == 1) by_n<float, 1>(a, Bt, s); else by_n<float, 2>(a, Bt, s);
+  }
+}
+
 }  // namespace rgnn

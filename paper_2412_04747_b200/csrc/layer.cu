@@ -65,8 +65,8 @@ void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
   RGNN_CHECK(d->dtype == F32 || d->dtype == BF16, RGNN_ERR_INVALID_ARG, "unknown dtype");
   RGNN_CHECK(d->d_out == 16 || d->d_out == 32 || d->d_out == 64 || d->d_out == 128, RGNN_ERR_UNSUPPORTED,
              "d_out must be one of 16, 32, 64, 128");
-  RGNN_CHECK(d->d_in > 0 && d->d_in % 16 == 0 && d->d_in <= 256, RGNN_ERR_UNSUPPORTED,
-             "d_in must be a multiple of 16 in [16, 256]");
+  RGNN_CHECK(d->d_in == 16 || d->d_in == 32 || d->d_in == 64 || d->d_in == 128 || d->d_in == 256,
+             RGNN_ERR_UNSUPPORTED, "d_in must be one of 16, 32, 64, 128, 256");
   if (d->model == RGNN_RGAT)
     RGNN_CHECK(d->d_in == d->d_out, RGNN_ERR_UNSUPPORTED, "RGAT needs d_in == d_out");
   RGNN_CHECK(d->norm_kind >= 0 && d->norm_kind <= 3, RGNN_ERR_INVALID_ARG, "unknown norm_kind");
@@ -110,6 +110,7 @@ void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
 
 struct FwdScratch {
   void* P = nullptr;  // RGCN P
+  void* bt = nullptr;  // tcgen05 path: K-major bf16 image of the GEMM weights
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
 };
@@ -128,6 +129,12 @@ struct BwdScratch {
 };
 
 void layout_fwd_scratch(const Ctx& c, Arena& ar, FwdScratch& o) {
+  if (c.dt == BF16) {
+    const int64_t R = c.g->R, T = c.g->T;
+    int64_t n = c.d->model == RGNN_HGT ? std::max(R * T * c.Din * 2 * c.D, T * c.Din * c.D)
+                                       : std::max(R, (int64_t)1) * c.Din * c.D;
+    o.bt = ar.take<char>(n * 2);
+  }
   if (c.d->model == RGNN_RGCN) {
     o.P = ar.take<char>(c.g->U * c.D * c.esz);
     if (c.d->norm_kind == RGNN_NORM_CUSTOM) {
@@ -219,10 +226,12 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     GemmArgs a;
     a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
     a.B = w->W; a.b_dtype = c.dt; a.Y = sc.P; a.y_dtype = c.dt; a.N = c.D;
+    a.num_w = g->R; a.bt_scratch = sc.bt;
     gemm(c, seg_pair_rel(g), a);
     if (c.d->self_loop) {
       GemmArgs b;
       b.A = X; b.a_dtype = c.dt; b.K = c.Din; b.B = w->W0; b.b_dtype = c.dt; b.Y = out; b.y_dtype = F32; b.N = c.D;
+      b.num_w = 1; b.bt_scratch = sc.bt;
       gemm(c, seg_all_nodes(g), b);
     }
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
@@ -236,6 +245,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
     a.B = w->W; a.b_dtype = c.dt; a.Y = sv.P; a.y_dtype = c.dt; a.N = c.D;
     a.dotvec = sv.a32; a.dotout = sv.spair;
+    a.num_w = g->R; a.bt_scratch = sc.bt;
     gemm(c, seg_pair_rel(g), a);
     rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, out, sv.stats, c.s);
   } else {
@@ -246,9 +256,11 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
     a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
     a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
+    a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
     gemm(c, seg_pair_rt(g), a);
     GemmArgs q;
     q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
+    q.num_w = g->T; q.bt_scratch = sc.bt;
     gemm(c, seg_node_type(g), q);
     hgt_fwd_traverse(g, c.dt, c.D, sv.P, sv.Q, out, sv.stats, c.s);
   }

@@ -24,6 +24,8 @@ struct GemmArgs {
   int N = 0;          // Y width (ldy = N)
   const float* dotvec = nullptr;  // optional epilogue: dotout[row] = sum_n Y_fp32[row][n] * dotvec[w][n]
   float* dotout = nullptr;
+  int num_w = 0;                  // number of weight matrices in B (tcgen05 path: K-major image size)
+  void* bt_scratch = nullptr;     // tcgen05 path: device buffer for num_w*K*N bf16 (K-major B image)
 };
 void gemm_simt(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& a);

@@ -65,7 +65,9 @@ def test_other_widths(model, d):
 
 @pytest.mark.parametrize("model", ["rgcn", "hgt"])
 def test_rectangular(model):
-    run_case(model, config_graph("tiny", seed=4, scale=0.5), 48, 32, "f32")
+    run_case(model, config_graph("tiny", seed=4, scale=0.5), 64, 32, "f32")
+    run_case(model, config_graph("tiny", seed=4, scale=0.5), 32, 128, "f32")
+    run_case(model, config_graph("tiny", seed=4, scale=0.5), 128, 64, "bf16")
 
 
 @pytest.mark.parametrize("norm", ["mean", "sym", "none"])
