@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Benchmark: one RGNN layer, forward + backward, edges/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mag_hgt] [--impl ours|reference]
+
+Default workload (BASELINE.json configs[3], the configuration the metric is quoted
+on): HGT layer, hidden 64, on the ogbn-mag-shaped synthetic heterograph (1.94M
+nodes, 4 node types, 21.1M edges, 4 relations), bf16 tensor-core path, full
+forward + backward (all weight gradients and dX) per step.
+
+A step = rgnn_layer_forward + rgnn_layer_backward over the whole graph (every row
+of SURVEY.md §8(a) A1-A8).  For N > 1 (torchrun) the graph is partitioned by
+destination range; each step also all-gathers X (NCCL), reduce-scatters dX and
+all-reduces dW; time is the max over ranks.
+
+The JSON line carries: value (device-timed, inputs resident in HBM), e2e (public
+API with pinned host buffers, H2D of X and dout and D2H of dX and dW inside the
+timed region), roofline of the dominant kernel (algorithmic bytes per launch /
+CUDA-event launch time, against MEASURED_PEAKS.json), per-kernel times, clocks
+sampled with nvidia-smi during the timed region, and the fp64 oracle timed on
+the host cores on a bounded sample (cpu_baseline).
+`--impl reference` times the oracle (the reference arm of this tier) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import config_graph, layer_inputs, upstream_grad  # noqa: E402
+from synth.inputs import round_bf16  # noqa: E402
+
+METRIC = "RGNN layer fwd+bwd edges/sec (RGAT/HGT, mag-shaped); HBM GB/s vs peak"
+UNIT = "edges/s"
+
+BENCH_CONFIGS = {
+    # name: graph config, layer, d_in, d_out, dtype, BASELINE.json configs index
+    "mag_hgt": dict(graph="mag", model="hgt", d=64, dtype="bf16", baseline=3),
+    "mag_hgt_f32": dict(graph="mag", model="hgt", d=64, dtype="f32", baseline=3),
+    "mag_rgat": dict(graph="mag", model="rgat", d=64, dtype="bf16", baseline=3),
+    "am_rgat": dict(graph="am", model="rgat", d=64, dtype="bf16", baseline=2),
+    "aifb_rgat": dict(graph="aifb", model="rgat", d=64, dtype="bf16", baseline=1),
+    "bgs_rgat": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1),
+    "wikikg2_rgcn": dict(graph="wikikg2", model="rgcn", d=64, dtype="bf16", baseline=4),
+    "tiny_rgcn": dict(graph="tiny", model="rgcn", d=16, dtype="f32", baseline=0),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------- algorithmic bytes per launch
+def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
+    """Bytes each kernel must move, per launch.
+    Each gathered row counts once per use even if L2 serves it; int32 indices; grads fp32."""
+    b = 2 if dtype == "bf16" else 4
+    out = {}
+    if model == "hgt":
+        out["gemm_pairs_fwd"] = U * (4 + d_in * b + 2 * d * b)
+        out["gemm_nodes_fwd"] = N * (d_in * b + d * b)
+        out["hgt_fwd_traverse"] = E * (4 + 2 * d * b) + N * (8 + d * b + 4 * d + 8)
+        out["hgt_bwd_dst"] = E * (4 + 2 * d * b + 8) + N * (8 + d * b + 4 * d + 4 * d + 8 + 4 * d)
+        out["hgt_bwd_pair"] = E * (4 + 4 + 8 + 4 * d + d * b) + U * (8 + 8 * d)
+        out["gemm_nodes_dx"] = N * (4 * d + 4 * d_in)
+        out["gemm_pairs_dx"] = U * (8 * d + 4 * d_in)
+        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
+        out["wgrad_pairs"] = U * (4 + d_in * b + 8 * d)
+        out["wgrad_nodes"] = N * (d_in * b + 4 * d)
+    elif model == "rgat":
+        out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b + 4)
+        out["rgat_fwd_traverse"] = E * (4 + 4 + d * b + 4 + 4 * d) + N * (8 + d_in * b + 4 * d + 8)
+        out["rgat_bwd_dst"] = E * (8 + d * b + 4 + 4 * d + 8) + N * (8 + d_in * b + 12 * d + 8)
+        out["rgat_bwd_pair"] = E * (4 + 4 + 8 + 4 * d) + U * (8 + 4 * d + 4)
+        out["gemm_pairs_dx"] = U * (4 * d + 4 * d_in)
+        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
+        out["wgrad_pairs"] = U * (4 + d_in * b + 4 * d)
+    else:
+        out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b)
+        out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)
+        out["rgcn_fwd_traverse"] = E * (4 + 4 + d * b) + N * (8 + 8 * d)
+        out["rgcn_bwd_pair"] = E * (4 + 4 + 4 * d) + U * (8 + 4 * d)
+        out["gemm_pairs_dx"] = U * (4 * d + 4 * d_in)
+        out["gemm_selfloop_dx"] = N * (4 * d + 4 * d_in)
+        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
+        out["wgrad_pairs"] = U * (4 + d_in * b + 4 * d)
+        out["wgrad_selfloop"] = N * (d_in * b + 4 * d)
+    return out
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        def parse(rows):
+            mhz, mx, reasons = [], [], set()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for _, p in rows:
+                try:
+                    mhz.append(float(p[1]))
+                    mx.append(float(p[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, p[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            return mhz, mx, reasons
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        window = "timed region"
+        if not inside:  # timed region shorter than the sampling period: nearest samples
+            inside = sorted(self.samples, key=lambda s: abs(s[0] - 0.5 * (t0 + t1)))[:3]
+            window = "nearest samples (timed region shorter than 50 ms sampling)"
+        mhz, mx, reasons = parse(inside)
+        if not mhz:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": "unavailable"}
+        return {"sm_mhz": float(np.median(mhz)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(mhz), "window": window}
+
+
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+# ----------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_sample(g, model, inp, Gh, target_s=15.0, seed=0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: the in-edge
+    subgraph of random destinations (exact per-destination computation), relabelled."""
+    from oracle import layers as L
+    from oracle import sample as S
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    n_dst = max(1, int(2000 * 10.0 / max(1.0, g.num_edges / g.num_nodes)))
+    elapsed, edges, last = 0.0, 0, None
+    while True:
+        dsts = rng.choice(g.num_nodes, size=min(n_dst, g.num_nodes), replace=False)
+        _, eids = S.in_edge_subgraph(g, dsts)
+        sub, nodes = S.compact_subgraph(g, eids)
+        loc = {k: (v[nodes] if k == "X" else v) for k, v in inp.items()}
+        kw = {"norm": L.rgcn_edge_norm(g, "mean")[eids]} if model == "rgcn" else {}
+        t = time.perf_counter()
+        L.forward(model, sub, loc, **kw)
+        L.backward(model, sub, loc, Gh[nodes], **kw)
+        dt = time.perf_counter() - t
+        elapsed += dt
+        edges += sub.num_edges
+        last = (len(dsts), sub.num_edges)
+        if elapsed >= 0.5 * target_s or n_dst >= g.num_nodes:
+            break
+        n_dst = int(min(g.num_nodes, n_dst * max(2.0, 0.6 * target_s / max(dt, 1e-3))))
+    return {"value": edges / elapsed, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+            "sample": f"fp64 numpy oracle, vanilla per-edge {model.upper()} fwd+bwd on in-edge subgraphs of random "
+                      f"destinations: {edges} edges in {elapsed:.1f} s (last sample {last[0]} dst / {last[1]} edges)",
+            "seconds": elapsed}
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="mag_hgt", choices=sorted(BENCH_CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gemm-impl", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = BENCH_CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2412_04747_b200 import Graph, Layer, rgnn
+    from paper_2412_04747_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    g = config_graph(cfg["graph"], seed=1)
+    model, d, dtype = cfg["model"], cfg["d"], cfg["dtype"]
+    ranges = D.partition_ranges(g.dst, g.num_nodes, world)
+    lo, hi = ranges[rank]
+    G = Graph.from_hetero(g, dst_range=(lo, hi) if world > 1 else None, device=dev)
+    info = G.info()
+    inp = layer_inputs(model, g, d, d)
+    if dtype == "bf16":
+        inp = {k: (round_bf16(v) if k not in ("mu",) else v) for k, v in inp.items()}
+    Gh = upstream_grad(g.num_nodes, d)
+    td = torch.float32 if dtype == "f32" else torch.bfloat16
+    w = {k: torch.tensor(np.asarray(v, np.float32), device=dev).to(torch.float32 if k == "mu" else td)
+         for k, v in inp.items() if k != "X"}
+    X_full = torch.tensor(np.asarray(inp["X"], np.float32), device=dev).to(td)
+    X_own = X_full[lo:hi].contiguous()
+    dout = torch.tensor(Gh, dtype=torch.float32, device=dev)
+    if world > 1:
+        dout = D.masked_rows(dout, lo, hi)
+    layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl)
+    wkeys = {"rgcn": ["dW", "dW0"], "rgat": ["dW", "da", "db"], "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[model]
+    grads = {k: torch.empty(w[k[1:]].shape, dtype=torch.float32, device=dev) for k in wkeys}
+    grads["dX"] = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
+    out = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
+
+    def step(X_local):
+        Xf = D.all_gather_rows(X_local, ranges, rank) if world > 1 else X_local
+        layer.forward(Xf, w, out=out)
+        gr = layer.backward(Xf, w, out, dout, grads=grads, need=wkeys)
+        if world > 1:
+            dx_own = D.reduce_scatter_rows(gr["dX"], ranges, rank)
+            D.all_reduce_grads(gr, wkeys)
+            return dx_own
+        return gr["dX"]
+
+    for _ in range(args.warmup):
+        step(X_own)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.15)
+
+    def timed(K):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        rgnn.profile_reset()
+        rgnn.profile_enable(True)
+        n0 = rgnn.launch_count()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.time()
+        e0.record(s)
+        for _ in range(K):
+            step(X_own)
+        e1.record(s)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if world > 1:
+            dist.barrier()
+        launches = rgnn.launch_count() - n0
+        prof = rgnn.profile_read()
+        rgnn.profile_enable(False)
+        ms = e0.elapsed_time(e1)
+        return ms, launches, prof, t0, t1
+
+    ms, launches, prof, t0, t1 = timed(args.steps)
+    time.sleep(0.12)
+    clocks = sampler.summary(t0, t1)
+    remeasured = False
+    if set(clocks["reasons"]) & BAD_REASONS:
+        remeasured = True
+        ms, launches, prof, t0, t1 = timed(args.steps)
+        time.sleep(0.12)
+        clocks = sampler.summary(t0, t1)
+    sampler.stop()
+    if world > 1:
+        tms = torch.tensor([ms], device=dev)
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        ms = float(tms.item())
+    ms_per_step = ms / args.steps
+    value = g.num_edges * args.steps / (ms / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = X_own.cpu().pin_memory()
+        douth = dout.cpu().pin_memory()
+        dxh = torch.empty((hi - lo, d) if world > 1 else (g.num_nodes, d), dtype=torch.float32).pin_memory()
+        dwh = {k: torch.empty(grads[k].shape, dtype=torch.float32).pin_memory() for k in wkeys}
+        Xd = torch.empty_like(X_own)
+        doutd = dout  # refreshed from host each step
+        h2d = Xh.numel() * Xh.element_size() + douth.numel() * douth.element_size()
+        d2h = dxh.numel() * 4 + sum(v.numel() * 4 for v in dwh.values())
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            doutd.copy_(douth, non_blocking=True)
+            dx = step(Xd)
+            dxh.copy_(dx, non_blocking=True)
+            for k in wkeys:
+                dwh[k].copy_(grads[k], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": g.num_edges * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
+               "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI) with pinned host X, dout in and dX, dW out"}
+
+    # ---- roofline of the dominant kernel
+    peaks = load_peaks()
+    gi = G.info()
+    U, E = gi["num_pairs"], gi["num_edges"]
+    alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
+    kernels = {k: {"launches": v["launches"], "ms_per_launch": v["ms"] / max(v["launches"], 1),
+                   "share": v["ms"] / max(sum(x["ms"] for x in prof.values()), 1e-9)} for k, v in prof.items()}
+    dom = max((k for k in prof if k in alg), key=lambda k: prof[k]["ms"], default=None)
+    roofline = None
+    if dom is not None:
+        per_launch_bytes = alg[dom]
+        ms_l = prof[dom]["ms"] / prof[dom]["launches"]
+        achieved = per_launch_bytes / (ms_l / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
+                    "frac_of_8TBps": achieved / 8000.0, "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                    "ms_per_launch": ms_l}
+        for k in kernels:
+            if k in alg:
+                pb = alg[k]
+                kernels[k]["achieved_gbs"] = pb / (kernels[k]["ms_per_launch"] / 1e3) / 1e9
+        step_bytes = sum(alg.values())
+        roofline["step_algorithmic_gb"] = step_bytes / 1e9
+        roofline["step_achieved_gbs"] = step_bytes / (ms_per_step / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(g, model, inp, Gh, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"{cfg['graph']}-shaped {model.upper()} layer fwd+bwd, hidden {d} "
+                                   f"(BASELINE.json configs[{cfg['baseline']}])",
+                       "graph": cfg["graph"], "layer": model, "d_in": d, "d_out": d,
+                       "nodes": g.num_nodes, "edges": int(g.num_edges), "pairs": int(info["num_pairs"]) if world == 1 else None,
+                       "relations": g.num_rels, "node_types": g.num_node_types,
+                       "compaction_ratio": info["compaction_ratio"], "max_in_degree": info["max_in_degree"],
+                       "parallelism": f"dst-partition x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (X %.2f GB, pair table %.2f GB, index arrays %.2f GB)" % (
+                           g.num_nodes * d * (2 if dtype == 'bf16' else 4) / 1e9,
+                           info["num_pairs"] * 2 * d * (2 if dtype == 'bf16' else 4) / 1e9,
+                           g.num_edges * 4 * 9 / 1e9),
+                       "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl]},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, world, rank):
+    """Reference arm of this tier: the fp64 oracle as it stands on the host cores; each step is
+    a bounded sample of the workload (in-edge subgraph of random destinations)."""
+    if rank != 0:
+        return
+    g = config_graph(cfg["graph"], seed=1)
+    model, d = cfg["model"], cfg["d"]
+    inp = layer_inputs(model, g, d, d)
+    if cfg["dtype"] == "bf16":
+        inp = {k: (round_bf16(v) if k not in ("mu",) else v) for k, v in inp.items()}
+    Gh = upstream_grad(g.num_nodes, d)
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup):
+        cpu_oracle_sample(g, model, inp, Gh, target_s=per_step / 4, seed=100 + i)
+    vals, secs, edges = [], 0.0, 0
+    last = None
+    for i in range(args.steps):
+        r = cpu_oracle_sample(g, model, inp, Gh, target_s=per_step, seed=i)
+        vals.append(r["value"])
+        secs += r["seconds"]
+        edges += r["value"] * r["seconds"]
+        last = r
+    value = edges / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg['graph']}-shaped {model.upper()} layer fwd+bwd, hidden {d} "
+                                   f"(BASELINE.json configs[{cfg['baseline']}]) — bounded sample per step",
+                       "graph": cfg["graph"], "layer": model, "d_in": d, "d_out": d},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

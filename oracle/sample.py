@@ -43,3 +43,15 @@ def masked_grad(G: np.ndarray, dst_nodes: np.ndarray) -> np.ndarray:
     idx = np.asarray(dst_nodes, np.int64)
     Gm[idx] = G[idx]
     return Gm
+
+
+def compact_subgraph(g: HeteroGraph, eids: np.ndarray) -> Tuple[HeteroGraph, np.ndarray]:
+    """The edges `eids` of g on a relabelled node set: the nodes they touch, in ascending
+    original id (node types stay contiguous).  Returns (subgraph, original ids of its nodes)."""
+    eids = np.asarray(eids, np.int64)
+    nodes = np.unique(np.concatenate([g.src[eids], g.dst[eids]]).astype(np.int64))
+    ptr = np.searchsorted(nodes, g.node_type_ptr).astype(np.int64)
+    remap = lambda a: np.searchsorted(nodes, a.astype(np.int64)).astype(np.int32)
+    sub = HeteroGraph(ptr, g.num_rels, remap(g.src[eids]), remap(g.dst[eids]), g.rel[eids].copy(),
+                      name=f"{g.name}[{len(eids)} edges]", rel_types=g.rel_types)
+    return sub, nodes

@@ -90,7 +90,7 @@ void gemm_dispatch(const GemmArgs& a, cudaStream_t s) {
   dim3 g(a.ntiles), b(256);
 #define RGNN_GEMM_CASE(NN)                                                                                  \
   case NN:                                                                                                  \
-    launch("gemm_simt", k_gemm_simt<TA, TB, TY, NN>, g, b, 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, \
+    launch(a.name, k_gemm_simt<TA, TB, TY, NN>, g, b, 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, \
            a.dotvec, a.dotout);                                                                             \
     break;
   switch (a.N) {
@@ -331,10 +331,10 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   if (p.count == 0) return;
   dim3 g(p.count, ceil_div(a.K1, 64), ceil_div(a.K2, 64));
   if (a.a_dtype == F32)
-    launch("wgrad", k_wgrad<float>, g, dim3(256), 0, s, p.tiles, static_cast<const float*>(a.A), a.K1, a.gather, a.Bm,
+    launch(a.name, k_wgrad<float>, g, dim3(256), 0, s, p.tiles, static_cast<const float*>(a.A), a.K1, a.gather, a.Bm,
            a.K2, a.partial);
   else
-    launch("wgrad", k_wgrad<bf16>, g, dim3(256), 0, s, p.tiles, static_cast<const bf16*>(a.A), a.K1, a.gather, a.Bm,
+    launch(a.name, k_wgrad<bf16>, g, dim3(256), 0, s, p.tiles, static_cast<const bf16*>(a.A), a.K1, a.gather, a.Bm,
            a.K2, a.partial);
   int64_t width = (int64_t)a.K1 * a.K2;
   launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,

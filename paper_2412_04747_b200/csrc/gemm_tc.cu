@@ -236,7 +236,7 @@ void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
     RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  launch("gemm_tc", k, dim3(a.ntiles), dim3(128), smem, s, a.tiles, static_cast<const bf16*>(a.A), a.gather, Bt,
+  launch(a.name, k, dim3(a.ntiles), dim3(128), smem, s, a.tiles, static_cast<const bf16*>(a.A), a.gather, Bt,
          static_cast<TY*>(a.Y), a.dotvec, a.dotout);
 }
 

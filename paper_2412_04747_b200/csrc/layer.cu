@@ -201,8 +201,9 @@ void gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
 }
 
 void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, const int32_t* gather, const float* Bm,
-              int K2, float* out, int num_w, float* partial) {
+              int K2, float* out, int num_w, float* partial, const char* name) {
   WgradArgs w;
+  w.name = name;
   w.plan = &plan(c.g, sg, WGRAD_ROWS, c.s);
   w.A = A;
   w.a_dtype = a_dt;
@@ -227,11 +228,13 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
     a.B = w->W; a.b_dtype = c.dt; a.Y = sc.P; a.y_dtype = c.dt; a.N = c.D;
     a.num_w = g->R; a.bt_scratch = sc.bt;
+    a.name = "gemm_pairs_fwd";
     gemm(c, seg_pair_rel(g), a);
     if (c.d->self_loop) {
       GemmArgs b;
       b.A = X; b.a_dtype = c.dt; b.K = c.Din; b.B = w->W0; b.b_dtype = c.dt; b.Y = out; b.y_dtype = F32; b.N = c.D;
       b.num_w = 1; b.bt_scratch = sc.bt;
+      b.name = "gemm_selfloop_fwd";
       gemm(c, seg_all_nodes(g), b);
     }
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
@@ -246,6 +249,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.B = w->W; a.b_dtype = c.dt; a.Y = sv.P; a.y_dtype = c.dt; a.N = c.D;
     a.dotvec = sv.a32; a.dotout = sv.spair;
     a.num_w = g->R; a.bt_scratch = sc.bt;
+    a.name = "gemm_pairs_fwd";
     gemm(c, seg_pair_rel(g), a);
     rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, out, sv.stats, c.s);
   } else {
@@ -257,10 +261,12 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
     a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
     a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
+    a.name = "gemm_pairs_fwd";
     gemm(c, seg_pair_rt(g), a);
     GemmArgs q;
     q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
     q.num_w = g->T; q.bt_scratch = sc.bt;
+    q.name = "gemm_nodes_fwd";
     gemm(c, seg_node_type(g), q);
     hgt_fwd_traverse(g, c.dt, c.D, sv.P, sv.Q, out, sv.stats, c.s);
   }
@@ -282,17 +288,19 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
         GemmArgs b;
         b.A = G; b.a_dtype = F32; b.K = c.D; b.B = w->W0; b.b_dtype = c.dt; b.transB = true;
         b.Y = dX; b.y_dtype = F32; b.N = c.Din;
+        b.name = "gemm_selfloop_dx";
         gemm(c, seg_all_nodes(g), b);
       }
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = F32; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, c.d->self_loop != 0, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial);
+    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
-      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, G, c.D, dW->dW0, 1, sc.partial);
+      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, G, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : sc.dQ;
     rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, sc.ebuf, dXt, c.s);
@@ -301,6 +309,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = F32; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
     }
@@ -309,7 +318,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       const Plan& dp = plan(g, seg_dpair_rel(g), WGRAD_ROWS, c.s);
       seg_wsum(&dp, sc.csum, X, c.dt, c.Din, g->dpair_dst, sc.Bsum, g->R, sc.partial, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial);
+    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW || dW->db) rgat_tpath_grads(g->R, c.Din, c.D, w->W, w->b, c.dt, sc.Bsum, dW->dW, dW->db, c.s);
     if (dW->da) {
       const Plan& pp = plan(g, seg_pair_rel(g), WGRAD_ROWS, c.s);
@@ -322,16 +331,18 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       GemmArgs q;
       q.A = sc.dQ; q.a_dtype = F32; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
       q.Y = dX; q.y_dtype = F32; q.N = c.Din;
+      q.name = "gemm_nodes_dx";
       gemm(c, seg_node_type(g), q);
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = F32; a.K = 2 * c.D; a.B = sv.F32; a.b_dtype = F32; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rt(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
     }
-    if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.D, dW->dWq, g->T, sc.partial);
+    if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {
-      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, 2 * c.D, sc.dF, g->R * g->T, sc.partial);
+      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, 2 * c.D, sc.dF, g->R * g->T, sc.partial, "wgrad_pairs");
       hgt_unfold(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, dW->dWk, dW->dWv,
                  dW->dWatt, dW->dWmsg, c.s);
     }

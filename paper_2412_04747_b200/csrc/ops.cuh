@@ -24,6 +24,7 @@ struct GemmArgs {
   int N = 0;          // Y width (ldy = N)
   const float* dotvec = nullptr;  // optional epilogue: dotout[row] = sum_n Y_fp32[row][n] * dotvec[w][n]
   float* dotout = nullptr;
+  const char* name = "gemm";      // profiling label of the launch
   int num_w = 0;                  // number of weight matrices in B (tcgen05 path: K-major image size)
   void* bt_scratch = nullptr;     // tcgen05 path: device buffer for num_w*K*N bf16 (K-major B image)
 };
@@ -44,6 +45,7 @@ struct WgradArgs {
   float* out = nullptr;  // [num_w][K1][K2]
   int num_w = 0;
   float* partial = nullptr;  // scratch [ntiles][K1][K2]
+  const char* name = "wgrad";
 };
 void wgrad(const WgradArgs& a, cudaStream_t s);
 
