@@ -6,6 +6,8 @@
 // has no fp32 kind (SURVEY.md §0 finding 8), so fp32 GEMMs run on FFMA.  At
 // d = 64 these GEMMs are HBM-bound (arithmetic intensity 16 flop/B fp32), so
 // the kernel is organised for coalesced gathers and stores, not for FLOPs.
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace rgnn {
@@ -107,9 +109,9 @@ void gemm_dispatch(const GemmArgs& a, cudaStream_t s) {
 
 // ---------------------------------------------------------------- weight gradient
 // grid (tiles, ceil(K1/64), ceil(K2/64)); 256 threads own a 4x4 block of a 64x64 output tile.
-template <class TA>
+template <class TA, class TB>
 __global__ void __launch_bounds__(256) k_wgrad(const Tile* __restrict__ tiles, const TA* __restrict__ A, int K1,
-                                               const int32_t* __restrict__ gather, const float* __restrict__ Bm,
+                                               const int32_t* __restrict__ gather, const TB* __restrict__ Bm,
                                                int K2, float* __restrict__ partial) {
   __shared__ __align__(16) float As[32][64 + 4];
   __shared__ __align__(16) float Bs[32][64 + 4];
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(256) k_wgrad(const Tile* __restrict__ tiles, c
     for (int c = 0; c < 8; ++c) {
       int k1 = k1_0 + lcol + c, k2 = k2_0 + lcol + c;
       As[lrow][lcol + c] = (ok && k1 < K1) ? to_f(A[ar * K1 + k1]) : 0.f;
-      Bs[lrow][lcol + c] = (ok && k2 < K2) ? Bm[(int64_t)r * K2 + k2] : 0.f;
+      Bs[lrow][lcol + c] = (ok && k2 < K2) ? to_f(Bm[(int64_t)r * K2 + k2]) : 0.f;
     }
     __syncthreads();
 #pragma unroll 8
@@ -330,12 +332,16 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));
   if (p.count == 0) return;
   dim3 g(p.count, ceil_div(a.K1, 64), ceil_div(a.K2, 64));
-  if (a.a_dtype == F32)
-    launch(a.name, k_wgrad<float>, g, dim3(256), 0, s, p.tiles, static_cast<const float*>(a.A), a.K1, a.gather, a.Bm,
-           a.K2, a.partial);
-  else
-    launch(a.name, k_wgrad<bf16>, g, dim3(256), 0, s, p.tiles, static_cast<const bf16*>(a.A), a.K1, a.gather, a.Bm,
-           a.K2, a.partial);
+  auto go = [&](auto* A, auto* B) {
+    using TA = std::remove_const_t<std::remove_pointer_t<decltype(A)>>;
+    using TB = std::remove_const_t<std::remove_pointer_t<decltype(B)>>;
+    launch(a.name, k_wgrad<TA, TB>, g, dim3(256), 0, s, p.tiles, A, a.K1, a.gather, B, a.K2, a.partial);
+  };
+  const bool a32 = a.a_dtype == F32, b32 = a.b_dtype == F32;
+  if (a32 && b32) go(static_cast<const float*>(a.A), static_cast<const float*>(a.Bm));
+  else if (a32) go(static_cast<const float*>(a.A), static_cast<const bf16*>(a.Bm));
+  else if (b32) go(static_cast<const bf16*>(a.A), static_cast<const float*>(a.Bm));
+  else go(static_cast<const bf16*>(a.A), static_cast<const bf16*>(a.Bm));
   int64_t width = (int64_t)a.K1 * a.K2;
   launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,
          p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);

@@ -9,6 +9,9 @@
 
 namespace rgnn {
 
+constexpr int SPLIT_THRESH = 1024;  // rows with more in-edges are split ...
+constexpr int SPLIT_CHUNK = 512;    // ... into chunks of this many edges
+
 // A contiguous row range [row0, row1) of one segment (weight index w).
 struct Tile {
   int32_t row0, row1, w, pad;
@@ -61,6 +64,14 @@ struct rgnn_graph_s {
   int32_t* dpair_dst = nullptr;      // [UD] (rel,dst) pairs ordered by (rel, dst)
   int32_t* dpair_csr_beg = nullptr;  // [UD]
   int32_t* dpair_cnt = nullptr;      // [UD]
+
+  // edge-balanced destination work list (skewed in-degrees): rows with more than
+  // SPLIT_THRESH in-edges are cut into chunks of SPLIT_CHUNK edges, each a separate
+  // warp item writing a partial state to slot w; heavy chunks are listed first.
+  int4* row_items = nullptr;   // [n_items] (row, edge begin, edge end, slot or -1)
+  int64_t n_items = 0;
+  int4* split_rows = nullptr;  // [n_split] (row, first slot, number of slots, 0)
+  int64_t n_split = 0, n_slots = 0;
 
   // lazily computed RGCN norms (by kind): per CSR entry and per CSC entry
   std::map<int, std::pair<float*, float*>> norms;

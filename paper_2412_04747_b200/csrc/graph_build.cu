@@ -222,6 +222,39 @@ void hist_prefix(Tmp& tmp, const int32_t* v, int64_t n, int64_t nbins, int32_t* 
 
 }  // namespace
 
+// Edge-balanced destination work list (see graph.cuh).  One-off host pass over row_ptr.
+void build_row_split(rgnn_graph_s* g, cudaStream_t s) {
+  const int64_t N = g->N;
+  std::vector<int32_t> rp(N + 1);
+  RGNN_CUDA(cudaMemcpyAsync(rp.data(), g->row_ptr, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  std::vector<int4> heavy, light, splits;
+  int64_t slots = 0;
+  for (int64_t v = 0; v < N; ++v) {
+    int32_t b = rp[v], e = rp[v + 1];
+    if (e - b > SPLIT_THRESH) {
+      int32_t n = 0;
+      for (int32_t c = b; c < e; c += SPLIT_CHUNK, ++n)
+        heavy.push_back(make_int4((int)v, c, std::min(e, c + SPLIT_CHUNK), (int)(slots + n)));
+      splits.push_back(make_int4((int)v, (int)slots, n, 0));
+      slots += n;
+    } else {
+      light.push_back(make_int4((int)v, b, e, -1));
+    }
+  }
+  heavy.insert(heavy.end(), light.begin(), light.end());
+  g->n_items = (int64_t)heavy.size();
+  g->n_split = (int64_t)splits.size();
+  g->n_slots = slots;
+  g->row_items = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(g->n_items, 1), s));
+  g->split_rows = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(g->n_split, 1), s));
+  if (g->n_items)
+    RGNN_CUDA(cudaMemcpyAsync(g->row_items, heavy.data(), heavy.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  if (g->n_split)
+    RGNN_CUDA(cudaMemcpyAsync(g->split_rows, splits.data(), splits.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));  // host staging goes out of scope
+}
+
 void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, const int32_t* rel_in,
                  int64_t E_in, cudaStream_t s) {
   const int64_t N = g->N;
@@ -393,6 +426,7 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   RGNN_CUDA(cudaStreamSynchronize(s));
   g->max_in_deg = (int64_t)h_stats[1];
   g->max_pair_deg = (int64_t)h_stats[2];
+  build_row_split(g, s);
 }
 
 }  // namespace rgnn

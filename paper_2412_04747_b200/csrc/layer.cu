@@ -109,16 +109,19 @@ void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
 }
 
 struct FwdScratch {
+  Partial pt;         // split-row partial states
   void* P = nullptr;  // RGCN P
   void* bt = nullptr;  // tcgen05 path: K-major bf16 image of the GEMM weights
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
 };
 struct BwdScratch {
+  Partial pt;
+  void* bt = nullptr;     // tcgen05 path: K-major bf16 weight image
   float2* ebuf = nullptr;
-  float* dP = nullptr;    // [U][D] or HGT [U][2D]
+  void* dP = nullptr;     // [U][D] or HGT [U][2D], layer dtype
   float* dXp = nullptr;   // [U][Din]
-  float* dQ = nullptr;    // HGT [N][D]; RGAT dX fallback [N][D]
+  void* dQ = nullptr;     // HGT [N][D] layer dtype; RGAT dX fallback [N][D] fp32
   float* wsum = nullptr;  // RGAT [U]
   float* csum = nullptr;  // RGAT [UD]
   float* Bsum = nullptr;  // RGAT [R][Din]
@@ -128,7 +131,13 @@ struct BwdScratch {
   float* csc_norm = nullptr;
 };
 
+void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
+  pt.acc = ar.take<float>(std::max<int64_t>(c.g->n_slots, 1) * c.D);
+  pt.stat = ar.take<float2>(std::max<int64_t>(c.g->n_slots, 1));
+}
+
 void layout_fwd_scratch(const Ctx& c, Arena& ar, FwdScratch& o) {
+  layout_partial(c, ar, o.pt);
   if (c.dt == BF16) {
     const int64_t R = c.g->R, T = c.g->T;
     int64_t n = c.d->model == RGNN_HGT ? std::max(R * T * c.Din * 2 * c.D, T * c.Din * c.D)
@@ -148,13 +157,19 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   const rgnn_graph_s* g = c.g;
   const int64_t U = g->U, N = g->N, E = g->E, R = g->R, T = g->T;
   const int model = c.d->model;
+  layout_partial(c, ar, o.pt);
+  if (c.dt == BF16) {
+    int64_t n = model == RGNN_HGT ? std::max(R * T * c.Din * 2 * c.D, T * c.Din * c.D)
+                                  : std::max(R, (int64_t)1) * c.Din * c.D;
+    o.bt = ar.take<char>(n * 2);
+  }
   int64_t width = 0, tiles = 0;
   auto need = [&](const Segs& sg, int64_t k1k2) {
     width = std::max(width, k1k2 * count_tiles(sg, WGRAD_ROWS));
     tiles = std::max(tiles, count_tiles(sg, WGRAD_ROWS));
   };
   if (model == RGNN_RGCN) {
-    o.dP = ar.take<float>(U * c.D);
+    o.dP = ar.take<char>(U * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
     if (c.d->norm_kind == RGNN_NORM_CUSTOM) {
       o.csr_norm = ar.take<float>(E);
@@ -164,7 +179,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     need(seg_all_nodes(g), (int64_t)c.Din * c.D);
   } else if (model == RGNN_RGAT) {
     o.ebuf = ar.take<float2>(E);
-    o.dP = ar.take<float>(U * c.D);
+    o.dP = ar.take<char>(U * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
     o.dQ = ar.take<float>(N * c.D);
     o.wsum = ar.take<float>(U);
@@ -174,9 +189,9 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     need(seg_dpair_rel(g), c.Din);
   } else {
     o.ebuf = ar.take<float2>(E);
-    o.dP = ar.take<float>(U * 2 * c.D);
+    o.dP = ar.take<char>(U * 2 * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
-    o.dQ = ar.take<float>(N * c.D);
+    o.dQ = ar.take<char>(N * c.D * c.esz);
     o.dF = ar.take<float>(R * T * c.Din * 2 * c.D);
     need(seg_pair_rt(g), (int64_t)c.Din * 2 * c.D);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
@@ -200,8 +215,8 @@ void gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
   gemm_simt(a, c.s);
 }
 
-void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, const int32_t* gather, const float* Bm,
-              int K2, float* out, int num_w, float* partial, const char* name) {
+void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, const int32_t* gather, const void* Bm,
+              int b_dt, int K2, float* out, int num_w, float* partial, const char* name) {
   WgradArgs w;
   w.name = name;
   w.plan = &plan(c.g, sg, WGRAD_ROWS, c.s);
@@ -210,6 +225,7 @@ void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, con
   w.K1 = K1;
   w.gather = gather;
   w.Bm = Bm;
+  w.b_dtype = b_dt;
   w.K2 = K2;
   w.out = out;
   w.num_w = num_w;
@@ -239,7 +255,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     }
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
     graph_norms(g, c.d->norm_kind, w->edge_norm, c.s, &cn, &xn);
-    rgcn_fwd_traverse(g, c.dt, c.D, cn, sc.P, out, c.d->self_loop != 0, c.s);
+    rgcn_fwd_traverse(g, c.dt, c.D, cn, sc.P, out, c.d->self_loop != 0, sc.pt, c.s);
   } else if (model == RGNN_RGAT) {
     RGNN_CHECK(w->W && w->a && w->b, RGNN_ERR_INVALID_ARG, "RGAT needs W, a, b");
     rgat_tpath_vectors(g->R, c.Din, c.D, w->W, w->b, c.dt, sv.y, c.s);
@@ -251,7 +267,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.num_w = g->R; a.bt_scratch = sc.bt;
     a.name = "gemm_pairs_fwd";
     gemm(c, seg_pair_rel(g), a);
-    rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, out, sv.stats, c.s);
+    rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, out, sv.stats, sc.pt, c.s);
   } else {
     RGNN_CHECK(w->Wk && w->Wq && w->Wv && w->Watt && w->Wmsg && w->mu, RGNN_ERR_INVALID_ARG,
                "HGT needs Wk, Wq, Wv, Watt, Wmsg, mu");
@@ -268,7 +284,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     q.num_w = g->T; q.bt_scratch = sc.bt;
     q.name = "gemm_nodes_fwd";
     gemm(c, seg_node_type(g), q);
-    hgt_fwd_traverse(g, c.dt, c.D, sv.P, sv.Q, out, sv.stats, c.s);
+    hgt_fwd_traverse(g, c.dt, c.D, sv.P, sv.Q, out, sv.stats, sc.pt, c.s);
   }
 }
 
@@ -282,7 +298,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   if (model == RGNN_RGCN) {
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
     graph_norms(g, c.d->norm_kind, w->edge_norm, c.s, &cn, &xn);
-    rgcn_bwd_pair(g, c.D, xn, G, sc.dP, c.s);
+    rgcn_bwd_pair(g, c.dt, c.D, xn, G, sc.dP, c.s);
     if (dX) {
       if (c.d->self_loop) {
         GemmArgs b;
@@ -292,23 +308,25 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
         gemm(c, seg_all_nodes(g), b);
       }
       GemmArgs a;
-      a.A = sc.dP; a.a_dtype = F32; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
+      a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, c.d->self_loop != 0, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
+    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
-      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, G, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
+      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, G, F32, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
   } else if (model == RGNN_RGAT) {
-    float* dXt = dX ? dX : sc.dQ;
-    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, sc.ebuf, dXt, c.s);
+    float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
+    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, sc.ebuf, dXt, sc.pt, c.s);
     rgat_bwd_pair(g, c.dt, c.D, sc.ebuf, G, w->a, sc.dP, sc.wsum, c.s);
     if (dX) {
       GemmArgs a;
-      a.A = sc.dP; a.a_dtype = F32; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
+      a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
@@ -318,31 +336,34 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       const Plan& dp = plan(g, seg_dpair_rel(g), WGRAD_ROWS, c.s);
       seg_wsum(&dp, sc.csum, X, c.dt, c.Din, g->dpair_dst, sc.Bsum, g->R, sc.partial, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
+    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW || dW->db) rgat_tpath_grads(g->R, c.Din, c.D, w->W, w->b, c.dt, sc.Bsum, dW->dW, dW->db, c.s);
     if (dW->da) {
       const Plan& pp = plan(g, seg_pair_rel(g), WGRAD_ROWS, c.s);
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
-    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.ebuf, sc.dQ, c.s);
+    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.ebuf, sc.dQ, sc.pt, c.s);
     hgt_bwd_pair(g, c.dt, c.D, sc.ebuf, G, sv.Q, sc.dP, c.s);
     if (dX) {
       GemmArgs q;
-      q.A = sc.dQ; q.a_dtype = F32; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
+      q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
       q.Y = dX; q.y_dtype = F32; q.N = c.Din;
+      q.num_w = g->T; q.bt_scratch = sc.bt;
       q.name = "gemm_nodes_dx";
       gemm(c, seg_node_type(g), q);
       GemmArgs a;
-      a.A = sc.dP; a.a_dtype = F32; a.K = 2 * c.D; a.B = sv.F32; a.b_dtype = F32; a.transB = true;
+      a.A = sc.dP; a.a_dtype = c.dt; a.K = 2 * c.D; a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
+      a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rt(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
     }
-    if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
+    if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {
-      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, 2 * c.D, sc.dF, g->R * g->T, sc.partial, "wgrad_pairs");
+      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, g->R * g->T, sc.partial, "wgrad_pairs");
       hgt_unfold(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, dW->dWk, dW->dWv,
                  dW->dWatt, dW->dWmsg, c.s);
     }

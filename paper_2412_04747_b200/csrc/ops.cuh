@@ -40,7 +40,8 @@ struct WgradArgs {
   int a_dtype = F32;
   int K1 = 0;
   const int32_t* gather = nullptr;
-  const float* Bm = nullptr;
+  const void* Bm = nullptr;  // [rows][K2], b_dtype
+  int b_dtype = F32;
   int K2 = 0;
   float* out = nullptr;  // [num_w][K1][K2]
   int num_w = 0;

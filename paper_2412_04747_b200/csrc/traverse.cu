@@ -58,6 +58,19 @@ __device__ __forceinline__ void ld4(const bf16* p, float* o) {
   o[2] = __uint_as_float(x.y << 16); o[3] = __uint_as_float(x.y & 0xffff0000u);
 }
 
+// store V floats / 4 floats into a row of the table type
+template <int V>
+__device__ __forceinline__ void st_tp(float* p, const float* v) { st_f32<V>(p, v); }
+template <int V>
+__device__ __forceinline__ void st_tp(bf16* p, const float* v) { store16(p, v); }
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st4(bf16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
 // sum over the LPR lanes of one group
 template <int LPR>
 __device__ __forceinline__ float gsum(float x) {
@@ -100,16 +113,19 @@ __device__ __forceinline__ void sum_groups(float* acc) {
 // ------------------------------------------------------------------ RGCN forward (A5)
 // out_v (+)= sum_e norm_e P[pair_e]     (Eq. 3.1; self-loop X W_0 already in out when accumulate)
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
                                                   const int32_t* __restrict__ csr_pair,
                                                   const float* __restrict__ norm, const TP* __restrict__ P,
                                                   float* __restrict__ out, bool accumulate) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= N) return;
+  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wi >= n_items) return;
+  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
+  const int64_t v = item.x;
+  const int slot = item.w;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = row_ptr[v], e = row_ptr[v + 1];
+  const int b = item.y, e = item.z;
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
@@ -137,6 +153,10 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t N, const int32_t* __re
     }
   }
   sum_groups<LPR, V>(acc);
+  if (slot >= 0) {  // chunk of a split row: partial sum, merged by k_merge_sum
+    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+    return;
+  }
   if (g == 0) {
     float* o = out + v * D + c * V;
     if (accumulate) {
@@ -152,16 +172,19 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t N, const int32_t* __re
 // ------------------------------------------------------------------ HGT forward (A3+A4+A5)
 // KM row of pair p = [K~_p | M_p] (2D wide);  l_e = K~_p . q_v;  out_v = sum softmax(l)_e M_p
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
                                                  const int32_t* __restrict__ csr_pair, const TP* __restrict__ KM,
                                                  const TP* __restrict__ Q, float* __restrict__ out,
                                                  float2* __restrict__ stats) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= N) return;
+  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wi >= n_items) return;
+  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
+  const int64_t v = item.x;
+  const int slot = item.w;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = row_ptr[v], e = row_ptr[v + 1];
+  const int b = item.y, e = item.z;
   float q[V];
   cvt16<TP>(ldg16(Q + v * D + c * V), q);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
@@ -210,6 +233,11 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t N, const int32_t* __res
     m = mx;
   }
   merge_groups<LPR, V>(m, s, acc);
+  if (slot >= 0) {  // chunk of a split row: unnormalised state, merged by k_merge_softmax
+    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+    if (lane == 0) pstat[slot] = make_float2(m, s);
+    return;
+  }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
@@ -221,7 +249,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t N, const int32_t* __res
 // z_e = s_p + x_v . y_r (reordered t-path), l = LeakyReLU(z), out_v = sum softmax(l)_e P_p.
 // Requires d_in == d_out == D (x_v chunk in registers).
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t N, const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
                                                   const int32_t* __restrict__ csr_pair,
                                                   const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                   const float* __restrict__ spair, const TP* __restrict__ X,
@@ -229,10 +257,13 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t N, const int32_t* __re
                                                   float2* __restrict__ stats) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= N) return;
+  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wi >= n_items) return;
+  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
+  const int64_t v = item.x;
+  const int slot = item.w;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = row_ptr[v], e = row_ptr[v + 1];
+  const int b = item.y, e = item.z;
   float x[V];
   cvt16<TP>(ldg16(X + v * D + c * V), x);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
@@ -287,6 +318,11 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t N, const int32_t* __re
     m = mx;
   }
   merge_groups<LPR, V>(m, s, acc);
+  if (slot >= 0) {  // chunk of a split row: unnormalised state, merged by k_merge_softmax
+    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+    if (lane == 0) pstat[slot] = make_float2(m, s);
+    return;
+  }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
@@ -298,18 +334,21 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t N, const int32_t* __re
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
 // dQ_v = sum_e dl_e K~_p ; ebuf[csr pos] = (alpha_e, dl_e)
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t N, const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
                                                      const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
                                                      const float* __restrict__ out, float2* __restrict__ ebuf,
-                                                     float* __restrict__ dQ) {
+                                                     TP* __restrict__ dQ) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= N) return;
+  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wi >= n_items) return;
+  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
+  const int64_t v = item.x;
+  const int slot = item.w;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = row_ptr[v], e = row_ptr[v + 1];
+  const int b = item.y, e = item.z;
   float dq[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dq[k] = 0.f;
@@ -362,14 +401,17 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t N, const int32_t* _
     }
   }
   sum_groups<LPR, V>(dq);
-  if (g == 0) st_f32<V>(dQ + v * D + c * V, dq);
+  if (g == 0) {
+    if (slot >= 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, dq);
+    else st_tp<V>(dQ + v * D + c * V, dq);
+  }
 }
 
 // ------------------------------------------------------------------ RGAT backward, dst-major (A6)
 // dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
 // dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path) ; ebuf[i] = (alpha_e, dz_e)
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t N, const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
                                                       const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
@@ -379,10 +421,13 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t N, const int32_t* 
                                                       float2* __restrict__ ebuf, float* __restrict__ dX) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= N) return;
+  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wi >= n_items) return;
+  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
+  const int64_t v = item.x;
+  const int slot = item.w;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = row_ptr[v], e = row_ptr[v + 1];
+  const int b = item.y, e = item.z;
   float dx[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dx[k] = 0.f;
@@ -442,7 +487,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t N, const int32_t* 
     }
   }
   sum_groups<LPR, V>(dx);
-  if (g == 0) st_f32<V>(dX + v * D + c * V, dx);
+  if (g == 0) st_f32<V>((slot >= 0 ? pacc + (int64_t)slot * D : dX + v * D) + c * V, dx);
 }
 
 // ------------------------------------------------------------------ pair-major backward (A7)
@@ -454,12 +499,12 @@ struct PGeo {
 };
 
 // RGCN: dP_p = sum_{e in p} norm_e G[d_e]
-template <int D>
+template <class TO, int D>
 __global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
                                                        const int32_t* __restrict__ pair_deg,
                                                        const int32_t* __restrict__ csc_dst,
                                                        const float* __restrict__ csc_norm,
-                                                       const float* __restrict__ Gr, float* __restrict__ dP) {
+                                                       const float* __restrict__ Gr, TO* __restrict__ dP) {
   constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
   int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
@@ -485,7 +530,7 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t U, const int32_t*
       acc[2] = fmaf(w[u], gr[u].z, acc[2]); acc[3] = fmaf(w[u], gr[u].w, acc[3]);
     }
   }
-  *reinterpret_cast<float4*>(dP + p * D + c * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  st4(dP + p * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
 }
 
 // RGAT: dP_p = sum alpha_e G[d_e] + (sum dz_e) a_r ; wsum_p = sum dz_e
@@ -496,7 +541,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t U, const int32_t*
                                                        const int32_t* __restrict__ csc_rel,
                                                        const int32_t* __restrict__ csc2csr,
                                                        const float2* __restrict__ ebuf, const float* __restrict__ Gr,
-                                                       const TW* __restrict__ avec, float* __restrict__ dP,
+                                                       const TW* __restrict__ avec, TW* __restrict__ dP,
                                                        float* __restrict__ wsum) {
   constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
@@ -528,8 +573,8 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t U, const int32_t*
   float a4[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) a4[k] = to_f(avec[(int64_t)r * D + c * 4 + k]);
-  *reinterpret_cast<float4*>(dP + p * D + c * 4) =
-      make_float4(fmaf(zs, a4[0], acc[0]), fmaf(zs, a4[1], acc[1]), fmaf(zs, a4[2], acc[2]), fmaf(zs, a4[3], acc[3]));
+  st4(dP + p * D + c * 4, fmaf(zs, a4[0], acc[0]), fmaf(zs, a4[1], acc[1]), fmaf(zs, a4[2], acc[2]),
+      fmaf(zs, a4[3], acc[3]));
   if (c == 0) wsum[p] = zs;
 }
 
@@ -540,7 +585,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t U, const int32_t* 
                                                       const int32_t* __restrict__ csc_dst,
                                                       const int32_t* __restrict__ csc2csr,
                                                       const float2* __restrict__ ebuf, const float* __restrict__ Gr,
-                                                      const TP* __restrict__ Q, float* __restrict__ dKM) {
+                                                      const TP* __restrict__ Q, TP* __restrict__ dKM) {
   constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
   int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
@@ -572,9 +617,9 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t U, const int32_t* 
       for (int k = 0; k < 4; ++k) ak[k] = fmaf(ab[u].y, qv[u][k], ak[k]);
     }
   }
-  float* o = dKM + p * 2 * D;
-  *reinterpret_cast<float4*>(o + c * 4) = make_float4(ak[0], ak[1], ak[2], ak[3]);
-  *reinterpret_cast<float4*>(o + D + c * 4) = make_float4(am[0], am[1], am[2], am[3]);
+  TP* o = dKM + p * 2 * D;
+  st4(o + c * 4, ak[0], ak[1], ak[2], ak[3]);
+  st4(o + D + c * 4, am[0], am[1], am[2], am[3]);
 }
 
 // c_{v,r} = sum of dz over the CSR run of (dst v, rel r)   (RGAT destination-side weight terms)
@@ -585,6 +630,62 @@ __global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const i
   float acc = 0.f;
   for (int i = beg[j], e = beg[j] + cnt[j]; i < e; ++i) acc += ebuf[i].y;
   csum[j] = acc;
+}
+
+
+// ------------------------------------------------------------------ split-row merges
+// Rows cut into chunks (graph.cuh SPLIT_*) leave one partial state per chunk; one warp per
+// split row combines them in chunk order (deterministic).  Lane c owns columns 4c..4c+3.
+template <int D>
+__global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const int4* __restrict__ splits,
+                                                       const float* __restrict__ pacc,
+                                                       const float2* __restrict__ pstat, float* __restrict__ out,
+                                                       float2* __restrict__ stats) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= n_split) return;
+  const int lane = threadIdx.x & 31;
+  const int4 sp = splits[j];
+  float m = -CUDART_INF_F;
+  for (int i = 0; i < sp.z; ++i) m = fmaxf(m, pstat[sp.y + i].x);
+  float s = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool act = lane * 4 < D;
+  for (int i = 0; i < sp.z; ++i) {
+    float2 st = pstat[sp.y + i];
+    float w = safe_exp_diff(st.x, m);
+    s = fmaf(st.y, w, s);
+    if (act) {
+      float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
+      acc[0] = fmaf(w, a.x, acc[0]); acc[1] = fmaf(w, a.y, acc[1]);
+      acc[2] = fmaf(w, a.z, acc[2]); acc[3] = fmaf(w, a.w, acc[3]);
+    }
+  }
+  float inv = s > 0.f ? 1.f / s : 0.f;
+  if (act)
+    *reinterpret_cast<float4*>(out + (int64_t)sp.x * D + lane * 4) =
+        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  if (lane == 0) stats[sp.x] = make_float2(m, s);
+}
+
+template <int D, class TO>
+__global__ void __launch_bounds__(256) k_merge_sum(int64_t n_split, const int4* __restrict__ splits,
+                                                   const float* __restrict__ pacc, TO* __restrict__ out,
+                                                   bool accumulate) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= n_split) return;
+  const int lane = threadIdx.x & 31;
+  if (lane * 4 >= D) return;
+  const int4 sp = splits[j];
+  TO* o = out + (int64_t)sp.x * D + lane * 4;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (accumulate) {  // fp32 outputs only
+    float4 prev = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o));
+    acc[0] = prev.x; acc[1] = prev.y; acc[2] = prev.z; acc[3] = prev.w;
+  }
+  for (int i = 0; i < sp.z; ++i) {
+    float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
+    acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+  }
+  st4(o, acc[0], acc[1], acc[2], acc[3]);
 }
 
 template <class F>
@@ -603,72 +704,89 @@ inline dim3 warp_grid(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
 }  // namespace
 
 void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* norm, const void* P, float* out,
-                       bool accumulate, cudaStream_t s) {
+                       bool accumulate, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
-      launch("rgcn_fwd_traverse", k_rgcn_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, norm, static_cast<const float*>(P), out, accumulate);
+      launch("rgcn_fwd_traverse", k_rgcn_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, norm, static_cast<const float*>(P), out, accumulate);
     else
-      launch("rgcn_fwd_traverse", k_rgcn_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, norm, static_cast<const bf16*>(P), out, accumulate);
+      launch("rgcn_fwd_traverse", k_rgcn_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, norm, static_cast<const bf16*>(P), out, accumulate);
+    launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split, g->split_rows,
+           (const float*)pt.acc, out, accumulate);
   });
 }
 
 void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
-                      float2* stats, cudaStream_t s) {
+                      float2* stats, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
-      launch("hgt_fwd_traverse", k_hgt_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q), out, stats);
+      launch("hgt_fwd_traverse", k_hgt_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q),
+             out, stats);
     else
-      launch("hgt_fwd_traverse", k_hgt_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q), out, stats);
+      launch("hgt_fwd_traverse", k_hgt_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q),
+             out, stats);
+    launch("merge_split_rows", k_merge_softmax<DD>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
+           g->split_rows, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                       const float* y, float slope, float* out, float2* stats, cudaStream_t s) {
+                       const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
-      launch("rgat_fwd_traverse", k_rgat_fwd<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair, static_cast<const float*>(X), y, slope,
-             out, stats);
+      launch("rgat_fwd_traverse", k_rgat_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair,
+             static_cast<const float*>(X), y, slope, out, stats);
     else
-      launch("rgat_fwd_traverse", k_rgat_fwd<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair, static_cast<const bf16*>(X), y, slope,
-             out, stats);
+      launch("rgat_fwd_traverse", k_rgat_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair,
+             static_cast<const bf16*>(X), y, slope, out, stats);
+    launch("merge_split_rows", k_merge_softmax<DD>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
+           g->split_rows, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, float2* ebuf, float* dQ, cudaStream_t s) {
+                 const float* G, const float* out, float2* ebuf, void* dQ, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("hgt_bwd_dst", k_hgt_bwd_dst<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q), stats, G, out, ebuf, dQ);
-    else
-      launch("hgt_bwd_dst", k_hgt_bwd_dst<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q), stats, G, out, ebuf, dQ);
+    if (dtype == F32) {
+      launch("hgt_bwd_dst", k_hgt_bwd_dst<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q),
+             stats, G, out, ebuf, static_cast<float*>(dQ));
+      launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
+             g->split_rows, (const float*)pt.acc, static_cast<float*>(dQ), false);
+    } else {
+      launch("hgt_bwd_dst", k_hgt_bwd_dst<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q),
+             stats, G, out, ebuf, static_cast<bf16*>(dQ));
+      launch("merge_split_rows", k_merge_sum<DD, bf16>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
+             g->split_rows, (const float*)pt.acc, static_cast<bf16*>(dQ), false);
+    }
   });
 }
 
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
-                  float* dX, cudaStream_t s) {
+                  float* dX, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
-      launch("rgat_bwd_dst", k_rgat_bwd_dst<float, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair, static_cast<const float*>(X), y, slope,
-             stats, G, out, ebuf, dX);
+      launch("rgat_bwd_dst", k_rgat_bwd_dst<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair,
+             static_cast<const float*>(X), y, slope, stats, G, out, ebuf, dX);
     else
-      launch("rgat_bwd_dst", k_rgat_bwd_dst<bf16, DD>, warp_grid(g->N), dim3(256), 0, s, g->N, g->row_ptr,
-             g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair, static_cast<const bf16*>(X), y, slope,
-             stats, G, out, ebuf, dX);
+      launch("rgat_bwd_dst", k_rgat_bwd_dst<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
+             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair,
+             static_cast<const bf16*>(X), y, slope, stats, G, out, ebuf, dX);
+    launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split, g->split_rows,
+           (const float*)pt.acc, dX, false);
   });
 }
 
@@ -677,39 +795,44 @@ static dim3 pair_grid(int64_t U, int D) {
   return dim3(ceil_div(ceil_div(U, eg) * (int64_t)32, 256));
 }
 
-void rgcn_bwd_pair(const rgnn_graph_s* g, int D, const float* csc_norm, const float* G, float* dP, cudaStream_t s) {
+void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
+                   cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    launch("rgcn_bwd_pair", k_rgcn_bwd_pair<DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-           g->pair_deg, g->csc_dst, csc_norm, G, dP);
+    if (dtype == F32)
+      launch("rgcn_bwd_pair", k_rgcn_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
+             g->pair_deg, g->csc_dst, csc_norm, G, static_cast<float*>(dP));
+    else
+      launch("rgcn_bwd_pair", k_rgcn_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
+             g->pair_deg, g->csc_dst, csc_norm, G, static_cast<bf16*>(dP));
   });
 }
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   float* dP, float* wsum, cudaStream_t s) {
+                   void* dP, float* wsum, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
       launch("rgat_bwd_pair", k_rgat_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
              g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const float*>(a),
-             dP, wsum);
+             static_cast<float*>(dP), wsum);
     else
       launch("rgat_bwd_pair", k_rgat_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
              g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const bf16*>(a),
-             dP, wsum);
+             static_cast<bf16*>(dP), wsum);
   });
 }
 
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
-                  float* dKM, cudaStream_t s) {
+                  void* dKM, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     if (dtype == F32)
       launch("hgt_bwd_pair", k_hgt_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const float*>(Q), dKM);
+             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const float*>(Q), static_cast<float*>(dKM));
     else
       launch("hgt_bwd_pair", k_hgt_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const bf16*>(Q), dKM);
+             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const bf16*>(Q), static_cast<bf16*>(dKM));
   });
 }
 

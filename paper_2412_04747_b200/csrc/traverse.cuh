@@ -3,21 +3,27 @@
 #include "graph.cuh"
 
 namespace rgnn {
+// Partial states of split rows (graph.cuh SPLIT_*): acc [n_slots][D] fp32, stat [n_slots] (m, sum).
+struct Partial {
+  float* acc = nullptr;
+  float2* stat = nullptr;
+};
 void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* norm, const void* P, float* out,
-                       bool accumulate, cudaStream_t s);
+                       bool accumulate, const Partial& pt, cudaStream_t s);
 void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
-                      float2* stats, cudaStream_t s);
+                      float2* stats, const Partial& pt, cudaStream_t s);
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                       const float* y, float slope, float* out, float2* stats, cudaStream_t s);
+                       const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s);
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, float2* ebuf, float* dQ, cudaStream_t s);
+                 const float* G, const float* out, float2* ebuf, void* dQ, const Partial& pt, cudaStream_t s);
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
-                  float* dX, cudaStream_t s);
-void rgcn_bwd_pair(const rgnn_graph_s* g, int D, const float* csc_norm, const float* G, float* dP, cudaStream_t s);
+                  float* dX, const Partial& pt, cudaStream_t s);
+void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
+                   cudaStream_t s);
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   float* dP, float* wsum, cudaStream_t s);
+                   void* dP, float* wsum, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
-                  float* dKM, cudaStream_t s);
+                  void* dKM, cudaStream_t s);
 void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
 }  // namespace rgnn

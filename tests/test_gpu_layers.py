@@ -116,3 +116,16 @@ def test_deterministic():
     assert torch.equal(outs[0][0], outs[1][0])
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+def test_split_heavy_rows(model, dtype):
+    """Destinations with > 1024 in-edges are cut into 512-edge chunks whose partial
+    (online-softmax) states are merged; a hub graph exercises that path."""
+    from synth.graphs import synth_heterograph
+    g = synth_heterograph([300, 2000], [(1, 0), (0, 0), (1, 1)], rel_sizes=[9000, 4000, 3000],
+                          a_src=0.3, a_dst=1.3, seed=5, name="hubs")
+    deg = np.bincount(g.dst, minlength=g.num_nodes)
+    assert deg.max() > 1024  # graph.cuh SPLIT_THRESH
+    run_case(model, g, 64, 64, dtype)
