@@ -76,30 +76,31 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + 2 * d * b)
         out["gemm_nodes_fwd"] = N * (d_in * b + d * b)
         out["hgt_fwd_traverse"] = E * (4 + 2 * d * b) + N * (8 + d * b + 4 * d + 8)
-        out["hgt_bwd_dst"] = E * (4 + 2 * d * b + 8) + N * (8 + d * b + 4 * d + 4 * d + 8 + 4 * d)
-        out["hgt_bwd_pair"] = E * (4 + 4 + 8 + 4 * d + d * b) + U * (8 + 8 * d)
-        out["gemm_nodes_dx"] = N * (4 * d + 4 * d_in)
-        out["gemm_pairs_dx"] = U * (8 * d + 4 * d_in)
+        # backward tables (dQ, [dK~|dM]) are stored in the layer dtype (b bytes)
+        out["hgt_bwd_dst"] = E * (4 + 2 * d * b + 8) + N * (8 + d * b + 4 * d + 4 * d + 8 + d * b)
+        out["hgt_bwd_pair"] = E * (4 + 4 + 8 + 4 * d + d * b) + U * (8 + 2 * d * b)
+        out["gemm_nodes_dx"] = N * (d * b + 4 * d_in)
+        out["gemm_pairs_dx"] = U * (2 * d * b + 4 * d_in)
         out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
-        out["wgrad_pairs"] = U * (4 + d_in * b + 8 * d)
-        out["wgrad_nodes"] = N * (d_in * b + 4 * d)
+        out["wgrad_pairs"] = U * (4 + d_in * b + 2 * d * b)
+        out["wgrad_nodes"] = N * (d_in * b + d * b)
     elif model == "rgat":
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b + 4)
         out["rgat_fwd_traverse"] = E * (4 + 4 + d * b + 4 + 4 * d) + N * (8 + d_in * b + 4 * d + 8)
         out["rgat_bwd_dst"] = E * (8 + d * b + 4 + 4 * d + 8) + N * (8 + d_in * b + 12 * d + 8)
-        out["rgat_bwd_pair"] = E * (4 + 4 + 8 + 4 * d) + U * (8 + 4 * d + 4)
-        out["gemm_pairs_dx"] = U * (4 * d + 4 * d_in)
+        out["rgat_bwd_pair"] = E * (4 + 4 + 8 + 4 * d) + U * (8 + d * b + 4)
+        out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
         out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
-        out["wgrad_pairs"] = U * (4 + d_in * b + 4 * d)
+        out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
     else:
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b)
         out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)
         out["rgcn_fwd_traverse"] = E * (4 + 4 + d * b) + N * (8 + 8 * d)
-        out["rgcn_bwd_pair"] = E * (4 + 4 + 4 * d) + U * (8 + 4 * d)
-        out["gemm_pairs_dx"] = U * (4 * d + 4 * d_in)
+        out["rgcn_bwd_pair"] = E * (4 + 4 + 4 * d) + U * (8 + d * b)
+        out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
         out["gemm_selfloop_dx"] = N * (4 * d + 4 * d_in)
         out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
-        out["wgrad_pairs"] = U * (4 + d_in * b + 4 * d)
+        out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
         out["wgrad_selfloop"] = N * (d_in * b + 4 * d)
     return out
 

@@ -332,6 +332,13 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));
   if (p.count == 0) return;
   dim3 g(p.count, ceil_div(a.K1, 64), ceil_div(a.K2, 64));
+  if (a.allow_tc && wgrad_tc_supported(a)) {
+    wgrad_tc(a, s);
+    int64_t width = (int64_t)a.K1 * a.K2;
+    launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,
+           p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
+    return;
+  }
   auto go = [&](auto* A, auto* B) {
     using TA = std::remove_const_t<std::remove_pointer_t<decltype(A)>>;
     using TB = std::remove_const_t<std::remove_pointer_t<decltype(B)>>;

@@ -223,6 +223,151 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
   if (warp == 0) tmem_dealloc<NCOLS>(tmem);
 }
 
+// ------------------------------------------------------------------ weight gradient on tcgen05
+// partial[tile] = (sum_{rows of tile} A[gather(row)]^T Bm[row])  as  D[m = k2][n = k1]:
+//   M = 128 covers K2 (the gradient width; for K2 = 64 the second 64-row half of the MMA
+//   re-reads the same smem block through LBO = 0 and its lanes are ignored),
+//   N = K1 (d_in), K = the rows, 16 per instruction.  Both operands are MN-major: a staged
+//   row (128 B = 64 elements) is one 128B-swizzle line, 8 rows form a 1024-B atom (SBO),
+//   64-element MN blocks sit at +LBO.  Rows past the tile end are zero-filled (cp.async
+//   src-size 0) so they contribute nothing.  Two smem stages overlap the next sub-tile's
+//   gather with the current MMAs; the accumulator stays in TMEM for the whole tile.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;  // stride between 64-element MN blocks
+  d |= (uint64_t)(1024 >> 4) << 32;                   // stride between 8-row K groups
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ uint32_t umma_idesc_bf16_mn(int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;                    // D fp32
+  d |= 1u << 7;                    // A bf16
+  d |= 1u << 10;                   // B bf16
+  d |= 1u << 15;                   // A MN-major
+  d |= 1u << 16;                   // B MN-major
+  d |= (uint32_t)(n >> 3) << 17;
+  d |= (uint32_t)(128 >> 4) << 24;
+  return d;
+}
+
+template <int K1, int K2>
+__global__ void __launch_bounds__(128) k_wgrad_tc(const Tile* __restrict__ tiles, const bf16* __restrict__ A,
+                                                  const int32_t* __restrict__ gather, const bf16* __restrict__ Bm,
+                                                  float* __restrict__ partial) {
+  constexpr int ROWS = 128;                  // rows per sub-tile (8 MMAs of K = 16)
+  constexpr int KB1 = K1 / 64, KB2 = K2 / 64;  // 64-element MN blocks
+  constexpr uint32_t BLK = ROWS * 128;       // bytes of one MN block of one sub-tile
+  constexpr uint32_t STAGE = (KB1 + KB2) * BLK;
+  constexpr int NCOLS = K1 <= 64 ? 64 : 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);  // [2] stage-free barriers + [1] done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Tile t = tiles[blockIdx.x];
+  const int nsub = (t.row1 - t.row0 + ROWS - 1) / ROWS;
+  const uint32_t s_base = smem_u32(smem);
+
+  if (warp == 0) tmem_alloc<NCOLS>(tslot);
+  if (tid == 32) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+
+  auto load = [&](int sub, int stage) {
+    const uint32_t sb = s_base + stage * STAGE;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      int idx = it * 128 + tid;
+      int r = idx >> 3, c = idx & 7;
+      int row = t.row0 + sub * ROWS + r;
+      bool ok = row < t.row1;
+      int rr = ok ? row : t.row0;
+      int64_t xa = gather ? (int64_t)gather[rr] : (int64_t)rr;
+      uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+#pragma unroll
+      for (int j = 0; j < KB2; ++j) cp_async16_zfill(sb + j * BLK + off, Bm + (int64_t)rr * K2 + j * 64 + c * 8, ok);
+#pragma unroll
+      for (int j = 0; j < KB1; ++j)
+        cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  load(0, 0);
+  __syncthreads();  // barrier init + TMEM address visible
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t idesc = umma_idesc_bf16_mn(K1);
+  for (int sub = 0; sub < nsub; ++sub) {
+    const int st = sub & 1;
+    if (sub + 1 < nsub) {
+      if (sub + 1 >= 2) mbar_wait(&bars[(sub + 1) & 1], ((sub - 1) >> 1) & 1);  // MMAs of sub-1 freed it
+      load(sub + 1, (sub + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t sb = s_base + st * STAGE;
+#pragma unroll
+      for (int k = 0; k < ROWS / 16; ++k) {
+        uint64_t da = umma_desc_mn_sw128(sb + k * 2048, KB2 == 2 ? BLK : 0);
+        uint64_t db = umma_desc_mn_sw128(sb + KB2 * BLK + k * 2048, BLK);
+        umma_bf16(tmem, da, db, idesc, (sub | k) ? 1u : 0u);
+      }
+      umma_commit(&bars[st]);
+      if (sub == nsub - 1) umma_commit(&bars[2]);
+    }
+  }
+  mbar_wait(&bars[2], 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // epilogue: lane m = k2 (rows 0..K2-1 of D), columns n = k1; partial[tile][k1][k2]
+  float* out = partial + (size_t)blockIdx.x * K1 * K2;
+  if (warp * 32 < K2) {
+#pragma unroll
+    for (int c0 = 0; c0 < K1; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      const int m = warp * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) out[(size_t)(c0 + i) * K2 + m] = v[i];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<NCOLS>(tmem);
+}
+
+template <int K1, int K2>
+void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
+  constexpr uint32_t STAGE = (K1 / 64 + K2 / 64) * 128 * 128;
+  size_t smem = 1024 + 2 * STAGE + 64;
+  auto k = k_wgrad_tc<K1, K2>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  launch(a.name, k, dim3(a.plan->count), dim3(128), smem, s, a.plan->tiles, static_cast<const bf16*>(a.A), a.gather,
+         static_cast<const bf16*>(a.Bm), a.partial);
+}
+
 template <class TY, int N, int KB>
 void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
@@ -253,6 +398,17 @@ void by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool wgrad_tc_supported(const WgradArgs& a) {
+  return a.a_dtype == BF16 && a.b_dtype == BF16 && (a.K1 == 64 || a.K1 == 128) && (a.K2 == 64 || a.K2 == 128);
+}
+
+void wgrad_tc(const WgradArgs& a, cudaStream_t s) {
+  if (a.K1 == 64 && a.K2 == 64) launch_wgrad_tc<64, 64>(a, s);
+  else if (a.K1 == 64 && a.K2 == 128) launch_wgrad_tc<64, 128>(a, s);
+  else if (a.K1 == 128 && a.K2 == 64) launch_wgrad_tc<128, 64>(a, s);
+  else launch_wgrad_tc<128, 128>(a, s);
+}
 
 bool gemm_tc_supported(const GemmArgs& a) {
   if (a.a_dtype != BF16 || a.b_dtype != BF16) return false;

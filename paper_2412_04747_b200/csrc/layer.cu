@@ -219,6 +219,7 @@ void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, con
               int b_dt, int K2, float* out, int num_w, float* partial, const char* name) {
   WgradArgs w;
   w.name = name;
+  w.allow_tc = c.d->gemm_impl == 2 || (c.d->gemm_impl == 0 && c.dt == BF16);
   w.plan = &plan(c.g, sg, WGRAD_ROWS, c.s);
   w.A = A;
   w.a_dtype = a_dt;

@@ -47,8 +47,11 @@ struct WgradArgs {
   int num_w = 0;
   float* partial = nullptr;  // scratch [ntiles][K1][K2]
   const char* name = "wgrad";
+  bool allow_tc = false;  // bf16 operands: tcgen05 kernel (MN-major) when the widths allow
 };
 void wgrad(const WgradArgs& a, cudaStream_t s);
+bool wgrad_tc_supported(const WgradArgs& a);
+void wgrad_tc(const WgradArgs& a, cudaStream_t s);
 
 // out[w][k] = sum_{rows of w} wt[row] * A[gather(row)][k]  (fp32 out; same two-level scheme)
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather,
