@@ -126,6 +126,8 @@ struct BwdScratch {
   float* csum = nullptr;  // RGAT [UD]
   float* Bsum = nullptr;  // RGAT [R][Din]
   float* dF = nullptr;    // HGT [R*T][Din][2D]
+  void* GQ = nullptr;     // HGT [N][2D] = [G_v | Q_v] layer dtype
+  float4* nst = nullptr;  // HGT [N] (m, 1/sum, G.out, 0)
   float* partial = nullptr;
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
@@ -188,11 +190,12 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     need(seg_pair_rel(g), (int64_t)c.Din * c.D);
     need(seg_dpair_rel(g), c.Din);
   } else {
-    o.ebuf = ar.take<float2>(E);
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
     o.dQ = ar.take<char>(N * c.D * c.esz);
     o.dF = ar.take<float>(R * T * c.Din * 2 * c.D);
+    o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
+    o.nst = ar.take<float4>(N);
     need(seg_pair_rt(g), (int64_t)c.Din * 2 * c.D);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
   }
@@ -344,8 +347,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
-    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.ebuf, sc.dQ, sc.pt, c.s);
-    hgt_bwd_pair(g, c.dt, c.D, sc.ebuf, G, sv.Q, sc.dP, c.s);
+    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, nullptr, sc.dQ, sc.pt, c.s);
+    hgt_bwd_pair_recompute(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.GQ, sc.nst, sc.dP, c.s);
     if (dX) {
       GemmArgs q;
       q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;

@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4
         if (i < e) {
 #pragma unroll
           for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
-          if (c == 0) ebuf[i] = make_float2(alpha, dl);
+          if (ebuf && c == 0) ebuf[i] = make_float2(alpha, dl);
         }
       }
     }
@@ -622,6 +622,98 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t U, const int32_t* 
   st4(o + D + c * 4, am[0], am[1], am[2], am[3]);
 }
 
+
+// ------------------------------------------------------------------ HGT pair-major backward, recomputing alpha
+// Per node (prep): GQ_v = [G_v | Q_v] in the table dtype, nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
+// Per pair p (one group of D/4 lanes): K~_p and M_p stay in registers; for each edge e of p (its CSC
+// segment) l_e = K~_p . Q_d, alpha_e = exp(l_e - m_d)/sum_d, dalpha_e = G_d . M_p,
+// dl_e = alpha_e (dalpha_e - G_d . out_d);  dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d.
+// One 2D-wide row gather + one 16-byte node record per edge; no per-edge buffer.
+template <int LPR>
+__device__ __forceinline__ float gsum_m(float x, unsigned mask) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
+  return x;
+}
+
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* __restrict__ Gr,
+                                                       const TP* __restrict__ Q, const float* __restrict__ out,
+                                                       const float2* __restrict__ stats, TP* __restrict__ GQ,
+                                                       float4* __restrict__ nst) {
+  constexpr int LPR = D / 4, EG = 32 / LPR;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (g * LPR));
+  const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (v >= N) return;
+  float4 gv = __ldg(reinterpret_cast<const float4*>(Gr + v * D + c * 4));
+  float4 ov = __ldg(reinterpret_cast<const float4*>(out + v * D + c * 4));
+  float qv[4];
+  ld4(Q + v * D + c * 4, qv);
+  float go = gsum_m<LPR>(gv.x * ov.x + gv.y * ov.y + gv.z * ov.z + gv.w * ov.w, gmask);
+  st4(GQ + v * 2 * D + c * 4, gv.x, gv.y, gv.z, gv.w);
+  st4(GQ + v * 2 * D + D + c * 4, qv[0], qv[1], qv[2], qv[3]);
+  if (c == 0) {
+    float2 st = stats[v];
+    nst[v] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
+  }
+}
+
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_hgt_bwd_pair_rc(int64_t U, const int32_t* __restrict__ pair_beg,
+                                                         const int32_t* __restrict__ pair_deg,
+                                                         const int32_t* __restrict__ csc_dst,
+                                                         const TP* __restrict__ KM, const TP* __restrict__ GQ,
+                                                         const float4* __restrict__ nst, TP* __restrict__ dKM) {
+  constexpr int LPR = D / 4, EG = 32 / LPR;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (g * LPR));
+  const int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (p >= U) return;
+  const int b = pair_beg[p], n = pair_deg[p];
+  float kx[4], mv[4];
+  ld4(KM + p * 2 * D + c * 4, kx);
+  ld4(KM + p * 2 * D + D + c * 4, mv);
+  float am[4] = {0.f, 0.f, 0.f, 0.f}, ak[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j0 = 0; j0 < n; j0 += UNR) {
+    float gr[UNR][4], qv[UNR][4];
+    float4 ns[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gr[u][k] = qv[u][k] = 0.f;
+      if (j0 + u < n) {
+        const int64_t d = csc_dst[b + j0 + u];
+        ld4(GQ + d * 2 * D + c * 4, gr[u]);
+        ld4(GQ + d * 2 * D + D + c * 4, qv[u]);
+        ns[u] = __ldg(nst + d);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float l = 0.f, da = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        l = fmaf(kx[k], qv[u][k], l);
+        da = fmaf(gr[u][k], mv[k], da);
+      }
+      l = gsum_m<LPR>(l, gmask);
+      da = gsum_m<LPR>(da, gmask);
+      float alpha = (j0 + u < n) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
+      float dl = alpha * (da - ns[u].z);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        am[k] = fmaf(alpha, gr[u][k], am[k]);
+        ak[k] = fmaf(dl, qv[u][k], ak[k]);
+      }
+    }
+  }
+  TP* o = dKM + p * 2 * D;
+  st4(o + c * 4, ak[0], ak[1], ak[2], ak[3]);
+  st4(o + D + c * 4, am[0], am[1], am[2], am[3]);
+}
+
 // c_{v,r} = sum of dz over the CSR run of (dst v, rel r)   (RGAT destination-side weight terms)
 __global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
                             const float2* __restrict__ ebuf, float* __restrict__ csum) {
@@ -833,6 +925,26 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, c
     else
       launch("hgt_bwd_pair", k_hgt_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
              g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const bf16*>(Q), static_cast<bf16*>(dKM));
+  });
+}
+
+void hgt_bwd_pair_recompute(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                            const float* G, const float* out, void* GQ, float4* nst, void* dKM, cudaStream_t s) {
+  by_width(D, [&](auto Dc) {
+    constexpr int DD = decltype(Dc)::value;
+    if (dtype == F32) {
+      launch("hgt_node_prep", k_hgt_node_prep<float, DD>, pair_grid(g->N, D), dim3(256), 0, s, g->N, G,
+             static_cast<const float*>(Q), out, stats, static_cast<float*>(GQ), nst);
+      launch("hgt_bwd_pair", k_hgt_bwd_pair_rc<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
+             g->pair_csc_beg, g->pair_deg, g->csc_dst, static_cast<const float*>(KM), static_cast<const float*>(GQ),
+             (const float4*)nst, static_cast<float*>(dKM));
+    } else {
+      launch("hgt_node_prep", k_hgt_node_prep<bf16, DD>, pair_grid(g->N, D), dim3(256), 0, s, g->N, G,
+             static_cast<const bf16*>(Q), out, stats, static_cast<bf16*>(GQ), nst);
+      launch("hgt_bwd_pair", k_hgt_bwd_pair_rc<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
+             g->pair_csc_beg, g->pair_deg, g->csc_dst, static_cast<const bf16*>(KM), static_cast<const bf16*>(GQ),
+             (const float4*)nst, static_cast<bf16*>(dKM));
+    }
   });
 }
 

@@ -25,5 +25,7 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, 
                    void* dP, float* wsum, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
                   void* dKM, cudaStream_t s);
+void hgt_bwd_pair_recompute(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                            const float* G, const float* out, void* GQ, float4* nst, void* dKM, cudaStream_t s);
 void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
 }  // namespace rgnn
