@@ -9,8 +9,21 @@
 
 namespace rgnn {
 
-constexpr int SPLIT_THRESH = 1024;  // rows with more in-edges are split ...
-constexpr int SPLIT_CHUNK = 512;    // ... into chunks of this many edges
+// Work classes of destination rows and compact pairs (by their number of edges):
+constexpr int SPLIT_THRESH = 1024;  // heavy: more edges than this -> chunks of SPLIT_CHUNK, one warp each,
+constexpr int SPLIT_CHUNK = 512;    //        partial states merged afterwards
+constexpr int LIGHT_MAX = 64;       // light: at most this many edges -> one lane group each; else one warp
+
+// Edge-balanced work list over "ids" (destination rows or pairs) whose edges are the
+// contiguous range [begin, begin + deg) of the CSR (rows) or CSC (pairs).
+struct WorkPlan {
+  int4* items = nullptr;   // (id, edge begin, edge end, partial slot or -1)
+  int64_t n_warp = 0;      // items [0, n_warp): heavy chunks then medium ids, one warp per item
+  int64_t n_items = 0;     // items [n_warp, n_items): light ids, one lane group per item
+  int4* splits = nullptr;  // (id, first slot, number of slots, 0) for every heavy id
+  int64_t n_split = 0;
+  int64_t n_slots = 0;
+};
 
 // A contiguous row range [row0, row1) of one segment (weight index w).
 struct Tile {
@@ -65,13 +78,9 @@ struct rgnn_graph_s {
   int32_t* dpair_csr_beg = nullptr;  // [UD]
   int32_t* dpair_cnt = nullptr;      // [UD]
 
-  // edge-balanced destination work list (skewed in-degrees): rows with more than
-  // SPLIT_THRESH in-edges are cut into chunks of SPLIT_CHUNK edges, each a separate
-  // warp item writing a partial state to slot w; heavy chunks are listed first.
-  int4* row_items = nullptr;   // [n_items] (row, edge begin, edge end, slot or -1)
-  int64_t n_items = 0;
-  int4* split_rows = nullptr;  // [n_split] (row, first slot, number of slots, 0)
-  int64_t n_split = 0, n_slots = 0;
+  // edge-balanced work lists (skewed in-degrees and pair degrees), see rgnn::WorkPlan
+  rgnn::WorkPlan rows;   // destination rows over the dst-CSR
+  rgnn::WorkPlan pairs;  // compact pairs over the src-CSC
 
   // lazily computed RGCN norms (by kind): per CSR entry and per CSC entry
   std::map<int, std::pair<float*, float*>> norms;

@@ -222,37 +222,56 @@ void hist_prefix(Tmp& tmp, const int32_t* v, int64_t n, int64_t nbins, int32_t* 
 
 }  // namespace
 
-// Edge-balanced destination work list (see graph.cuh).  One-off host pass over row_ptr.
-void build_row_split(rgnn_graph_s* g, cudaStream_t s) {
-  const int64_t N = g->N;
-  std::vector<int32_t> rp(N + 1);
-  RGNN_CUDA(cudaMemcpyAsync(rp.data(), g->row_ptr, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  RGNN_CUDA(cudaStreamSynchronize(s));
-  std::vector<int4> heavy, light, splits;
+// Edge-balanced work list (graph.cuh WorkPlan) from per-id (begin, degree); one-off host pass.
+void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std::vector<int32_t>& deg,
+                     WorkPlan& wp, cudaStream_t s) {
+  std::vector<int4> heavy, medium, light, splits;
   int64_t slots = 0;
-  for (int64_t v = 0; v < N; ++v) {
-    int32_t b = rp[v], e = rp[v + 1];
-    if (e - b > SPLIT_THRESH) {
+  for (size_t id = 0; id < beg.size(); ++id) {
+    int32_t b = beg[id], e = beg[id] + deg[id];
+    if (deg[id] > SPLIT_THRESH) {
       int32_t n = 0;
       for (int32_t c = b; c < e; c += SPLIT_CHUNK, ++n)
-        heavy.push_back(make_int4((int)v, c, std::min(e, c + SPLIT_CHUNK), (int)(slots + n)));
-      splits.push_back(make_int4((int)v, (int)slots, n, 0));
+        heavy.push_back(make_int4((int)id, c, std::min(e, c + SPLIT_CHUNK), (int)(slots + n)));
+      splits.push_back(make_int4((int)id, (int)slots, n, 0));
       slots += n;
+    } else if (deg[id] > LIGHT_MAX) {
+      medium.push_back(make_int4((int)id, b, e, -1));
     } else {
-      light.push_back(make_int4((int)v, b, e, -1));
+      light.push_back(make_int4((int)id, b, e, -1));
     }
   }
+  wp.n_warp = (int64_t)(heavy.size() + medium.size());
+  heavy.insert(heavy.end(), medium.begin(), medium.end());
   heavy.insert(heavy.end(), light.begin(), light.end());
-  g->n_items = (int64_t)heavy.size();
-  g->n_split = (int64_t)splits.size();
-  g->n_slots = slots;
-  g->row_items = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(g->n_items, 1), s));
-  g->split_rows = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(g->n_split, 1), s));
-  if (g->n_items)
-    RGNN_CUDA(cudaMemcpyAsync(g->row_items, heavy.data(), heavy.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-  if (g->n_split)
-    RGNN_CUDA(cudaMemcpyAsync(g->split_rows, splits.data(), splits.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  wp.n_items = (int64_t)heavy.size();
+  wp.n_split = (int64_t)splits.size();
+  wp.n_slots = slots;
+  wp.items = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(wp.n_items, 1), s));
+  wp.splits = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(wp.n_split, 1), s));
+  if (wp.n_items)
+    RGNN_CUDA(cudaMemcpyAsync(wp.items, heavy.data(), heavy.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  if (wp.n_split)
+    RGNN_CUDA(cudaMemcpyAsync(wp.splits, splits.data(), splits.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
   RGNN_CUDA(cudaStreamSynchronize(s));  // host staging goes out of scope
+}
+
+void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
+  const int64_t N = g->N, U = g->U;
+  std::vector<int32_t> rp(N + 1), pb(U), pd(U);
+  RGNN_CUDA(cudaMemcpyAsync(rp.data(), g->row_ptr, (N + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (U) {
+    RGNN_CUDA(cudaMemcpyAsync(pb.data(), g->pair_csc_beg, U * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RGNN_CUDA(cudaMemcpyAsync(pd.data(), g->pair_deg, U * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  }
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> rb(N), rd(N);
+  for (int64_t v = 0; v < N; ++v) {
+    rb[v] = rp[v];
+    rd[v] = rp[v + 1] - rp[v];
+  }
+  build_work_plan(g, rb, rd, g->rows, s);
+  build_work_plan(g, pb, pd, g->pairs, s);
 }
 
 void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, const int32_t* rel_in,
@@ -426,7 +445,7 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   RGNN_CUDA(cudaStreamSynchronize(s));
   g->max_in_deg = (int64_t)h_stats[1];
   g->max_pair_deg = (int64_t)h_stats[2];
-  build_row_split(g, s);
+  build_work_plans(g, s);
 }
 
 }  // namespace rgnn

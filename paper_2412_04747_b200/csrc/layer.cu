@@ -134,8 +134,10 @@ struct BwdScratch {
 };
 
 void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
-  pt.acc = ar.take<float>(std::max<int64_t>(c.g->n_slots, 1) * c.D);
-  pt.stat = ar.take<float2>(std::max<int64_t>(c.g->n_slots, 1));
+  const int64_t rows = c.g->rows.n_slots * c.D;
+  const int64_t pairs = c.g->pairs.n_slots * (c.d->model == RGNN_HGT ? 2 * c.D : c.D);
+  pt.acc = ar.take<float>(std::max<int64_t>(std::max(rows, pairs), 1));
+  pt.stat = ar.take<float2>(std::max<int64_t>(std::max(c.g->rows.n_slots, c.g->pairs.n_slots), 1));
 }
 
 void layout_fwd_scratch(const Ctx& c, Arena& ar, FwdScratch& o) {
@@ -302,7 +304,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   if (model == RGNN_RGCN) {
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
     graph_norms(g, c.d->norm_kind, w->edge_norm, c.s, &cn, &xn);
-    rgcn_bwd_pair(g, c.dt, c.D, xn, G, sc.dP, c.s);
+    rgcn_bwd_pair(g, c.dt, c.D, xn, G, sc.dP, sc.pt, c.s);
     if (dX) {
       if (c.d->self_loop) {
         GemmArgs b;
@@ -325,7 +327,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
     rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, sc.ebuf, dXt, sc.pt, c.s);
-    rgat_bwd_pair(g, c.dt, c.D, sc.ebuf, G, w->a, sc.dP, sc.wsum, c.s);
+    rgat_bwd_pair(g, c.dt, c.D, sc.ebuf, G, w->a, sc.dP, sc.wsum, sc.pt, c.s);
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
@@ -347,8 +349,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
-    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, nullptr, sc.dQ, sc.pt, c.s);
-    hgt_bwd_pair_recompute(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.GQ, sc.nst, sc.dP, c.s);
+    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.pt, c.s);
+    hgt_bwd_pair(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
     if (dX) {
       GemmArgs q;
       q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;

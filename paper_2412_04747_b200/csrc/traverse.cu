@@ -1,22 +1,26 @@
 // Edge-traversal kernels.
 //
-// Forward, destination-major over the dst-CSR (one warp per destination row v):
+// Forward, destination-major over the dst-CSR:
 //   A3 edge logits (g-SDDMM; RGAT: LeakyReLU(s_p + x_v . y_r), lst:ir_example
 //      P:739-745 after reordering; HGT: K~_p . q_v with K~ pre-scaled by mu_r/sqrt(d)),
 //   A4 edge softmax (lst:ir_example P:730-738) as an online max/sum rescale,
 //   A5 attention- or norm-weighted aggregation of the compact pair rows (g-SpMM),
-// all fused, so logits and attention never touch HBM; only (m_v, sum_v) are saved.
-// The warp is split into EG = 32 / LPR edge groups of LPR lanes; a group owns one
-// edge at a time and each lane moves one 16-byte vector of the gathered row, so a
-// warp has EG rows in flight per step and UNR steps are unrolled.  Each group keeps
-// its own online-softmax state; the states are merged with shuffles at the end.
+// all fused: logits and attention never touch HBM, only (m_v, sum_v) are saved.
 //
-// Backward, destination-major (A6): recompute logits/alpha from (m_v, sum_v), the
-// softmax backward row term sum_e alpha_e dalpha_e = G_v . out_v, per-edge
-// (alpha_e, dl_e or dz_e) to a CSR-ordered buffer, dQ_v (HGT) or the t-path dX_v (RGAT).
-// Backward, pair-major over the src-CSC (A7): one group per compact pair p, summing
-// over its edges (contiguous in the CSC) -> dP_p / [dK~_p | dM_p].  No atomics.
+// Work is edge-balanced (graph.cuh WorkPlan): heavy rows are cut into 512-edge chunks
+// whose partial states are merged afterwards (k_merge_*), medium rows get one warp, and
+// light rows (<= 64 edges) get one group of LPR lanes.  A lane always moves one 16-byte
+// vector of a gathered row; in warp mode the EG = 32 / LPR groups stride over the row's
+// edges, each with its own online-softmax state, merged by shuffles at the end.  UNR
+// edges per group are loaded before they are used.
+//
+// Backward, destination-major (A6): recompute logits/alpha from (m_v, sum_v); the softmax
+// backward row term sum_e alpha_e dalpha_e = G_v . out_v; dQ_v (HGT) or the t-path dX_v and
+// per-edge (alpha_e, dz_e) (RGAT).  Backward, pair-major over the src-CSC (A7): per compact
+// pair p the edges are contiguous in the CSC -> dP_p / [dK~_p | dM_p].  No float atomics.
 #include <math_constants.h>
+
+#include <type_traits>
 
 #include "ops.cuh"
 #include "traverse.cuh"
@@ -30,7 +34,7 @@ template <class TP, int D>
 struct Geo {
   static constexpr int V = Vec<TP>::N;  // elements per lane-vector
   static constexpr int LPR = D / V;     // lanes per row
-  static constexpr int EG = 32 / LPR;   // edge groups per warp
+  static constexpr int EG = 32 / LPR;   // lane groups per warp
   static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "unsupported row width");
 };
 
@@ -57,8 +61,6 @@ __device__ __forceinline__ void ld4(const bf16* p, float* o) {
   o[0] = __uint_as_float(x.x << 16); o[1] = __uint_as_float(x.x & 0xffff0000u);
   o[2] = __uint_as_float(x.y << 16); o[3] = __uint_as_float(x.y & 0xffff0000u);
 }
-
-// store V floats / 4 floats into a row of the table type
 template <int V>
 __device__ __forceinline__ void st_tp(float* p, const float* v) { st_f32<V>(p, v); }
 template <int V>
@@ -71,19 +73,23 @@ __device__ __forceinline__ void st4(bf16* p, float a, float b, float c, float d)
   *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
 }
 
-// sum over the LPR lanes of one group
+// sum over the LPR lanes of one group (mask = the lanes executing this call)
 template <int LPR>
-__device__ __forceinline__ float gsum(float x) {
+__device__ __forceinline__ float gsum(float x, unsigned mask) {
 #pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  for (int o = LPR / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
   return x;
+}
+template <int LPR>
+__device__ __forceinline__ unsigned group_mask(int g) {
+  return LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (g * LPR);
 }
 
 __device__ __forceinline__ float safe_exp_diff(float a, float b) {  // exp(a - b), 0 when a = -inf
   return a == -CUDART_INF_F ? 0.f : __expf(a - b);
 }
 
-// Merge the online-softmax states of the EG groups (lanes with equal lane % LPR).
+// Merge the online-softmax states of the EG groups of a warp (lanes with equal lane % LPR).
 template <int LPR, int V>
 __device__ __forceinline__ void merge_groups(float& m, float& s, float* acc) {
 #pragma unroll
@@ -110,38 +116,61 @@ __device__ __forceinline__ void sum_groups(float* acc) {
     for (int k = 0; k < V; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
 }
 
+// Work-item bookkeeping shared by every kernel: warp mode (GROUP = false) gives one item to
+// the whole warp and lets its groups stride over the edges; group mode gives one item per
+// lane group.  init() returns false if this lane has no item (whole warp or whole group).
+template <bool GROUP, int LPR>
+struct Work {
+  static constexpr int EG = 32 / LPR;
+  int lane, g, c;
+  unsigned mask;
+  int first, step;
+  int4 item;
+  __device__ __forceinline__ bool init(int64_t n, const int4* __restrict__ items) {
+    lane = threadIdx.x & 31;
+    g = lane / LPR;
+    c = lane % LPR;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wi = GROUP ? w * EG + g : w;
+    mask = GROUP ? group_mask<LPR>(g) : 0xffffffffu;
+    first = GROUP ? 0 : g;
+    step = GROUP ? 1 : EG;
+    if (wi >= n) return false;
+    item = items[wi];
+    return true;
+  }
+  __device__ __forceinline__ bool writer() const { return GROUP || g == 0; }
+  __device__ __forceinline__ bool leader() const { return GROUP ? c == 0 : lane == 0; }
+};
+
 // ------------------------------------------------------------------ RGCN forward (A5)
 // out_v (+)= sum_e norm_e P[pair_e]     (Eq. 3.1; self-loop X W_0 already in out when accumulate)
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
                                                   const int32_t* __restrict__ csr_pair,
                                                   const float* __restrict__ norm, const TP* __restrict__ P,
                                                   float* __restrict__ out, bool accumulate) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wi >= n_items) return;
-  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
-  const int64_t v = item.x;
-  const int slot = item.w;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = item.y, e = item.z;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t v = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
-    const int i0 = base + g;
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     uint4 raw[UNR];
-    float w[UNR];
+    float wt[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      int i = i0 + u * EG;
-      w[u] = 0.f;
+      int i = i0 + u * w.step;
+      wt[u] = 0.f;
       raw[u] = make_uint4(0, 0, 0, 0);
       if (i < e) {
-        int p = csr_pair[i];
-        w[u] = norm[i];
-        raw[u] = ldg16(P + (int64_t)p * D + c * V);
+        wt[u] = norm[i];
+        raw[u] = ldg16(P + (int64_t)csr_pair[i] * D + c * V);
       }
     }
 #pragma unroll
@@ -149,54 +178,50 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n_items, const int4* _
       float x[V];
       cvt16<TP>(raw[u], x);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = fmaf(w[u], x[k], acc[k]);
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wt[u], x[k], acc[k]);
     }
   }
-  sum_groups<LPR, V>(acc);
-  if (slot >= 0) {  // chunk of a split row: partial sum, merged by k_merge_sum
-    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+  if (!GROUP) sum_groups<LPR, V>(acc);
+  if (!w.writer()) return;
+  if (slot >= 0) {  // chunk of a heavy row: partial sum, merged by k_merge_sum
+    st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
     return;
   }
-  if (g == 0) {
-    float* o = out + v * D + c * V;
-    if (accumulate) {
-      float prev[V];
-      ld_f32<V>(o, prev);
+  float* o = out + v * D + c * V;
+  if (accumulate) {
+    float prev[V];
+    ld_f32<V>(o, prev);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] += prev[k];
-    }
-    st_f32<V>(o, acc);
+    for (int k = 0; k < V; ++k) acc[k] += prev[k];
   }
+  st_f32<V>(o, acc);
 }
 
 // ------------------------------------------------------------------ HGT forward (A3+A4+A5)
 // KM row of pair p = [K~_p | M_p] (2D wide);  l_e = K~_p . q_v;  out_v = sum softmax(l)_e M_p
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
-                                                 const int32_t* __restrict__ csr_pair, const TP* __restrict__ KM,
-                                                 const TP* __restrict__ Q, float* __restrict__ out,
-                                                 float2* __restrict__ stats) {
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
+                                                 float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
+                                                 const TP* __restrict__ KM, const TP* __restrict__ Q,
+                                                 float* __restrict__ out, float2* __restrict__ stats) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wi >= n_items) return;
-  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
-  const int64_t v = item.x;
-  const int slot = item.w;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = item.y, e = item.z;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t v = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float q[V];
   cvt16<TP>(ldg16(Q + v * D + c * V), q);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
-    const int i0 = base + g;
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     uint4 rk[UNR], rm[UNR];
     bool ok[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      int i = i0 + u * EG;
+      int i = i0 + u * w.step;
       ok[u] = i < e;
       rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
       if (ok[u]) {
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n_items, const int4* __
       float d = 0.f;
 #pragma unroll
       for (int k = 0; k < V; ++k) d = fmaf(kx[k], q[k], d);
-      d = gsum<LPR>(d);
+      d = gsum<LPR>(d, w.mask);
       l[u] = ok[u] ? d : -CUDART_INF_F;
       mx = fmaxf(mx, l[u]);
     }
@@ -223,60 +248,57 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n_items, const int4* __
     for (int k = 0; k < V; ++k) acc[k] *= sc;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      float w = safe_exp_diff(l[u], mx);
-      s += w;
+      float wt = safe_exp_diff(l[u], mx);
+      s += wt;
       float mv[V];
       cvt16<TP>(rm[u], mv);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = fmaf(w, mv[k], acc[k]);
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wt, mv[k], acc[k]);
     }
     m = mx;
   }
-  merge_groups<LPR, V>(m, s, acc);
-  if (slot >= 0) {  // chunk of a split row: unnormalised state, merged by k_merge_softmax
-    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
-    if (lane == 0) pstat[slot] = make_float2(m, s);
+  if (!GROUP) merge_groups<LPR, V>(m, s, acc);
+  if (slot >= 0) {  // chunk of a heavy row: unnormalised state, merged by k_merge_softmax
+    if (w.writer()) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+    if (w.leader()) pstat[slot] = make_float2(m, s);
     return;
   }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
-  if (g == 0) st_f32<V>(out + v * D + c * V, acc);
-  if (lane == 0) stats[v] = make_float2(m, s);
+  if (w.writer()) st_f32<V>(out + v * D + c * V, acc);
+  if (w.leader()) stats[v] = make_float2(m, s);
 }
 
 // ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
 // z_e = s_p + x_v . y_r (reordered t-path), l = LeakyReLU(z), out_v = sum softmax(l)_e P_p.
-// Requires d_in == d_out == D (x_v chunk in registers).
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
-                                                  const int32_t* __restrict__ csr_pair,
+// Requires d_in == d_out == D (the x_v chunk lives in the same lanes as the row chunk).
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
+                                                  float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
                                                   const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                   const float* __restrict__ spair, const TP* __restrict__ X,
                                                   const float* __restrict__ y, float slope, float* __restrict__ out,
                                                   float2* __restrict__ stats) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wi >= n_items) return;
-  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
-  const int64_t v = item.x;
-  const int slot = item.w;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = item.y, e = item.z;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t v = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float x[V];
   cvt16<TP>(ldg16(X + v * D + c * V), x);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
-    const int i0 = base + g;
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     uint4 rp[UNR];
     float sp[UNR], yv[UNR][V];
     bool ok[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      int i = i0 + u * EG;
+      int i = i0 + u * w.step;
       ok[u] = i < e;
       rp[u] = make_uint4(0, 0, 0, 0);
       sp[u] = 0.f;
@@ -296,7 +318,7 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n_items, const int4* _
       float t = 0.f;
 #pragma unroll
       for (int k = 0; k < V; ++k) t = fmaf(x[k], yv[u][k], t);
-      t = gsum<LPR>(t);
+      t = gsum<LPR>(t, w.mask);
       float z = sp[u] + t;
       float lz = z > 0.f ? z : slope * z;
       l[u] = ok[u] ? lz : -CUDART_INF_F;
@@ -308,47 +330,43 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n_items, const int4* _
     for (int k = 0; k < V; ++k) acc[k] *= sc;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      float w = safe_exp_diff(l[u], mx);
-      s += w;
+      float wt = safe_exp_diff(l[u], mx);
+      s += wt;
       float pv[V];
       cvt16<TP>(rp[u], pv);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = fmaf(w, pv[k], acc[k]);
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wt, pv[k], acc[k]);
     }
     m = mx;
   }
-  merge_groups<LPR, V>(m, s, acc);
-  if (slot >= 0) {  // chunk of a split row: unnormalised state, merged by k_merge_softmax
-    if (g == 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
-    if (lane == 0) pstat[slot] = make_float2(m, s);
+  if (!GROUP) merge_groups<LPR, V>(m, s, acc);
+  if (slot >= 0) {
+    if (w.writer()) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+    if (w.leader()) pstat[slot] = make_float2(m, s);
     return;
   }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
-  if (g == 0) st_f32<V>(out + v * D + c * V, acc);
-  if (lane == 0) stats[v] = make_float2(m, s);
+  if (w.writer()) st_f32<V>(out + v * D + c * V, acc);
+  if (w.leader()) stats[v] = make_float2(m, s);
 }
 
 // ------------------------------------------------------------------ HGT backward, dst-major (A6)
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
-// dQ_v = sum_e dl_e K~_p ; ebuf[csr pos] = (alpha_e, dl_e)
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
-                                                     const int32_t* __restrict__ csr_pair,
+// dQ_v = sum_e dl_e K~_p   (layer dtype; heavy rows: fp32 partials merged by k_merge_sum)
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
+                                                     float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
-                                                     const float* __restrict__ out, float2* __restrict__ ebuf,
-                                                     TP* __restrict__ dQ) {
+                                                     const float* __restrict__ out, TP* __restrict__ dQ) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wi >= n_items) return;
-  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
-  const int64_t v = item.x;
-  const int slot = item.w;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = item.y, e = item.z;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t v = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float dq[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dq[k] = 0.f;
@@ -360,15 +378,15 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4
     float go = 0.f;
 #pragma unroll
     for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
-    go = gsum<LPR>(go);
+    go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
-    for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
-    const int i0 = base + g;
+    for (int base = b; base < e; base += w.step * UNR) {
+      const int i0 = base + w.first;
       uint4 rk[UNR], rm[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        int i = i0 + u * EG;
+        int i = i0 + u * w.step;
         rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
         if (i < e) {
           int64_t p = csr_pair[i];
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        int i = i0 + u * EG;
+        int i = i0 + u * w.step;
         float kx[V], mv[V];
         cvt16<TP>(rk[u], kx);
         cvt16<TP>(rm[u], mv);
@@ -388,31 +406,26 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n_items, const int4
           l = fmaf(kx[k], q[k], l);
           da = fmaf(gv[k], mv[k], da);
         }
-        l = gsum<LPR>(l);
-        da = gsum<LPR>(da);
-        float alpha = __expf(l - st.x) * inv;
-        float dl = alpha * (da - go);
-        if (i < e) {
+        l = gsum<LPR>(l, w.mask);
+        da = gsum<LPR>(da, w.mask);
+        float dl = (i < e) ? __expf(l - st.x) * inv * (da - go) : 0.f;
 #pragma unroll
-          for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
-          if (ebuf && c == 0) ebuf[i] = make_float2(alpha, dl);
-        }
+        for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
       }
     }
   }
-  sum_groups<LPR, V>(dq);
-  if (g == 0) {
-    if (slot >= 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, dq);
-    else st_tp<V>(dQ + v * D + c * V, dq);
-  }
+  if (!GROUP) sum_groups<LPR, V>(dq);
+  if (!w.writer()) return;
+  if (slot >= 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, dq);
+  else st_tp<V>(dQ + v * D + c * V, dq);
 }
 
 // ------------------------------------------------------------------ RGAT backward, dst-major (A6)
 // dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
 // dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path) ; ebuf[i] = (alpha_e, dz_e)
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
-                                                      const int32_t* __restrict__ csr_pair,
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
+                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
                                                       const float* __restrict__ y, float slope,
@@ -420,14 +433,11 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int
                                                       const float* __restrict__ Gr, const float* __restrict__ out,
                                                       float2* __restrict__ ebuf, float* __restrict__ dX) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
-  const int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wi >= n_items) return;
-  const int4 item = items[wi];  // (row, edge begin, edge end, partial slot or -1)
-  const int64_t v = item.x;
-  const int slot = item.w;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int b = item.y, e = item.z;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t v = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float dx[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dx[k] = 0.f;
@@ -439,16 +449,16 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int
     float go = 0.f;
 #pragma unroll
     for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
-    go = gsum<LPR>(go);
+    go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
-    for (int base = b; base < e; base += EG * UNR) {  // warp-uniform trip count (shuffles inside)
-    const int i0 = base + g;
+    for (int base = b; base < e; base += w.step * UNR) {
+      const int i0 = base + w.first;
       uint4 rp[UNR];
       float sp[UNR], yv[UNR][V];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        int i = i0 + u * EG;
+        int i = i0 + u * w.step;
         rp[u] = make_uint4(0, 0, 0, 0);
         sp[u] = 0.f;
 #pragma unroll
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        int i = i0 + u * EG;
+        int i = i0 + u * w.step;
         float pv[V];
         cvt16<TP>(rp[u], pv);
         float t = 0.f, da = 0.f;
@@ -472,8 +482,8 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int
           t = fmaf(x[k], yv[u][k], t);
           da = fmaf(gv[k], pv[k], da);
         }
-        t = gsum<LPR>(t);
-        da = gsum<LPR>(da);
+        t = gsum<LPR>(t, w.mask);
+        da = gsum<LPR>(da, w.mask);
         float z = sp[u] + t;
         float l = z > 0.f ? z : slope * z;
         float alpha = __expf(l - st.x) * inv;
@@ -486,78 +496,79 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n_items, const int
       }
     }
   }
-  sum_groups<LPR, V>(dx);
-  if (g == 0) st_f32<V>((slot >= 0 ? pacc + (int64_t)slot * D : dX + v * D) + c * V, dx);
+  if (!GROUP) sum_groups<LPR, V>(dx);
+  if (!w.writer()) return;
+  st_f32<V>((slot >= 0 ? pacc + (int64_t)slot * D : dX + v * D) + c * V, dx);
 }
 
 // ------------------------------------------------------------------ pair-major backward (A7)
-// One group of D/4 lanes per compact pair p; each lane owns 4 fp32 columns.
-template <int D>
-struct PGeo {
-  static constexpr int LPR = D / 4;
-  static constexpr int EG = 32 / LPR;
-};
+// One group of LPR = D/4 lanes per light pair, one warp per medium pair or heavy chunk;
+// each lane owns 4 fp32 columns.  The edges of pair p are csc[item.y, item.z).
 
 // RGCN: dP_p = sum_{e in p} norm_e G[d_e]
-template <class TO, int D>
-__global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
-                                                       const int32_t* __restrict__ pair_deg,
-                                                       const int32_t* __restrict__ csc_dst,
+template <class TO, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t n, const int4* __restrict__ items,
+                                                       float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                        const float* __restrict__ csc_norm,
                                                        const float* __restrict__ Gr, TO* __restrict__ dP) {
-  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
-  if (p >= U) return;
-  const int b = pair_beg[p], n = pair_deg[p];
+  constexpr int LPR = D / 4;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int j0 = 0; j0 < n; j0 += UNR) {
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     float4 gr[UNR];
-    float w[UNR];
+    float wt[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * w.step;
       gr[u] = make_float4(0, 0, 0, 0);
-      w[u] = 0.f;
-      if (j0 + u < n) {
-        int i = b + j0 + u;
-        w[u] = csc_norm[i];
+      wt[u] = 0.f;
+      if (i < e) {
+        wt[u] = csc_norm[i];
         gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
       }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      acc[0] = fmaf(w[u], gr[u].x, acc[0]); acc[1] = fmaf(w[u], gr[u].y, acc[1]);
-      acc[2] = fmaf(w[u], gr[u].z, acc[2]); acc[3] = fmaf(w[u], gr[u].w, acc[3]);
+      acc[0] = fmaf(wt[u], gr[u].x, acc[0]); acc[1] = fmaf(wt[u], gr[u].y, acc[1]);
+      acc[2] = fmaf(wt[u], gr[u].z, acc[2]); acc[3] = fmaf(wt[u], gr[u].w, acc[3]);
     }
   }
-  st4(dP + p * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
+  if (!GROUP) sum_groups<LPR, 4>(acc);
+  if (!w.writer()) return;
+  if (slot >= 0) st4(pacc + (int64_t)slot * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
+  else st4(dP + p * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
 }
 
 // RGAT: dP_p = sum alpha_e G[d_e] + (sum dz_e) a_r ; wsum_p = sum dz_e
-template <class TW, int D>
-__global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
-                                                       const int32_t* __restrict__ pair_deg,
+template <class TW, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
+                                                       float* __restrict__ pacc, float2* __restrict__ pstat,
                                                        const int32_t* __restrict__ csc_dst,
                                                        const int32_t* __restrict__ csc_rel,
                                                        const int32_t* __restrict__ csc2csr,
                                                        const float2* __restrict__ ebuf, const float* __restrict__ Gr,
                                                        const TW* __restrict__ avec, TW* __restrict__ dP,
                                                        float* __restrict__ wsum) {
-  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
-  if (p >= U) return;
-  const int b = pair_beg[p], n = pair_deg[p];
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, zs = 0.f;
-  for (int j0 = 0; j0 < n; j0 += UNR) {
+  constexpr int LPR = D / 4;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};  // 4 columns + sum dz
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     float4 gr[UNR];
     float2 ab[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * w.step;
       gr[u] = make_float4(0, 0, 0, 0);
       ab[u] = make_float2(0.f, 0.f);
-      if (j0 + u < n) {
-        int i = b + j0 + u;
+      if (i < e) {
         ab[u] = ebuf[csc2csr[i]];
         gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
       }
@@ -566,76 +577,31 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t U, const int32_t*
     for (int u = 0; u < UNR; ++u) {
       acc[0] = fmaf(ab[u].x, gr[u].x, acc[0]); acc[1] = fmaf(ab[u].x, gr[u].y, acc[1]);
       acc[2] = fmaf(ab[u].x, gr[u].z, acc[2]); acc[3] = fmaf(ab[u].x, gr[u].w, acc[3]);
-      zs += ab[u].y;
+      acc[4] += ab[u].y;
     }
+  }
+  if (!GROUP) sum_groups<LPR, 5>(acc);
+  if (!w.writer()) return;
+  if (slot >= 0) {
+    st4(pacc + (int64_t)slot * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
+    if (c == 0) pstat[slot] = make_float2(acc[4], 0.f);
+    return;
   }
   const int r = csc_rel[b];
   float a4[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) a4[k] = to_f(avec[(int64_t)r * D + c * 4 + k]);
+  const float zs = acc[4];
   st4(dP + p * D + c * 4, fmaf(zs, a4[0], acc[0]), fmaf(zs, a4[1], acc[1]), fmaf(zs, a4[2], acc[2]),
       fmaf(zs, a4[3], acc[3]));
   if (c == 0) wsum[p] = zs;
 }
 
-// HGT: dM_p = sum alpha_e G[d_e] ; dK~_p = sum dl_e q_{d_e} ; dKM_p = [dK~_p | dM_p]
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t U, const int32_t* __restrict__ pair_beg,
-                                                      const int32_t* __restrict__ pair_deg,
-                                                      const int32_t* __restrict__ csc_dst,
-                                                      const int32_t* __restrict__ csc2csr,
-                                                      const float2* __restrict__ ebuf, const float* __restrict__ Gr,
-                                                      const TP* __restrict__ Q, TP* __restrict__ dKM) {
-  constexpr int LPR = PGeo<D>::LPR, EG = PGeo<D>::EG;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
-  if (p >= U) return;
-  const int b = pair_beg[p], n = pair_deg[p];
-  float am[4] = {0.f, 0.f, 0.f, 0.f}, ak[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int j0 = 0; j0 < n; j0 += UNR) {
-    float4 gr[UNR];
-    float qv[UNR][4];
-    float2 ab[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      gr[u] = make_float4(0, 0, 0, 0);
-      ab[u] = make_float2(0.f, 0.f);
-      qv[u][0] = qv[u][1] = qv[u][2] = qv[u][3] = 0.f;
-      if (j0 + u < n) {
-        int i = b + j0 + u;
-        int64_t d = csc_dst[i];
-        ab[u] = ebuf[csc2csr[i]];
-        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + d * D + c * 4));
-        ld4(Q + d * D + c * 4, qv[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      am[0] = fmaf(ab[u].x, gr[u].x, am[0]); am[1] = fmaf(ab[u].x, gr[u].y, am[1]);
-      am[2] = fmaf(ab[u].x, gr[u].z, am[2]); am[3] = fmaf(ab[u].x, gr[u].w, am[3]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ak[k] = fmaf(ab[u].y, qv[u][k], ak[k]);
-    }
-  }
-  TP* o = dKM + p * 2 * D;
-  st4(o + c * 4, ak[0], ak[1], ak[2], ak[3]);
-  st4(o + D + c * 4, am[0], am[1], am[2], am[3]);
-}
-
-
-// ------------------------------------------------------------------ HGT pair-major backward, recomputing alpha
-// Per node (prep): GQ_v = [G_v | Q_v] in the table dtype, nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
-// Per pair p (one group of D/4 lanes): K~_p and M_p stay in registers; for each edge e of p (its CSC
-// segment) l_e = K~_p . Q_d, alpha_e = exp(l_e - m_d)/sum_d, dalpha_e = G_d . M_p,
-// dl_e = alpha_e (dalpha_e - G_d . out_d);  dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d.
-// One 2D-wide row gather + one 16-byte node record per edge; no per-edge buffer.
-template <int LPR>
-__device__ __forceinline__ float gsum_m(float x, unsigned mask) {
-#pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
-  return x;
-}
-
+// HGT, recomputing alpha per edge from a per-node record (no per-edge buffer):
+// prep:  GQ_v = [G_v | Q_v] in the table dtype, nst_v = (m_v, 1/sum_v, G_v . out_v, 0);
+// pair:  K~_p and M_p in registers; per edge e of p: l_e = K~_p . Q_d, alpha_e = exp(l_e - m_d)/sum_d,
+//        dalpha_e = G_d . M_p, dl_e = alpha_e (dalpha_e - G_d . out_d);
+//        dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d  ->  dKM_p = [dK~_p | dM_p].
 template <class TP, int D>
 __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* __restrict__ Gr,
                                                        const TP* __restrict__ Q, const float* __restrict__ out,
@@ -643,14 +609,13 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* _
                                                        float4* __restrict__ nst) {
   constexpr int LPR = D / 4, EG = 32 / LPR;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (g * LPR));
   const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
   if (v >= N) return;
   float4 gv = __ldg(reinterpret_cast<const float4*>(Gr + v * D + c * 4));
   float4 ov = __ldg(reinterpret_cast<const float4*>(out + v * D + c * 4));
   float qv[4];
   ld4(Q + v * D + c * 4, qv);
-  float go = gsum_m<LPR>(gv.x * ov.x + gv.y * ov.y + gv.z * ov.z + gv.w * ov.w, gmask);
+  float go = gsum<LPR>(gv.x * ov.x + gv.y * ov.y + gv.z * ov.z + gv.w * ov.w, group_mask<LPR>(g));
   st4(GQ + v * 2 * D + c * 4, gv.x, gv.y, gv.z, gv.w);
   st4(GQ + v * 2 * D + D + c * 4, qv[0], qv[1], qv[2], qv[3]);
   if (c == 0) {
@@ -659,32 +624,32 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* _
   }
 }
 
-template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_bwd_pair_rc(int64_t U, const int32_t* __restrict__ pair_beg,
-                                                         const int32_t* __restrict__ pair_deg,
-                                                         const int32_t* __restrict__ csc_dst,
-                                                         const TP* __restrict__ KM, const TP* __restrict__ GQ,
-                                                         const float4* __restrict__ nst, TP* __restrict__ dKM) {
-  constexpr int LPR = D / 4, EG = 32 / LPR;
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const unsigned gmask = (LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u) << (g * LPR));
-  const int64_t p = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
-  if (p >= U) return;
-  const int b = pair_beg[p], n = pair_deg[p];
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
+                                                      float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
+                                                      const TP* __restrict__ KM, const TP* __restrict__ GQ,
+                                                      const float4* __restrict__ nst, TP* __restrict__ dKM) {
+  constexpr int LPR = D / 4;
+  Work<GROUP, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float kx[4], mv[4];
   ld4(KM + p * 2 * D + c * 4, kx);
   ld4(KM + p * 2 * D + D + c * 4, mv);
-  float am[4] = {0.f, 0.f, 0.f, 0.f}, ak[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int j0 = 0; j0 < n; j0 += UNR) {
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // [dK~ 4 | dM 4]
+  for (int base = b; base < e; base += w.step * UNR) {
+    const int i0 = base + w.first;
     float gr[UNR][4], qv[UNR][4];
     float4 ns[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
+      int i = i0 + u * w.step;
       ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int k = 0; k < 4; ++k) gr[u][k] = qv[u][k] = 0.f;
-      if (j0 + u < n) {
-        const int64_t d = csc_dst[b + j0 + u];
+      if (i < e) {
+        const int64_t d = csc_dst[i];
         ld4(GQ + d * 2 * D + c * 4, gr[u]);
         ld4(GQ + d * 2 * D + D + c * 4, qv[u]);
         ns[u] = __ldg(nst + d);
@@ -698,20 +663,28 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair_rc(int64_t U, const int32_
         l = fmaf(kx[k], qv[u][k], l);
         da = fmaf(gr[u][k], mv[k], da);
       }
-      l = gsum_m<LPR>(l, gmask);
-      da = gsum_m<LPR>(da, gmask);
-      float alpha = (j0 + u < n) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
+      l = gsum<LPR>(l, w.mask);
+      da = gsum<LPR>(da, w.mask);
+      float alpha = (i0 + u * w.step < e) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
       float dl = alpha * (da - ns[u].z);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        am[k] = fmaf(alpha, gr[u][k], am[k]);
-        ak[k] = fmaf(dl, qv[u][k], ak[k]);
+        acc[k] = fmaf(dl, qv[u][k], acc[k]);
+        acc[4 + k] = fmaf(alpha, gr[u][k], acc[4 + k]);
       }
     }
   }
-  TP* o = dKM + p * 2 * D;
-  st4(o + c * 4, ak[0], ak[1], ak[2], ak[3]);
-  st4(o + D + c * 4, am[0], am[1], am[2], am[3]);
+  if (!GROUP) sum_groups<LPR, 8>(acc);
+  if (!w.writer()) return;
+  if (slot >= 0) {
+    float* o = pacc + (int64_t)slot * 2 * D;
+    st4(o + c * 4, acc[0], acc[1], acc[2], acc[3]);
+    st4(o + D + c * 4, acc[4], acc[5], acc[6], acc[7]);
+  } else {
+    TP* o = dKM + p * 2 * D;
+    st4(o + c * 4, acc[0], acc[1], acc[2], acc[3]);
+    st4(o + D + c * 4, acc[4], acc[5], acc[6], acc[7]);
+  }
 }
 
 // c_{v,r} = sum of dz over the CSR run of (dst v, rel r)   (RGAT destination-side weight terms)
@@ -724,10 +697,9 @@ __global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const i
   csum[j] = acc;
 }
 
-
-// ------------------------------------------------------------------ split-row merges
-// Rows cut into chunks (graph.cuh SPLIT_*) leave one partial state per chunk; one warp per
-// split row combines them in chunk order (deterministic).  Lane c owns columns 4c..4c+3.
+// ------------------------------------------------------------------ heavy-id merges
+// One warp per heavy id combines its chunks' partial states in chunk order (deterministic).
+// Lane c owns columns 4c..4c+3 of a W-wide row.
 template <int D>
 __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const int4* __restrict__ splits,
                                                        const float* __restrict__ pacc,
@@ -743,12 +715,12 @@ __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const in
   const bool act = lane * 4 < D;
   for (int i = 0; i < sp.z; ++i) {
     float2 st = pstat[sp.y + i];
-    float w = safe_exp_diff(st.x, m);
-    s = fmaf(st.y, w, s);
+    float wt = safe_exp_diff(st.x, m);
+    s = fmaf(st.y, wt, s);
     if (act) {
       float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
-      acc[0] = fmaf(w, a.x, acc[0]); acc[1] = fmaf(w, a.y, acc[1]);
-      acc[2] = fmaf(w, a.z, acc[2]); acc[3] = fmaf(w, a.w, acc[3]);
+      acc[0] = fmaf(wt, a.x, acc[0]); acc[1] = fmaf(wt, a.y, acc[1]);
+      acc[2] = fmaf(wt, a.z, acc[2]); acc[3] = fmaf(wt, a.w, acc[3]);
     }
   }
   float inv = s > 0.f ? 1.f / s : 0.f;
@@ -758,26 +730,55 @@ __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const in
   if (lane == 0) stats[sp.x] = make_float2(m, s);
 }
 
-template <int D, class TO>
+template <int W, class TO>
 __global__ void __launch_bounds__(256) k_merge_sum(int64_t n_split, const int4* __restrict__ splits,
                                                    const float* __restrict__ pacc, TO* __restrict__ out,
                                                    bool accumulate) {
   const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (j >= n_split) return;
   const int lane = threadIdx.x & 31;
-  if (lane * 4 >= D) return;
   const int4 sp = splits[j];
-  TO* o = out + (int64_t)sp.x * D + lane * 4;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  if (accumulate) {  // fp32 outputs only
-    float4 prev = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o));
-    acc[0] = prev.x; acc[1] = prev.y; acc[2] = prev.z; acc[3] = prev.w;
+  for (int col = lane * 4; col < W; col += 128) {
+    TO* o = out + (int64_t)sp.x * W + col;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (accumulate) {  // fp32 outputs only
+      float4 prev = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o));
+      acc[0] = prev.x; acc[1] = prev.y; acc[2] = prev.z; acc[3] = prev.w;
+    }
+    for (int i = 0; i < sp.z; ++i) {
+      float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * W + col);
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    }
+    st4(o, acc[0], acc[1], acc[2], acc[3]);
   }
+}
+
+// RGAT heavy pairs: dP_p = sum acc_i + (sum zs_i) a_r ; wsum_p = sum zs_i
+template <class TW, int D>
+__global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const int4* __restrict__ splits,
+                                                         const float* __restrict__ pacc,
+                                                         const float2* __restrict__ pstat,
+                                                         const int32_t* __restrict__ pair_csc_beg,
+                                                         const int32_t* __restrict__ csc_rel,
+                                                         const TW* __restrict__ avec, TW* __restrict__ dP,
+                                                         float* __restrict__ wsum) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= n_split) return;
+  const int lane = threadIdx.x & 31;
+  const int4 sp = splits[j];
+  float zs = 0.f;
+  for (int i = 0; i < sp.z; ++i) zs += pstat[sp.y + i].x;
+  if (lane == 0) wsum[sp.x] = zs;
+  if (lane * 4 >= D) return;
+  const int r = csc_rel[pair_csc_beg[sp.x]];
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int i = 0; i < sp.z; ++i) {
     float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
     acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
   }
-  st4(o, acc[0], acc[1], acc[2], acc[3]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = fmaf(zs, to_f(avec[(int64_t)r * D + lane * 4 + k]), acc[k]);
+  st4(dP + (int64_t)sp.x * D + lane * 4, acc[0], acc[1], acc[2], acc[3]);
 }
 
 template <class F>
@@ -791,7 +792,22 @@ void by_width(int D, F&& f) {
   }
 }
 
-inline dim3 warp_grid(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
+template <class F>
+void by_dtype(int dtype, F&& f) {
+  if (dtype == F32) f((float*)nullptr);
+  else f((bf16*)nullptr);
+}
+
+inline dim3 warps(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
+inline dim3 groups(int64_t n, int lpr) { return dim3(ceil_div(ceil_div(n, 32 / lpr) * (int64_t)32, 256)); }
+
+// Launch a work-plan kernel pair: warp mode over items [0, n_warp), group mode over the rest.
+template <class KW, class KG, class... Args>
+void launch_plan(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, cudaStream_t s, Args... args) {
+  launch(name, kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp, (const int4*)wp.items, args...);
+  const int64_t nl = wp.n_items - wp.n_warp;
+  launch(name, kg, groups(nl, lpr), dim3(256), 0, s, nl, (const int4*)(wp.items + wp.n_warp), args...);
+}
 
 }  // namespace
 
@@ -799,14 +815,13 @@ void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* nor
                        bool accumulate, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("rgcn_fwd_traverse", k_rgcn_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, norm, static_cast<const float*>(P), out, accumulate);
-    else
-      launch("rgcn_fwd_traverse", k_rgcn_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, norm, static_cast<const bf16*>(P), out, accumulate);
-    launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split, g->split_rows,
-           (const float*)pt.acc, out, accumulate);
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgcn_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_rgcn_fwd<TP, DD, false>, k_rgcn_fwd<TP, DD, true>,
+                  s, pt.acc, (const int32_t*)g->csr_pair, norm, static_cast<const TP*>(P), out, accumulate);
+    });
+    launch("merge_heavy_rows", k_merge_sum<DD, float>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+           (const int4*)g->rows.splits, (const float*)pt.acc, out, accumulate);
   });
 }
 
@@ -814,16 +829,14 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, c
                       float2* stats, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("hgt_fwd_traverse", k_hgt_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q),
-             out, stats);
-    else
-      launch("hgt_fwd_traverse", k_hgt_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q),
-             out, stats);
-    launch("merge_split_rows", k_merge_softmax<DD>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
-           g->split_rows, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("hgt_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_hgt_fwd<TP, DD, false>, k_hgt_fwd<TP, DD, true>,
+                  s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                  static_cast<const TP*>(Q), out, stats);
+    });
+    launch("merge_heavy_rows", k_merge_softmax<DD>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+           (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
@@ -831,36 +844,29 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
                        const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("rgat_fwd_traverse", k_rgat_fwd<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair,
-             static_cast<const float*>(X), y, slope, out, stats);
-    else
-      launch("rgat_fwd_traverse", k_rgat_fwd<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair,
-             static_cast<const bf16*>(X), y, slope, out, stats);
-    launch("merge_split_rows", k_merge_softmax<DD>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
-           g->split_rows, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_rgat_fwd<TP, DD, false>, k_rgat_fwd<TP, DD, true>,
+                  s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
+                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, out, stats);
+    });
+    launch("merge_heavy_rows", k_merge_softmax<DD>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+           (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, float2* ebuf, void* dQ, const Partial& pt, cudaStream_t s) {
+                 const float* G, const float* out, void* dQ, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32) {
-      launch("hgt_bwd_dst", k_hgt_bwd_dst<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const float*>(KM), static_cast<const float*>(Q),
-             stats, G, out, ebuf, static_cast<float*>(dQ));
-      launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
-             g->split_rows, (const float*)pt.acc, static_cast<float*>(dQ), false);
-    } else {
-      launch("hgt_bwd_dst", k_hgt_bwd_dst<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, static_cast<const bf16*>(KM), static_cast<const bf16*>(Q),
-             stats, G, out, ebuf, static_cast<bf16*>(dQ));
-      launch("merge_split_rows", k_merge_sum<DD, bf16>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split,
-             g->split_rows, (const float*)pt.acc, static_cast<bf16*>(dQ), false);
-    }
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false>,
+                  k_hgt_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                  static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ));
+      launch("merge_heavy_rows", k_merge_sum<DD, TP>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+             (const int4*)g->rows.splits, (const float*)pt.acc, static_cast<TP*>(dQ), false);
+    });
   });
 }
 
@@ -869,82 +875,63 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
                   float* dX, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("rgat_bwd_dst", k_rgat_bwd_dst<float, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const float*>(P), spair,
-             static_cast<const float*>(X), y, slope, stats, G, out, ebuf, dX);
-    else
-      launch("rgat_bwd_dst", k_rgat_bwd_dst<bf16, DD>, warp_grid(g->n_items), dim3(256), 0, s, g->n_items,
-             g->row_items, pt.acc, pt.stat, g->csr_pair, g->csr_rel, static_cast<const bf16*>(P), spair,
-             static_cast<const bf16*>(X), y, slope, stats, G, out, ebuf, dX);
-    launch("merge_split_rows", k_merge_sum<DD, float>, warp_grid(g->n_split), dim3(256), 0, s, g->n_split, g->split_rows,
-           (const float*)pt.acc, dX, false);
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_rgat_bwd_dst<TP, DD, false>,
+                  k_rgat_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
+                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, stats, G, out, ebuf, dX);
+    });
+    launch("merge_heavy_rows", k_merge_sum<DD, float>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+           (const int4*)g->rows.splits, (const float*)pt.acc, dX, false);
   });
 }
 
-static dim3 pair_grid(int64_t U, int D) {
-  int eg = 32 / (D / 4);
-  return dim3(ceil_div(ceil_div(U, eg) * (int64_t)32, 256));
-}
-
 void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
-                   cudaStream_t s) {
+                   const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("rgcn_bwd_pair", k_rgcn_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, csc_norm, G, static_cast<float*>(dP));
-    else
-      launch("rgcn_bwd_pair", k_rgcn_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, csc_norm, G, static_cast<bf16*>(dP));
+    by_dtype(dtype, [&](auto* tp) {
+      using TO = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgcn_bwd_pair", g->pairs, DD / 4, k_rgcn_bwd_pair<TO, DD, false>, k_rgcn_bwd_pair<TO, DD, true>, s,
+                  pt.acc, (const int32_t*)g->csc_dst, csc_norm, G, static_cast<TO*>(dP));
+      launch("merge_heavy_pairs", k_merge_sum<DD, TO>, warps(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
+             (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TO*>(dP), false);
+    });
   });
 }
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   void* dP, float* wsum, cudaStream_t s) {
+                   void* dP, float* wsum, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("rgat_bwd_pair", k_rgat_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
-             g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const float*>(a),
-             static_cast<float*>(dP), wsum);
-    else
-      launch("rgat_bwd_pair", k_rgat_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
-             g->pair_csc_beg, g->pair_deg, g->csc_dst, g->csc_rel, g->csc2csr, ebuf, G, static_cast<const bf16*>(a),
-             static_cast<bf16*>(dP), wsum);
+    by_dtype(dtype, [&](auto* tp) {
+      using TW = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgat_bwd_pair", g->pairs, DD / 4, k_rgat_bwd_pair<TW, DD, false>, k_rgat_bwd_pair<TW, DD, true>, s,
+                  pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc_rel,
+                  (const int32_t*)g->csc2csr, ebuf, G, static_cast<const TW*>(a), static_cast<TW*>(dP), wsum);
+      launch("merge_heavy_pairs", k_merge_rgat_pair<TW, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
+             g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
+             (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TW*>(a),
+             static_cast<TW*>(dP), wsum);
+    });
   });
 }
 
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
-                  void* dKM, cudaStream_t s) {
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                  const float* G, const float* out, void* GQ, float4* nst, void* dKM, const Partial& pt,
+                  cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32)
-      launch("hgt_bwd_pair", k_hgt_bwd_pair<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const float*>(Q), static_cast<float*>(dKM));
-    else
-      launch("hgt_bwd_pair", k_hgt_bwd_pair<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U, g->pair_csc_beg,
-             g->pair_deg, g->csc_dst, g->csc2csr, ebuf, G, static_cast<const bf16*>(Q), static_cast<bf16*>(dKM));
-  });
-}
-
-void hgt_bwd_pair_recompute(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                            const float* G, const float* out, void* GQ, float4* nst, void* dKM, cudaStream_t s) {
-  by_width(D, [&](auto Dc) {
-    constexpr int DD = decltype(Dc)::value;
-    if (dtype == F32) {
-      launch("hgt_node_prep", k_hgt_node_prep<float, DD>, pair_grid(g->N, D), dim3(256), 0, s, g->N, G,
-             static_cast<const float*>(Q), out, stats, static_cast<float*>(GQ), nst);
-      launch("hgt_bwd_pair", k_hgt_bwd_pair_rc<float, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
-             g->pair_csc_beg, g->pair_deg, g->csc_dst, static_cast<const float*>(KM), static_cast<const float*>(GQ),
-             (const float4*)nst, static_cast<float*>(dKM));
-    } else {
-      launch("hgt_node_prep", k_hgt_node_prep<bf16, DD>, pair_grid(g->N, D), dim3(256), 0, s, g->N, G,
-             static_cast<const bf16*>(Q), out, stats, static_cast<bf16*>(GQ), nst);
-      launch("hgt_bwd_pair", k_hgt_bwd_pair_rc<bf16, DD>, pair_grid(g->U, D), dim3(256), 0, s, g->U,
-             g->pair_csc_beg, g->pair_deg, g->csc_dst, static_cast<const bf16*>(KM), static_cast<const bf16*>(GQ),
-             (const float4*)nst, static_cast<bf16*>(dKM));
-    }
+    by_dtype(dtype, [&](auto* tp) {
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->N, DD / 4), dim3(256), 0, s, g->N, G,
+             static_cast<const TP*>(Q), out, stats, static_cast<TP*>(GQ), nst);
+      launch_plan("hgt_bwd_pair", g->pairs, DD / 4, k_hgt_bwd_pair<TP, DD, false>, k_hgt_bwd_pair<TP, DD, true>, s,
+                  pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ),
+                  (const float4*)nst, static_cast<TP*>(dKM));
+      launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, warps(g->pairs.n_split), dim3(256), 0, s,
+             g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
+    });
   });
 }
 

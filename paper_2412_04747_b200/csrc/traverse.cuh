@@ -3,7 +3,8 @@
 #include "graph.cuh"
 
 namespace rgnn {
-// Partial states of split rows (graph.cuh SPLIT_*): acc [n_slots][D] fp32, stat [n_slots] (m, sum).
+// Partial states of heavy (split) rows / pairs (graph.cuh WorkPlan):
+// acc [n_slots][width] fp32, stat [n_slots] ((m, sum) for softmax rows, (sum dz, 0) for RGAT pairs).
 struct Partial {
   float* acc = nullptr;
   float2* stat = nullptr;
@@ -15,17 +16,16 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, c
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                        const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s);
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, float2* ebuf, void* dQ, const Partial& pt, cudaStream_t s);
+                 const float* G, const float* out, void* dQ, const Partial& pt, cudaStream_t s);
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
                   float* dX, const Partial& pt, cudaStream_t s);
 void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
-                   cudaStream_t s);
+                   const Partial& pt, cudaStream_t s);
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   void* dP, float* wsum, cudaStream_t s);
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* Q,
-                  void* dKM, cudaStream_t s);
-void hgt_bwd_pair_recompute(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                            const float* G, const float* out, void* GQ, float4* nst, void* dKM, cudaStream_t s);
+                   void* dP, float* wsum, const Partial& pt, cudaStream_t s);
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+                  const float* G, const float* out, void* GQ, float4* nst, void* dKM, const Partial& pt,
+                  cudaStream_t s);
 void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
 }  // namespace rgnn
