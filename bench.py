@@ -370,22 +370,25 @@ def main():
     gi = G.info()
     U, E = gi["num_pairs"], gi["num_edges"]
     alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
-    kernels = {k: {"launches": v["launches"], "ms_per_launch": v["ms"] / max(v["launches"], 1),
-                   "share": v["ms"] / max(sum(x["ms"] for x in prof.values()), 1e-9)} for k, v in prof.items()}
+    # per-step view of each kernel label (a label may cover several launches per step, e.g. the
+    # warp-mode and group-mode launches of one traversal); bytes are per step as well
+    tot_ms = sum(x["ms"] for x in prof.values())
+    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                   "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}
+    for k in kernels:
+        if k in alg:
+            kernels[k]["algorithmic_bytes_per_step"] = int(alg[k])
+            kernels[k]["achieved_gbs"] = alg[k] / (kernels[k]["ms_per_step"] / 1e3) / 1e9
     dom = max((k for k in prof if k in alg), key=lambda k: prof[k]["ms"], default=None)
     roofline = None
     if dom is not None:
-        per_launch_bytes = alg[dom]
-        ms_l = prof[dom]["ms"] / prof[dom]["launches"]
-        achieved = per_launch_bytes / (ms_l / 1e3) / 1e9
+        ms_k = kernels[dom]["ms_per_step"]
+        achieved = alg[dom] / (ms_k / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
-                    "frac_of_8TBps": achieved / 8000.0, "algorithmic_bytes_per_launch": int(per_launch_bytes),
-                    "ms_per_launch": ms_l}
-        for k in kernels:
-            if k in alg:
-                pb = alg[k]
-                kernels[k]["achieved_gbs"] = pb / (kernels[k]["ms_per_launch"] / 1e3) / 1e9
+                    "frac_of_8TBps": achieved / 8000.0, "algorithmic_bytes_per_step": int(alg[dom]),
+                    "launches_per_step": kernels[dom]["launches_per_step"], "ms_per_step": ms_k,
+                    "note": "bytes and time per step of the kernel label (all its launches in one step)"}
         step_bytes = sum(alg.values())
         roofline["step_algorithmic_gb"] = step_bytes / 1e9
         roofline["step_achieved_gbs"] = step_bytes / (ms_per_step / 1e3) / 1e9
@@ -405,6 +408,7 @@ def main():
                        "nodes": g.num_nodes, "edges": int(g.num_edges), "pairs": int(info["num_pairs"]) if world == 1 else None,
                        "relations": g.num_rels, "node_types": g.num_node_types,
                        "compaction_ratio": info["compaction_ratio"], "max_in_degree": info["max_in_degree"],
+                       "max_pair_degree": info["max_pair_degree"],
                        "parallelism": f"dst-partition x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (X %.2f GB, pair table %.2f GB, index arrays %.2f GB)" % (
                            g.num_nodes * d * (2 if dtype == 'bf16' else 4) / 1e9,

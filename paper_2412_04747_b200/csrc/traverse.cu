@@ -607,83 +607,96 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* _
                                                        const TP* __restrict__ Q, const float* __restrict__ out,
                                                        const float2* __restrict__ stats, TP* __restrict__ GQ,
                                                        float4* __restrict__ nst) {
-  constexpr int LPR = D / 4, EG = 32 / LPR;
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
   const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
   if (v >= N) return;
-  float4 gv = __ldg(reinterpret_cast<const float4*>(Gr + v * D + c * 4));
-  float4 ov = __ldg(reinterpret_cast<const float4*>(out + v * D + c * 4));
-  float qv[4];
-  ld4(Q + v * D + c * 4, qv);
-  float go = gsum<LPR>(gv.x * ov.x + gv.y * ov.y + gv.z * ov.z + gv.w * ov.w, group_mask<LPR>(g));
-  st4(GQ + v * 2 * D + c * 4, gv.x, gv.y, gv.z, gv.w);
-  st4(GQ + v * 2 * D + D + c * 4, qv[0], qv[1], qv[2], qv[3]);
+  float gv[V], ov[V], qv[V];
+  ld_f32<V>(Gr + v * D + c * V, gv);
+  ld_f32<V>(out + v * D + c * V, ov);
+  cvt16<TP>(ldg16(Q + v * D + c * V), qv);
+  float go = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
+  go = gsum<LPR>(go, group_mask<LPR>(g));
+  st_tp<V>(GQ + v * 2 * D + c * V, gv);
+  st_tp<V>(GQ + v * 2 * D + D + c * V, qv);
   if (c == 0) {
     float2 st = stats[v];
     nst[v] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
   }
 }
 
+// One lane moves 16 bytes of the G half and 16 bytes of the Q half of a GQ row (V columns each).
 template <class TP, int D, bool GROUP>
 __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                       const TP* __restrict__ KM, const TP* __restrict__ GQ,
                                                       const float4* __restrict__ nst, TP* __restrict__ dKM) {
-  constexpr int LPR = D / 4;
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t p = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
-  float kx[4], mv[4];
-  ld4(KM + p * 2 * D + c * 4, kx);
-  ld4(KM + p * 2 * D + D + c * 4, mv);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // [dK~ 4 | dM 4]
+  float kx[V], mv[V];
+  cvt16<TP>(ldg16(KM + p * 2 * D + c * V), kx);
+  cvt16<TP>(ldg16(KM + p * 2 * D + D + c * V), mv);
+  float ak[V], am[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
   for (int base = b; base < e; base += w.step * UNR) {
     const int i0 = base + w.first;
-    float gr[UNR][4], qv[UNR][4];
+    uint4 rg[UNR], rq[UNR];
     float4 ns[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       int i = i0 + u * w.step;
       ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) gr[u][k] = qv[u][k] = 0.f;
+      rg[u] = rq[u] = make_uint4(0, 0, 0, 0);
       if (i < e) {
         const int64_t d = csc_dst[i];
-        ld4(GQ + d * 2 * D + c * 4, gr[u]);
-        ld4(GQ + d * 2 * D + D + c * 4, qv[u]);
+        rg[u] = ldg16(GQ + d * 2 * D + c * V);
+        rq[u] = ldg16(GQ + d * 2 * D + D + c * V);
         ns[u] = __ldg(nst + d);
       }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
+      float gr[V], qv[V];
+      cvt16<TP>(rg[u], gr);
+      cvt16<TP>(rq[u], qv);
       float l = 0.f, da = 0.f;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        l = fmaf(kx[k], qv[u][k], l);
-        da = fmaf(gr[u][k], mv[k], da);
+      for (int k = 0; k < V; ++k) {
+        l = fmaf(kx[k], qv[k], l);
+        da = fmaf(gr[k], mv[k], da);
       }
       l = gsum<LPR>(l, w.mask);
       da = gsum<LPR>(da, w.mask);
       float alpha = (i0 + u * w.step < e) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
       float dl = alpha * (da - ns[u].z);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[k] = fmaf(dl, qv[u][k], acc[k]);
-        acc[4 + k] = fmaf(alpha, gr[u][k], acc[4 + k]);
+      for (int k = 0; k < V; ++k) {
+        ak[k] = fmaf(dl, qv[k], ak[k]);
+        am[k] = fmaf(alpha, gr[k], am[k]);
       }
     }
   }
-  if (!GROUP) sum_groups<LPR, 8>(acc);
+  if (!GROUP) {
+    sum_groups<LPR, V>(ak);
+    sum_groups<LPR, V>(am);
+  }
   if (!w.writer()) return;
   if (slot >= 0) {
     float* o = pacc + (int64_t)slot * 2 * D;
-    st4(o + c * 4, acc[0], acc[1], acc[2], acc[3]);
-    st4(o + D + c * 4, acc[4], acc[5], acc[6], acc[7]);
+    st_f32<V>(o + c * V, ak);
+    st_f32<V>(o + D + c * V, am);
   } else {
     TP* o = dKM + p * 2 * D;
-    st4(o + c * 4, acc[0], acc[1], acc[2], acc[3]);
-    st4(o + D + c * 4, acc[4], acc[5], acc[6], acc[7]);
+    st_tp<V>(o + c * V, ak);
+    st_tp<V>(o + D + c * V, am);
   }
 }
 
@@ -924,9 +937,10 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->N, DD / 4), dim3(256), 0, s, g->N, G,
+      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->N, Geo<TP, DD>::LPR), dim3(256), 0, s, g->N, G,
              static_cast<const TP*>(Q), out, stats, static_cast<TP*>(GQ), nst);
-      launch_plan("hgt_bwd_pair", g->pairs, DD / 4, k_hgt_bwd_pair<TP, DD, false>, k_hgt_bwd_pair<TP, DD, true>, s,
+      launch_plan("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false>,
+                  k_hgt_bwd_pair<TP, DD, true>, s,
                   pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ),
                   (const float4*)nst, static_cast<TP*>(dKM));
       launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, warps(g->pairs.n_split), dim3(256), 0, s,
