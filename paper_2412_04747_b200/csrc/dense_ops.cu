@@ -227,7 +227,7 @@ __global__ void k_hgt_fold(int R, int T, int d_in, int d, const TW* Wk, const TW
                            const float* mu, float* F, TW* Fdt) {
   int rt = blockIdx.x, r = rt / T, t = rt % T;
   float c = mu[r] * rsqrtf((float)d);
-  for (int idx = threadIdx.x; idx < d_in * 2 * d; idx += blockDim.x) {
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < d_in * 2 * d; idx += blockDim.x * gridDim.y) {
     int k = idx / (2 * d), n2 = idx % (2 * d);
     bool key = n2 < d;
     int n = key ? n2 : n2 - d;
@@ -389,11 +389,11 @@ void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b
 void hgt_fold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
               const float* mu, int dtype, float* F, void* Fdt, cudaStream_t s) {
   if (dtype == F32)
-    launch("hgt_fold", k_hgt_fold<float>, dim3(R * T), dim3(256), 0, s, R, T, d_in, d, static_cast<const float*>(Wk),
+    launch("hgt_fold", k_hgt_fold<float>, dim3(R * T, ceil_div(d_in * 2 * d, 256)), dim3(256), 0, s, R, T, d_in, d, static_cast<const float*>(Wk),
            static_cast<const float*>(Wv), static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, F,
            static_cast<float*>(nullptr));
   else
-    launch("hgt_fold", k_hgt_fold<bf16>, dim3(R * T), dim3(256), 0, s, R, T, d_in, d, static_cast<const bf16*>(Wk),
+    launch("hgt_fold", k_hgt_fold<bf16>, dim3(R * T, ceil_div(d_in * 2 * d, 256)), dim3(256), 0, s, R, T, d_in, d, static_cast<const bf16*>(Wk),
            static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, F,
            static_cast<bf16*>(Fdt));
 }

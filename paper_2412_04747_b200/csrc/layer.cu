@@ -349,8 +349,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
-    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.pt, c.s);
-    hgt_bwd_pair(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
+    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst, sc.pt, c.s);
+    hgt_bwd_pair(g, c.dt, c.D, sv.P, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
     if (dX) {
       GemmArgs q;
       q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;

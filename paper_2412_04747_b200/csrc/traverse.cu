@@ -28,7 +28,8 @@
 namespace rgnn {
 namespace {
 
-constexpr int UNR = 4;
+constexpr int UNR = 4;    // edges per group loaded ahead (dst-major and pair kernels)
+constexpr int UNR_P = 2;  // HGT pair kernel: two 16-byte row halves + a node record per edge
 
 template <class TP, int D>
 struct Geo {
@@ -360,7 +361,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
-                                                     const float* __restrict__ out, TP* __restrict__ dQ) {
+                                                     const float* __restrict__ out, TP* __restrict__ dQ,
+                                                     TP* __restrict__ GQ, float4* __restrict__ nst) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
@@ -381,6 +383,11 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
     go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
+    if (slot < 0 && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
+      st_tp<V>(GQ + v * 2 * D + c * V, gv);
+      st_tp<V>(GQ + v * 2 * D + D + c * V, q);
+      if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
+    }
     for (int base = b; base < e; base += w.step * UNR) {
       const int i0 = base + w.first;
       uint4 rk[UNR], rm[UNR];
@@ -603,15 +610,17 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t n, const int4* __
 //        dalpha_e = G_d . M_p, dl_e = alpha_e (dalpha_e - G_d . out_d);
 //        dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d  ->  dKM_p = [dK~_p | dM_p].
 template <class TP, int D>
-__global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* __restrict__ Gr,
+__global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __restrict__ rows,
+                                                       const float* __restrict__ Gr,
                                                        const TP* __restrict__ Q, const float* __restrict__ out,
                                                        const float2* __restrict__ stats, TP* __restrict__ GQ,
                                                        float4* __restrict__ nst) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
-  const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
-  if (v >= N) return;
+  const int64_t j = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (j >= n) return;
+  const int64_t v = rows[j].x;
   float gv[V], ov[V], qv[V];
   ld_f32<V>(Gr + v * D + c * V, gv);
   ld_f32<V>(out + v * D + c * V, ov);
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t N, const float* _
 
 // One lane moves 16 bytes of the G half and 16 bytes of the Q half of a GQ row (V columns each).
 template <class TP, int D, bool GROUP>
-__global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
+__global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                       const TP* __restrict__ KM, const TP* __restrict__ GQ,
                                                       const float4* __restrict__ nst, TP* __restrict__ dKM) {
@@ -646,12 +655,12 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t n, const int4* __r
   float ak[V], am[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-  for (int base = b; base < e; base += w.step * UNR) {
+  for (int base = b; base < e; base += w.step * UNR_P) {
     const int i0 = base + w.first;
-    uint4 rg[UNR], rq[UNR];
-    float4 ns[UNR];
+    uint4 rg[UNR_P], rq[UNR_P];
+    float4 ns[UNR_P];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+    for (int u = 0; u < UNR_P; ++u) {
       int i = i0 + u * w.step;
       ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       rg[u] = rq[u] = make_uint4(0, 0, 0, 0);
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_pair(int64_t n, const int4* __r
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+    for (int u = 0; u < UNR_P; ++u) {
       float gr[V], qv[V];
       cvt16<TP>(rg[u], gr);
       cvt16<TP>(rq[u], qv);
@@ -711,22 +720,29 @@ __global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const i
 }
 
 // ------------------------------------------------------------------ heavy-id merges
-// One warp per heavy id combines its chunks' partial states in chunk order (deterministic).
-// Lane c owns columns 4c..4c+3 of a W-wide row.
+// One CTA per heavy id: warp w folds chunks w, w+8, ... of the id (lane c owns columns 4c..4c+3
+// of a W-wide row, looping over W in steps of 128); the 8 warp results are then combined in warp
+// order through shared memory.  Fixed orders throughout: deterministic.
 template <int D>
 __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const int4* __restrict__ splits,
                                                        const float* __restrict__ pacc,
                                                        const float2* __restrict__ pstat, float* __restrict__ out,
                                                        float2* __restrict__ stats) {
-  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (j >= n_split) return;
-  const int lane = threadIdx.x & 31;
-  const int4 sp = splits[j];
+  __shared__ float sm_m[8], sm_s[8];
+  __shared__ __align__(16) float sm_acc[8][D];
+  const int4 sp = splits[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   float m = -CUDART_INF_F;
-  for (int i = 0; i < sp.z; ++i) m = fmaxf(m, pstat[sp.y + i].x);
+  for (int i = tid; i < sp.z; i += 256) m = fmaxf(m, pstat[sp.y + i].x);
+  m = warp_max(m);
+  if (lane == 0) sm_m[warp] = m;
+  __syncthreads();
+  m = sm_m[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) m = fmaxf(m, sm_m[k]);
   float s = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
   const bool act = lane * 4 < D;
-  for (int i = 0; i < sp.z; ++i) {
+  for (int i = warp; i < sp.z; i += 8) {
     float2 st = pstat[sp.y + i];
     float wt = safe_exp_diff(st.x, m);
     s = fmaf(st.y, wt, s);
@@ -736,33 +752,56 @@ __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const in
       acc[2] = fmaf(wt, a.z, acc[2]); acc[3] = fmaf(wt, a.w, acc[3]);
     }
   }
-  float inv = s > 0.f ? 1.f / s : 0.f;
-  if (act)
-    *reinterpret_cast<float4*>(out + (int64_t)sp.x * D + lane * 4) =
-        make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-  if (lane == 0) stats[sp.x] = make_float2(m, s);
+  __syncthreads();
+  if (lane == 0) sm_s[warp] = s;
+  if (act) *reinterpret_cast<float4*>(&sm_acc[warp][lane * 4]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  __syncthreads();
+  if (warp == 0) {
+    float st = 0.f, a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      st += sm_s[k];
+      if (act)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a4[j] += sm_acc[k][lane * 4 + j];
+    }
+    float inv = st > 0.f ? 1.f / st : 0.f;
+    if (act)
+      *reinterpret_cast<float4*>(out + (int64_t)sp.x * D + lane * 4) =
+          make_float4(a4[0] * inv, a4[1] * inv, a4[2] * inv, a4[3] * inv);
+    if (lane == 0) stats[sp.x] = make_float2(m, st);
+  }
 }
 
 template <int W, class TO>
 __global__ void __launch_bounds__(256) k_merge_sum(int64_t n_split, const int4* __restrict__ splits,
                                                    const float* __restrict__ pacc, TO* __restrict__ out,
                                                    bool accumulate) {
-  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (j >= n_split) return;
-  const int lane = threadIdx.x & 31;
-  const int4 sp = splits[j];
+  __shared__ __align__(16) float sm_acc[8][W];
+  const int4 sp = splits[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = lane * 4; col < W; col += 128) {
-    TO* o = out + (int64_t)sp.x * W + col;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    if (accumulate) {  // fp32 outputs only
-      float4 prev = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o));
-      acc[0] = prev.x; acc[1] = prev.y; acc[2] = prev.z; acc[3] = prev.w;
-    }
-    for (int i = 0; i < sp.z; ++i) {
+    for (int i = warp; i < sp.z; i += 8) {
       float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * W + col);
       acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
     }
-    st4(o, acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(&sm_acc[warp][col]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  for (int col = lane * 4; col < W; col += 128) {
+    TO* o = out + (int64_t)sp.x * W + col;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (accumulate) {  // fp32 outputs only
+      float4 prev = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(o));
+      a4[0] = prev.x; a4[1] = prev.y; a4[2] = prev.z; a4[3] = prev.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a4[j] += sm_acc[k][col + j];
+    st4(o, a4[0], a4[1], a4[2], a4[3]);
   }
 }
 
@@ -833,7 +872,7 @@ void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* nor
       launch_plan("rgcn_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_rgcn_fwd<TP, DD, false>, k_rgcn_fwd<TP, DD, true>,
                   s, pt.acc, (const int32_t*)g->csr_pair, norm, static_cast<const TP*>(P), out, accumulate);
     });
-    launch("merge_heavy_rows", k_merge_sum<DD, float>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+    launch("merge_heavy_rows", k_merge_sum<DD, float>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, out, accumulate);
   });
 }
@@ -848,7 +887,7 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, c
                   s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
                   static_cast<const TP*>(Q), out, stats);
     });
-    launch("merge_heavy_rows", k_merge_softmax<DD>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+    launch("merge_heavy_rows", k_merge_softmax<DD>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
@@ -863,21 +902,25 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
                   s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
                   static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, out, stats);
     });
-    launch("merge_heavy_rows", k_merge_softmax<DD>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+    launch("merge_heavy_rows", k_merge_softmax<DD>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, void* dQ, const Partial& pt, cudaStream_t s) {
+                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
+                 cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       launch_plan("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false>,
                   k_hgt_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
-                  static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ));
-      launch("merge_heavy_rows", k_merge_sum<DD, TP>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+                  static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ), static_cast<TP*>(GQ), nst);
+      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
+             g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
+             static_cast<TP*>(GQ), nst);
+      launch("merge_heavy_rows", k_merge_sum<DD, TP>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
              (const int4*)g->rows.splits, (const float*)pt.acc, static_cast<TP*>(dQ), false);
     });
   });
@@ -894,7 +937,7 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
                   k_rgat_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
                   static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, stats, G, out, ebuf, dX);
     });
-    launch("merge_heavy_rows", k_merge_sum<DD, float>, warps(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+    launch("merge_heavy_rows", k_merge_sum<DD, float>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, dX, false);
   });
 }
@@ -907,7 +950,7 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
       using TO = std::remove_pointer_t<decltype(tp)>;
       launch_plan("rgcn_bwd_pair", g->pairs, DD / 4, k_rgcn_bwd_pair<TO, DD, false>, k_rgcn_bwd_pair<TO, DD, true>, s,
                   pt.acc, (const int32_t*)g->csc_dst, csc_norm, G, static_cast<TO*>(dP));
-      launch("merge_heavy_pairs", k_merge_sum<DD, TO>, warps(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
+      launch("merge_heavy_pairs", k_merge_sum<DD, TO>, dim3(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
              (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TO*>(dP), false);
     });
   });
@@ -930,20 +973,17 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, 
   });
 }
 
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                  const float* G, const float* out, void* GQ, float4* nst, void* dKM, const Partial& pt,
-                  cudaStream_t s) {
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
+                  void* dKM, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->N, Geo<TP, DD>::LPR), dim3(256), 0, s, g->N, G,
-             static_cast<const TP*>(Q), out, stats, static_cast<TP*>(GQ), nst);
       launch_plan("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false>,
                   k_hgt_bwd_pair<TP, DD, true>, s,
-                  pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ),
-                  (const float4*)nst, static_cast<TP*>(dKM));
-      launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, warps(g->pairs.n_split), dim3(256), 0, s,
+                  pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ), nst,
+                  static_cast<TP*>(dKM));
+      launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
     });
   });

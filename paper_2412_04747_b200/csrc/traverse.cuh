@@ -15,8 +15,11 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, c
                       float2* stats, const Partial& pt, cudaStream_t s);
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                        const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s);
+// also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) of every
+// destination with in-edges (read by hgt_bwd_pair)
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, void* dQ, const Partial& pt, cudaStream_t s);
+                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
+                 cudaStream_t s);
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
                   float* dX, const Partial& pt, cudaStream_t s);
@@ -24,8 +27,7 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
                    const Partial& pt, cudaStream_t s);
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
                    void* dP, float* wsum, const Partial& pt, cudaStream_t s);
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
-                  const float* G, const float* out, void* GQ, float4* nst, void* dKM, const Partial& pt,
-                  cudaStream_t s);
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
+                  void* dKM, const Partial& pt, cudaStream_t s);
 void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
 }  // namespace rgnn
