@@ -77,11 +77,13 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["gemm_nodes_fwd"] = N * (d_in * b + d * b)
         out["hgt_fwd_traverse"] = E * (4 + 2 * d * b) + N * (8 + d * b + 4 * d + 8)
         # backward tables (dQ, [dK~|dM]) are stored in the layer dtype (b bytes)
-        out["hgt_bwd_dst"] = E * (4 + 2 * d * b + 8) + N * (8 + d * b + 4 * d + 4 * d + 8 + d * b)
-        out["hgt_bwd_pair"] = E * (4 + 4 + 8 + 4 * d + d * b) + U * (8 + 2 * d * b)
-        out["gemm_nodes_dx"] = N * (d * b + 4 * d_in)
+        # A6 also writes the node record [G_v | Q_v] (2d*b) + (m, 1/sum, G.out) (16 B) per node
+        out["hgt_bwd_dst"] = E * (4 + 2 * d * b) + N * (16 + d * b + 4 * d + 4 * d + 8 + d * b + 2 * d * b + 16)
+        # A7 per edge: CSC dst index, the [G|Q] row of the destination, its 16-B record; per pair: KM row, dKM row
+        out["hgt_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 2 * d * b + 2 * d * b)
+        # node dX GEMM with the per-source reduction of the pair dX rows fused into its epilogue
+        out["gemm_nodes_dx"] = N * (d * b + 4 * d_in + 8) + U * (4 + 4 * d_in)
         out["gemm_pairs_dx"] = U * (2 * d * b + 4 * d_in)
-        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + 2 * d * b)
         out["wgrad_nodes"] = N * (d_in * b + d * b)
     elif model == "rgat":

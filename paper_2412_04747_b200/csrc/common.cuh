@@ -88,6 +88,7 @@ struct Arena {
 // Every kernel launch goes through launch(); with profiling on, CUDA events
 // bracket it on its stream (rgnn_profile_*).
 void profile_begin(const char* name, cudaStream_t s, int* slot);
+const char* intern(const std::string& name);  // stable C string for profile labels
 void profile_end(int slot, cudaStream_t s);
 void count_launch();
 
@@ -104,6 +105,11 @@ void launch(const char* name, Kernel k, dim3 grid, dim3 block, size_t smem, cuda
 }
 
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+// Fork/join a per-thread side stream off `s` so two independent launches overlap (e.g. the
+// warp-mode and group-mode halves of a traversal).  Capture-safe (events only).
+cudaStream_t fork_side(cudaStream_t s);
+void join_side(cudaStream_t s);
 
 // ------------------------------------------------------------------ element types
 typedef __nv_bfloat16 bf16;

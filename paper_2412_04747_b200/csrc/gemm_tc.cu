@@ -138,7 +138,9 @@ template <class TY, int N, int KB>
 __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles, const bf16* __restrict__ A,
                                                  const int32_t* __restrict__ gather, const bf16* __restrict__ Bt,
                                                  TY* __restrict__ Y, const float* __restrict__ dotvec,
-                                                 float* __restrict__ dotout) {
+                                                 float* __restrict__ dotout, const int32_t* __restrict__ red_ptr,
+                                                 const int32_t* __restrict__ red_list,
+                                                 const float* __restrict__ red_rows) {
   constexpr int K = KB * 64;
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   constexpr uint32_t A_BYTES = 128 * 128;  // per K block
@@ -213,6 +215,16 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
     if (dotvec) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
+    }
+    if (red_ptr && valid) {  // fused per-row reduction of gathered fp32 rows
+      for (int j = red_ptr[row], je = red_ptr[row + 1]; j < je; ++j) {
+        const float* rr = red_rows + (int64_t)red_list[j] * N + c0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 x = __ldg(reinterpret_cast<const float4*>(rr + i));
+          v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
+        }
+      }
     }
     if (valid) store_row32(Y + row * N + c0, v);
   }
@@ -382,7 +394,7 @@ void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
     attr_set = true;
   }
   launch(a.name, k, dim3(a.ntiles), dim3(128), smem, s, a.tiles, static_cast<const bf16*>(a.A), a.gather, Bt,
-         static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+         static_cast<TY*>(a.Y), a.dotvec, a.dotout, a.red_ptr, a.red_list, a.red_rows);
 }
 
 template <class TY, int KB>

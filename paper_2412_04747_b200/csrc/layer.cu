@@ -205,19 +205,21 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
 }
 
 // ---------------------------------------------------------------- GEMM selection
-void gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
+// Returns true when the tcgen05 kernel ran (it honours the fused row reduction; SIMT does not).
+bool gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
   bool want_tc = c.d->gemm_impl == 2 || (c.d->gemm_impl == 0 && c.dt == BF16);
   if (want_tc && gemm_tc_supported(a)) {
     const Plan& p = plan(c.g, sg, TC_ROWS, c.s);
     a.tiles = p.tiles;
     a.ntiles = p.count;
     gemm_tc(a, c.s);
-    return;
+    return true;
   }
   const Plan& p = plan(c.g, sg, GEMM_ROWS, c.s);
   a.tiles = p.tiles;
   a.ntiles = p.count;
   gemm_simt(a, c.s);
+  return false;
 }
 
 void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, const int32_t* gather, const void* Bm,
@@ -352,12 +354,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst, sc.pt, c.s);
     hgt_bwd_pair(g, c.dt, c.D, sv.P, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
     if (dX) {
-      GemmArgs q;
-      q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
-      q.Y = dX; q.y_dtype = F32; q.N = c.Din;
-      q.num_w = g->T; q.bt_scratch = sc.bt;
-      q.name = "gemm_nodes_dx";
-      gemm(c, seg_node_type(g), q);
+      // per-pair rows first, then the node GEMM whose epilogue adds them per source (tcgen05 path)
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = 2 * c.D; a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
       a.transB = true;
@@ -365,7 +362,14 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rt(g), a);
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
+      GemmArgs q;
+      q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
+      q.Y = dX; q.y_dtype = F32; q.N = c.Din;
+      q.num_w = g->T; q.bt_scratch = sc.bt;
+      q.red_ptr = g->src_pair_ptr; q.red_list = g->src_pairs; q.red_rows = sc.dXp;
+      q.name = "gemm_nodes_dx";
+      if (!gemm(c, seg_node_type(g), q))
+        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
     }
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {

@@ -35,6 +35,41 @@ void Allocator::put(void* p, cudaStream_t s) const {
   else cudaFreeAsync(p, s);
 }
 
+struct Side {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+static thread_local Side g_side;
+
+cudaStream_t fork_side(cudaStream_t s) {
+  int dev = 0;
+  RGNN_CUDA(cudaGetDevice(&dev));
+  if (g_side.stream == nullptr || g_side.device != dev) {
+    RGNN_CUDA(cudaStreamCreateWithFlags(&g_side.stream, cudaStreamNonBlocking));
+    RGNN_CUDA(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
+    RGNN_CUDA(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
+    g_side.device = dev;
+  }
+  RGNN_CUDA(cudaEventRecord(g_side.fork, s));
+  RGNN_CUDA(cudaStreamWaitEvent(g_side.stream, g_side.fork, 0));
+  return g_side.stream;
+}
+
+void join_side(cudaStream_t s) {
+  RGNN_CUDA(cudaEventRecord(g_side.join, g_side.stream));
+  RGNN_CUDA(cudaStreamWaitEvent(s, g_side.join, 0));
+}
+
+const char* intern(const std::string& name) {
+  static std::mutex mu;
+  static std::map<std::string, std::string> table;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = table.find(name);
+  if (it == table.end()) it = table.emplace(name, name).first;
+  return it->second.c_str();
+}
+
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

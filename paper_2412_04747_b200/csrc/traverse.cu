@@ -853,12 +853,20 @@ void by_dtype(int dtype, F&& f) {
 inline dim3 warps(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
 inline dim3 groups(int64_t n, int lpr) { return dim3(ceil_div(ceil_div(n, 32 / lpr) * (int64_t)32, 256)); }
 
-// Launch a work-plan kernel pair: warp mode over items [0, n_warp), group mode over the rest.
+// Launch a work-plan kernel pair: warp mode over items [0, n_warp) on `s`, group mode over the
+// rest concurrently on the side stream (the long heavy-row warps overlap the light-row groups).
 template <class KW, class KG, class... Args>
 void launch_plan(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, cudaStream_t s, Args... args) {
-  launch(name, kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp, (const int4*)wp.items, args...);
   const int64_t nl = wp.n_items - wp.n_warp;
-  launch(name, kg, groups(nl, lpr), dim3(256), 0, s, nl, (const int4*)(wp.items + wp.n_warp), args...);
+  int slot = -1;
+  profile_begin(name, s, &slot);  // the whole traversal (both halves) as one profile region
+  cudaStream_t side = fork_side(s);
+  launch(intern(std::string(name) + "/warp"), kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp,
+         (const int4*)wp.items, args...);
+  launch(intern(std::string(name) + "/group"), kg, groups(nl, lpr), dim3(256), 0, side, nl,
+         (const int4*)(wp.items + wp.n_warp), args...);
+  join_side(s);
+  profile_end(slot, s);
 }
 
 }  // namespace
