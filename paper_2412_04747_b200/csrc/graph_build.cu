@@ -241,6 +241,11 @@ void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std
       light.push_back(make_int4((int)id, b, e, -1));
     }
   }
+  // longest first within each class: medium rows start early (shorter tail), and neighbouring
+  // light items (one warp = 32 / LPR of them) have similar lengths (little idle lane time)
+  auto longer = [](const int4& a, const int4& b) { return (a.z - a.y) > (b.z - b.y); };
+  std::stable_sort(medium.begin(), medium.end(), longer);
+  std::stable_sort(light.begin(), light.end(), longer);
   wp.n_warp = (int64_t)(heavy.size() + medium.size());
   heavy.insert(heavy.end(), medium.begin(), medium.end());
   heavy.insert(heavy.end(), light.begin(), light.end());

@@ -119,29 +119,41 @@ __device__ __forceinline__ void sum_groups(float* acc) {
 
 // Work-item bookkeeping shared by every kernel: warp mode (GROUP = false) gives one item to
 // the whole warp and lets its groups stride over the edges; group mode gives one item per
-// lane group.  init() returns false if this lane has no item (whole warp or whole group).
+// lane group.  The loop trip count `span` is warp-uniform in both modes (group mode: the
+// longest item of the warp; light items are sorted by length so neighbours are alike), so
+// the warp never diverges and shuffles always use the full mask.  init() returns false only
+// when the whole warp has no item; lanes of an idle group see an empty range (has = false).
 template <bool GROUP, int LPR>
 struct Work {
   static constexpr int EG = 32 / LPR;
   int lane, g, c;
-  unsigned mask;
-  int first, step;
+  int first, step, span;
+  bool has;
   int4 item;
   __device__ __forceinline__ bool init(int64_t n, const int4* __restrict__ items) {
     lane = threadIdx.x & 31;
     g = lane / LPR;
     c = lane % LPR;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t wi = GROUP ? w * EG + g : w;
-    mask = GROUP ? group_mask<LPR>(g) : 0xffffffffu;
     first = GROUP ? 0 : g;
     step = GROUP ? 1 : EG;
-    if (wi >= n) return false;
-    item = items[wi];
+    if (GROUP) {
+      if (w * EG >= n) return false;
+      const int64_t wi = w * EG + g;
+      has = wi < n;
+      item = has ? items[wi] : make_int4(0, 0, 0, -1);
+      span = __reduce_max_sync(0xffffffffu, item.z - item.y);
+    } else {
+      if (w >= n) return false;
+      has = true;
+      item = items[w];
+      span = item.z - item.y;
+    }
     return true;
   }
-  __device__ __forceinline__ bool writer() const { return GROUP || g == 0; }
-  __device__ __forceinline__ bool leader() const { return GROUP ? c == 0 : lane == 0; }
+  __device__ __forceinline__ bool writer() const { return has && (GROUP || g == 0); }
+  __device__ __forceinline__ bool leader() const { return has && (GROUP ? c == 0 : lane == 0); }
+  static constexpr unsigned mask = 0xffffffffu;
 };
 
 // ------------------------------------------------------------------ RGCN forward (A5)
@@ -160,8 +172,8 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n, const int4* __restr
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += w.step * UNR) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR) {
+    const int i0 = b + t + w.first;
     uint4 raw[UNR];
     float wt[UNR];
 #pragma unroll
@@ -216,8 +228,8 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += w.step * UNR) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR) {
+    const int i0 = b + t + w.first;
     uint4 rk[UNR], rm[UNR];
     bool ok[UNR];
 #pragma unroll
@@ -292,8 +304,8 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int base = b; base < e; base += w.step * UNR) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR) {
+    const int i0 = b + t + w.first;
     uint4 rp[UNR];
     float sp[UNR], yv[UNR][V];
     bool ok[UNR];
@@ -372,7 +384,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
   float dq[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dq[k] = 0.f;
-  if (e > b) {
+  if (w.span > 0) {
     float q[V], gv[V], ov[V];
     cvt16<TP>(ldg16(Q + v * D + c * V), q);
     ld_f32<V>(Gr + v * D + c * V, gv);
@@ -383,13 +395,13 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
     go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
-    if (slot < 0 && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
+    if (slot < 0 && e > b && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
       st_tp<V>(GQ + v * 2 * D + c * V, gv);
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
       if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
     }
-    for (int base = b; base < e; base += w.step * UNR) {
-      const int i0 = base + w.first;
+    for (int t = 0; t < w.span; t += w.step * UNR) {
+      const int i0 = b + t + w.first;
       uint4 rk[UNR], rm[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
   float dx[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dx[k] = 0.f;
-  if (e > b) {
+  if (w.span > 0) {
     float x[V], gv[V], ov[V];
     cvt16<TP>(ldg16(X + v * D + c * V), x);
     ld_f32<V>(Gr + v * D + c * V, gv);
@@ -459,8 +471,8 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
     go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
-    for (int base = b; base < e; base += w.step * UNR) {
-      const int i0 = base + w.first;
+    for (int t = 0; t < w.span; t += w.step * UNR) {
+      const int i0 = b + t + w.first;
       uint4 rp[UNR];
       float sp[UNR], yv[UNR][V];
 #pragma unroll
@@ -524,8 +536,8 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t n, const int4* __
   const int64_t p = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int base = b; base < e; base += w.step * UNR) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR) {
+    const int i0 = b + t + w.first;
     float4 gr[UNR];
     float wt[UNR];
 #pragma unroll
@@ -566,8 +578,8 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t n, const int4* __
   const int64_t p = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};  // 4 columns + sum dz
-  for (int base = b; base < e; base += w.step * UNR) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR) {
+    const int i0 = b + t + w.first;
     float4 gr[UNR];
     float2 ab[UNR];
 #pragma unroll
@@ -655,8 +667,8 @@ __global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* 
   float ak[V], am[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-  for (int base = b; base < e; base += w.step * UNR_P) {
-    const int i0 = base + w.first;
+  for (int t = 0; t < w.span; t += w.step * UNR_P) {
+    const int i0 = b + t + w.first;
     uint4 rg[UNR_P], rq[UNR_P];
     float4 ns[UNR_P];
 #pragma unroll
