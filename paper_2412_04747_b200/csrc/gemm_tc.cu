@@ -111,13 +111,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void store_row32(float* y, const float* v) {
+// Stage 32 accumulator columns of one row into the warp's smem tile (row-major, 16-byte
+// chunks XOR-swizzled by the row so the 32 lanes' stores and the later coalesced reads
+// spread over all banks).  CH = 16-byte chunks per row (power of two).
+template <int CH>
+__device__ __forceinline__ void stage_row32(uint8_t* row_base, int row, int chunk0, const float* v, float*) {
 #pragma unroll
-  for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(y + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  for (int q = 0; q < 8; ++q) {
+    int j = chunk0 + q;
+    *reinterpret_cast<float4*>(row_base + ((j ^ (row & (CH - 1))) << 4)) =
+        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
 }
-__device__ __forceinline__ void store_row32(bf16* y, const float* v) {
+template <int CH>
+__device__ __forceinline__ void stage_row32(uint8_t* row_base, int row, int chunk0, const float* v, bf16*) {
 #pragma unroll
-  for (int i = 0; i < 32; i += 8) store16(y + i, v + i);
+  for (int q = 0; q < 4; ++q) {
+    int j = chunk0 + q;
+    store16(reinterpret_cast<bf16*>(row_base + ((j ^ (row & (CH - 1))) << 4)), v + 8 * q);
+  }
 }
 
 // K-major bf16 copy of the weights: Wt[w][n][k] = W[w][k][n] (or of W^T when transB: Wt[w][n][k] = W[w][n][k]).
@@ -149,7 +161,9 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + KB * A_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + KB * B_BYTES);
+  constexpr uint32_t OPS = KB * (A_BYTES + B_BYTES) > 128u * N * sizeof(TY) ? KB * (A_BYTES + B_BYTES)
+                                                                            : 128u * N * sizeof(TY);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OPS);  // after operands / epilogue staging
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -203,7 +217,11 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
   mbar_wait(bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 
-  // ---- epilogue: thread = tile row (TMEM lane 32*warp + lane)
+  // ---- epilogue: thread = tile row (TMEM lane 32*warp + lane); rows are staged per warp in
+  // the (now idle) operand smem and written back as contiguous, coalesced 16-byte chunks.
+  constexpr int RB = N * (int)sizeof(TY);  // bytes per output row
+  constexpr int CH = RB / 16;
+  uint8_t* stage = smem + warp * 32 * RB;
   const int r = warp * 32 + lane;
   const bool valid = r < nrows;
   const int64_t row = t.row0 + r;
@@ -226,9 +244,19 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
         }
       }
     }
-    if (valid) store_row32(Y + row * N + c0, v);
+    stage_row32<CH>(stage + lane * RB, lane, c0 * (int)sizeof(TY) / 16, v, (TY*)nullptr);
   }
   if (dotvec && valid) dotout[row] = dot;
+  __syncwarp();
+  const int rows_here = min(32, nrows - warp * 32);
+  uint8_t* ybase = reinterpret_cast<uint8_t*>(Y) + (t.row0 + (int64_t)warp * 32) * RB;
+#pragma unroll 4
+  for (int k = lane; k < 32 * CH; k += 32) {
+    const int rr = k / CH, j = k % CH;
+    if (rr < rows_here)
+      *reinterpret_cast<uint4*>(ybase + (int64_t)rr * RB + j * 16) =
+          *reinterpret_cast<const uint4*>(stage + rr * RB + ((j ^ (rr & (CH - 1))) << 4));
+  }
 
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -383,7 +411,8 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
 template <class TY, int N, int KB>
 void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
-  size_t smem = 1024 + KB * (128 * 128 + N * 128) + 64;
+  // operands, reused by the epilogue's row staging (128 rows x N x sizeof(TY)) once the MMAs are done
+  size_t smem = 1024 + std::max<size_t>(KB * (128 * 128 + N * 128), 128 * N * sizeof(TY)) + 64;
   // keep concurrent CTAs per SM within the 512 TMEM columns (alloc never waits)
   size_t floor_smem = (size_t)(232448 / (512 / NCOLS + 1)) + 1;
   smem = std::max(smem, floor_smem);

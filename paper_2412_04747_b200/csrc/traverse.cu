@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  Pref<GROUP && (LPR % UNR == 0), LPR> pf;
+  Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
   for (int t = 0; t < w.span; t += w.step * UNR) {
     pf.refill(csr_pair, t, b, e, c);
     const int i0 = b + t + w.first;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
       if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
     }
-    Pref<GROUP && (LPR % UNR == 0), LPR> pf;
+    Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
     for (int t = 0; t < w.span; t += w.step * UNR) {
       pf.refill(csr_pair, t, b, e, c);
       const int i0 = b + t + w.first;
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* 
   float ak[V], am[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-  Pref<GROUP && (LPR % UNR_P == 0), LPR> pf;
+  Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
   for (int t = 0; t < w.span; t += w.step * UNR_P) {
     pf.refill(csc_dst, t, b, e, c);
     const int i0 = b + t + w.first;
