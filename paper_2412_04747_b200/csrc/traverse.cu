@@ -156,22 +156,6 @@ struct Work {
   static constexpr unsigned mask = 0xffffffffu;
 };
 
-// Group mode: the LPR lanes of a group load the next LPR edge indices of their item with one
-// coalesced access and hand them out by shuffle, so the row gathers of later steps do not wait
-// on a dependent index load (needs LPR to be a multiple of the unroll).
-template <bool ON, int LPR>
-struct Pref {
-  int val = 0;
-  __device__ __forceinline__ void refill(const int32_t* __restrict__ arr, int t, int b, int e, int c) {
-    if (ON && (t & (LPR - 1)) == 0) val = (b + t + c < e) ? __ldg(arr + b + t + c) : 0;
-  }
-  // index of edge i = b + t + u (group mode); all lanes of the warp must call it
-  __device__ __forceinline__ int get(const int32_t* __restrict__ arr, int i, int e, int t, int u, int g) const {
-    if (ON) return __shfl_sync(0xffffffffu, val, g * LPR + ((t + u) & (LPR - 1)));
-    return i < e ? __ldg(arr + i) : 0;
-  }
-};
-
 // ------------------------------------------------------------------ RGCN forward (A5)
 // out_v (+)= sum_e norm_e P[pair_e]     (Eq. 3.1; self-loop X W_0 already in out when accumulate)
 template <class TP, int D, bool GROUP>
@@ -244,9 +228,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
   for (int t = 0; t < w.span; t += w.step * UNR) {
-    pf.refill(csr_pair, t, b, e, c);
     const int i0 = b + t + w.first;
     uint4 rk[UNR], rm[UNR];
     bool ok[UNR];
@@ -255,8 +237,8 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
       int i = i0 + u * w.step;
       ok[u] = i < e;
       rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
-      const int64_t p = pf.get(csr_pair, i, e, t, u, w.g);
       if (ok[u]) {
+        int64_t p = csr_pair[i];
         rk[u] = ldg16(KM + p * 2 * D + c * V);
         rm[u] = ldg16(KM + p * 2 * D + D + c * V);
       }
@@ -418,17 +400,15 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
       if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
     }
-    Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
     for (int t = 0; t < w.span; t += w.step * UNR) {
-      pf.refill(csr_pair, t, b, e, c);
       const int i0 = b + t + w.first;
       uint4 rk[UNR], rm[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
         rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
-        const int64_t p = pf.get(csr_pair, i, e, t, u, w.g);
         if (i < e) {
+          int64_t p = csr_pair[i];
           rk[u] = ldg16(KM + p * 2 * D + c * V);
           rm[u] = ldg16(KM + p * 2 * D + D + c * V);
         }
@@ -687,9 +667,7 @@ __global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* 
   float ak[V], am[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-  Pref<false, LPR> pf;  // index prefetch measured slower on mag (run 13)
   for (int t = 0; t < w.span; t += w.step * UNR_P) {
-    pf.refill(csc_dst, t, b, e, c);
     const int i0 = b + t + w.first;
     uint4 rg[UNR_P], rq[UNR_P];
     float4 ns[UNR_P];
@@ -698,8 +676,8 @@ __global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* 
       int i = i0 + u * w.step;
       ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       rg[u] = rq[u] = make_uint4(0, 0, 0, 0);
-      const int64_t d = pf.get(csc_dst, i, e, t, u, w.g);
       if (i < e) {
+        const int64_t d = csc_dst[i];
         rg[u] = ldg16(GQ + d * 2 * D + c * V);
         rq[u] = ldg16(GQ + d * 2 * D + D + c * V);
         ns[u] = __ldg(nst + d);
