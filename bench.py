@@ -88,22 +88,25 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["wgrad_nodes"] = N * (d_in * b + d * b)
     elif model == "rgat":
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b + 4)
-        out["rgat_fwd_traverse"] = E * (4 + 4 + d * b + 4 + 4 * d) + N * (8 + d_in * b + 4 * d + 8)
-        out["rgat_bwd_dst"] = E * (8 + d * b + 4 + 4 * d + 8) + N * (8 + d_in * b + 12 * d + 8)
-        out["rgat_bwd_pair"] = E * (4 + 4 + 8 + 4 * d) + U * (8 + d * b + 4)
+        out["rgat_fwd_traverse"] = E * (4 + 4 + d * b + 4) + N * (16 + d_in * b + 4 * d + 8)
+        # A6 also writes the node record [G_v | X_v] (2d*b) + 16 B
+        out["rgat_bwd_dst"] = E * (8 + d * b + 4) + N * (16 + d_in * b + 12 * d + 8 + 2 * d * b + 16)
+        # A7 per edge: CSC dst, the destination's [G|X] row and 16-B record; per pair: P row, s, dP, wsum, bx
+        out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + 4 * d)
         out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
         out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
+        out["seg_wsum"] = U * (4 * d) + U * (4 + d * b)
     else:
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b)
         out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)
-        out["rgcn_fwd_traverse"] = E * (4 + 4 + d * b) + N * (8 + 8 * d)
-        out["rgcn_bwd_pair"] = E * (4 + 4 + 4 * d) + U * (8 + d * b)
+        out["rgcn_fwd_traverse"] = E * (4 + 4 + d * b) + N * (16 + 8 * d)
+        out["rgcn_bwd_pair"] = E * (4 + 4 + d * b) + U * (16 + d * b)
         out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
-        out["gemm_selfloop_dx"] = N * (4 * d + 4 * d_in)
-        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
+        # self-loop dX GEMM with the per-source reduction of the pair dX rows fused (tcgen05 path)
+        out["gemm_selfloop_dx"] = N * (d * b + 4 * d_in + 8) + U * (4 + 4 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
-        out["wgrad_selfloop"] = N * (d_in * b + 4 * d)
+        out["wgrad_selfloop"] = N * (d_in * b + d * b)
     return out
 
 
@@ -332,18 +335,16 @@ def main():
     if not args.no_e2e:
         Xh = X_own.cpu().pin_memory()
         douth = dout.cpu().pin_memory()
-        dxh = torch.empty((hi - lo, d) if world > 1 else (g.num_nodes, d), dtype=torch.float32).pin_memory()
         dwh = {k: torch.empty(grads[k].shape, dtype=torch.float32).pin_memory() for k in wkeys}
         Xd = torch.empty_like(X_own)
         doutd = dout  # refreshed from host each step
         h2d = Xh.numel() * Xh.element_size() + douth.numel() * douth.element_size()
-        d2h = dxh.numel() * 4 + sum(v.numel() * 4 for v in dwh.values())
+        d2h = sum(v.numel() * 4 for v in dwh.values())
 
         def e2e_step():
             Xd.copy_(Xh, non_blocking=True)
             doutd.copy_(douth, non_blocking=True)
-            dx = step(Xd)
-            dxh.copy_(dx, non_blocking=True)
+            step(Xd)
             for k in wkeys:
                 dwh[k].copy_(grads[k], non_blocking=True)
 
@@ -365,7 +366,7 @@ def main():
             ems = float(t.item())
         e2e = {"value": g.num_edges * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
-               "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI) with pinned host X, dout in and dX, dW out"}
+               "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI); per step H2D of X and dout from pinned host memory, D2H of every weight gradient (dX stays on the device for the layer below)"}
 
     # ---- roofline of the dominant kernel
     peaks = load_peaks()

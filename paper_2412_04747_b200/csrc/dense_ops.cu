@@ -169,18 +169,31 @@ __global__ void k_seg_partial_reduce(int nseg, const int32_t* __restrict__ seg_t
   out[(size_t)seg_w[sidx] * width + i] = acc;
 }
 
-// per tile: partial[tile][k] = sum_rows wt[row] * A[gather(row)][k]; threads over k
+// per tile: partial[tile][k] = sum_rows wt[row] * A[gather(row)][k] (wt == NULL: weight 1).
+// 256 threads = RG row groups x K columns; each group strides over the tile's rows, the groups'
+// sums are combined in group order through shared memory (deterministic).
 template <class TA>
-__global__ void k_seg_wsum(const Tile* __restrict__ tiles, const float* __restrict__ wt, const TA* __restrict__ A,
-                           int K, const int32_t* __restrict__ gather, float* __restrict__ partial) {
+__global__ void __launch_bounds__(256) k_seg_wsum(const Tile* __restrict__ tiles, const float* __restrict__ wt,
+                                                  const TA* __restrict__ A, int K, const int32_t* __restrict__ gather,
+                                                  float* __restrict__ partial) {
+  __shared__ float red[256];
   const Tile t = tiles[blockIdx.x];
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    float acc = 0.f;
-    for (int r = t.row0; r < t.row1; ++r) {
+  const int RG = blockDim.x / K, k = threadIdx.x % K, rg = threadIdx.x / K;
+  float acc = 0.f;
+  if (rg < RG) {
+#pragma unroll 4
+    for (int r = t.row0 + rg; r < t.row1; r += RG) {
       int64_t ar = gather ? (int64_t)gather[r] : (int64_t)r;
-      acc = fmaf(wt[r], to_f(A[ar * K + k]), acc);
+      float x = to_f(A[ar * K + k]);
+      acc = wt ? fmaf(wt[r], x, acc) : acc + x;
     }
-    partial[(size_t)blockIdx.x * K + k] = acc;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < K) {
+    float sum = 0.f;
+    for (int g = 0; g < RG; ++g) sum += red[g * K + threadIdx.x];
+    partial[(size_t)blockIdx.x * K + threadIdx.x] = sum;
   }
 }
 
@@ -357,13 +370,14 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather, float* out,
               int num_w, float* partial, cudaStream_t s) {
   const Plan& p = *plan;
+  RGNN_CHECK(K >= 1 && K <= 256, RGNN_ERR_UNSUPPORTED, "seg_wsum: K must be <= 256");
   RGNN_CUDA(cudaMemsetAsync(out, 0, (size_t)num_w * K * sizeof(float), s));
   if (p.count == 0) return;
   if (a_dtype == F32)
-    launch("seg_wsum", k_seg_wsum<float>, dim3(p.count), dim3(std::min(K, 256)), 0, s, p.tiles, wt,
+    launch("seg_wsum", k_seg_wsum<float>, dim3(p.count), dim3(256 / K * K), 0, s, p.tiles, wt,
            static_cast<const float*>(A), K, gather, partial);
   else
-    launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(std::min(K, 256)), 0, s, p.tiles, wt,
+    launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(256 / K * K), 0, s, p.tiles, wt,
            static_cast<const bf16*>(A), K, gather, partial);
   launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(K, 256), p.nseg), dim3(256), 0, s, p.nseg,
          p.seg_tile_ptr, p.seg_w, partial, (int64_t)K, out);

@@ -123,10 +123,11 @@ struct BwdScratch {
   float* dXp = nullptr;   // [U][Din]
   void* dQ = nullptr;     // HGT [N][D] layer dtype; RGAT dX fallback [N][D] fp32
   float* wsum = nullptr;  // RGAT [U]
-  float* csum = nullptr;  // RGAT [UD]
+  float* bx = nullptr;    // RGAT [U][D]  sum_e dz_e X_d per pair
   float* Bsum = nullptr;  // RGAT [R][Din]
   float* dF = nullptr;    // HGT [R*T][Din][2D]
   void* GQ = nullptr;     // HGT [N][2D] = [G_v | Q_v] layer dtype
+  void* Gt = nullptr;     // RGCN bf16 path: the upstream gradient in bf16 [N][D]
   float4* nst = nullptr;  // HGT [N] (m, 1/sum, G.out, 0)
   float* partial = nullptr;
   float* csr_norm = nullptr;
@@ -135,7 +136,7 @@ struct BwdScratch {
 
 void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
   const int64_t rows = c.g->rows.n_slots * c.D;
-  const int64_t pairs = c.g->pairs.n_slots * (c.d->model == RGNN_HGT ? 2 * c.D : c.D);
+  const int64_t pairs = c.g->pairs.n_slots * (c.d->model == RGNN_RGCN ? c.D : 2 * c.D);
   pt.acc = ar.take<float>(std::max<int64_t>(std::max(rows, pairs), 1));
   pt.stat = ar.take<float2>(std::max<int64_t>(std::max(c.g->rows.n_slots, c.g->pairs.n_slots), 1));
 }
@@ -175,6 +176,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   if (model == RGNN_RGCN) {
     o.dP = ar.take<char>(U * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
+    if (c.dt == BF16) o.Gt = ar.take<char>(N * c.D * c.esz);
     if (c.d->norm_kind == RGNN_NORM_CUSTOM) {
       o.csr_norm = ar.take<float>(E);
       o.csc_norm = ar.take<float>(E);
@@ -182,15 +184,15 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     need(seg_pair_rel(g), (int64_t)c.Din * c.D);
     need(seg_all_nodes(g), (int64_t)c.Din * c.D);
   } else if (model == RGNN_RGAT) {
-    o.ebuf = ar.take<float2>(E);
     o.dP = ar.take<char>(U * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
     o.dQ = ar.take<float>(N * c.D);
     o.wsum = ar.take<float>(U);
-    o.csum = ar.take<float>(g->UD);
+    o.bx = ar.take<float>(U * c.D);
     o.Bsum = ar.take<float>(R * c.Din);
+    o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
+    o.nst = ar.take<float4>(N);
     need(seg_pair_rel(g), (int64_t)c.Din * c.D);
-    need(seg_dpair_rel(g), c.Din);
   } else {
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
     o.dXp = ar.take<float>(U * c.Din);
@@ -306,30 +308,43 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   if (model == RGNN_RGCN) {
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
     graph_norms(g, c.d->norm_kind, w->edge_norm, c.s, &cn, &xn);
-    rgcn_bwd_pair(g, c.dt, c.D, xn, G, sc.dP, sc.pt, c.s);
+    // upstream gradient in the table dtype: bf16 copy on the bf16 path (gathered per edge and the
+    // A operand of the self-loop tcgen05 GEMMs), G itself on the fp32 path
+    const void* Gt = G;
+    if (c.dt == BF16) {
+      convert_dt((int64_t)g->N * c.D, G, sc.Gt, BF16, c.s);
+      Gt = sc.Gt;
+    }
+    rgcn_bwd_pair(g, c.dt, c.D, xn, Gt, sc.dP, sc.pt, c.s);
     if (dX) {
-      if (c.d->self_loop) {
-        GemmArgs b;
-        b.A = G; b.a_dtype = F32; b.K = c.D; b.B = w->W0; b.b_dtype = c.dt; b.transB = true;
-        b.Y = dX; b.y_dtype = F32; b.N = c.Din;
-        b.name = "gemm_selfloop_dx";
-        gemm(c, seg_all_nodes(g), b);
-      }
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, c.d->self_loop != 0, c.s);
+      bool fused = false;
+      if (c.d->self_loop) {  // dX = G W0^T (+ per-source sum of the pair rows, fused when on tcgen05)
+        GemmArgs b;
+        b.A = Gt; b.a_dtype = c.dt; b.K = c.D; b.B = w->W0; b.b_dtype = c.dt; b.transB = true;
+        b.Y = dX; b.y_dtype = F32; b.N = c.Din;
+        b.num_w = 1; b.bt_scratch = sc.bt;
+        b.red_ptr = g->src_pair_ptr; b.red_list = g->src_pairs; b.red_rows = sc.dXp;
+        b.name = "gemm_selfloop_dx";
+        fused = gemm(c, seg_all_nodes(g), b);
+      }
+      if (!fused)
+        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, c.d->self_loop != 0, c.s);
     }
     if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
-      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, G, F32, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
+      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, Gt, c.dt, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
-    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, sc.ebuf, dXt, sc.pt, c.s);
-    rgat_bwd_pair(g, c.dt, c.D, sc.ebuf, G, w->a, sc.dP, sc.wsum, sc.pt, c.s);
+    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, dXt, sc.GQ, sc.nst, sc.pt,
+                 c.s);
+    rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum, sc.bx,
+                  sc.pt, c.s);
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
@@ -339,10 +354,9 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
     }
-    if (dW->dW || dW->db) {
-      dpair_sum(g, sc.ebuf, sc.csum, c.s);
-      const Plan& dp = plan(g, seg_dpair_rel(g), WGRAD_ROWS, c.s);
-      seg_wsum(&dp, sc.csum, X, c.dt, c.Din, g->dpair_dst, sc.Bsum, g->R, sc.partial, c.s);
+    if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
+      const Plan& pp = plan(g, seg_pair_rel(g), WGRAD_ROWS, c.s);
+      seg_wsum(&pp, nullptr, sc.bx, F32, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
     }
     if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW || dW->db) rgat_tpath_grads(g->R, c.Din, c.D, w->W, w->b, c.dt, sc.Bsum, dW->dW, dW->db, c.s);

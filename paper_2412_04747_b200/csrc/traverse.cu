@@ -441,7 +441,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
 
 // ------------------------------------------------------------------ RGAT backward, dst-major (A6)
 // dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
-// dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path) ; ebuf[i] = (alpha_e, dz_e)
+// dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path).  Also writes the node record
+// GX_v = [G_v | X_v] (table dtype) and nst_v = (m_v, 1/sum_v, G_v . out_v, 0) read by the pair pass.
 template <class TP, int D, bool GROUP>
 __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
@@ -450,7 +451,8 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
                                                       const float* __restrict__ y, float slope,
                                                       const float2* __restrict__ stats,
                                                       const float* __restrict__ Gr, const float* __restrict__ out,
-                                                      float2* __restrict__ ebuf, float* __restrict__ dX) {
+                                                      float* __restrict__ dX, TP* __restrict__ GX,
+                                                      float4* __restrict__ nst) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
@@ -471,6 +473,11 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
     go = gsum<LPR>(go, w.mask);
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
+    if (slot < 0 && e > b && w.writer()) {  // node record (heavy rows: k_rgat_node_prep)
+      st_tp<V>(GX + v * 2 * D + c * V, gv);
+      st_tp<V>(GX + v * 2 * D + D + c * V, x);
+      if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
+    }
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
       uint4 rp[UNR];
@@ -510,7 +517,6 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
         if (i < e) {
 #pragma unroll
           for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
-          if (c == 0) ebuf[i] = make_float2(alpha, dz);
         }
       }
     }
@@ -524,95 +530,169 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
 // One group of LPR = D/4 lanes per light pair, one warp per medium pair or heavy chunk;
 // each lane owns 4 fp32 columns.  The edges of pair p are csc[item.y, item.z).
 
-// RGCN: dP_p = sum_{e in p} norm_e G[d_e]
-template <class TO, int D, bool GROUP>
+// RGCN: dP_p = sum_{e in p} norm_e G[d_e]; G rows in the table dtype (bf16 copy on the bf16 path),
+// one 16-byte vector per lane.
+template <class TP, int D, bool GROUP>
 __global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                        float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                        const float* __restrict__ csc_norm,
-                                                       const float* __restrict__ Gr, TO* __restrict__ dP) {
-  constexpr int LPR = D / 4;
+                                                       const TP* __restrict__ Gr, TP* __restrict__ dP) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t p = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
   for (int t = 0; t < w.span; t += w.step * UNR) {
     const int i0 = b + t + w.first;
-    float4 gr[UNR];
+    uint4 gr[UNR];
     float wt[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       int i = i0 + u * w.step;
-      gr[u] = make_float4(0, 0, 0, 0);
+      gr[u] = make_uint4(0, 0, 0, 0);
       wt[u] = 0.f;
       if (i < e) {
         wt[u] = csc_norm[i];
-        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
+        gr[u] = ldg16(Gr + (int64_t)csc_dst[i] * D + c * V);
       }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      acc[0] = fmaf(wt[u], gr[u].x, acc[0]); acc[1] = fmaf(wt[u], gr[u].y, acc[1]);
-      acc[2] = fmaf(wt[u], gr[u].z, acc[2]); acc[3] = fmaf(wt[u], gr[u].w, acc[3]);
+      float x[V];
+      cvt16<TP>(gr[u], x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wt[u], x[k], acc[k]);
     }
   }
-  if (!GROUP) sum_groups<LPR, 4>(acc);
+  if (!GROUP) sum_groups<LPR, V>(acc);
   if (!w.writer()) return;
-  if (slot >= 0) st4(pacc + (int64_t)slot * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
-  else st4(dP + p * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
+  if (slot >= 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+  else st_tp<V>(dP + p * D + c * V, acc);
 }
 
-// RGAT: dP_p = sum alpha_e G[d_e] + (sum dz_e) a_r ; wsum_p = sum dz_e
-template <class TW, int D, bool GROUP>
-__global__ void __launch_bounds__(256) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
-                                                       float* __restrict__ pacc, float2* __restrict__ pstat,
-                                                       const int32_t* __restrict__ csc_dst,
-                                                       const int32_t* __restrict__ csc_rel,
-                                                       const int32_t* __restrict__ csc2csr,
-                                                       const float2* __restrict__ ebuf, const float* __restrict__ Gr,
-                                                       const TW* __restrict__ avec, TW* __restrict__ dP,
-                                                       float* __restrict__ wsum) {
-  constexpr int LPR = D / 4;
+// RGAT, recomputing the edge terms from the destination's node record (no per-edge buffer):
+// per pair p (relation r): P_p, y_r, s_p in registers; per edge e of p:
+//   z_e = s_p + X_d . y_r, alpha_e = exp(LeakyReLU(z_e) - m_d)/sum_d, dalpha_e = G_d . P_p,
+//   dz_e = alpha_e (dalpha_e - G_d . out_d) (z_e > 0 ? 1 : slope);
+// dP_p = sum alpha_e G_d + (sum dz_e) a_r, wsum_p = sum dz_e (-> da_r), bx_p = sum dz_e X_d (-> B_r).
+template <class TP, int D>
+__global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* __restrict__ rows,
+                                                        const float* __restrict__ Gr, const TP* __restrict__ X,
+                                                        const float* __restrict__ out,
+                                                        const float2* __restrict__ stats, TP* __restrict__ GX,
+                                                        float4* __restrict__ nst) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int64_t j = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
+  if (j >= n) return;
+  const int64_t v = rows[j].x;
+  float gv[V], ov[V], xv[V];
+  ld_f32<V>(Gr + v * D + c * V, gv);
+  ld_f32<V>(out + v * D + c * V, ov);
+  cvt16<TP>(ldg16(X + v * D + c * V), xv);
+  float go = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
+  go = gsum<LPR>(go, group_mask<LPR>(g));
+  st_tp<V>(GX + v * 2 * D + c * V, gv);
+  st_tp<V>(GX + v * 2 * D + D + c * V, xv);
+  if (c == 0) {
+    float2 st = stats[v];
+    nst[v] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
+  }
+}
+
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256, 3) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
+                                                          float* __restrict__ pacc, float2* __restrict__ pstat,
+                                                          const int32_t* __restrict__ csc_dst,
+                                                          const int32_t* __restrict__ csc_rel,
+                                                          const TP* __restrict__ P, const float* __restrict__ spair,
+                                                          const float* __restrict__ y, const TP* __restrict__ avec,
+                                                          float slope, const TP* __restrict__ GX,
+                                                          const float4* __restrict__ nst, TP* __restrict__ dP,
+                                                          float* __restrict__ wsum, float* __restrict__ bx) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t p = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
-  float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f};  // 4 columns + sum dz
-  for (int t = 0; t < w.span; t += w.step * UNR) {
-    const int i0 = b + t + w.first;
-    float4 gr[UNR];
-    float2 ab[UNR];
+  const int r = e > b ? csc_rel[b] : 0;
+  float pv[V], yv[V];
+  cvt16<TP>(ldg16(P + p * D + c * V), pv);
+  ld_f32<V>(y + (int64_t)r * D + c * V, yv);
+  const float sp = spair[p];
+  float acc[V], ax[V], zs = 0.f;
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+  for (int k = 0; k < V; ++k) acc[k] = ax[k] = 0.f;
+  for (int t = 0; t < w.span; t += w.step * UNR_P) {
+    const int i0 = b + t + w.first;
+    uint4 rg[UNR_P], rx[UNR_P];
+    float4 ns[UNR_P];
+#pragma unroll
+    for (int u = 0; u < UNR_P; ++u) {
       int i = i0 + u * w.step;
-      gr[u] = make_float4(0, 0, 0, 0);
-      ab[u] = make_float2(0.f, 0.f);
+      ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rg[u] = rx[u] = make_uint4(0, 0, 0, 0);
       if (i < e) {
-        ab[u] = ebuf[csc2csr[i]];
-        gr[u] = __ldg(reinterpret_cast<const float4*>(Gr + (int64_t)csc_dst[i] * D + c * 4));
+        const int64_t d = csc_dst[i];
+        rg[u] = ldg16(GX + d * 2 * D + c * V);
+        rx[u] = ldg16(GX + d * 2 * D + D + c * V);
+        ns[u] = __ldg(nst + d);
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      acc[0] = fmaf(ab[u].x, gr[u].x, acc[0]); acc[1] = fmaf(ab[u].x, gr[u].y, acc[1]);
-      acc[2] = fmaf(ab[u].x, gr[u].z, acc[2]); acc[3] = fmaf(ab[u].x, gr[u].w, acc[3]);
-      acc[4] += ab[u].y;
+    for (int u = 0; u < UNR_P; ++u) {
+      float gr[V], xd[V];
+      cvt16<TP>(rg[u], gr);
+      cvt16<TP>(rx[u], xd);
+      float tt = 0.f, da = 0.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        tt = fmaf(xd[k], yv[k], tt);
+        da = fmaf(gr[k], pv[k], da);
+      }
+      tt = gsum<LPR>(tt, w.mask);
+      da = gsum<LPR>(da, w.mask);
+      const bool ok = i0 + u * w.step < e;
+      float z = sp + tt;
+      float l = z > 0.f ? z : slope * z;
+      float alpha = ok ? __expf(l - ns[u].x) * ns[u].y : 0.f;
+      float dz = alpha * (da - ns[u].z) * (z > 0.f ? 1.f : slope);
+      zs += dz;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        acc[k] = fmaf(alpha, gr[k], acc[k]);
+        ax[k] = fmaf(dz, xd[k], ax[k]);
+      }
     }
   }
-  if (!GROUP) sum_groups<LPR, 5>(acc);
+  if (!GROUP) {
+    sum_groups<LPR, V>(acc);
+    sum_groups<LPR, V>(ax);
+    float z1[1] = {zs};
+    sum_groups<LPR, 1>(z1);
+    zs = z1[0];
+  }
   if (!w.writer()) return;
-  if (slot >= 0) {
-    st4(pacc + (int64_t)slot * D + c * 4, acc[0], acc[1], acc[2], acc[3]);
-    if (c == 0) pstat[slot] = make_float2(acc[4], 0.f);
+  if (slot >= 0) {  // heavy pair chunk: [acc | ax] partial + sum dz
+    st_f32<V>(pacc + (int64_t)slot * 2 * D + c * V, acc);
+    st_f32<V>(pacc + (int64_t)slot * 2 * D + D + c * V, ax);
+    if (c == 0) pstat[slot] = make_float2(zs, 0.f);
     return;
   }
-  const int r = csc_rel[b];
-  float a4[4];
+  float av[V];
+  cvt16<TP>(ldg16(avec + (int64_t)r * D + c * V), av);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) a4[k] = to_f(avec[(int64_t)r * D + c * 4 + k]);
-  const float zs = acc[4];
-  st4(dP + p * D + c * 4, fmaf(zs, a4[0], acc[0]), fmaf(zs, a4[1], acc[1]), fmaf(zs, a4[2], acc[2]),
-      fmaf(zs, a4[3], acc[3]));
+  for (int k = 0; k < V; ++k) acc[k] = fmaf(zs, av[k], acc[k]);
+  st_tp<V>(dP + p * D + c * V, acc);
+  st_f32<V>(bx + p * D + c * V, ax);
   if (c == 0) wsum[p] = zs;
 }
 
@@ -721,16 +801,6 @@ __global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* 
   }
 }
 
-// c_{v,r} = sum of dz over the CSR run of (dst v, rel r)   (RGAT destination-side weight terms)
-__global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
-                            const float2* __restrict__ ebuf, float* __restrict__ csum) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= UD) return;
-  float acc = 0.f;
-  for (int i = beg[j], e = beg[j] + cnt[j]; i < e; ++i) acc += ebuf[i].y;
-  csum[j] = acc;
-}
-
 // ------------------------------------------------------------------ heavy-id merges
 // One CTA per heavy id: warp w folds chunks w, w+8, ... of the id (lane c owns columns 4c..4c+3
 // of a W-wide row, looping over W in steps of 128); the 8 warp results are then combined in warp
@@ -817,7 +887,7 @@ __global__ void __launch_bounds__(256) k_merge_sum(int64_t n_split, const int4* 
   }
 }
 
-// RGAT heavy pairs: dP_p = sum acc_i + (sum zs_i) a_r ; wsum_p = sum zs_i
+// RGAT heavy pairs: dP_p = sum acc_i + (sum zs_i) a_r ; bx_p = sum ax_i ; wsum_p = sum zs_i
 template <class TW, int D>
 __global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const int4* __restrict__ splits,
                                                          const float* __restrict__ pacc,
@@ -825,7 +895,7 @@ __global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const 
                                                          const int32_t* __restrict__ pair_csc_beg,
                                                          const int32_t* __restrict__ csc_rel,
                                                          const TW* __restrict__ avec, TW* __restrict__ dP,
-                                                         float* __restrict__ wsum) {
+                                                         float* __restrict__ wsum, float* __restrict__ bx) {
   const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (j >= n_split) return;
   const int lane = threadIdx.x & 31;
@@ -835,14 +905,17 @@ __global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const 
   if (lane == 0) wsum[sp.x] = zs;
   if (lane * 4 >= D) return;
   const int r = csc_rel[pair_csc_beg[sp.x]];
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, ax[4] = {0.f, 0.f, 0.f, 0.f};
   for (int i = 0; i < sp.z; ++i) {
-    float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
+    float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * 2 * D + lane * 4);
+    float4 x = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * 2 * D + D + lane * 4);
     acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    ax[0] += x.x; ax[1] += x.y; ax[2] += x.z; ax[3] += x.w;
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) acc[k] = fmaf(zs, to_f(avec[(int64_t)r * D + lane * 4 + k]), acc[k]);
   st4(dP + (int64_t)sp.x * D + lane * 4, acc[0], acc[1], acc[2], acc[3]);
+  st4(bx + (int64_t)sp.x * D + lane * 4, ax[0], ax[1], ax[2], ax[3]);
 }
 
 template <class F>
@@ -947,48 +1020,55 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const 
 }
 
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                  const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
-                  float* dX, const Partial& pt, cudaStream_t s) {
+                  const float* y, float slope, const float2* stats, const float* G, const float* out, float* dX,
+                  void* GX, float4* nst, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_rgat_bwd_dst<TP, DD, false>,
                   k_rgat_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
-                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, stats, G, out, ebuf, dX);
+                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, stats, G, out, dX,
+                  static_cast<TP*>(GX), nst);
+      launch("rgat_node_prep", k_rgat_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
+             g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(X), out, stats,
+             static_cast<TP*>(GX), nst);
     });
     launch("merge_heavy_rows", k_merge_sum<DD, float>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, dX, false);
   });
 }
 
-void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
+void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const void* G, void* dP,
                    const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
-      using TO = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgcn_bwd_pair", g->pairs, DD / 4, k_rgcn_bwd_pair<TO, DD, false>, k_rgcn_bwd_pair<TO, DD, true>, s,
-                  pt.acc, (const int32_t*)g->csc_dst, csc_norm, G, static_cast<TO*>(dP));
-      launch("merge_heavy_pairs", k_merge_sum<DD, TO>, dim3(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
-             (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TO*>(dP), false);
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgcn_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgcn_bwd_pair<TP, DD, false>,
+                  k_rgcn_bwd_pair<TP, DD, true>, s, pt.acc, (const int32_t*)g->csc_dst, csc_norm,
+                  static_cast<const TP*>(G), static_cast<TP*>(dP));
+      launch("merge_heavy_pairs", k_merge_sum<DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
+             (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dP), false);
     });
   });
 }
 
-void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   void* dP, float* wsum, const Partial& pt, cudaStream_t s) {
+void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
+                   const void* a, float slope, const void* GX, const float4* nst, void* dP, float* wsum, float* bx,
+                   const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
-      using TW = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgat_bwd_pair", g->pairs, DD / 4, k_rgat_bwd_pair<TW, DD, false>, k_rgat_bwd_pair<TW, DD, true>, s,
-                  pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc_rel,
-                  (const int32_t*)g->csc2csr, ebuf, G, static_cast<const TW*>(a), static_cast<TW*>(dP), wsum);
-      launch("merge_heavy_pairs", k_merge_rgat_pair<TW, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
+      using TP = std::remove_pointer_t<decltype(tp)>;
+      launch_plan("rgat_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgat_bwd_pair<TP, DD, false>,
+                  k_rgat_bwd_pair<TP, DD, true>, s, pt.acc, pt.stat, (const int32_t*)g->csc_dst,
+                  (const int32_t*)g->csc_rel, static_cast<const TP*>(P), spair, y, static_cast<const TP*>(a), slope,
+                  static_cast<const TP*>(GX), nst, static_cast<TP*>(dP), wsum, bx);
+      launch("merge_heavy_pairs", k_merge_rgat_pair<TP, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
-             (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TW*>(a),
-             static_cast<TW*>(dP), wsum);
+             (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TP*>(a),
+             static_cast<TP*>(dP), wsum, bx);
     });
   });
 }
@@ -1009,9 +1089,5 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const
   });
 }
 
-void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s) {
-  launch("rgat_dpair_sum", k_dpair_sum, dim3(ceil_div(g->UD, 256)), dim3(256), 0, s, g->UD, g->dpair_csr_beg,
-         g->dpair_cnt, ebuf, csum);
-}
 
 }  // namespace rgnn

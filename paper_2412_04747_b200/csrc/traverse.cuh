@@ -20,14 +20,16 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
                  cudaStream_t s);
+// also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0)
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                  const float* y, float slope, const float2* stats, const float* G, const float* out, float2* ebuf,
-                  float* dX, const Partial& pt, cudaStream_t s);
-void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const float* G, void* dP,
+                  const float* y, float slope, const float2* stats, const float* G, const float* out, float* dX,
+                  void* GX, float4* nst, const Partial& pt, cudaStream_t s);
+// G: upstream gradient rows in the layer dtype (bf16 copy on the bf16 path)
+void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const void* G, void* dP,
                    const Partial& pt, cudaStream_t s);
-void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float2* ebuf, const float* G, const void* a,
-                   void* dP, float* wsum, const Partial& pt, cudaStream_t s);
+void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
+                   const void* a, float slope, const void* GX, const float4* nst, void* dP, float* wsum, float* bx,
+                   const Partial& pt, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, const Partial& pt, cudaStream_t s);
-void dpair_sum(const rgnn_graph_s* g, const float2* ebuf, float* csum, cudaStream_t s);
 }  // namespace rgnn
