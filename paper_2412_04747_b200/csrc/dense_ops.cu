@@ -197,27 +197,46 @@ __global__ void __launch_bounds__(256) k_seg_wsum(const Tile* __restrict__ tiles
   }
 }
 
-// warp per node u: out[u] (+)= sum of rows Y[list[i]]
-__global__ void k_seg_reduce_rows(int64_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ list,
-                                  const float* __restrict__ Y, int K, float* __restrict__ out, bool accumulate) {
-  int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (u >= n) return;
-  int b = ptr[u], e = ptr[u + 1];
-  for (int c = lane * 4; c < K; c += 128) {
-    float4 acc = accumulate ? *reinterpret_cast<const float4*>(out + u * K + c) : make_float4(0, 0, 0, 0);
-    int i = b;
-    for (; i + 1 < e; i += 2) {
-      float4 v0 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i] * K + c));
-      float4 v1 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i + 1] * K + c));
-      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+// out[u] (+)= sum of rows Y[list[i]], i in [ptr[u], ptr[u+1]).  One group of K*sizeof(TY)/16 lanes
+// per node (one 16-byte vector per lane), 4 rows loaded ahead; the loop count is the longest
+// list of the warp's nodes, so the warp stays converged.  Fixed summation order (deterministic).
+template <class TY, int K>
+__global__ void __launch_bounds__(256) k_seg_reduce_rows(int64_t n, const int32_t* __restrict__ ptr,
+                                                         const int32_t* __restrict__ list, const TY* __restrict__ Y,
+                                                         float* __restrict__ out, bool accumulate) {
+  constexpr int V = Vec<TY>::N, LPR = K / V, EG = 32 / LPR, UN = 4;
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w * EG >= n) return;
+  const int64_t u = w * EG + g;
+  const bool has = u < n;
+  const int b = has ? ptr[u] : 0, e = has ? ptr[u + 1] : 0;
+  const int span = __reduce_max_sync(0xffffffffu, e - b);
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  for (int t = 0; t < span; t += UN) {
+    uint4 raw[UN];
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      raw[q] = make_uint4(0, 0, 0, 0);
+      if (b + t + q < e) raw[q] = ldg16(Y + (int64_t)list[b + t + q] * K + c * V);
     }
-    if (i < e) {
-      float4 v0 = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)list[i] * K + c));
-      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      float x[V];
+      cvt16<TY>(raw[q], x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += x[k];
     }
-    *reinterpret_cast<float4*>(out + u * K + c) = acc;
+  }
+  if (!has) return;
+  float* o = out + u * K + c * V;
+#pragma unroll
+  for (int k = 0; k < V; k += 4) {
+    float4 prev = accumulate ? *reinterpret_cast<const float4*>(o + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(o + k) =
+        make_float4(prev.x + acc[k], prev.y + acc[k + 1], prev.z + acc[k + 2], prev.w + acc[k + 3]);
   }
 }
 
@@ -383,11 +402,30 @@ void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int
          p.seg_tile_ptr, p.seg_w, partial, (int64_t)K, out);
 }
 
-void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const float* Y, int K, float* out,
+void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const void* Y, int y_dtype, int K, float* out,
                      bool accumulate, cudaStream_t s) {
-  RGNN_CHECK(K % 4 == 0, RGNN_ERR_UNSUPPORTED, "row width must be a multiple of 4");
-  launch("seg_reduce_rows", k_seg_reduce_rows, dim3(ceil_div(n * 32, 256)), dim3(256), 0, s, n, ptr, list, Y, K, out,
-         accumulate);
+  auto go = [&](auto* ty, auto kc) {
+    using TY = std::remove_pointer_t<decltype(ty)>;
+    constexpr int KK = decltype(kc)::value;
+    constexpr int LPR = KK / Vec<TY>::N;
+    if constexpr (LPR >= 1 && LPR <= 32)
+      launch("seg_reduce_rows", k_seg_reduce_rows<TY, KK>, dim3(ceil_div(ceil_div(n, 32 / LPR) * 32, 256)),
+             dim3(256), 0, s, n, ptr, list, static_cast<const TY*>(Y), out, accumulate);
+    else
+      RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "seg_reduce_rows: fp32 rows wider than 128");
+  };
+  auto by_k = [&](auto* ty) {
+    switch (K) {
+      case 16: go(ty, std::integral_constant<int, 16>()); break;
+      case 32: go(ty, std::integral_constant<int, 32>()); break;
+      case 64: go(ty, std::integral_constant<int, 64>()); break;
+      case 128: go(ty, std::integral_constant<int, 128>()); break;
+      case 256: go(ty, std::integral_constant<int, 256>()); break;
+      default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "seg_reduce_rows: width");
+    }
+  };
+  if (y_dtype == F32) by_k((float*)nullptr);
+  else by_k((bf16*)nullptr);
 }
 
 void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b, int dtype, float* y,

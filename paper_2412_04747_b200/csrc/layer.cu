@@ -22,6 +22,7 @@ namespace {
 constexpr int GEMM_ROWS = 64;    // SIMT GEMM tile rows
 constexpr int TC_ROWS = 128;     // tcgen05 tile rows
 constexpr int WGRAD_ROWS = 2048;  // rows per weight-gradient partial
+constexpr int WSUM_ROWS = 256;    // rows per weighted-row-sum partial (seg_wsum)
 
 struct Segs {
   std::string key;
@@ -120,7 +121,7 @@ struct BwdScratch {
   void* bt = nullptr;     // tcgen05 path: K-major bf16 weight image
   float2* ebuf = nullptr;
   void* dP = nullptr;     // [U][D] or HGT [U][2D], layer dtype
-  float* dXp = nullptr;   // [U][Din]
+  void* dXp = nullptr;    // [U][Din] layer dtype
   void* dQ = nullptr;     // HGT [N][D] layer dtype; RGAT dX fallback [N][D] fp32
   float* wsum = nullptr;  // RGAT [U]
   float* bx = nullptr;    // RGAT [U][D]  sum_e dz_e X_d per pair
@@ -175,7 +176,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   };
   if (model == RGNN_RGCN) {
     o.dP = ar.take<char>(U * c.D * c.esz);
-    o.dXp = ar.take<float>(U * c.Din);
+    o.dXp = ar.take<char>(U * c.Din * c.esz);
     if (c.dt == BF16) o.Gt = ar.take<char>(N * c.D * c.esz);
     if (c.d->norm_kind == RGNN_NORM_CUSTOM) {
       o.csr_norm = ar.take<float>(E);
@@ -185,7 +186,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     need(seg_all_nodes(g), (int64_t)c.Din * c.D);
   } else if (model == RGNN_RGAT) {
     o.dP = ar.take<char>(U * c.D * c.esz);
-    o.dXp = ar.take<float>(U * c.Din);
+    o.dXp = ar.take<char>(U * c.Din * c.esz);
     o.dQ = ar.take<float>(N * c.D);
     o.wsum = ar.take<float>(U);
     o.bx = ar.take<float>(U * c.D);
@@ -193,9 +194,10 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
     o.nst = ar.take<float4>(N);
     need(seg_pair_rel(g), (int64_t)c.Din * c.D);
+    width = std::max(width, (int64_t)c.D * count_tiles(seg_pair_rel(g), WSUM_ROWS));
   } else {
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
-    o.dXp = ar.take<float>(U * c.Din);
+    o.dXp = ar.take<char>(U * c.Din * c.esz);
     o.dQ = ar.take<char>(N * c.D * c.esz);
     o.dF = ar.take<float>(R * T * c.Din * 2 * c.D);
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
@@ -319,22 +321,19 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
-      a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
-      bool fused = false;
-      if (c.d->self_loop) {  // dX = G W0^T (+ per-source sum of the pair rows, fused when on tcgen05)
+      if (c.d->self_loop) {  // dX = G W0^T, then + the per-source sum of the pair rows
         GemmArgs b;
         b.A = Gt; b.a_dtype = c.dt; b.K = c.D; b.B = w->W0; b.b_dtype = c.dt; b.transB = true;
         b.Y = dX; b.y_dtype = F32; b.N = c.Din;
         b.num_w = 1; b.bt_scratch = sc.bt;
-        b.red_ptr = g->src_pair_ptr; b.red_list = g->src_pairs; b.red_rows = sc.dXp;
         b.name = "gemm_selfloop_dx";
-        fused = gemm(c, seg_all_nodes(g), b);
+        gemm(c, seg_all_nodes(g), b);
       }
-      if (!fused)
-        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, c.d->self_loop != 0, c.s);
+      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, c.d->self_loop != 0, c.s);
     }
     if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
@@ -348,20 +347,20 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
-      a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rel(g), a);
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
+      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
     }
     if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
-      const Plan& pp = plan(g, seg_pair_rel(g), WGRAD_ROWS, c.s);
+      const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
       seg_wsum(&pp, nullptr, sc.bx, F32, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
     }
     if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW || dW->db) rgat_tpath_grads(g->R, c.Din, c.D, w->W, w->b, c.dt, sc.Bsum, dW->dW, dW->db, c.s);
     if (dW->da) {
-      const Plan& pp = plan(g, seg_pair_rel(g), WGRAD_ROWS, c.s);
+      const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
@@ -372,7 +371,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = 2 * c.D; a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
       a.transB = true;
-      a.Y = sc.dXp; a.y_dtype = F32; a.N = c.Din;
+      a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rt(g), a);
@@ -380,10 +379,9 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
       q.Y = dX; q.y_dtype = F32; q.N = c.Din;
       q.num_w = g->T; q.bt_scratch = sc.bt;
-      q.red_ptr = g->src_pair_ptr; q.red_list = g->src_pairs; q.red_rows = sc.dXp;
       q.name = "gemm_nodes_dx";
-      if (!gemm(c, seg_node_type(g), q))
-        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.Din, dX, true, c.s);
+      gemm(c, seg_node_type(g), q);
+      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
     }
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {

@@ -63,7 +63,7 @@ void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int
               float* out, int num_w, float* partial, cudaStream_t s);
 
 // out[u][:] (+)= sum_{i in [ptr[u], ptr[u+1])} Y[list[i]][:]   (fp32 rows of width K)
-void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const float* Y, int K, float* out,
+void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const void* Y, int y_dtype, int K, float* out,
                      bool accumulate, cudaStream_t s);
 
 // A2 (linear-operator reordering): weight-weight products.
