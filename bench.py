@@ -226,6 +226,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm-impl", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-compact", action="store_true",
+                    help="vanilla materialization (one projected row per edge): the C ablation of tab:optimizations")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = BENCH_CONFIGS[args.config]
@@ -251,7 +253,7 @@ def main():
     model, d, dtype = cfg["model"], cfg["d"], cfg["dtype"]
     ranges = D.partition_ranges(g.dst, g.num_nodes, world)
     lo, hi = ranges[rank]
-    G = Graph.from_hetero(g, dst_range=(lo, hi) if world > 1 else None, device=dev)
+    G = Graph.from_hetero(g, dst_range=(lo, hi) if world > 1 else None, device=dev, compact=not args.no_compact)
     info = G.info()
     inp = layer_inputs(model, g, d, d)
     if dtype == "bf16":
@@ -417,7 +419,8 @@ def main():
                            g.num_nodes * d * (2 if dtype == 'bf16' else 4) / 1e9,
                            info["num_pairs"] * 2 * d * (2 if dtype == 'bf16' else 4) / 1e9,
                            g.num_edges * 4 * 9 / 1e9),
-                       "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl]},
+                       "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
+                       "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
         }

@@ -93,6 +93,23 @@ RGNN_API rgnn_status rgnn_graph_build(int64_t num_nodes, int32_t num_node_types,
                              const int32_t* rel, int64_t dst_lo, int64_t dst_hi, rgnn_alloc_fn alloc,
                              rgnn_free_fn free_fn, void* alloc_ctx, void* stream, rgnn_graph_t* out);
 
+/* Build options. */
+typedef struct {
+  int32_t compact;      /* 1: one projected row per distinct (relation, source) pair ("compact
+                           materialization", §3.3.2; the default of rgnn_graph_build);
+                           0: one row per edge ("vanilla materialization"): the "pairs" are the
+                           edges ordered by (rel, src, dst, eid), U = E, edge_pair a bijection. */
+  int32_t reserved[7];  /* must be 0 */
+} rgnn_graph_opts;
+
+/* rgnn_graph_build with options (NULL is not allowed; zero-initialise and set `compact`).
+ * Same arguments, contract and errors as rgnn_graph_build, plus INVALID_ARG for bad options. */
+RGNN_API rgnn_status rgnn_graph_build_opts(int64_t num_nodes, int32_t num_node_types, const int64_t* node_type_ptr,
+                                           int32_t num_rels, int64_t num_edges, const int32_t* src,
+                                           const int32_t* dst, const int32_t* rel, int64_t dst_lo, int64_t dst_hi,
+                                           const rgnn_graph_opts* opts, rgnn_alloc_fn alloc, rgnn_free_fn free_fn,
+                                           void* alloc_ctx, void* stream, rgnn_graph_t* out);
+
 typedef struct {
   int64_t num_nodes;
   int64_t num_edges;        /* edges kept (dst in [dst_lo, dst_hi)) */

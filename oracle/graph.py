@@ -21,7 +21,11 @@ from typing import Dict
 import numpy as np
 
 
-def build(num_nodes: int, num_rels: int, src: np.ndarray, dst: np.ndarray, rel: np.ndarray) -> Dict[str, np.ndarray]:
+def build(num_nodes: int, num_rels: int, src: np.ndarray, dst: np.ndarray, rel: np.ndarray,
+          compact: bool = True) -> Dict[str, np.ndarray]:
+    """C1 arrays.  compact=False is vanilla materialization ("the row number is the
+    edge index"): one row ("pair") per edge, rows in etype-sorted order with ties by
+    (src, dst, eid), so pair_rel_ptr = etype_ptr and edge_pair is a bijection."""
     src = np.asarray(src, np.int64)
     dst = np.asarray(dst, np.int64)
     rel = np.asarray(rel, np.int64)
@@ -37,10 +41,17 @@ def build(num_nodes: int, num_rels: int, src: np.ndarray, dst: np.ndarray, rel: 
     csc = np.lexsort((eid, dst, rel, src))
     col_ptr = np.concatenate([[0], np.cumsum(np.bincount(src, minlength=n))])
 
-    key = rel * n + src
-    ukey, edge_pair = np.unique(key, return_inverse=True)
-    pair_rel = ukey // n
-    pair_src = ukey % n
+    if compact:
+        key = rel * n + src
+        ukey, edge_pair = np.unique(key, return_inverse=True)
+        pair_rel = ukey // n
+        pair_src = ukey % n
+    else:
+        order = np.lexsort((eid, dst, src, rel))
+        edge_pair = np.empty(e, dtype=np.int64)
+        edge_pair[order] = np.arange(e)
+        pair_rel, pair_src = rel[order], src[order]
+        ukey = order
     pair_rel_ptr = np.concatenate([[0], np.cumsum(np.bincount(pair_rel, minlength=r))])
 
     i32 = lambda a: np.asarray(a, np.int32)

@@ -158,42 +158,62 @@ __global__ void __launch_bounds__(256) k_wgrad(const Tile* __restrict__ tiles, c
   }
 }
 
-// out[seg_w[s]][i] = sum over tiles of segment s (in order) of partial[tile][i]
-__global__ void k_seg_partial_reduce(int nseg, const int32_t* __restrict__ seg_tile_ptr, const int32_t* __restrict__ seg_w,
-                                     const float* __restrict__ partial, int64_t width, float* __restrict__ out) {
-  int sidx = blockIdx.y;
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (sidx >= nseg || i >= width) return;
+// out[seg_w[s]][i] = sum over the tiles of segment s of partial[tile][i].  Block = (segment, 32
+// consecutive elements); its 8 warps take interleaved tiles (lane = element), then the 8 warp sums
+// are added in warp order: a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) k_seg_partial_reduce(int nseg, const int32_t* __restrict__ seg_tile_ptr,
+                                                            const int32_t* __restrict__ seg_w,
+                                                            const float* __restrict__ partial, int64_t width,
+                                                            float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int sidx = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * (int64_t)32 + lane;
   float acc = 0.f;
-  for (int t = seg_tile_ptr[sidx]; t < seg_tile_ptr[sidx + 1]; ++t) acc += partial[(size_t)t * width + i];
-  out[(size_t)seg_w[sidx] * width + i] = acc;
+  if (i < width)
+    for (int t = seg_tile_ptr[sidx] + warp; t < seg_tile_ptr[sidx + 1]; t += 8) acc += partial[(size_t)t * width + i];
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && i < width) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][lane];
+    out[(size_t)seg_w[sidx] * width + i] = s;
+  }
 }
 
 // per tile: partial[tile][k] = sum_rows wt[row] * A[gather(row)][k] (wt == NULL: weight 1).
-// 256 threads = RG row groups x K columns; each group strides over the tile's rows, the groups'
-// sums are combined in group order through shared memory (deterministic).
+// Lanes move 16-byte vectors: LPR = K / V lanes per row, RG = 256 / LPR row groups striding over
+// the tile's rows; the groups' sums are combined in group order in shared memory (deterministic).
 template <class TA>
 __global__ void __launch_bounds__(256) k_seg_wsum(const Tile* __restrict__ tiles, const float* __restrict__ wt,
                                                   const TA* __restrict__ A, int K, const int32_t* __restrict__ gather,
                                                   float* __restrict__ partial) {
-  __shared__ float red[256];
+  constexpr int V = Vec<TA>::N;
+  __shared__ __align__(16) float red[256 * V];
   const Tile t = tiles[blockIdx.x];
-  const int RG = blockDim.x / K, k = threadIdx.x % K, rg = threadIdx.x / K;
-  float acc = 0.f;
+  const int LPR = K / V, RG = 256 / LPR;
+  const int c = threadIdx.x % LPR, rg = threadIdx.x / LPR;
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
   if (rg < RG) {
-#pragma unroll 4
+#pragma unroll 2
     for (int r = t.row0 + rg; r < t.row1; r += RG) {
       int64_t ar = gather ? (int64_t)gather[r] : (int64_t)r;
-      float x = to_f(A[ar * K + k]);
-      acc = wt ? fmaf(wt[r], x, acc) : acc + x;
+      float x[V];
+      cvt16<TA>(ldg16(A + ar * K + c * V), x);
+      const float wr = wt ? wt[r] : 1.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wr, x[k], acc[k]);
     }
   }
-  red[threadIdx.x] = acc;
+#pragma unroll
+  for (int k = 0; k < V; ++k) red[threadIdx.x * V + k] = acc[k];
   __syncthreads();
-  if (threadIdx.x < K) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
     float sum = 0.f;
-    for (int g = 0; g < RG; ++g) sum += red[g * K + threadIdx.x];
-    partial[(size_t)blockIdx.x * K + threadIdx.x] = sum;
+    for (int g = 0; g < RG; ++g) sum += red[(g * LPR + k / V) * V + k % V];
+    partial[(size_t)blockIdx.x * K + k] = sum;
   }
 }
 
@@ -367,7 +387,7 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   if (a.allow_tc && wgrad_tc_supported(a)) {
     wgrad_tc(a, s);
     int64_t width = (int64_t)a.K1 * a.K2;
-    launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,
+    launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
            p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
     return;
   }
@@ -382,23 +402,24 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   else if (b32) go(static_cast<const bf16*>(a.A), static_cast<const float*>(a.Bm));
   else go(static_cast<const bf16*>(a.A), static_cast<const bf16*>(a.Bm));
   int64_t width = (int64_t)a.K1 * a.K2;
-  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 256), p.nseg), dim3(256), 0, s, p.nseg,
+  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
          p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
 }
 
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather, float* out,
               int num_w, float* partial, cudaStream_t s) {
   const Plan& p = *plan;
-  RGNN_CHECK(K >= 1 && K <= 256, RGNN_ERR_UNSUPPORTED, "seg_wsum: K must be <= 256");
+  RGNN_CHECK(K % (a_dtype == F32 ? 4 : 8) == 0 && K <= (a_dtype == F32 ? 1024 : 2048), RGNN_ERR_UNSUPPORTED,
+             "seg_wsum: K must be a multiple of the 16-byte vector width");
   RGNN_CUDA(cudaMemsetAsync(out, 0, (size_t)num_w * K * sizeof(float), s));
   if (p.count == 0) return;
   if (a_dtype == F32)
-    launch("seg_wsum", k_seg_wsum<float>, dim3(p.count), dim3(256 / K * K), 0, s, p.tiles, wt,
+    launch("seg_wsum", k_seg_wsum<float>, dim3(p.count), dim3(256), 0, s, p.tiles, wt,
            static_cast<const float*>(A), K, gather, partial);
   else
-    launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(256 / K * K), 0, s, p.tiles, wt,
+    launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(256), 0, s, p.tiles, wt,
            static_cast<const bf16*>(A), K, gather, partial);
-  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(K, 256), p.nseg), dim3(256), 0, s, p.nseg,
+  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(K, 32), p.nseg), dim3(256), 0, s, p.nseg,
          p.seg_tile_ptr, p.seg_w, partial, (int64_t)K, out);
 }
 

@@ -46,6 +46,7 @@ struct rgnn_graph_s {
   int32_t T = 0, R = 0;
   int64_t dst_lo = 0, dst_hi = 0;
   int64_t max_in_deg = 0, max_pair_deg = 0;
+  int compact = 1;  // 1: rows per distinct (rel, src) pair; 0: one row per edge (vanilla materialization)
   int nb = 0, rb = 0;  // key bit widths
 
   std::vector<int64_t> node_type_ptr;    // host [T+1]

@@ -142,7 +142,20 @@ rgnn_status rgnn_graph_build(int64_t num_nodes, int32_t num_node_types, const in
                              int32_t num_rels, int64_t num_edges, const int32_t* src, const int32_t* dst,
                              const int32_t* rel, int64_t dst_lo, int64_t dst_hi, rgnn_alloc_fn alloc,
                              rgnn_free_fn free_fn, void* alloc_ctx, void* stream, rgnn_graph_t* out) {
+  rgnn_graph_opts opts{};
+  opts.compact = 1;
+  return rgnn_graph_build_opts(num_nodes, num_node_types, node_type_ptr, num_rels, num_edges, src, dst, rel, dst_lo,
+                               dst_hi, &opts, alloc, free_fn, alloc_ctx, stream, out);
+}
+
+rgnn_status rgnn_graph_build_opts(int64_t num_nodes, int32_t num_node_types, const int64_t* node_type_ptr,
+                                  int32_t num_rels, int64_t num_edges, const int32_t* src, const int32_t* dst,
+                                  const int32_t* rel, int64_t dst_lo, int64_t dst_hi, const rgnn_graph_opts* opts,
+                                  rgnn_alloc_fn alloc, rgnn_free_fn free_fn, void* alloc_ctx, void* stream,
+                                  rgnn_graph_t* out) {
   return guarded([&] {
+    RGNN_CHECK(opts != nullptr && (opts->compact == 0 || opts->compact == 1), RGNN_ERR_INVALID_ARG,
+               "opts->compact must be 0 or 1");
     RGNN_CHECK(out != nullptr, RGNN_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     RGNN_CHECK(num_nodes >= 1 && num_node_types >= 1 && num_rels >= 1 && num_edges >= 0, RGNN_ERR_INVALID_ARG,
@@ -166,6 +179,7 @@ rgnn_status rgnn_graph_build(int64_t num_nodes, int32_t num_node_types, const in
     g->dst_lo = dst_lo;
     g->dst_hi = dst_hi;
     g->node_type_ptr.assign(node_type_ptr, node_type_ptr + num_node_types + 1);
+    g->compact = opts->compact;
     try {
       build_graph(g, src, dst, rel, num_edges, static_cast<cudaStream_t>(stream));
     } catch (...) {

@@ -66,11 +66,11 @@ __global__ void k_histogram(int64_t E, const int32_t* v, int32_t* count) {
   if (i < E) atomicAdd(&count[v[i]], 1);  // integer: order-independent result
 }
 
-// heads of runs of equal (a, b) in a sorted sequence
-__global__ void k_run_heads(int64_t E, const int32_t* a, const int32_t* b, int32_t* flag) {
+// heads of runs of equal (a, b) in a sorted sequence (every position when `all`)
+__global__ void k_run_heads(int64_t E, const int32_t* a, const int32_t* b, int32_t* flag, bool all) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= E) return;
-  flag[i] = (i == 0) || a[i] != a[i - 1] || b[i] != b[i - 1];
+  flag[i] = all || (i == 0) || a[i] != a[i - 1] || b[i] != b[i - 1];
 }
 
 __global__ void k_run_info(int64_t nruns, int64_t E, const int32_t* head_pos, const int32_t* a, const int32_t* b,
@@ -356,9 +356,11 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   int32_t* head_pos = tmp.get<int32_t>(E);
   int32_t* dflag = tmp.get<int32_t>(E);
   int32_t* dhead_pos = tmp.get<int32_t>(E);
-  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csc_src, g->csc_rel, flag);
+  // compact materialization: one pair per run of equal (src, rel); vanilla: one "pair" per edge
+  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csc_src, g->csc_rel, flag,
+         !g->compact);
   select_flagged(tmp, flag, head_pos, d_num, E, s);
-  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csr_dst, g->csr_rel, dflag);
+  launch("graph_heads", k_run_heads, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, csr_dst, g->csr_rel, dflag, false);
   select_flagged(tmp, dflag, dhead_pos, d_num + 1, E, s);
   int32_t h_counts[2] = {0, 0};
   RGNN_CUDA(cudaMemcpyAsync(h_counts, d_num, sizeof(h_counts), cudaMemcpyDeviceToHost, s));

@@ -25,7 +25,8 @@ DTYPES = {"f32": F32, "bf16": BF16}
 NORMS = {"mean": 0, "sym": 1, "none": 2, "custom": 3}
 ARRAYS = ["etype_ptr", "row_ptr", "csr_src", "csr_rel", "csr_eid", "col_ptr", "csc_dst", "csc_rel", "csc_eid",
           "pair_rel_ptr", "pair_src", "edge_pair", "csr_pair", "csc_pair"]
-EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_get_info", "rgnn_graph_export",
+EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_build_opts", "rgnn_graph_get_info",
+            "rgnn_graph_export",
             "rgnn_graph_array_size", "rgnn_graph_destroy", "rgnn_layer_workspace", "rgnn_layer_forward",
             "rgnn_layer_backward", "rgnn_profile_enable", "rgnn_profile_reset", "rgnn_profile_read",
             "rgnn_launch_count"]
@@ -39,6 +40,10 @@ class GraphInfo(C.Structure):
                 ("max_in_degree", C.c_int64), ("max_pair_degree", C.c_int64), ("dst_lo", C.c_int64),
                 ("dst_hi", C.c_int64), ("num_node_types", C.c_int32), ("num_rels", C.c_int32),
                 ("compaction_ratio", C.c_double)]
+
+
+class GraphOptsC(C.Structure):
+    _fields_ = [("compact", C.c_int32), ("reserved", C.c_int32 * 7)]
 
 
 class LayerDescC(C.Structure):
@@ -85,6 +90,10 @@ def lib() -> C.CDLL:
         L.rgnn_graph_build.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int64,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, ALLOC_FN, FREE_FN,
                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.rgnn_graph_build_opts.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int64,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                            C.POINTER(GraphOptsC), ALLOC_FN, FREE_FN, C.c_void_p, C.c_void_p,
+                                            C.POINTER(C.c_void_p)]
         L.rgnn_graph_get_info.argtypes = [C.c_void_p, C.POINTER(GraphInfo)]
         L.rgnn_graph_export.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
         L.rgnn_graph_array_size.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64)]
@@ -153,10 +162,11 @@ class _TorchAllocator:
 
 
 class Graph:
-    """A built typed graph (rgnn_graph_build).  src/dst/rel: int32 tensors (moved to the device)."""
+    """A built typed graph (rgnn_graph_build_opts).  src/dst/rel: int32 tensors (moved to the device).
+    compact=False builds vanilla materialization (one projected row per edge) for the C ablation."""
 
     def __init__(self, num_nodes: int, node_type_ptr, num_rels: int, src: torch.Tensor, dst: torch.Tensor,
-                 rel: torch.Tensor, dst_range=None, device="cuda"):
+                 rel: torch.Tensor, dst_range=None, device="cuda", compact: bool = True):
         self.device = torch.device(device)
         self._alloc = _TorchAllocator(self.device)
         ntp = (C.c_int64 * len(node_type_ptr))(*[int(x) for x in node_type_ptr])
@@ -166,18 +176,21 @@ class Graph:
         lo, hi = (0, int(num_nodes)) if dst_range is None else (int(dst_range[0]), int(dst_range[1]))
         h = C.c_void_p()
         e = int(src.numel())
-        _check(lib().rgnn_graph_build(int(num_nodes), len(node_type_ptr) - 1, ntp, int(num_rels), e,
-                                      src.data_ptr() if e else None, dst.data_ptr() if e else None,
-                                      rel.data_ptr() if e else None, lo, hi, self._alloc.alloc_cb,
-                                      self._alloc.free_cb, None, _stream(), C.byref(h)))
+        opts = GraphOptsC()
+        opts.compact = int(bool(compact))
+        _check(lib().rgnn_graph_build_opts(int(num_nodes), len(node_type_ptr) - 1, ntp, int(num_rels), e,
+                                           src.data_ptr() if e else None, dst.data_ptr() if e else None,
+                                           rel.data_ptr() if e else None, lo, hi, C.byref(opts),
+                                           self._alloc.alloc_cb, self._alloc.free_cb, None, _stream(), C.byref(h)))
         self.handle = h
         self.node_type_ptr = [int(x) for x in node_type_ptr]
 
     @classmethod
-    def from_hetero(cls, g, dst_range=None, device="cuda") -> "Graph":
+    def from_hetero(cls, g, dst_range=None, device="cuda", compact: bool = True) -> "Graph":
         """From a synth.HeteroGraph-like object (node_type_ptr, num_rels, src, dst, rel)."""
         return cls(int(g.node_type_ptr[-1]), list(g.node_type_ptr), int(g.num_rels), torch.from_numpy(g.src),
-                   torch.from_numpy(g.dst), torch.from_numpy(g.rel), dst_range=dst_range, device=device)
+                   torch.from_numpy(g.dst), torch.from_numpy(g.rel), dst_range=dst_range, device=device,
+                   compact=compact)
 
     def info(self) -> Dict[str, float]:
         i = GraphInfo()

@@ -73,3 +73,15 @@ def test_empty_and_errors():
 @pytest.mark.slow
 def test_mag_bit_exact():
     _check(config_graph("mag", seed=1))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_vanilla_build_bit_exact(seed):
+    """compact=0: vanilla materialization, one row per edge, bit-exact vs the oracle."""
+    from paper_2412_04747_b200 import Graph
+    g = random_small_graph(300 + seed, allow_multi=(seed % 2 == 0)) if seed < 10 else config_graph("tiny", seed=seed)
+    G = Graph.from_hetero(g, compact=False)
+    ref = og.build(g.num_nodes, g.num_rels, g.src, g.dst, g.rel, compact=False)
+    assert G.info()["num_pairs"] == g.num_edges
+    for name in ARRAYS:
+        assert np.array_equal(G.export(name).cpu().numpy().astype(np.int64), np.asarray(ref[name], np.int64)), name

@@ -16,7 +16,7 @@ from tests.helpers import TOL, prepare, rel_err, to_device
 pytestmark = pytest.mark.gpu
 
 
-def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0):
+def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0, compact=True):
     from paper_2412_04747_b200 import Graph, Layer
     inp = prepare(layer_inputs(model, g, d_in, d_out, seed_x=2 + seed, seed_w=3 + seed), dtype)
     Gh = upstream_grad(g.num_nodes, d_out, seed=4 + seed)
@@ -26,7 +26,7 @@ def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_imp
     ref_out, _ = L.forward(model, g, inp, **kw)
     ref_grads = L.backward(model, g, inp, Gh, **kw)
 
-    G = Graph.from_hetero(g)
+    G = Graph.from_hetero(g, compact=compact)
     layer = Layer(G, model, d_in, d_out, dtype=dtype, self_loop=self_loop, norm=norm, gemm_impl=gemm_impl)
     dev = to_device(inp, dtype)
     X = dev.pop("X")
@@ -143,3 +143,10 @@ def test_split_heavy_pairs(model, dtype):
     b = og.build(g.num_nodes, g.num_rels, g.src, g.dst, g.rel)
     assert np.bincount(b["edge_pair"]).max() > 1024
     run_case(model, g, 32, 32, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+def test_vanilla_materialization(model, dtype):
+    """compact=0 (one projected row per edge) gives the same layer (compaction is exact)."""
+    run_case(model, config_graph("aifb", seed=2, scale=0.5), 64, 64, dtype, compact=False)

@@ -113,3 +113,23 @@ def test_generator_compaction_calibration():
     b = og.build(g.num_nodes, g.num_rels, g.src, g.dst, g.rel)
     ratio = og.compaction_ratio(int(b["num_pairs"]), g.num_edges)
     assert 0.45 < ratio < 0.70, ratio
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_vanilla_build_matches_brute_force(seed):
+    """Vanilla materialization: one row per edge, rows ordered by (rel, src, dst, eid)."""
+    g = random_small_graph(seed, allow_multi=(seed % 3 == 0))
+    b = og.build(g.num_nodes, g.num_rels, g.src, g.dst, g.rel, compact=False)
+    rows = sorted(range(g.num_edges), key=lambda e: (int(g.rel[e]), int(g.src[e]), int(g.dst[e]), e))
+    assert int(b["num_pairs"]) == g.num_edges
+    assert list(b["pair_src"]) == [int(g.src[e]) for e in rows]
+    assert list(b["pair_rel_ptr"]) == list(b["etype_ptr"])
+    assert sorted(b["edge_pair"].tolist()) == list(range(g.num_edges))
+    for k, e in enumerate(rows):
+        assert b["edge_pair"][e] == k
+
+
+def test_vanilla_g7_seven_rows():
+    g = g7()
+    b = og.build(g.num_nodes, g.num_rels, g.src, g.dst, g.rel, compact=False)
+    assert int(b["num_pairs"]) == 7   # "the materialized tensor involves seven rows" (P:771)
