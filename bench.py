@@ -226,6 +226,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm-impl", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cuda-graph", action="store_true",
+                    help="N=1: capture one fwd+bwd step in a CUDA graph and replay it (launch-bound small graphs); "
+                         "per-kernel times then come from a separate un-captured profiling pass")
     ap.add_argument("--no-compact", action="store_true",
                     help="vanilla materialization (one projected row per edge): the C ablation of tab:optimizations")
     args = ap.parse_args()
@@ -286,24 +289,38 @@ def main():
     for _ in range(args.warmup):
         step(X_own)
     torch.cuda.synchronize()
+    graph = None
+    if args.cuda_graph and world == 1:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            step(X_own)  # warm the capture stream
+        torch.cuda.current_stream().wait_stream(cs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(X_own)
+        torch.cuda.synchronize()
 
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.15)
 
-    def timed(K):
+    def timed(K, use_graph=False):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         rgnn.profile_reset()
-        rgnn.profile_enable(True)
+        rgnn.profile_enable(not use_graph)
         n0 = rgnn.launch_count()
         s = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.time()
         e0.record(s)
         for _ in range(K):
-            step(X_own)
+            if use_graph:
+                graph.replay()
+            else:
+                step(X_own)
         e1.record(s)
         torch.cuda.synchronize()
         t1 = time.time()
@@ -315,15 +332,18 @@ def main():
         ms = e0.elapsed_time(e1)
         return ms, launches, prof, t0, t1
 
-    ms, launches, prof, t0, t1 = timed(args.steps)
+    use_graph = graph is not None
+    ms, launches, prof, t0, t1 = timed(args.steps, use_graph)
     time.sleep(0.12)
     clocks = sampler.summary(t0, t1)
     remeasured = False
     if set(clocks["reasons"]) & BAD_REASONS:
         remeasured = True
-        ms, launches, prof, t0, t1 = timed(args.steps)
+        ms, launches, prof, t0, t1 = timed(args.steps, use_graph)
         time.sleep(0.12)
         clocks = sampler.summary(t0, t1)
+    if use_graph:  # launches inside the graph: counted and profiled on an un-captured pass
+        _, launches, prof, _, _ = timed(args.steps, False)
     sampler.stop()
     if world > 1:
         tms = torch.tensor([ms], device=dev)
@@ -420,7 +440,8 @@ def main():
                            info["num_pairs"] * 2 * d * (2 if dtype == 'bf16' else 4) / 1e9,
                            g.num_edges * 4 * 9 / 1e9),
                        "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
-                       "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)"},
+                       "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
+                       "cuda_graph": bool(use_graph)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
         }
