@@ -29,7 +29,13 @@ namespace rgnn {
 namespace {
 
 constexpr int UNR = 4;    // edges per group loaded ahead (dst-major and pair kernels)
-constexpr int UNR_P = 2;  // HGT pair kernel: two 16-byte row halves + a node record per edge
+#ifndef RGNN_UNR_P
+#define RGNN_UNR_P 2
+#endif
+#ifndef RGNN_PAIR_MINB
+#define RGNN_PAIR_MINB 3
+#endif
+constexpr int UNR_P = RGNN_UNR_P;  // pair kernels with node records: two 16-byte row halves + a record per edge
 
 template <class TP, int D>
 struct Geo {
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* _
 }
 
 template <class TP, int D, bool GROUP>
-__global__ void __launch_bounds__(256, 3) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
+__global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                           float* __restrict__ pacc, float2* __restrict__ pstat,
                                                           const int32_t* __restrict__ csc_dst,
                                                           const int32_t* __restrict__ csc_rel,
@@ -731,7 +737,7 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __
 
 // One lane moves 16 bytes of the G half and 16 bytes of the Q half of a GQ row (V columns each).
 template <class TP, int D, bool GROUP>
-__global__ void __launch_bounds__(256, 3) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
+__global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                       const TP* __restrict__ KM, const TP* __restrict__ GQ,
                                                       const float4* __restrict__ nst, TP* __restrict__ dKM) {
