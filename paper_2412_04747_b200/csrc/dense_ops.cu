@@ -294,48 +294,72 @@ __global__ void k_hgt_fold(int R, int T, int d_in, int d, const TW* Wk, const TW
   }
 }
 
-// Unfold dF[r*T+t] (d_in x 2d) into the four HGT weight gradients (fixed summation order).
+// Unfold dF[r*T+t] (d_in x 2d) into the four HGT weight gradients.  Block = 32 consecutive
+// outputs (lane) x 8 warps that split the reduction range; the warp partials are added in warp
+// order through shared memory (fixed order: deterministic).
+//   dWk[t][k][j] = sum_r c_r sum_n dF[rt][k][n] Watt[r][j][n],  dWv[t][k][j] = sum_r sum_n dF[rt][k][d+n] Wmsg[r][j][n]
 template <class TW>
-__global__ void k_hgt_unfold_node(int R, int T, int d_in, int d, const TW* Watt, const TW* Wmsg, const float* mu,
-                                  const float* dF, float* dWk, float* dWv) {
-  // one thread per (t, k, j) of dWk / dWv
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)T * d_in * d) return;
-  int t = idx / (d_in * d), k = (idx / d) % d_in, j = idx % d;
+__global__ void __launch_bounds__(256) k_hgt_unfold_node(int R, int T, int d_in, int d, const TW* Watt,
+                                                         const TW* Wmsg, const float* mu, const float* dF,
+                                                         float* dWk, float* dWv) {
+  __shared__ float rk[8][33], rv[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t idx = blockIdx.x * (int64_t)32 + lane;
+  const bool ok = idx < (int64_t)T * d_in * d;
+  const int t = ok ? idx / (d_in * d) : 0, k = ok ? (idx / d) % d_in : 0, j = ok ? idx % d : 0;
   float ak = 0.f, av = 0.f;
-  for (int r = 0; r < R; ++r) {
+  for (int q = warp; q < R * d; q += 8) {  // q = (r, n)
+    const int r = q / d, n = q % d;
     const float* f = dF + ((size_t)(r * T + t) * d_in + k) * 2 * d;
-    float c = mu[r] * rsqrtf((float)d);
-    float sk = 0.f, sv = 0.f;
-    for (int n = 0; n < d; ++n) {
-      sk = fmaf(f[n], to_f(Watt[((size_t)r * d + j) * d + n]), sk);
-      sv = fmaf(f[d + n], to_f(Wmsg[((size_t)r * d + j) * d + n]), sv);
-    }
-    ak = fmaf(c, sk, ak);
-    av += sv;
+    const float c = mu[r] * rsqrtf((float)d);
+    ak = fmaf(c * f[n], to_f(Watt[((size_t)r * d + j) * d + n]), ak);
+    av = fmaf(f[d + n], to_f(Wmsg[((size_t)r * d + j) * d + n]), av);
   }
-  if (dWk) dWk[idx] = ak;
-  if (dWv) dWv[idx] = av;
+  rk[warp][lane] = ak;
+  rv[warp][lane] = av;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float sk = 0.f, sv = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      sk += rk[w][lane];
+      sv += rv[w][lane];
+    }
+    if (dWk) dWk[idx] = sk;
+    if (dWv) dWv[idx] = sv;
+  }
 }
 
+//   dWatt[r][j][n] = c_r sum_t sum_k Wk[t][k][j] dF[rt][k][n],  dWmsg[r][j][n] = sum_t sum_k Wv[t][k][j] dF[rt][k][d+n]
 template <class TW>
-__global__ void k_hgt_unfold_rel(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const float* mu,
-                                 const float* dF, float* dWatt, float* dWmsg) {
-  // one thread per (r, j, n)
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)R * d * d) return;
-  int r = idx / (d * d), j = (idx / d) % d, n = idx % d;
-  float c = mu[r] * rsqrtf((float)d);
+__global__ void __launch_bounds__(256) k_hgt_unfold_rel(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv,
+                                                        const float* mu, const float* dF, float* dWatt,
+                                                        float* dWmsg) {
+  __shared__ float rk[8][33], rv[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t idx = blockIdx.x * (int64_t)32 + lane;
+  const bool ok = idx < (int64_t)R * d * d;
+  const int r = ok ? idx / (d * d) : 0, j = ok ? (idx / d) % d : 0, n = ok ? idx % d : 0;
   float ak = 0.f, av = 0.f;
-  for (int t = 0; t < T; ++t) {
-    const float* f = dF + (size_t)(r * T + t) * d_in * 2 * d;
-    for (int k = 0; k < d_in; ++k) {
-      ak = fmaf(to_f(Wk[((size_t)t * d_in + k) * d + j]), f[(size_t)k * 2 * d + n], ak);
-      av = fmaf(to_f(Wv[((size_t)t * d_in + k) * d + j]), f[(size_t)k * 2 * d + d + n], av);
-    }
+  for (int q = warp; q < T * d_in; q += 8) {  // q = (t, k)
+    const int t = q / d_in, k = q % d_in;
+    const float* f = dF + ((size_t)(r * T + t) * d_in + k) * 2 * d;
+    ak = fmaf(to_f(Wk[((size_t)t * d_in + k) * d + j]), f[n], ak);
+    av = fmaf(to_f(Wv[((size_t)t * d_in + k) * d + j]), f[d + n], av);
   }
-  if (dWatt) dWatt[idx] = c * ak;
-  if (dWmsg) dWmsg[idx] = av;
+  rk[warp][lane] = ak;
+  rv[warp][lane] = av;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float sk = 0.f, sv = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      sk += rk[w][lane];
+      sv += rv[w][lane];
+    }
+    if (dWatt) dWatt[idx] = mu[r] * rsqrtf((float)d) * sk;
+    if (dWmsg) dWmsg[idx] = sv;
+  }
 }
 
 // dW_r += Bsum_r^T b_r (outer product, destination side of the t-path); db_r = Bsum_r W_r
@@ -477,17 +501,17 @@ void hgt_unfold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, c
   int64_t nn = (int64_t)T * d_in * d, nr = (int64_t)R * d * d;
   if (dtype == F32) {
     if (dWk || dWv)
-      launch("hgt_unfold_node", k_hgt_unfold_node<float>, dim3(ceil_div(nn, 128)), dim3(128), 0, s, R, T, d_in, d,
+      launch("hgt_unfold_node", k_hgt_unfold_node<float>, dim3(ceil_div(nn, 32)), dim3(256), 0, s, R, T, d_in, d,
              static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, dF, dWk, dWv);
     if (dWatt || dWmsg)
-      launch("hgt_unfold_rel", k_hgt_unfold_rel<float>, dim3(ceil_div(nr, 128)), dim3(128), 0, s, R, T, d_in, d,
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<float>, dim3(ceil_div(nr, 32)), dim3(256), 0, s, R, T, d_in, d,
              static_cast<const float*>(Wk), static_cast<const float*>(Wv), mu, dF, dWatt, dWmsg);
   } else {
     if (dWk || dWv)
-      launch("hgt_unfold_node", k_hgt_unfold_node<bf16>, dim3(ceil_div(nn, 128)), dim3(128), 0, s, R, T, d_in, d,
+      launch("hgt_unfold_node", k_hgt_unfold_node<bf16>, dim3(ceil_div(nn, 32)), dim3(256), 0, s, R, T, d_in, d,
              static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, dF, dWk, dWv);
     if (dWatt || dWmsg)
-      launch("hgt_unfold_rel", k_hgt_unfold_rel<bf16>, dim3(ceil_div(nr, 128)), dim3(128), 0, s, R, T, d_in, d,
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<bf16>, dim3(ceil_div(nr, 32)), dim3(256), 0, s, R, T, d_in, d,
              static_cast<const bf16*>(Wk), static_cast<const bf16*>(Wv), mu, dF, dWatt, dWmsg);
   }
 }

@@ -33,7 +33,7 @@ constexpr int UNR = 4;    // edges per group loaded ahead (dst-major and pair ke
 #define RGNN_UNR_P 2
 #endif
 #ifndef RGNN_PAIR_MINB
-#define RGNN_PAIR_MINB 3
+#define RGNN_PAIR_MINB 4
 #endif
 constexpr int UNR_P = RGNN_UNR_P;  // pair kernels with node records: two 16-byte row halves + a record per edge
 
