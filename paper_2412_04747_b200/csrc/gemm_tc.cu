@@ -16,6 +16,9 @@
 // (32 flop/B vs a ~213 flop/B ridge), so the design goal is bytes in flight.
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace rgnn {
@@ -66,6 +69,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent warp-specialized GEMM (k_gemm_ws) unless RGNN_GEMM_WS=0 in the environment.
+bool ws_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RGNN_GEMM_WS");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 template <int NCOLS>
@@ -408,8 +425,197 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
          static_cast<const bf16*>(a.Bm), a.partial);
 }
 
+// ------------------------------------------------------------------ persistent warp-specialized GEMM
+// One CTA per SM loops over tiles (static round robin).  Warps 0-1 gather the A rows
+// (X[gather(row)]) and the segment's K-major weight rows of one (tile, 64-wide K block) per smem
+// stage with cp.async (S stages in a ring; a stage is released to the MMA warp after the
+// producers' own copies landed and were fenced for the async proxy); warp 2 issues the
+// tcgen05.mma (M = 128, N, K = 16) into one of two TMEM accumulators and commits the stage back
+// to the producers and the accumulator to the epilogue; warps 4-7 drain the accumulator of the
+// previous tile (tcgen05.ld, per-row dot epilogue, bf16/fp32 pack, swizzled per-warp smem
+// staging, coalesced row stores) while the next tile is gathered and multiplied.
+template <int N, class TY>
+struct WsCfg {
+  static constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  static constexpr uint32_t A_BYTES = 128 * 128;
+  static constexpr uint32_t B_BYTES = N * 128;
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr uint32_t RB = N * sizeof(TY);          // output row bytes
+  static constexpr uint32_t STAGING = 4 * 32 * RB;        // epilogue staging, 4 warps x 32 rows
+  static constexpr int S = (int)((200 * 1024 - STAGING) / STAGE) < 8 ? (int)((200 * 1024 - STAGING) / STAGE) : 8;
+  static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + STAGING + 256;
+};
+
+template <class TY, int N, int KB>
+__global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ tiles, int ntiles,
+                                                    const bf16* __restrict__ A, const int32_t* __restrict__ gather,
+                                                    const bf16* __restrict__ Bt, TY* __restrict__ Y,
+                                                    const float* __restrict__ dotvec, float* __restrict__ dotout) {
+  using C = WsCfg<N, TY>;
+  constexpr int K = KB * 64, S = C::S, CH = C::RB / 16;
+  static_assert(S >= 2, "not enough shared memory for two stages");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* staging = smem + S * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t s_base = smem_u32(smem);
+
+  if (warp == 3) tmem_alloc<2 * C::NCOLS>(tslot);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 64);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp < 2) {
+    // ------------------------------------------------ producers (64 threads)
+    int st = 0, prev = -1;
+    uint32_t ph = 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      const Tile t = tiles[ti];
+      const int nrows = t.row1 - t.row0;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[st], ph ^ 1);
+        const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
+#pragma unroll 4
+        for (int idx = tid; idx < 128 * 8; idx += 64) {
+          const int r = idx >> 3, c = idx & 7;
+          const int rr = r < nrows ? r : nrows - 1;
+          const int64_t src = gather ? (int64_t)gather[t.row0 + rr] : (int64_t)(t.row0 + rr);
+          cp_async16(sa + r * 128 + ((c ^ (r & 7)) << 4), A + src * K + kb * 64 + c * 8);
+        }
+        const bf16* Bw = Bt + (size_t)t.w * N * K;
+#pragma unroll 4
+        for (int idx = tid; idx < N * 8; idx += 64) {
+          const int r = idx >> 3, c = idx & 7;
+          cp_async16(sb + r * 128 + ((c ^ (r & 7)) << 4), Bw + (int64_t)r * K + kb * 64 + c * 8);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (prev >= 0) {  // the previous stage's copies have landed: hand it to the MMA warp
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_arrive(&full[prev]);
+        }
+        prev = st;
+        if (++st == S) { st = 0; ph ^= 1; }
+      }
+    }
+    if (prev >= 0) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(&full[prev]);
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(N);
+      int st = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);  // the epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d_tmem = tmem + acc * C::NCOLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+          umma_commit(&empty[st]);  // stage free once these MMAs have read it
+          if (++st == S) { st = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull[acc]);  // accumulator complete
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (4 warps, TMEM lane quarter warp % 4)
+    const int q = warp & 3;
+    uint8_t* stg = staging + q * 32 * C::RB;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      const Tile t = tiles[ti];
+      const int nrows = t.row1 - t.row0;
+      const int r = q * 32 + lane;
+      const bool valid = r < nrows;
+      const int64_t row = t.row0 + r;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      float dot = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < N; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + acc * C::NCOLS + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (dotvec) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
+        }
+        stage_row32<CH>(stg + lane * C::RB, lane, c0 * (int)sizeof(TY) / 16, v, (TY*)nullptr);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&tempty[acc]);  // TMEM reads done: the MMA warp may reuse this accumulator
+      if (dotvec && valid) dotout[row] = dot;
+      __syncwarp();
+      const int rows_here = min(32, nrows - q * 32);
+      uint8_t* ybase = reinterpret_cast<uint8_t*>(Y) + (t.row0 + (int64_t)q * 32) * C::RB;
+#pragma unroll 4
+      for (int k = lane; k < 32 * CH; k += 32) {
+        const int rr = k / CH, j = k % CH;
+        if (rr < rows_here)
+          *reinterpret_cast<uint4*>(ybase + (int64_t)rr * C::RB + j * 16) =
+              *reinterpret_cast<const uint4*>(stg + rr * C::RB + ((j ^ (rr & (CH - 1))) << 4));
+      }
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 3) tmem_dealloc<2 * C::NCOLS>(tmem);
+}
+
+template <class TY, int N, int KB>
+void launch_ws(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  using C = WsCfg<N, TY>;
+  auto k = k_gemm_ws<TY, N, KB>;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    RGNN_CUDA(cudaGetDevice(&dev));
+    RGNN_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  }
+  const int grid = std::min(a.ntiles, num_sms);
+  launch(a.name, k, dim3(grid), dim3(256), C::SMEM, s, a.tiles, a.ntiles, static_cast<const bf16*>(a.A), a.gather, Bt,
+         static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+}
+
 template <class TY, int N, int KB>
 void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  if constexpr (WsCfg<N, TY>::S >= 2) {
+    if (a.red_ptr == nullptr && ws_enabled()) {
+      launch_ws<TY, N, KB>(a, Bt, s);
+      return;
+    }
+  }
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   // operands, reused by the epilogue's row staging (128 rows x N x sizeof(TY)) once the MMAs are done
   size_t smem = 1024 + std::max<size_t>(KB * (128 * 128 + N * 128), 128 * N * sizeof(TY)) + 64;
