@@ -75,14 +75,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Persistent warp-specialized GEMM (k_gemm_ws) unless RGNN_GEMM_WS=0 in the environment.
-bool ws_enabled() {
+// Persistent warp-specialized GEMM (k_gemm_ws) for contiguous A rows; the gathered GEMM
+// (A = X[pair_src]) stays on k_gemm_tc, whose ~9 resident CTAs per SM keep more independent
+// row gathers in flight (measured on B200: ws 0.30 vs 0.24 ms for mag pairs_fwd, while ws wins
+// 5-17% on the ungathered GEMMs).  RGNN_GEMM_WS=0: never ws; RGNN_GEMM_WS=2: ws for all.
+int ws_mode() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("RGNN_GEMM_WS");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }
-  return on == 1;
+  return on;
 }
 
 template <int NCOLS>
@@ -195,15 +198,21 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
 
   // ---- gather A rows and B rows into swizzled smem (8 lanes per 128-byte row: coalesced)
   const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+  // the 8 gathered row indices of this thread, loaded together before any copy is issued
+  int64_t src_row[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = (it * 128 + tid) >> 3;
+    const int rr = r < nrows ? r : nrows - 1;
+    src_row[it] = gather ? (int64_t)__ldg(gather + t.row0 + rr) : (int64_t)(t.row0 + rr);
+  }
 #pragma unroll
   for (int kb = 0; kb < KB; ++kb) {
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       int idx = it * 128 + tid;
       int r = idx >> 3, c = idx & 7;
-      int rr = r < nrows ? r : nrows - 1;
-      int64_t src_row = gather ? (int64_t)gather[t.row0 + rr] : (int64_t)(t.row0 + rr);
-      cp_async16(sA_u + kb * A_BYTES + r * 128 + ((c ^ (r & 7)) << 4), A + src_row * K + kb * 64 + c * 8);
+      cp_async16(sA_u + kb * A_BYTES + r * 128 + ((c ^ (r & 7)) << 4), A + src_row[it] * K + kb * 64 + c * 8);
     }
     const bf16* Bw = Bt + (size_t)t.w * N * K;
     for (int idx = tid; idx < N * 8; idx += 128) {
@@ -426,14 +435,15 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ persistent warp-specialized GEMM
-// One CTA per SM loops over tiles (static round robin).  Warps 0-1 gather the A rows
+// One CTA per SM loops over tiles (static round robin).  Warps 4-7 gather the A rows
 // (X[gather(row)]) and the segment's K-major weight rows of one (tile, 64-wide K block) per smem
-// stage with cp.async (S stages in a ring; a stage is released to the MMA warp after the
-// producers' own copies landed and were fenced for the async proxy); warp 2 issues the
-// tcgen05.mma (M = 128, N, K = 16) into one of two TMEM accumulators and commits the stage back
-// to the producers and the accumulator to the epilogue; warps 4-7 drain the accumulator of the
-// previous tile (tcgen05.ld, per-row dot epilogue, bf16/fp32 pack, swizzled per-warp smem
-// staging, coalesced row stores) while the next tile is gathered and multiplied.
+// stage with cp.async (S stages in a ring, up to S-1 in flight; a stage is released to the MMA
+// warp once the producers' own copies landed and were fenced for the async proxy); warp 8 issues
+// the tcgen05.mma (M = 128, N, K = 16) into one of two TMEM accumulators and commits the stage
+// back to the producers and the accumulator to the epilogue; warps 0-3 (TMEM lane quarters)
+// drain the accumulator of the previous tile (tcgen05.ld, per-row dot epilogue, bf16/fp32 pack,
+// swizzled per-warp smem staging, coalesced row stores) while the next tile is gathered and
+// multiplied; warp 9 owns the TMEM allocation.
 template <int N, class TY>
 struct WsCfg {
   static constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
@@ -447,7 +457,7 @@ struct WsCfg {
 };
 
 template <class TY, int N, int KB>
-__global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ tiles, int ntiles,
                                                     const bf16* __restrict__ A, const int32_t* __restrict__ gather,
                                                     const bf16* __restrict__ Bt, TY* __restrict__ Y,
                                                     const float* __restrict__ dotvec, float* __restrict__ dotout) {
@@ -465,10 +475,10 @@ __global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ til
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t s_base = smem_u32(smem);
 
-  if (warp == 3) tmem_alloc<2 * C::NCOLS>(tslot);
+  if (warp == 9) tmem_alloc<2 * C::NCOLS>(tslot);
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 64);
+      mbar_init(&full[i], 128);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -482,45 +492,62 @@ __global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ til
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
 
-  if (warp < 2) {
-    // ------------------------------------------------ producers (64 threads)
-    int st = 0, prev = -1;
+  if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------ producers (warps 4-7, 128 threads)
+    // up to S-1 stages in flight per thread: a stage is handed to the MMA warp once it is the
+    // oldest of S-1 committed groups (cp.async.wait_group S-2), after the proxy fence
+    // thread ptid copies chunk ptid % 8 of rows ptid / 8 + 16 i (i < 8); the next tile's row
+    // indices are loaded while this tile's copies are issued, so the gather never stalls issue
+    const int ptid = tid - 128, c = ptid & 7, r0 = ptid >> 3;
+    int st = 0, pend = 0, old = 0;
     uint32_t ph = 0;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    int64_t nxt[8];
+    auto load_rows = [&](int ti) {
       const Tile t = tiles[ti];
       const int nrows = t.row1 - t.row0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 16 * i, rr = r < nrows ? r : nrows - 1;
+        nxt[i] = gather ? (int64_t)__ldg(gather + t.row0 + rr) : (int64_t)(t.row0 + rr);
+      }
+    };
+    if (blockIdx.x < ntiles) load_rows(blockIdx.x);
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      const Tile t = tiles[ti];
+      int64_t cur[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+      if (ti + (int)gridDim.x < ntiles) load_rows(ti + gridDim.x);
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&empty[st], ph ^ 1);
         const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
-#pragma unroll 4
-        for (int idx = tid; idx < 128 * 8; idx += 64) {
-          const int r = idx >> 3, c = idx & 7;
-          const int rr = r < nrows ? r : nrows - 1;
-          const int64_t src = gather ? (int64_t)gather[t.row0 + rr] : (int64_t)(t.row0 + rr);
-          cp_async16(sa + r * 128 + ((c ^ (r & 7)) << 4), A + src * K + kb * 64 + c * 8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          cp_async16(sa + r * 128 + ((c ^ (r & 7)) << 4), A + cur[i] * K + kb * 64 + c * 8);
         }
         const bf16* Bw = Bt + (size_t)t.w * N * K;
 #pragma unroll 4
-        for (int idx = tid; idx < N * 8; idx += 64) {
-          const int r = idx >> 3, c = idx & 7;
+        for (int r = r0; r < N; r += 16)
           cp_async16(sb + r * 128 + ((c ^ (r & 7)) << 4), Bw + (int64_t)r * K + kb * 64 + c * 8);
-        }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        if (prev >= 0) {  // the previous stage's copies have landed: hand it to the MMA warp
-          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        if (++pend == S - 1) {
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          mbar_arrive(&full[prev]);
+          mbar_arrive(&full[old]);
+          if (++old == S) old = 0;
+          --pend;
         }
-        prev = st;
         if (++st == S) { st = 0; ph ^= 1; }
       }
     }
-    if (prev >= 0) {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_arrive(&full[prev]);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (; pend > 0; --pend) {
+      mbar_arrive(&full[old]);
+      if (++old == S) old = 0;
     }
-  } else if (warp == 2) {
+  } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(N);
@@ -545,9 +572,9 @@ __global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ til
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    // ------------------------------------------------ epilogue (4 warps, TMEM lane quarter warp % 4)
-    const int q = warp & 3;
+  } else if (warp < 4) {
+    // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quarters)
+    const int q = warp;
     uint8_t* stg = staging + q * 32 * C::RB;
     int acc = 0;
     uint32_t aph = 0;
@@ -589,7 +616,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_ws(const Tile* __restrict__ til
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 3) tmem_dealloc<2 * C::NCOLS>(tmem);
+  if (warp == 9) tmem_dealloc<2 * C::NCOLS>(tmem);
 }
 
 template <class TY, int N, int KB>
@@ -604,14 +631,15 @@ void launch_ws(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
     RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   }
   const int grid = std::min(a.ntiles, num_sms);
-  launch(a.name, k, dim3(grid), dim3(256), C::SMEM, s, a.tiles, a.ntiles, static_cast<const bf16*>(a.A), a.gather, Bt,
+  launch(a.name, k, dim3(grid), dim3(320), C::SMEM, s, a.tiles, a.ntiles, static_cast<const bf16*>(a.A), a.gather, Bt,
          static_cast<TY*>(a.Y), a.dotvec, a.dotout);
 }
 
 template <class TY, int N, int KB>
 void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   if constexpr (WsCfg<N, TY>::S >= 2) {
-    if (a.red_ptr == nullptr && ws_enabled()) {
+    const int mode = ws_mode();
+    if (a.red_ptr == nullptr && (mode == 2 || (mode == 1 && a.gather == nullptr))) {
       launch_ws<TY, N, KB>(a, Bt, s);
       return;
     }
