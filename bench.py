@@ -81,9 +81,11 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["hgt_bwd_dst"] = E * (4 + 2 * d * b) + N * (16 + d * b + 4 * d + 4 * d + 8 + d * b + 2 * d * b + 16)
         # A7 per edge: CSC dst index, the [G|Q] row of the destination, its 16-B record; per pair: KM row, dKM row
         out["hgt_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 2 * d * b + 2 * d * b)
-        # node dX GEMM with the per-source reduction of the pair dX rows fused into its epilogue
-        out["gemm_nodes_dx"] = N * (d * b + 4 * d_in + 8) + U * (4 + 4 * d_in)
-        out["gemm_pairs_dx"] = U * (2 * d * b + 4 * d_in)
+        # dX: per-pair rows dXp = dKM F^T (layer dtype), node rows dX = dQ Wq^T (fp32), then the
+        # per-source sum of the pair rows added into dX (seg_reduce_rows)
+        out["gemm_pairs_dx"] = U * (2 * d * b + d_in * b)
+        out["gemm_nodes_dx"] = N * (d * b + 4 * d_in)
+        out["seg_reduce_rows"] = U * (4 + d_in * b) + N * (4 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + 2 * d * b)
         out["wgrad_nodes"] = N * (d_in * b + d * b)
     elif model == "rgat":
@@ -93,8 +95,8 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["rgat_bwd_dst"] = E * (8 + d * b + 4) + N * (16 + d_in * b + 12 * d + 8 + 2 * d * b + 16)
         # A7 per edge: CSC dst, the destination's [G|X] row and 16-B record; per pair: P row, s, dP, wsum, bx
         out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + 4 * d)
-        out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
-        out["seg_reduce_rows"] = U * (4 + 4 * d_in) + N * (8 + 8 * d_in)
+        out["gemm_pairs_dx"] = U * (d * b + d_in * b)
+        out["seg_reduce_rows"] = U * (4 + d_in * b) + N * (4 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
         out["seg_wsum"] = U * (4 * d) + U * (4 + d * b)
     else:
@@ -102,9 +104,11 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)
         out["rgcn_fwd_traverse"] = E * (4 + 4 + d * b) + N * (16 + 8 * d)
         out["rgcn_bwd_pair"] = E * (4 + 4 + d * b) + U * (16 + d * b)
-        out["gemm_pairs_dx"] = U * (d * b + 4 * d_in)
-        # self-loop dX GEMM with the per-source reduction of the pair dX rows fused (tcgen05 path)
-        out["gemm_selfloop_dx"] = N * (d * b + 4 * d_in + 8) + U * (4 + 4 * d_in)
+        out["gemm_pairs_dx"] = U * (d * b + d_in * b)
+        out["gemm_selfloop_dx"] = N * (d * b + 4 * d_in)
+        out["seg_reduce_rows"] = U * (4 + d_in * b) + N * (4 + 8 * d_in)
+        if b == 2:  # the upstream gradient's bf16 copy (gathered per edge and the self-loop A operand)
+            out["from_f32"] = N * d * (4 + b)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
         out["wgrad_selfloop"] = N * (d_in * b + d * b)
     return out

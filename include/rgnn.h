@@ -225,6 +225,43 @@ RGNN_API rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* 
                                 const float* out, const void* saved, const float* dout, float* dX,
                                 const rgnn_weight_grads* dW, void* scratch, void* stream);
 
+/* ------------------------------------------------------------------ A1 primitive: typed segment GEMM
+ * The paper's GEMM template Y[S] = X[G] x W[T] (§3.3.3, algo:gemm_template P:901-918),
+ * the operator the layer calls for every projection (compact rows P:764-776), exported on its own
+ * so a caller (and the D3 d-sweep) can run it at any width.  Rows 0..R-1 are split into
+ * num_segments contiguous segments; for every row i of segment s
+ *     Y[i][0:N] = X[G(i)][0:K] . W[w(s)]        G(i) = gather[i] (identity when gather is NULL),
+ *                                               w(s) = seg_weight[s] (s when seg_weight is NULL).
+ * A plan holds the row tiles of one segmentation (tiles never cross a segment); it is built once
+ * and reused by every call with that segmentation. */
+typedef struct rgnn_segments_s* rgnn_segments_t;
+
+/* seg_ptr: host int64[num_segments+1], non-decreasing, seg_ptr[0] = 0 (R = seg_ptr[num_segments]).
+ * seg_weight: host int32[num_segments] or NULL.  Device memory through alloc/free_fn (NULL: the
+ * library's cudaMallocAsync on `stream`).  The call synchronises `stream` once (tile upload).
+ * Errors: INVALID_ARG (decreasing seg_ptr, negative weight index, NULL out), OOM, CUDA. */
+RGNN_API rgnn_status rgnn_segment_plan_create(int32_t num_segments, const int64_t* seg_ptr, const int32_t* seg_weight,
+                                              rgnn_alloc_fn alloc, rgnn_free_fn free_fn, void* alloc_ctx, void* stream,
+                                              rgnn_segments_t* out);
+RGNN_API rgnn_status rgnn_segment_plan_destroy(rgnn_segments_t p);
+
+/* Scratch bytes of rgnn_segment_gemm for these widths (the K-major bf16 weight image of the
+ * tensor-core path; 0 for f32).  num_weights = number of matrices in W. */
+RGNN_API rgnn_status rgnn_segment_gemm_workspace(rgnn_segments_t p, int32_t dtype, int32_t K, int32_t N,
+                                                 int32_t num_weights, size_t* scratch_bytes);
+
+/* X: device [*][K] in `dtype`; gather: device int32[R] or NULL; W: device [num_weights][K][N] in
+ * `dtype` ([num_weights][N][K] when trans_w = 1, i.e. Y = X W^T); Y: device [R][N] in y_dtype
+ * (BF16 only for dtype BF16; F32 always), fully overwritten; scratch: >= the workspace size.
+ * dtype BF16 runs on the tcgen05 tensor cores (fp32 accumulation in TMEM): K a multiple of 64,
+ * K <= 8192, N in {16, 32, 64, 128} or a multiple of 256 (<= 8192).  dtype F32 runs the SIMT FFMA
+ * kernel (no TF32): K a multiple of 16, N in {16, 32, 64, 128, 256}.  Enqueued on `stream`.
+ * Errors: INVALID_ARG (NULL pointers, weight index >= num_weights is not checked on the device:
+ * caller contract), UNSUPPORTED (widths), CUDA. */
+RGNN_API rgnn_status rgnn_segment_gemm(rgnn_segments_t p, int32_t dtype, const void* X, const int32_t* gather, int32_t K,
+                                       const void* W, int32_t num_weights, int32_t N, int32_t trans_w, void* Y,
+                                       int32_t y_dtype, void* scratch, size_t scratch_bytes, void* stream);
+
 /* ------------------------------------------------------------------ profiling
  * When enabled, every kernel the library launches is bracketed by CUDA events
  * on its launch stream.  rgnn_profile_read synchronises those events and

@@ -13,6 +13,7 @@ Contents
   dense.py   independent dense (matrix-level) formulations used as pins:
              GCN A*XW, g-SpMM / g-SDDMM with a dense masked
              adjacency, GAT / masked dot-product attention
+  gemm.py    A1 typed segment GEMM Y[S] = X[G] x W[T] (GEMM template)
   fd.py      central finite differences of L = sum(out * G) (reading g12)
   sample.py  subgraph extraction so that sampled output rows of a large
              graph can be evaluated exactly by the same functions

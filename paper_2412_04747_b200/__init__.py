@@ -4,6 +4,6 @@ The compute lives in librgnn.so (csrc/, C-ABI in include/rgnn.h); `rgnn` is its
 ctypes binding.  Build with `python -m paper_2412_04747_b200.build`.
 """
 from . import rgnn
-from .rgnn import Graph, Layer, RGNNError, lib, version
+from .rgnn import Graph, Layer, RGNNError, SegmentPlan, lib, segment_gemm, version
 
-__all__ = ["rgnn", "Graph", "Layer", "RGNNError", "lib", "version"]
+__all__ = ["rgnn", "Graph", "Layer", "RGNNError", "SegmentPlan", "lib", "segment_gemm", "version"]

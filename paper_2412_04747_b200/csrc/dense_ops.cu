@@ -392,6 +392,19 @@ __global__ void k_from_f32(int64_t n, const float* in, TO* out) {
   if (i < n) out[i] = from_f<TO>(in[i]);
 }
 
+// fp32 -> bf16, 8 elements per thread (two 16-byte loads, one 16-byte store); scalar tail
+__global__ void k_from_f32_bf16(int64_t n, const float* __restrict__ in, bf16* __restrict__ out) {
+  const int64_t n8 = n >> 3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(in) + 2 * i);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(in) + 2 * i + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    store16(out + 8 * i, v);
+  }
+  const int64_t t = 8 * n8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) out[t] = __float2bfloat16_rn(in[t]);
+}
+
 }  // namespace
 
 void gemm_simt(const GemmArgs& a, cudaStream_t s) {
@@ -536,8 +549,11 @@ void convert_f32(int64_t n, const void* in, int dtype, float* out, cudaStream_t 
 void convert_dt(int64_t n, const float* in, void* out, int dtype, cudaStream_t s) {
   if (dtype == F32)
     RGNN_CUDA(cudaMemcpyAsync(out, in, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-  else
+  else if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     launch("from_f32", k_from_f32<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, n, in, static_cast<bf16*>(out));
+  else
+    launch("from_f32", k_from_f32_bf16, dim3(std::min<int64_t>(std::max<int64_t>(ceil_div(n / 8, 256), 1), 148 * 16)),
+           dim3(256), 0, s, n, in, static_cast<bf16*>(out));
 }
 
 }  // namespace rgnn

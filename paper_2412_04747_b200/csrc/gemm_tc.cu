@@ -131,24 +131,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Stage 32 accumulator columns of one row into the warp's smem tile (row-major, 16-byte
-// chunks XOR-swizzled by the row so the 32 lanes' stores and the later coalesced reads
-// spread over all banks).  CH = 16-byte chunks per row (power of two).
-template <int CH>
-__device__ __forceinline__ void stage_row32(uint8_t* row_base, int row, int chunk0, const float* v, float*) {
+// NV accumulator values (one row) -> the row's staged chunk, 16-byte piece p0.. XOR-swizzled by row.
+template <class TY, int NV, int PC>
+__device__ __forceinline__ void stage_vals(uint8_t* rowp, int row, int p0, const float* v) {
+  constexpr int VPP = 16 / sizeof(TY);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    int j = chunk0 + q;
-    *reinterpret_cast<float4*>(row_base + ((j ^ (row & (CH - 1))) << 4)) =
-        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  }
-}
-template <int CH>
-__device__ __forceinline__ void stage_row32(uint8_t* row_base, int row, int chunk0, const float* v, bf16*) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    int j = chunk0 + q;
-    store16(reinterpret_cast<bf16*>(row_base + ((j ^ (row & (CH - 1))) << 4)), v + 8 * q);
+  for (int q = 0; q < NV / VPP; ++q) {
+    const int p = (p0 + q) ^ (row & (PC - 1));
+    store16(reinterpret_cast<TY*>(rowp + (p << 4)), v + VPP * q);
   }
 }
 
@@ -251,6 +241,7 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
   const int r = warp * 32 + lane;
   const bool valid = r < nrows;
   const int64_t row = t.row0 + r;
+  constexpr int NV = N < 32 ? N : 32;  // valid columns per 32-column TMEM load
   float dot = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += 32) {
@@ -258,19 +249,19 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
     if (dotvec) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
+      for (int i = 0; i < NV; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
     }
     if (red_ptr && valid) {  // fused per-row reduction of gathered fp32 rows
       for (int j = red_ptr[row], je = red_ptr[row + 1]; j < je; ++j) {
         const float* rr = red_rows + (int64_t)red_list[j] * N + c0;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
+        for (int i = 0; i < NV; i += 4) {
           float4 x = __ldg(reinterpret_cast<const float4*>(rr + i));
           v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
         }
       }
     }
-    stage_row32<CH>(stage + lane * RB, lane, c0 * (int)sizeof(TY) / 16, v, (TY*)nullptr);
+    stage_vals<TY, NV, CH>(stage + lane * RB, lane, c0 * (int)sizeof(TY) / 16, v);
   }
   if (dotvec && valid) dotout[row] = dot;
   __syncwarp();
@@ -435,35 +426,42 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ persistent warp-specialized GEMM
-// One CTA per SM loops over tiles (static round robin).  Warps 4-7 gather the A rows
-// (X[gather(row)]) and the segment's K-major weight rows of one (tile, 64-wide K block) per smem
-// stage with cp.async (S stages in a ring, up to S-1 in flight; a stage is released to the MMA
-// warp once the producers' own copies landed and were fenced for the async proxy); warp 8 issues
-// the tcgen05.mma (M = 128, N, K = 16) into one of two TMEM accumulators and commits the stage
-// back to the producers and the accumulator to the epilogue; warps 0-3 (TMEM lane quarters)
-// drain the accumulator of the previous tile (tcgen05.ld, per-row dot epilogue, bf16/fp32 pack,
-// swizzled per-warp smem staging, coalesced row stores) while the next tile is gathered and
-// multiplied; warp 9 owns the TMEM allocation.
-template <int N, class TY>
+// One CTA per SM loops over work items (tile, n-block) in static round robin; an item is a
+// 128-row tile of one weight segment times an NT-column block of that segment's weight.
+// Warps 4-7 gather the A rows (X[gather(row)]) and the weight's K-major rows of one 64-wide K
+// block per smem stage with cp.async (S stages in a ring, up to S-1 in flight; a stage is handed
+// to the MMA warp once the producers' own copies landed and were fenced for the async proxy);
+// warp 8 issues the tcgen05.mma (M = 128, N = NT, K = 16) into one of two TMEM accumulators and
+// commits the stage back to the producers and the accumulator to the epilogue; warps 0-3 (TMEM
+// lane quarters) drain the previous item's accumulator (tcgen05.ld, optional per-row dot,
+// bf16/fp32 pack, swizzled 128-byte row chunks staged per warp, coalesced row stores) while the
+// next item is gathered and multiplied; warp 9 owns the TMEM allocation.  K is a runtime
+// multiple of 64, so the same kernel serves the layer (d = 64/128) and the d-sweep of D3.
+template <int NT, class TY>
 struct WsCfg {
-  static constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  static constexpr int NCOLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
   static constexpr uint32_t A_BYTES = 128 * 128;
-  static constexpr uint32_t B_BYTES = N * 128;
+  static constexpr uint32_t B_BYTES = NT * 128;
   static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-  static constexpr uint32_t RB = N * sizeof(TY);          // output row bytes
-  static constexpr uint32_t STAGING = 4 * 32 * RB;        // epilogue staging, 4 warps x 32 rows
-  static constexpr int S = (int)((200 * 1024 - STAGING) / STAGE) < 8 ? (int)((200 * 1024 - STAGING) / STAGE) : 8;
+  static constexpr uint32_t RB = NT * sizeof(TY);       // tile row bytes
+  static constexpr uint32_t CB = RB < 128 ? RB : 128;   // staged row-chunk bytes
+  static constexpr int CC = CB / sizeof(TY);            // columns per staged chunk
+  static constexpr int PC = CB / 16;                    // 16-byte pieces per row chunk
+  static constexpr uint32_t STAGING = 4 * 32 * CB;      // 4 epilogue warps x 32 rows
+  static constexpr int S_FIT = (int)((220 * 1024 - STAGING) / STAGE);
+  static constexpr int S = S_FIT < 8 ? S_FIT : 8;
   static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + STAGING + 256;
 };
 
-template <class TY, int N, int KB>
-__global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ tiles, int ntiles,
+template <class TY, int NT>
+__global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ tiles, int ntiles, int nblk,
                                                     const bf16* __restrict__ A, const int32_t* __restrict__ gather,
-                                                    const bf16* __restrict__ Bt, TY* __restrict__ Y,
+                                                    int K, const bf16* __restrict__ Bt, int ntot, TY* __restrict__ Y,
                                                     const float* __restrict__ dotvec, float* __restrict__ dotout) {
-  using C = WsCfg<N, TY>;
-  constexpr int K = KB * 64, S = C::S, CH = C::RB / 16;
+  using C = WsCfg<NT, TY>;
+  constexpr int S = C::S;
   static_assert(S >= 2, "not enough shared memory for two stages");
+  const int KB = K >> 6, nitems = ntiles * nblk;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* staging = smem + S * C::STAGE;
@@ -494,16 +492,14 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
 
   if (warp >= 4 && warp < 8) {
     // ------------------------------------------------ producers (warps 4-7, 128 threads)
-    // up to S-1 stages in flight per thread: a stage is handed to the MMA warp once it is the
-    // oldest of S-1 committed groups (cp.async.wait_group S-2), after the proxy fence
-    // thread ptid copies chunk ptid % 8 of rows ptid / 8 + 16 i (i < 8); the next tile's row
-    // indices are loaded while this tile's copies are issued, so the gather never stalls issue
+    // thread ptid copies 16-byte chunk ptid % 8 of rows ptid / 8 + 16 i; the next item's row
+    // indices are loaded while this item's copies are issued, so the gather never stalls issue
     const int ptid = tid - 128, c = ptid & 7, r0 = ptid >> 3;
     int st = 0, pend = 0, old = 0;
     uint32_t ph = 0;
     int64_t nxt[8];
-    auto load_rows = [&](int ti) {
-      const Tile t = tiles[ti];
+    auto load_rows = [&](int item) {
+      const Tile t = tiles[item / nblk];
       const int nrows = t.row1 - t.row0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -511,13 +507,15 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
         nxt[i] = gather ? (int64_t)__ldg(gather + t.row0 + rr) : (int64_t)(t.row0 + rr);
       }
     };
-    if (blockIdx.x < ntiles) load_rows(blockIdx.x);
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-      const Tile t = tiles[ti];
+    if (blockIdx.x < nitems) load_rows(blockIdx.x);
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int ti = it / nblk, nb = it - ti * nblk;
+      const int w = tiles[ti].w;
       int64_t cur[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-      if (ti + (int)gridDim.x < ntiles) load_rows(ti + gridDim.x);
+      if (it + (int)gridDim.x < nitems) load_rows(it + gridDim.x);
+      const bf16* Bw = Bt + ((size_t)w * ntot + (size_t)nb * NT) * K;
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&empty[st], ph ^ 1);
         const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
@@ -526,9 +524,8 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
           const int r = r0 + 16 * i;
           cp_async16(sa + r * 128 + ((c ^ (r & 7)) << 4), A + cur[i] * K + kb * 64 + c * 8);
         }
-        const bf16* Bw = Bt + (size_t)t.w * N * K;
 #pragma unroll 4
-        for (int r = r0; r < N; r += 16)
+        for (int r = r0; r < NT; r += 16)
           cp_async16(sb + r * 128 + ((c ^ (r & 7)) << 4), Bw + (int64_t)r * K + kb * 64 + c * 8);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         if (++pend == S - 1) {
@@ -550,10 +547,10 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
   } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(N);
+      const uint32_t idesc = umma_idesc_bf16(NT);
       int st = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         mbar_wait(&tempty[acc], aph ^ 1);  // the epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t d_tmem = tmem + acc * C::NCOLS;
@@ -574,43 +571,48 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
     __syncwarp();
   } else if (warp < 4) {
     // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quarters)
+    constexpr int NV = C::CC < 32 ? C::CC : 32;
     const int q = warp;
-    uint8_t* stg = staging + q * 32 * C::RB;
+    uint8_t* stg = staging + q * 32 * C::CB;
     int acc = 0;
     uint32_t aph = 0;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int ti = it / nblk, nb = it - ti * nblk;
       const Tile t = tiles[ti];
       const int nrows = t.row1 - t.row0;
-      const int r = q * 32 + lane;
-      const bool valid = r < nrows;
-      const int64_t row = t.row0 + r;
+      const int rows_here = min(32, nrows - q * 32);
+      const int64_t row = t.row0 + q * 32 + lane;
+      uint8_t* ybase = reinterpret_cast<uint8_t*>(Y + (t.row0 + (int64_t)q * 32) * ntot + (int64_t)nb * NT);
+      const int64_t ystride = (int64_t)ntot * sizeof(TY);
       mbar_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tb = tmem + acc * C::NCOLS + ((uint32_t)(q * 32) << 16);
       float dot = 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += C::CC) {
 #pragma unroll
-      for (int c0 = 0; c0 < N; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + acc * C::NCOLS + ((uint32_t)(q * 32) << 16) + c0, v);
-        if (dotvec) {
+        for (int s0 = 0; s0 < C::CC; s0 += 32) {
+          float v[32];
+          tmem_ld32(tb + c0 + s0, v);
+          if (dotvec) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
+            for (int i = 0; i < NV; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * ntot + c0 + s0 + i), dot);
+          }
+          stage_vals<TY, NV, C::PC>(stg + lane * C::CB, lane, s0 * (int)sizeof(TY) / 16, v);
         }
-        stage_row32<CH>(stg + lane * C::RB, lane, c0 * (int)sizeof(TY) / 16, v, (TY*)nullptr);
+        __syncwarp();
+#pragma unroll
+        for (int k = lane; k < 32 * C::PC; k += 32) {
+          const int rr = k / C::PC, j = k % C::PC;
+          if (rr < rows_here)
+            *reinterpret_cast<uint4*>(ybase + rr * ystride + c0 * (int)sizeof(TY) + j * 16) =
+                *reinterpret_cast<const uint4*>(stg + rr * C::CB + ((j ^ (rr & (C::PC - 1))) << 4));
+        }
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       mbar_arrive(&tempty[acc]);  // TMEM reads done: the MMA warp may reuse this accumulator
-      if (dotvec && valid) dotout[row] = dot;
-      __syncwarp();
-      const int rows_here = min(32, nrows - q * 32);
-      uint8_t* ybase = reinterpret_cast<uint8_t*>(Y) + (t.row0 + (int64_t)q * 32) * C::RB;
-#pragma unroll 4
-      for (int k = lane; k < 32 * CH; k += 32) {
-        const int rr = k / CH, j = k % CH;
-        if (rr < rows_here)
-          *reinterpret_cast<uint4*>(ybase + (int64_t)rr * C::RB + j * 16) =
-              *reinterpret_cast<const uint4*>(stg + rr * C::RB + ((j ^ (rr & (CH - 1))) << 4));
-      }
-      __syncwarp();
+      if (dotvec && lane < rows_here) dotout[row] = dot;
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   }
@@ -619,10 +621,10 @@ __global__ void __launch_bounds__(320, 1) k_gemm_ws(const Tile* __restrict__ til
   if (warp == 9) tmem_dealloc<2 * C::NCOLS>(tmem);
 }
 
-template <class TY, int N, int KB>
+template <class TY, int NT>
 void launch_ws(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
-  using C = WsCfg<N, TY>;
-  auto k = k_gemm_ws<TY, N, KB>;
+  using C = WsCfg<NT, TY>;
+  auto k = k_gemm_ws<TY, NT>;
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -630,20 +632,26 @@ void launch_ws(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
     RGNN_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   }
-  const int grid = std::min(a.ntiles, num_sms);
-  launch(a.name, k, dim3(grid), dim3(320), C::SMEM, s, a.tiles, a.ntiles, static_cast<const bf16*>(a.A), a.gather, Bt,
-         static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+  const int nblk = a.N / NT;
+  const int grid = std::min(a.ntiles * nblk, num_sms);
+  launch(a.name, k, dim3(grid), dim3(320), C::SMEM, s, a.tiles, a.ntiles, nblk, static_cast<const bf16*>(a.A),
+         a.gather, a.K, Bt, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+}
+
+template <class TY>
+void ws_by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  switch (a.N < 256 ? a.N : 256) {
+    case 16: launch_ws<TY, 16>(a, Bt, s); break;
+    case 32: launch_ws<TY, 32>(a, Bt, s); break;
+    case 64: launch_ws<TY, 64>(a, Bt, s); break;
+    case 128: launch_ws<TY, 128>(a, Bt, s); break;
+    case 256: launch_ws<TY, 256>(a, Bt, s); break;
+    default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "tcgen05 gemm: N");
+  }
 }
 
 template <class TY, int N, int KB>
 void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
-  if constexpr (WsCfg<N, TY>::S >= 2) {
-    const int mode = ws_mode();
-    if (a.red_ptr == nullptr && (mode == 2 || (mode == 1 && a.gather == nullptr))) {
-      launch_ws<TY, N, KB>(a, Bt, s);
-      return;
-    }
-  }
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   // operands, reused by the epilogue's row staging (128 rows x N x sizeof(TY)) once the MMAs are done
   size_t smem = 1024 + std::max<size_t>(KB * (128 * 128 + N * 128), 128 * N * sizeof(TY)) + 64;
@@ -672,6 +680,16 @@ void by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   }
 }
 
+// k_gemm_tc holds a whole tile's K in shared memory: K <= 128, N <= 256, not both at the maximum.
+bool fits_tc(const GemmArgs& a) { return a.K <= 128 && a.N <= 256 && !(a.K == 128 && a.N == 256); }
+
+bool use_ws(const GemmArgs& a) {
+  if (a.red_ptr != nullptr) return false;  // the fused reduce epilogue exists only in k_gemm_tc
+  if (!fits_tc(a)) return true;
+  const int mode = ws_mode();
+  return mode == 2 || (mode == 1 && a.gather == nullptr);
+}
+
 }  // namespace
 
 bool wgrad_tc_supported(const WgradArgs& a) {
@@ -686,11 +704,13 @@ void wgrad_tc(const WgradArgs& a, cudaStream_t s) {
 }
 
 bool gemm_tc_supported(const GemmArgs& a) {
-  if (a.a_dtype != BF16 || a.b_dtype != BF16) return false;
-  if (a.K % 64 != 0 || a.K > 128) return false;
-  if (!(a.N == 16 || a.N == 32 || a.N == 64 || a.N == 128 || a.N == 256)) return false;
-  if (a.K / 64 == 2 && a.N == 256) return false;  // smem budget
-  return a.bt_scratch != nullptr;
+  if (a.a_dtype != BF16 || a.b_dtype != BF16 || a.bt_scratch == nullptr) return false;
+  if (a.K <= 0 || a.K % 64 != 0 || a.K > 8192) return false;
+  const bool n_ok = a.N == 16 || a.N == 32 || a.N == 64 || a.N == 128 || (a.N % 256 == 0 && a.N <= 8192);
+  if (!n_ok) return false;
+  if (a.N > 256 && a.dotvec != nullptr) return false;  // the dot epilogue needs the whole row in one item
+  if (a.red_ptr != nullptr && !fits_tc(a)) return false;
+  return true;
 }
 
 void gemm_tc(const GemmArgs& a, cudaStream_t s) {
@@ -699,6 +719,10 @@ void gemm_tc(const GemmArgs& a, cudaStream_t s) {
   bf16* Bt = static_cast<bf16*>(a.bt_scratch);
   launch("gemm_tc_prep_b", k_transpose_kmajor<bf16>, dim3(ceil_div(total, 256)), dim3(256), 0, s, (int64_t)a.num_w,
          a.K, a.N, static_cast<const bf16*>(a.B), a.transB, Bt);
+  if (use_ws(a)) {
+    if (a.y_dtype == BF16) ws_by_n<bf16>(a, Bt, s); else ws_by_n<float>(a, Bt, s);
+    return;
+  }
   const int KB = a.K / 64;
   if (a.y_dtype == BF16) {
     if (KB == 1) by_n<bf16, 1>(a, Bt, s); else by_n<bf16, 2>(a, Bt, s);

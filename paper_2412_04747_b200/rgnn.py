@@ -29,7 +29,8 @@ EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_b
             "rgnn_graph_export",
             "rgnn_graph_array_size", "rgnn_graph_destroy", "rgnn_layer_workspace", "rgnn_layer_forward",
             "rgnn_layer_backward", "rgnn_profile_enable", "rgnn_profile_reset", "rgnn_profile_read",
-            "rgnn_launch_count"]
+            "rgnn_launch_count", "rgnn_segment_plan_create", "rgnn_segment_plan_destroy",
+            "rgnn_segment_gemm_workspace", "rgnn_segment_gemm"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -105,6 +106,14 @@ def lib() -> C.CDLL:
         L.rgnn_layer_backward.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.c_void_p, C.POINTER(WeightsC),
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GradsC),
                                           C.c_void_p, C.c_void_p]
+        L.rgnn_segment_plan_create.argtypes = [C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32), ALLOC_FN,
+                                               FREE_FN, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.rgnn_segment_plan_destroy.argtypes = [C.c_void_p]
+        L.rgnn_segment_gemm_workspace.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                  C.POINTER(C.c_size_t)]
+        L.rgnn_segment_gemm.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                        C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                        C.c_size_t, C.c_void_p]
         L.rgnn_profile_enable.argtypes = [C.c_int32]
         L.rgnn_profile_read.argtypes = [C.c_char_p, C.c_size_t]
         _lib = L
@@ -280,6 +289,61 @@ class Layer:
                                          _ptr(self.saved), _ptr(dout), _ptr(grads.get("dX")) if need_dX else None,
                                          C.byref(gc), _ptr(self.scratch), _stream()))
         return grads
+
+
+class SegmentPlan:
+    """Row tiles of one segmentation for the A1 segment GEMM (rgnn_segment_plan_create).
+    seg_ptr: host sequence of num_segments+1 row offsets; seg_weight: optional weight index per segment."""
+
+    def __init__(self, seg_ptr, seg_weight=None, device="cuda"):
+        self.device = torch.device(device)
+        self._alloc = _TorchAllocator(self.device)
+        ptr = [int(x) for x in seg_ptr]
+        self.num_segments = len(ptr) - 1
+        self.rows = ptr[-1]
+        cp = (C.c_int64 * len(ptr))(*ptr)
+        cw = None if seg_weight is None else (C.c_int32 * self.num_segments)(*[int(x) for x in seg_weight])
+        h = C.c_void_p()
+        _check(lib().rgnn_segment_plan_create(self.num_segments, cp, cw, self._alloc.alloc_cb, self._alloc.free_cb,
+                                              None, _stream(), C.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().rgnn_segment_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def segment_gemm(plan: SegmentPlan, X: torch.Tensor, W: torch.Tensor, gather: Optional[torch.Tensor] = None,
+                 trans_w: bool = False, out_dtype: Optional[torch.dtype] = None, out: Optional[torch.Tensor] = None,
+                 scratch: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Y[i] = X[gather[i]] . W[w(seg(i))] for every row of the plan (rgnn_segment_gemm).
+    X: [*, K] float32 or bfloat16; W: [num_weights, K, N] (or [num_weights, N, K] with trans_w)."""
+    dt = {torch.float32: F32, torch.bfloat16: BF16}[X.dtype]
+    if W.dtype != X.dtype:
+        raise TypeError("W must have X's dtype")
+    K = X.shape[1]
+    nw = W.shape[0]
+    N = W.shape[1] if trans_w else W.shape[2]
+    ydt = out_dtype or torch.float32
+    if out is None:
+        out = torch.empty(plan.rows, N, dtype=ydt, device=X.device)
+    if scratch is None:
+        sb = C.c_size_t()
+        _check(lib().rgnn_segment_gemm_workspace(plan.handle, dt, K, N, nw, C.byref(sb)))
+        scratch = torch.empty(max(sb.value, 1), dtype=torch.uint8, device=X.device)
+    if gather is not None and gather.dtype != torch.int32:
+        raise TypeError("gather must be int32")
+    _check(lib().rgnn_segment_gemm(plan.handle, dt, _ptr(X), _ptr(gather), K, _ptr(W), nw, N, int(trans_w), _ptr(out),
+                                   {torch.float32: F32, torch.bfloat16: BF16}[out.dtype], _ptr(scratch),
+                                   scratch.numel(), _stream()))
+    return out
 
 
 def profile_enable(on: bool = True) -> None:

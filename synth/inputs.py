@@ -68,3 +68,24 @@ def to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """uint16 bf16 bit patterns of round_bf16(x) (for uploading to the device)."""
     f = round_bf16(x).astype(np.float32)
     return (f.view(np.uint32) >> 16).astype(np.uint16)
+
+
+def segment_inputs(seed: int, seg_lens, K: int, N: int, num_src: int = 0, num_weights: int = 0,
+                   gather: bool = True, shuffle_weights: bool = False) -> Dict[str, np.ndarray]:
+    """Inputs of one A1 typed segment GEMM (Y[S] = X[G] x W[T]): segment row offsets from
+    `seg_lens` (zeros allowed = empty segments), X ~ U(-1,1) [num_src, K], Glorot W [nw, K, N],
+    a uniform random gather index per row (or none), and optionally a random weight per segment."""
+    rng = np.random.default_rng(seed)
+    seg_ptr = np.concatenate([[0], np.cumsum(np.asarray(seg_lens, np.int64))]).astype(np.int64)
+    rows = int(seg_ptr[-1])
+    S = len(seg_lens)
+    nw = num_weights or S
+    num_src = num_src or max(rows, 1)
+    out: Dict[str, np.ndarray] = {
+        "seg_ptr": seg_ptr,
+        "X": rng.uniform(-1.0, 1.0, size=(num_src, K)),
+        "W": _glorot(rng, (nw, K, N), K, N),
+        "gather": rng.integers(0, num_src, size=rows).astype(np.int32) if gather else None,
+        "seg_weight": rng.integers(0, nw, size=S).astype(np.int32) if shuffle_weights else None,
+    }
+    return out

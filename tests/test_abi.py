@@ -60,3 +60,21 @@ def test_sass_is_sm100a(lib):
     r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True)
     assert r.returncode == 0
     assert "sm_100a" in r.stdout
+
+
+def test_segment_plan_argument_errors(lib):
+    """rgnn_segment_plan_create validates seg_ptr on the host before touching the device."""
+    from paper_2412_04747_b200 import rgnn
+    out = C.c_void_p()
+    bad = (C.c_int64 * 3)(0, 5, 3)
+    st = lib.rgnn_segment_plan_create(2, bad, None, rgnn.ALLOC_FN(0), rgnn.FREE_FN(0), None, None, C.byref(out))
+    assert st == 1 and "decreases at segment 1" in lib.rgnn_last_error().decode()
+    nz = (C.c_int64 * 2)(1, 5)
+    st = lib.rgnn_segment_plan_create(1, nz, None, rgnn.ALLOC_FN(0), rgnn.FREE_FN(0), None, None, C.byref(out))
+    assert st == 1 and "seg_ptr[0]" in lib.rgnn_last_error().decode()
+    ok = (C.c_int64 * 2)(0, 5)
+    negw = (C.c_int32 * 1)(-1)
+    st = lib.rgnn_segment_plan_create(1, ok, negw, rgnn.ALLOC_FN(0), rgnn.FREE_FN(0), None, None, C.byref(out))
+    assert st == 1 and "negative weight" in lib.rgnn_last_error().decode()
+    assert lib.rgnn_segment_gemm(None, 1, None, None, 64, None, 1, 64, 0, None, 1, None, 0, None) == 1
+    assert lib.rgnn_segment_plan_destroy(None) == 0
