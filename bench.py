@@ -48,6 +48,8 @@ BENCH_CONFIGS = {
     "mag_hgt_f32": dict(graph="mag", model="hgt", d=64, dtype="f32", baseline=3),
     "mag_rgat": dict(graph="mag", model="rgat", d=64, dtype="bf16", baseline=3),
     "am_rgat": dict(graph="am", model="rgat", d=64, dtype="bf16", baseline=2),
+    "am_hgt": dict(graph="am", model="hgt", d=64, dtype="bf16", baseline=2),
+    "aifb_hgt": dict(graph="aifb", model="hgt", d=64, dtype="bf16", baseline=1),
     "aifb_rgat": dict(graph="aifb", model="rgat", d=64, dtype="bf16", baseline=1),
     "bgs_rgat": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1),
     "wikikg2_rgcn": dict(graph="wikikg2", model="rgcn", d=64, dtype="bf16", baseline=4),
@@ -235,6 +237,10 @@ def main():
                          "per-kernel times then come from a separate un-captured profiling pass")
     ap.add_argument("--no-compact", action="store_true",
                     help="vanilla materialization (one projected row per edge): the C ablation of tab:optimizations")
+    ap.add_argument("--no-reorder", action="store_true",
+                    help="linear-operator reordering off (HGT): the R ablation of tab:optimizations")
+    ap.add_argument("--infer", action="store_true",
+                    help="inference: a step is the forward pass only (the 'Inference' columns of tab:optimizations)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = BENCH_CONFIGS[args.config]
@@ -274,7 +280,7 @@ def main():
     dout = torch.tensor(Gh, dtype=torch.float32, device=dev)
     if world > 1:
         dout = D.masked_rows(dout, lo, hi)
-    layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl)
+    layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl, reorder=not args.no_reorder)
     wkeys = {"rgcn": ["dW", "dW0"], "rgat": ["dW", "da", "db"], "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[model]
     grads = {k: torch.empty(w[k[1:]].shape, dtype=torch.float32, device=dev) for k in wkeys}
     grads["dX"] = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
@@ -283,6 +289,8 @@ def main():
     def step(X_local):
         Xf = D.all_gather_rows(X_local, ranges, rank) if world > 1 else X_local
         layer.forward(Xf, w, out=out)
+        if args.infer:
+            return out
         gr = layer.backward(Xf, w, out, dout, grads=grads, need=wkeys)
         if world > 1:
             dx_own = D.reduce_scatter_rows(gr["dX"], ranges, rank)
@@ -362,13 +370,18 @@ def main():
         Xh = X_own.cpu().pin_memory()
         douth = dout.cpu().pin_memory()
         dwh = {k: torch.empty(grads[k].shape, dtype=torch.float32).pin_memory() for k in wkeys}
+        outh = torch.empty(out.shape, dtype=torch.float32).pin_memory() if args.infer else None
         Xd = torch.empty_like(X_own)
         doutd = dout  # refreshed from host each step
-        h2d = Xh.numel() * Xh.element_size() + douth.numel() * douth.element_size()
-        d2h = sum(v.numel() * 4 for v in dwh.values())
+        h2d = Xh.numel() * Xh.element_size() + (0 if args.infer else douth.numel() * douth.element_size())
+        d2h = outh.numel() * 4 if args.infer else sum(v.numel() * 4 for v in dwh.values())
 
         def e2e_step():
             Xd.copy_(Xh, non_blocking=True)
+            if args.infer:
+                step(Xd)
+                outh.copy_(out, non_blocking=True)
+                return
             doutd.copy_(douth, non_blocking=True)
             step(Xd)
             for k in wkeys:
@@ -422,8 +435,18 @@ def main():
         roofline["step_algorithmic_gb"] = step_bytes / 1e9
         roofline["step_achieved_gbs"] = step_bytes / (ms_per_step / 1e3) / 1e9
 
+    gi = G.info()
+    memory = {"graph_index_bytes": int(gi["device_bytes"]), "saved_bytes": int(layer.saved.numel()),
+              "scratch_bytes": int(layer.scratch.numel()),
+              "features_bytes": int(X_full.numel() * X_full.element_size() + out.numel() * 4 +
+                                    (0 if args.infer else dout.numel() * 4 + grads["dX"].numel() * 4)),
+              "weights_bytes": int(sum(v.numel() * v.element_size() for v in w.values())),
+              "peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+              "note": "saved = forward->backward activations (compact: U rows; vanilla: E rows), scratch = "
+                      "per-call temporaries; the graph handle also holds the work lists and cached tile plans"}
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.infer:
         cpu = cpu_oracle_sample(g, model, inp, Gh, target_s=args.cpu_seconds)
 
     if rank == 0:
@@ -445,9 +468,10 @@ def main():
                            g.num_edges * 4 * 9 / 1e9),
                        "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
                        "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
+                       "reorder": not args.no_reorder, "mode": "inference (forward only)" if args.infer else "training (forward + backward)",
                        "cuda_graph": bool(use_graph)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
+            "clocks": clocks, "remeasured_for_clocks": remeasured, "memory": memory, "kernels": kernels,
         }
         print(json.dumps(line))
     if world > 1:

@@ -120,6 +120,8 @@ typedef struct {
   int32_t num_node_types;
   int32_t num_rels;
   double compaction_ratio;  /* U / E (1.0 if E == 0), §3.4.3 */
+  int64_t device_bytes;     /* device memory the handle owns now (index arrays, work lists, cached
+                               tile plans and norms; grows when a layer first uses a new plan) */
 } rgnn_graph_info;
 
 RGNN_API rgnn_status rgnn_graph_get_info(rgnn_graph_t g, rgnn_graph_info* out_host);
@@ -168,6 +170,12 @@ typedef struct {
   int32_t norm_kind;   /* RGCN: rgnn_norm_kind */
   float leaky_slope;   /* RGAT LeakyReLU slope (reading g6: 0.2) */
   int32_t gemm_impl;   /* 0 auto (bf16 -> tcgen05 when d_in % 64 == 0), 1 force SIMT, 2 force tcgen05 */
+  int32_t no_reorder;  /* 1: linear-operator reordering off (F1 ablation, tab:optimizations P:1142-1188).
+                          HGT projects K = X Wk, V = X Wv per node and then K~ = K[src] Watt, M = V[src] Wmsg
+                          per (rel, src) pair instead of folding Wk Watt / Wv Wmsg; RGAT computes the
+                          destination term as (X[dst] W_r) . b_r per (rel, dst) pair (lst:ir_example's ht,
+                          attt) instead of X[dst] . (W_r b_r) (fig:linear_opt).  Ignored for RGCN
+                          (no weight-weight product).  0 = the default reordered path. */
 } rgnn_layer_desc;
 
 /* Layer weights, device pointers in the layer dtype (mu and edge_norm: float).

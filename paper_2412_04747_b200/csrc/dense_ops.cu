@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(256) k_seg_partial_reduce(int nseg, const int3
                                                             float* __restrict__ out) {
   __shared__ float red[8][33];
   const int sidx = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // an empty segment contributes nothing (out was zeroed); several may share a weight index
+  if (seg_tile_ptr[sidx] == seg_tile_ptr[sidx + 1]) return;
   const int64_t i = blockIdx.x * (int64_t)32 + lane;
   float acc = 0.f;
   if (i < width)
@@ -274,91 +276,173 @@ __global__ void k_rgat_y(int d_in, int d_out, const TW* W, const TW* b, float* y
 }
 
 // F[r*T+t] = [ (mu_r/sqrt(d)) Wk_t Watt_r | Wv_t Wmsg_r ]   (d_in x 2d)
+// A2 for HGT: one folded weight per ACTIVE (r, t) combination a (pairs of relation r whose source
+// has type t): F[a] = [mu_r/sqrt(d) Wk_t Watt_r | Wv_t Wmsg_r]  (d_in x 2d).
 template <class TW>
-__global__ void k_hgt_fold(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt, const TW* Wmsg,
-                           const float* mu, float* F, TW* Fdt) {
-  int rt = blockIdx.x, r = rt / T, t = rt % T;
-  float c = mu[r] * rsqrtf((float)d);
+__global__ void k_hgt_fold(int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt, const TW* Wmsg,
+                           const float* mu, const int32_t* act_rt, float* F, TW* Fdt) {
+  const int a = blockIdx.x, rt = act_rt[a], r = rt / T, t = rt % T;
+  const float c = mu[r] * rsqrtf((float)d);
   for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < d_in * 2 * d; idx += blockDim.x * gridDim.y) {
-    int k = idx / (2 * d), n2 = idx % (2 * d);
-    bool key = n2 < d;
-    int n = key ? n2 : n2 - d;
+    const int k = idx / (2 * d), n2 = idx % (2 * d);
+    const bool key = n2 < d;
+    const int n = key ? n2 : n2 - d;
     const TW* L = key ? Wk : Wv;
     const TW* Rm = key ? Watt : Wmsg;
     float acc = 0.f;
     for (int j = 0; j < d; ++j)
       acc = fmaf(to_f(L[((size_t)t * d_in + k) * d + j]), to_f(Rm[((size_t)r * d + j) * d + n]), acc);
     if (key) acc *= c;
-    F[(size_t)rt * d_in * 2 * d + idx] = acc;
-    if (Fdt) Fdt[(size_t)rt * d_in * 2 * d + idx] = from_f<TW>(acc);
+    F[(size_t)a * d_in * 2 * d + idx] = acc;
+    if (Fdt) Fdt[(size_t)a * d_in * 2 * d + idx] = from_f<TW>(acc);
   }
 }
 
-// Unfold dF[r*T+t] (d_in x 2d) into the four HGT weight gradients.  Block = 32 consecutive
-// outputs (lane) x 8 warps that split the reduction range; the warp partials are added in warp
-// order through shared memory (fixed order: deterministic).
-//   dWk[t][k][j] = sum_r c_r sum_n dF[rt][k][n] Watt[r][j][n],  dWv[t][k][j] = sum_r sum_n dF[rt][k][d+n] Wmsg[r][j][n]
+// F1 ablation, HGT without linear-operator reordering (R off): the un-folded weights
+//   Wkv[t] = [Wk_t | Wv_t]                         (d_in x 2d, node GEMM KV = X Wkv_type)
+//   Bd[r]  = blockdiag(mu_r/sqrt(d) Watt_r, Wmsg_r)  (2d x 2d, pair GEMM [K~|M] = KV[src] Bd_rel)
 template <class TW>
-__global__ void __launch_bounds__(256) k_hgt_unfold_node(int R, int T, int d_in, int d, const TW* Watt,
-                                                         const TW* Wmsg, const float* mu, const float* dF,
-                                                         float* dWk, float* dWv) {
-  __shared__ float rk[8][33], rv[8][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t idx = blockIdx.x * (int64_t)32 + lane;
-  const bool ok = idx < (int64_t)T * d_in * d;
-  const int t = ok ? idx / (d_in * d) : 0, k = ok ? (idx / d) % d_in : 0, j = ok ? idx % d : 0;
-  float ak = 0.f, av = 0.f;
-  for (int q = warp; q < R * d; q += 8) {  // q = (r, n)
-    const int r = q / d, n = q % d;
-    const float* f = dF + ((size_t)(r * T + t) * d_in + k) * 2 * d;
-    const float c = mu[r] * rsqrtf((float)d);
-    ak = fmaf(c * f[n], to_f(Watt[((size_t)r * d + j) * d + n]), ak);
-    av = fmaf(f[d + n], to_f(Wmsg[((size_t)r * d + j) * d + n]), av);
-  }
-  rk[warp][lane] = ak;
-  rv[warp][lane] = av;
-  __syncthreads();
-  if (warp == 0 && ok) {
-    float sk = 0.f, sv = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      sk += rk[w][lane];
-      sv += rv[w][lane];
-    }
-    if (dWk) dWk[idx] = sk;
-    if (dWv) dWv[idx] = sv;
+__global__ void k_hgt_nr_weights(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt,
+                                 const TW* Wmsg, const float* mu, TW* Wkv, TW* Bd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n1 = (int64_t)T * d_in * 2 * d, n2 = (int64_t)R * 4 * d * d;
+  if (i < n1) {
+    const int64_t tk = i / (2 * d);
+    const int c = (int)(i % (2 * d));
+    Wkv[i] = c < d ? Wk[tk * d + c] : Wv[tk * d + c - d];
+  } else if (i < n1 + n2) {
+    const int64_t j = i - n1;
+    const int r = (int)(j / (4 * d * d)), rem = (int)(j % (4 * d * d)), a = rem / (2 * d), b = rem % (2 * d);
+    float v = 0.f;
+    if (a < d && b < d) v = mu[r] * rsqrtf((float)d) * to_f(Watt[((size_t)r * d + a) * d + b]);
+    else if (a >= d && b >= d) v = to_f(Wmsg[((size_t)r * d + a - d) * d + b - d]);
+    Bd[j] = from_f<TW>(v);
   }
 }
 
-//   dWatt[r][j][n] = c_r sum_t sum_k Wk[t][k][j] dF[rt][k][n],  dWmsg[r][j][n] = sum_t sum_k Wv[t][k][j] dF[rt][k][d+n]
-template <class TW>
-__global__ void __launch_bounds__(256) k_hgt_unfold_rel(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv,
-                                                        const float* mu, const float* dF, float* dWatt,
-                                                        float* dWmsg) {
-  __shared__ float rk[8][33], rv[8][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t idx = blockIdx.x * (int64_t)32 + lane;
-  const bool ok = idx < (int64_t)R * d * d;
-  const int r = ok ? idx / (d * d) : 0, j = ok ? (idx / d) % d : 0, n = ok ? idx % d : 0;
-  float ak = 0.f, av = 0.f;
-  for (int q = warp; q < T * d_in; q += 8) {  // q = (t, k)
-    const int t = q / d_in, k = q % d_in;
-    const float* f = dF + ((size_t)(r * T + t) * d_in + k) * 2 * d;
-    ak = fmaf(to_f(Wk[((size_t)t * d_in + k) * d + j]), f[n], ak);
-    av = fmaf(to_f(Wv[((size_t)t * d_in + k) * d + j]), f[d + n], av);
+// The weight gradients of the R-off path from dBd [R][2d][2d] and dWkv [T][d_in][2d] (diagonal
+// blocks and column halves; the off-diagonal blocks of Bd are not parameters).
+__global__ void k_hgt_nr_split(int R, int T, int d_in, int d, const float* dBd, const float* dWkv, const float* mu,
+                               float* dWk, float* dWv, float* dWatt, float* dWmsg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n1 = (int64_t)R * d * d, n2 = (int64_t)T * d_in * d;
+  if (i < n1) {
+    const int r = (int)(i / (d * d)), a = (int)(i % (d * d)) / d, b = (int)(i % d);
+    if (dBd && dWatt) dWatt[i] = mu[r] * rsqrtf((float)d) * dBd[((size_t)r * 2 * d + a) * 2 * d + b];
+    if (dBd && dWmsg) dWmsg[i] = dBd[((size_t)r * 2 * d + d + a) * 2 * d + d + b];
+  } else if (i < n1 + n2) {
+    const int64_t j = i - n1, tk = j / d;
+    const int c = (int)(j % d);
+    if (dWkv && dWk) dWk[j] = dWkv[tk * 2 * d + c];
+    if (dWkv && dWv) dWv[j] = dWkv[tk * 2 * d + d + c];
   }
-  rk[warp][lane] = ak;
-  rv[warp][lane] = av;
+}
+
+// F1 ablation, RGAT without reordering: the destination logit term per (rel, dst) pair j
+// (a run of the dst-CSR) expanded to its CSR entries, and dz summed back per run (warp per run,
+// fixed-order shuffle reduction).
+__global__ void k_dpair_expand(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
+                               const float* __restrict__ tdp, float* __restrict__ te) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= UD) return;
+  const int lane = threadIdx.x & 31;
+  const float v = tdp[j];
+  for (int q = lane; q < cnt[j]; q += 32) te[beg[j] + q] = v;
+}
+
+__global__ void k_dpair_sum(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
+                            const float* __restrict__ dz, float* __restrict__ dt) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= UD) return;
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int q = lane; q < cnt[j]; q += 32) acc += dz[beg[j] + q];
+  acc = group_sum<32>(acc);
+  if (lane == 0) dt[j] = acc;
+}
+
+// dPt[row][:] = dt[row] * b[w][:] over the rows of each tile (w = relation)
+template <class TW>
+__global__ void k_dpair_outer(const Tile* __restrict__ tiles, const float* __restrict__ dt, const TW* __restrict__ b,
+                              int D, TW* __restrict__ dPt) {
+  const Tile t = tiles[blockIdx.x];
+  for (int64_t idx = threadIdx.x; idx < (int64_t)(t.row1 - t.row0) * D; idx += blockDim.x) {
+    const int64_t row = t.row0 + idx / D;
+    const int k = (int)(idx % D);
+    dPt[row * D + k] = from_f<TW>(dt[row] * to_f(b[(size_t)t.w * D + k]));
+  }
+}
+
+// y += x (fp32, 16-byte vectors when aligned)
+__global__ void k_add_f32(int64_t n, const float* __restrict__ x, float* __restrict__ y) {
+  const int64_t n4 = n >> 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(x) + i);
+    float4 b = reinterpret_cast<float4*>(y)[i];
+    b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
+    reinterpret_cast<float4*>(y)[i] = b;
+  }
+  const int64_t t = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) y[t] += x[t];
+}
+
+// Unfold dF[a] (d_in x 2d, one per active (r, t)) into the four HGT weight gradients; every
+// output is a fixed-order sum over the active combinations (deterministic).
+//   dWk[t][k][j] = sum_{a=(r,t)} c_r sum_n dF[a][k][n] Watt[r][j][n],   dWv likewise with dF[a][k][d+n], Wmsg
+// Step 1, block (a, k), 2d threads: P[a][k][j] = c_r dF[a][k][0:d] . Watt_r[j][:] (j < d) and
+// P[a][k][d+j] = dF[a][k][d:2d] . Wmsg_r[j][:] (the dF row staged in shared memory, weight rows
+// read as 16-byte vectors).  Step 2, block (t, k): the sum of P over the combinations of type t.
+template <class TW>
+__global__ void k_hgt_unfold_node_p(int T, int d_in, int d, const TW* Watt, const TW* Wmsg, const float* mu,
+                                    const int32_t* act_rt, const float* dF, float* P) {
+  extern __shared__ float fsm[];  // [2d]
+  constexpr int V = Vec<TW>::N;
+  const int a = blockIdx.x, k = blockIdx.y, tid = threadIdx.x, r = act_rt[a] / T;
+  const size_t row = ((size_t)a * d_in + k) * 2 * d;
+  fsm[tid] = dF[row + tid];
   __syncthreads();
-  if (warp == 0 && ok) {
-    float sk = 0.f, sv = 0.f;
+  const bool key = tid < d;
+  const int j = key ? tid : tid - d;
+  const TW* W = (key ? Watt : Wmsg) + ((size_t)r * d + j) * d;
+  const float* f = fsm + (key ? 0 : d);
+  float acc = 0.f;
+  for (int n0 = 0; n0 < d; n0 += V) {
+    float w[V];
+    load16(W + n0, w);
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      sk += rk[w][lane];
-      sv += rv[w][lane];
-    }
-    if (dWatt) dWatt[idx] = mu[r] * rsqrtf((float)d) * sk;
-    if (dWmsg) dWmsg[idx] = sv;
+    for (int i = 0; i < V; ++i) acc = fmaf(f[n0 + i], w[i], acc);
+  }
+  P[row + tid] = key ? mu[r] * rsqrtf((float)d) * acc : acc;
+}
+
+__global__ void k_hgt_unfold_node_sum(int d_in, int d, const int32_t* t_act_ptr, const int32_t* t_act, const float* P,
+                                      float* dWk, float* dWv) {
+  const int t = blockIdx.x, k = blockIdx.y, tid = threadIdx.x;
+  float acc = 0.f;
+  for (int i = t_act_ptr[t]; i < t_act_ptr[t + 1]; ++i) acc += P[((size_t)t_act[i] * d_in + k) * 2 * d + tid];
+  float* out = tid < d ? dWk : dWv;
+  if (out) out[((size_t)t * d_in + k) * d + (tid < d ? tid : tid - d)] = acc;
+}
+
+//   dWatt[r][j][n] = c_r sum_{a=(r,t)} sum_k Wk[t][k][j] dF[a][k][n],  dWmsg[r][j][n] = sum_a sum_k Wv[t][k][j] dF[a][k][d+n]
+// Block (r, j), 2d threads: thread n < d -> dWatt[r][j][n], thread d + n -> dWmsg[r][j][n] (coalesced dF rows).
+template <class TW>
+__global__ void k_hgt_unfold_rel(int T, int d_in, int d, const TW* Wk, const TW* Wv, const float* mu,
+                                 const int32_t* act_rt, const int32_t* r_act_ptr, const float* dF, float* dWatt,
+                                 float* dWmsg) {
+  const int r = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const bool key = tid < d;
+  float acc = 0.f;
+  for (int a = r_act_ptr[r]; a < r_act_ptr[r + 1]; ++a) {
+    const int t = act_rt[a] % T;
+    const TW* W = (key ? Wk : Wv) + (size_t)t * d_in * d + j;
+    const float* f = dF + (size_t)a * d_in * 2 * d + tid;
+    for (int k = 0; k < d_in; ++k) acc = fmaf(to_f(W[(size_t)k * d]), f[(size_t)k * 2 * d], acc);
+  }
+  if (key) {
+    if (dWatt) dWatt[((size_t)r * d + j) * d + tid] = mu[r] * rsqrtf((float)d) * acc;
+  } else if (dWmsg) {
+    dWmsg[((size_t)r * d + j) * d + tid - d] = acc;
   }
 }
 
@@ -496,37 +580,39 @@ void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b
            static_cast<const bf16*>(W), static_cast<const bf16*>(b), y);
 }
 
-void hgt_fold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
-              const float* mu, int dtype, float* F, void* Fdt, cudaStream_t s) {
+void hgt_fold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+              const void* Wmsg, const float* mu, int dtype, float* F, void* Fdt, cudaStream_t s) {
+  const dim3 grid(g->n_act, ceil_div(d_in * 2 * d, 256));
   if (dtype == F32)
-    launch("hgt_fold", k_hgt_fold<float>, dim3(R * T, ceil_div(d_in * 2 * d, 256)), dim3(256), 0, s, R, T, d_in, d, static_cast<const float*>(Wk),
-           static_cast<const float*>(Wv), static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, F,
-           static_cast<float*>(nullptr));
+    launch("hgt_fold", k_hgt_fold<float>, grid, dim3(256), 0, s, g->T, d_in, d, static_cast<const float*>(Wk),
+           static_cast<const float*>(Wv), static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu,
+           g->act_rt, F, static_cast<float*>(nullptr));
   else
-    launch("hgt_fold", k_hgt_fold<bf16>, dim3(R * T, ceil_div(d_in * 2 * d, 256)), dim3(256), 0, s, R, T, d_in, d, static_cast<const bf16*>(Wk),
-           static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, F,
-           static_cast<bf16*>(Fdt));
+    launch("hgt_fold", k_hgt_fold<bf16>, grid, dim3(256), 0, s, g->T, d_in, d, static_cast<const bf16*>(Wk),
+           static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu,
+           g->act_rt, F, static_cast<bf16*>(Fdt));
 }
 
-void hgt_unfold(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
-                const float* mu, int dtype, const float* dF, float* dWk, float* dWv, float* dWatt, float* dWmsg,
-                cudaStream_t s) {
-  int64_t nn = (int64_t)T * d_in * d, nr = (int64_t)R * d * d;
-  if (dtype == F32) {
+void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+                const void* Wmsg, const float* mu, int dtype, const float* dF, float* P, float* dWk, float* dWv,
+                float* dWatt, float* dWmsg, cudaStream_t s) {
+  const int R = g->R, T = g->T;
+  const size_t sm = 2 * d * sizeof(float);
+  auto go = [&](auto* tw) {
+    using TW = std::remove_pointer_t<decltype(tw)>;
+    if ((dWk || dWv) && g->n_act > 0) {
+      launch("hgt_unfold_node", k_hgt_unfold_node_p<TW>, dim3(g->n_act, d_in), dim3(2 * d), sm, s, T, d_in, d,
+             static_cast<const TW*>(Watt), static_cast<const TW*>(Wmsg), mu, g->act_rt, dF, P);
+    }
     if (dWk || dWv)
-      launch("hgt_unfold_node", k_hgt_unfold_node<float>, dim3(ceil_div(nn, 32)), dim3(256), 0, s, R, T, d_in, d,
-             static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu, dF, dWk, dWv);
+      launch("hgt_unfold_node", k_hgt_unfold_node_sum, dim3(T, d_in), dim3(2 * d), 0, s, d_in, d, g->t_act_ptr,
+             g->t_act, P, dWk, dWv);
     if (dWatt || dWmsg)
-      launch("hgt_unfold_rel", k_hgt_unfold_rel<float>, dim3(ceil_div(nr, 32)), dim3(256), 0, s, R, T, d_in, d,
-             static_cast<const float*>(Wk), static_cast<const float*>(Wv), mu, dF, dWatt, dWmsg);
-  } else {
-    if (dWk || dWv)
-      launch("hgt_unfold_node", k_hgt_unfold_node<bf16>, dim3(ceil_div(nn, 32)), dim3(256), 0, s, R, T, d_in, d,
-             static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu, dF, dWk, dWv);
-    if (dWatt || dWmsg)
-      launch("hgt_unfold_rel", k_hgt_unfold_rel<bf16>, dim3(ceil_div(nr, 32)), dim3(256), 0, s, R, T, d_in, d,
-             static_cast<const bf16*>(Wk), static_cast<const bf16*>(Wv), mu, dF, dWatt, dWmsg);
-  }
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<TW>, dim3(R, d), dim3(2 * d), 0, s, T, d_in, d,
+             static_cast<const TW*>(Wk), static_cast<const TW*>(Wv), mu, g->act_rt, g->r_act_ptr, dF, dWatt, dWmsg);
+  };
+  if (dtype == F32) go(static_cast<float*>(nullptr));
+  else go(static_cast<bf16*>(nullptr));
 }
 
 void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, int dtype, const float* Bsum,
@@ -537,6 +623,52 @@ void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, 
   else
     launch("rgat_tpath_grads", k_rgat_tpath_grads<bf16>, dim3(R), dim3(256), 0, s, R, d_in, d_out,
            static_cast<const bf16*>(W), static_cast<const bf16*>(b), Bsum, dW, db);
+}
+
+void hgt_nr_weights(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+                    const float* mu, int dtype, void* Wkv, void* Bd, cudaStream_t s) {
+  const int64_t n = (int64_t)T * d_in * 2 * d + (int64_t)R * 4 * d * d;
+  if (dtype == F32)
+    launch("hgt_nr_weights", k_hgt_nr_weights<float>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d,
+           static_cast<const float*>(Wk), static_cast<const float*>(Wv), static_cast<const float*>(Watt),
+           static_cast<const float*>(Wmsg), mu, static_cast<float*>(Wkv), static_cast<float*>(Bd));
+  else
+    launch("hgt_nr_weights", k_hgt_nr_weights<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d,
+           static_cast<const bf16*>(Wk), static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt),
+           static_cast<const bf16*>(Wmsg), mu, static_cast<bf16*>(Wkv), static_cast<bf16*>(Bd));
+}
+
+void hgt_nr_split(int R, int T, int d_in, int d, const float* dBd, const float* dWkv, const float* mu, float* dWk,
+                  float* dWv, float* dWatt, float* dWmsg, cudaStream_t s) {
+  const int64_t n = (int64_t)R * d * d + (int64_t)T * d_in * d;
+  launch("hgt_nr_split", k_hgt_nr_split, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d, dBd, dWkv, mu, dWk,
+         dWv, dWatt, dWmsg);
+}
+
+void dpair_expand(const rgnn_graph_s* g, const float* tdp, float* te, cudaStream_t s) {
+  launch("dpair_expand", k_dpair_expand, dim3(ceil_div(g->UD * 32, 256)), dim3(256), 0, s, g->UD,
+         (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, tdp, te);
+}
+
+void dpair_sum(const rgnn_graph_s* g, const float* dz, float* dt, cudaStream_t s) {
+  launch("dpair_sum", k_dpair_sum, dim3(ceil_div(g->UD * 32, 256)), dim3(256), 0, s, g->UD,
+         (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, dz, dt);
+}
+
+void dpair_outer(const Plan& p, const float* dt, const void* b, int dtype, int D, void* dPt, cudaStream_t s) {
+  if (dtype == F32)
+    launch("dpair_outer", k_dpair_outer<float>, dim3(p.count), dim3(256), 0, s, p.tiles, dt,
+           static_cast<const float*>(b), D, static_cast<float*>(dPt));
+  else
+    launch("dpair_outer", k_dpair_outer<bf16>, dim3(p.count), dim3(256), 0, s, p.tiles, dt,
+           static_cast<const bf16*>(b), D, static_cast<bf16*>(dPt));
+}
+
+void add_f32(int64_t n, const float* x, float* y, cudaStream_t s) {
+  RGNN_CHECK(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0, RGNN_ERR_INVALID_ARG,
+             "add_f32: unaligned buffers");
+  launch("add_rows", k_add_f32, dim3(std::min<int64_t>(std::max<int64_t>(ceil_div(n / 4, 256), 1), 148 * 16)),
+         dim3(256), 0, s, n, x, y);
 }
 
 void convert_f32(int64_t n, const void* in, int dtype, float* out, cudaStream_t s) {

@@ -70,6 +70,14 @@ struct rgnn_graph_s {
   int32_t* edge_pair = nullptr;
   int32_t* kept_eid = nullptr;       // [E] original edge id of each kept edge (partitioned builds)
   int32_t* pair_rel_ptr = nullptr;   // [R+1]
+  int32_t* pair_rt_ptr = nullptr;    // [R*T+1] pairs by (rel, src type)
+  // HGT A2 folds one weight per (r, t) combination that has pairs ("active"); a = 0..n_act-1 in rt order
+  int32_t n_act = 0;
+  std::vector<int32_t> act_of_rt_h;  // host [R*T]: active index, or 0 for an empty combination (no tiles)
+  int32_t* act_rt = nullptr;         // [n_act] rt = r*T + t of each active combination
+  int32_t* t_act_ptr = nullptr;      // [T+1] active combinations grouped by source type ...
+  int32_t* t_act = nullptr;          // [n_act] ... (active indices, ascending r)
+  int32_t* r_act_ptr = nullptr;      // [R+1] active indices of relation r are r_act_ptr[r] .. r_act_ptr[r+1]-1
   int32_t* pair_src = nullptr;       // [U]
   int32_t* pair_csc_beg = nullptr;   // [U] first CSC position of the pair's edges
   int32_t* pair_deg = nullptr;       // [U] number of edges of the pair
@@ -78,6 +86,8 @@ struct rgnn_graph_s {
   int32_t* dpair_dst = nullptr;      // [UD] (rel,dst) pairs ordered by (rel, dst)
   int32_t* dpair_csr_beg = nullptr;  // [UD]
   int32_t* dpair_cnt = nullptr;      // [UD]
+  int32_t* dst_dpair_ptr = nullptr;  // [N+1] lazily (ensure_dst_dpairs): dpairs grouped by destination
+  int32_t* dst_dpairs = nullptr;     // [UD]
 
   // edge-balanced work lists (skewed in-degrees and pair degrees), see rgnn::WorkPlan
   rgnn::WorkPlan rows;   // destination rows over the dst-CSR
@@ -88,15 +98,18 @@ struct rgnn_graph_s {
   // cached tile plans
   std::map<std::string, rgnn::Plan> plans;
   std::vector<void*> owned;  // everything allocated through `alloc`
+  int64_t owned_bytes = 0;   // their total size (rgnn_graph_info.device_bytes)
 
   int32_t* dev_i32(size_t n, cudaStream_t s) {
     void* p = alloc.get((n ? n : 1) * sizeof(int32_t), s);
     owned.push_back(p);
+    owned_bytes += (int64_t)(n ? n : 1) * sizeof(int32_t);
     return static_cast<int32_t*>(p);
   }
   float* dev_f32(size_t n, cudaStream_t s) {
     void* p = alloc.get((n ? n : 1) * sizeof(float), s);
     owned.push_back(p);
+    owned_bytes += (int64_t)(n ? n : 1) * sizeof(float);
     return static_cast<float*>(p);
   }
 };
@@ -108,4 +121,5 @@ const Plan& get_plan(rgnn_graph_s* g, const std::string& key, const std::vector<
                      const std::vector<int32_t>& w_of_seg, int rows, cudaStream_t s);
 void graph_norms(rgnn_graph_s* g, int kind, const float* custom, cudaStream_t s, float** csr_norm,
                  float** csc_norm);
+void ensure_dst_dpairs(rgnn_graph_s* g, cudaStream_t s);
 }  // namespace rgnn

@@ -120,6 +120,7 @@ const Plan& get_plan(rgnn_graph_s* g, const std::string& key, const std::vector<
   size_t pb_al = (pb + 15) & ~size_t(15);
   char* blk = reinterpret_cast<char*>(g->alloc.get(tb + pb_al + wb, s));
   g->owned.push_back(blk);
+  g->owned_bytes += (int64_t)(tb + pb_al + wb);
   p.tiles = reinterpret_cast<Tile*>(blk);
   p.seg_tile_ptr = reinterpret_cast<int32_t*>(blk + tb);
   p.seg_w = reinterpret_cast<int32_t*>(blk + tb + pb_al);
@@ -202,6 +203,7 @@ rgnn_status rgnn_graph_get_info(rgnn_graph_t g, rgnn_graph_info* o) {
     o->dst_hi = g->dst_hi;
     o->num_node_types = g->T;
     o->num_rels = g->R;
+    o->device_bytes = g->owned_bytes;
     o->compaction_ratio = g->E == 0 ? 1.0 : (double)g->U / (double)g->E;
   });
 }

@@ -44,6 +44,11 @@ __global__ void k_iota(int64_t n, int32_t* out) {
   if (i < n) out[i] = (int32_t)i;
 }
 
+__global__ void k_key1(int64_t n, const int32_t* a, uint64_t* key) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) key[i] = (uint64_t)(uint32_t)a[i];
+}
+
 // key = (a << (wb + wc)) | (b << wc) | c
 __global__ void k_make_key(int64_t E, const int32_t* a, const int32_t* b, const int32_t* c, int wb, int wc,
                            uint64_t* key) {
@@ -279,6 +284,62 @@ void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
   build_work_plan(g, pb, pd, g->pairs, s);
 }
 
+// The (rel, dst) pairs grouped by destination (ascending rel within a destination; stable sort of
+// the (rel, dst)-ordered list by dst), built on first use by the RGAT path without reordering.
+void ensure_dst_dpairs(rgnn_graph_s* g, cudaStream_t s) {
+  if (g->dst_dpair_ptr) return;
+  const int64_t UD = g->UD, N = g->N;
+  Tmp tmp(g->alloc, s);
+  int32_t* ptr = g->dev_i32(N + 1, s);
+  int32_t* list = g->dev_i32(UD, s);
+  hist_prefix(tmp, g->dpair_dst, UD, N, ptr, s);
+  if (UD > 0) {
+    uint64_t* kin = tmp.get<uint64_t>(UD);
+    uint64_t* kout = tmp.get<uint64_t>(UD);
+    int32_t* vin = tmp.get<int32_t>(UD);
+    launch("graph_key", k_key1, dim3(ceil_div(UD, TB)), dim3(TB), 0, s, UD, (const int32_t*)g->dpair_dst, kin);
+    launch("graph_iota", k_iota, dim3(ceil_div(UD, TB)), dim3(TB), 0, s, UD, vin);
+    radix_pairs(tmp, kin, kout, vin, list, UD, bits_for(N), s);
+  }
+  RGNN_CUDA(cudaStreamSynchronize(s));  // temporaries are released when `tmp` goes out of scope
+  g->dst_dpair_ptr = ptr;
+  g->dst_dpairs = list;
+}
+
+// Active (relation, source type) combinations of the pairs (HGT A2 folds one weight per active
+// combination only; with R*T combinations and one source type per relation most are empty).
+void build_active_combos(rgnn_graph_s* g, cudaStream_t s) {
+  const int R = g->R, T = g->T;
+  std::vector<int32_t> act_rt, t_ptr(T + 1, 0), t_list, r_ptr(R + 1, 0);
+  g->act_of_rt_h.assign((size_t)R * T, 0);
+  for (int rt = 0; rt < R * T; ++rt)
+    if (g->pair_rt_ptr_h[rt + 1] > g->pair_rt_ptr_h[rt]) {
+      g->act_of_rt_h[rt] = (int32_t)act_rt.size();
+      act_rt.push_back(rt);
+      ++t_ptr[rt % T + 1];
+      ++r_ptr[rt / T + 1];
+    }
+  for (int t = 0; t < T; ++t) t_ptr[t + 1] += t_ptr[t];
+  for (int r = 0; r < R; ++r) r_ptr[r + 1] += r_ptr[r];
+  t_list.resize(act_rt.size());
+  std::vector<int32_t> fill(t_ptr.begin(), t_ptr.end() - 1);
+  for (size_t a = 0; a < act_rt.size(); ++a) t_list[fill[act_rt[a] % T]++] = (int32_t)a;
+  g->n_act = (int32_t)act_rt.size();
+  const size_t na = std::max<size_t>(act_rt.size(), 1);
+  std::vector<int32_t> host(2 * na + (T + 1) + (R + 1), 0);
+  std::copy(act_rt.begin(), act_rt.end(), host.begin());
+  std::copy(t_ptr.begin(), t_ptr.end(), host.begin() + na);
+  std::copy(t_list.begin(), t_list.end(), host.begin() + na + T + 1);
+  std::copy(r_ptr.begin(), r_ptr.end(), host.begin() + 2 * na + T + 1);
+  int32_t* d = g->dev_i32(host.size(), s);
+  g->act_rt = d;
+  g->t_act_ptr = d + na;
+  g->t_act = d + na + T + 1;
+  g->r_act_ptr = d + 2 * na + T + 1;
+  RGNN_CUDA(cudaMemcpyAsync(d, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));  // `host` goes out of scope; one-off per graph
+}
+
 void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, const int32_t* rel_in,
                  int64_t E_in, cudaStream_t s) {
   const int64_t N = g->N;
@@ -431,7 +492,7 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   // (rel, src type) sub-segments of the pairs
   int64_t* d_ntp = tmp.get<int64_t>(T + 1);
   RGNN_CUDA(cudaMemcpyAsync(d_ntp, g->node_type_ptr.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  int32_t* rt = tmp.get<int32_t>((int64_t)R * T + 1);
+  int32_t* rt = g->pair_rt_ptr = g->dev_i32((int64_t)R * T + 1, s);
   launch("graph_rt_bounds", k_rt_bounds, dim3(ceil_div((int64_t)R * T + 1, TB)), dim3(TB), 0, s, R, T, d_ntp, nb,
          rkey_sorted, U, rt);
 
@@ -452,6 +513,7 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   RGNN_CUDA(cudaStreamSynchronize(s));
   g->max_in_deg = (int64_t)h_stats[1];
   g->max_pair_deg = (int64_t)h_stats[2];
+  build_active_combos(g, s);
   build_work_plans(g, s);
 }
 

@@ -33,8 +33,9 @@ struct Segs {
 Segs seg_pair_rel(const rgnn_graph_s* g) {
   return {"pair_rel", std::vector<int64_t>(g->pair_rel_ptr_h.begin(), g->pair_rel_ptr_h.end()), {}};
 }
+// pairs by (rel, src type); the weight of a non-empty segment is its active-combination index
 Segs seg_pair_rt(const rgnn_graph_s* g) {
-  return {"pair_rt", std::vector<int64_t>(g->pair_rt_ptr_h.begin(), g->pair_rt_ptr_h.end()), {}};
+  return {"pair_rt", std::vector<int64_t>(g->pair_rt_ptr_h.begin(), g->pair_rt_ptr_h.end()), g->act_of_rt_h};
 }
 Segs seg_node_type(const rgnn_graph_s* g) { return {"node_type", g->node_type_ptr, {}}; }
 Segs seg_all_nodes(const rgnn_graph_s* g) { return {"all_nodes", {0, g->N}, {0}}; }
@@ -72,7 +73,12 @@ void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
     RGNN_CHECK(d->d_in == d->d_out, RGNN_ERR_UNSUPPORTED, "RGAT needs d_in == d_out");
   RGNN_CHECK(d->norm_kind >= 0 && d->norm_kind <= 3, RGNN_ERR_INVALID_ARG, "unknown norm_kind");
   RGNN_CHECK(d->gemm_impl >= 0 && d->gemm_impl <= 2, RGNN_ERR_INVALID_ARG, "unknown gemm_impl");
+  RGNN_CHECK(d->no_reorder == 0 || d->no_reorder == 1, RGNN_ERR_INVALID_ARG, "no_reorder must be 0 or 1");
 }
+
+// linear-operator reordering off (F1 ablation)
+bool hgt_nr(const rgnn_layer_desc* d) { return d->model == RGNN_HGT && d->no_reorder; }
+bool rgat_nr(const rgnn_layer_desc* d) { return d->model == RGNN_RGAT && d->no_reorder; }
 
 // ---------------------------------------------------------------- workspace layout
 struct Saved {
@@ -82,8 +88,15 @@ struct Saved {
   float2* stats = nullptr; // RGAT/HGT (m, sum) [N]
   float* y = nullptr;      // RGAT y [R][D]
   float* a32 = nullptr;    // RGAT a as fp32 [R][D]
-  float* F32 = nullptr;    // HGT folded weights fp32 [R*T][Din][2D]
+  float* F32 = nullptr;    // HGT folded weights fp32 [n_act][Din][2D] (active (r, t) combinations)
   void* Fdt = nullptr;     // HGT folded weights in bf16
+  void* KV = nullptr;      // HGT, reordering off: [K|V] = X [Wk|Wv]_type  [N][2D] (layer dtype)
+  void* Wkv = nullptr;     //   [T][Din][2D]   [Wk_t | Wv_t]
+  void* Bd = nullptr;      //   [R][2D][2D]    blockdiag(mu_r/sqrt(d) Watt_r, Wmsg_r)
+  void* Pt = nullptr;      // RGAT, reordering off: X[dst] W_rel per (rel, dst) pair [UD][D] (layer dtype)
+  float* tdp = nullptr;    //   Pt . b_rel per (rel, dst) pair [UD]
+  float* te = nullptr;     //   the same per CSR entry [E]
+  float* b32 = nullptr;    //   b as fp32 [R][D]
 };
 
 void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
@@ -98,13 +111,26 @@ void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
       o.stats = ar.take<float2>(N);
       o.y = ar.take<float>(R * c.D);
       o.a32 = ar.take<float>(R * c.D);
+      if (rgat_nr(c.d)) {
+        o.Pt = ar.take<char>(g->UD * c.D * c.esz);
+        o.tdp = ar.take<float>(g->UD);
+        o.te = ar.take<float>(g->E);
+        o.b32 = ar.take<float>(R * c.D);
+      }
       break;
     case RGNN_HGT:
       o.P = ar.take<char>(U * 2 * c.D * c.esz);
       o.Q = ar.take<char>(N * c.D * c.esz);
       o.stats = ar.take<float2>(N);
-      o.F32 = ar.take<float>(R * T * c.Din * 2 * c.D);
-      if (c.dt == BF16) o.Fdt = ar.take<char>(R * T * c.Din * 2 * c.D * c.esz);
+      if (hgt_nr(c.d)) {
+        o.KV = ar.take<char>(N * 2 * c.D * c.esz);
+        o.Wkv = ar.take<char>(T * c.Din * 2 * c.D * c.esz);
+        o.Bd = ar.take<char>(R * 4 * c.D * c.D * c.esz);
+      } else {
+        const int64_t A = std::max<int64_t>(g->n_act, 1);
+        o.F32 = ar.take<float>(A * c.Din * 2 * c.D);
+        if (c.dt == BF16) o.Fdt = ar.take<char>(A * c.Din * 2 * c.D * c.esz);
+      }
       break;
   }
 }
@@ -126,14 +152,33 @@ struct BwdScratch {
   float* wsum = nullptr;  // RGAT [U]
   float* bx = nullptr;    // RGAT [U][D]  sum_e dz_e X_d per pair
   float* Bsum = nullptr;  // RGAT [R][Din]
-  float* dF = nullptr;    // HGT [R*T][Din][2D]
+  float* dF = nullptr;    // HGT [n_act][Din][2D]
+  float* dFu = nullptr;   // HGT [n_act][Din][2D] per-combination unfold products
   void* GQ = nullptr;     // HGT [N][2D] = [G_v | Q_v] layer dtype
   void* Gt = nullptr;     // RGCN bf16 path: the upstream gradient in bf16 [N][D]
   float4* nst = nullptr;  // HGT [N] (m, 1/sum, G.out, 0)
+  float* dKV32 = nullptr;  // HGT reordering off: per-node [dK|dV] [N][2D] fp32
+  void* dKVdt = nullptr;   //   the same in the layer dtype (bf16 path; = dKV32 on the fp32 path)
+  float* dXkv = nullptr;   //   dKV [Wk|Wv]^T  [N][Din]
+  float* dBd = nullptr;    //   [R][2D][2D]
+  float* dWkv = nullptr;   //   [T][Din][2D]
+  float* dz = nullptr;     // RGAT reordering off: dz per CSR entry [E]
+  float* dt = nullptr;     //   per (rel, dst) pair [UD]
+  void* dPt = nullptr;     //   dt (x) b_rel [UD][D] layer dtype
+  void* dXd = nullptr;     //   dPt W_rel^T [UD][Din] layer dtype
+  float* dWt = nullptr;    //   X[dst]^T dPt per relation [R][Din][D]
   float* partial = nullptr;
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
 };
+
+// elements of the largest K-major weight image any GEMM of the layer builds (tcgen05 path)
+int64_t bt_elems(const Ctx& c) {
+  const int64_t R = c.g->R, T = c.g->T, Din = c.Din, D = c.D;
+  if (c.d->model != RGNN_HGT) return std::max(R, (int64_t)1) * Din * D;
+  const int64_t A = std::max<int64_t>(c.g->n_act, 1);
+  return std::max({A * Din * 2 * D, T * Din * D, R * 4 * D * D, T * Din * 2 * D});
+}
 
 void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
   const int64_t rows = c.g->rows.n_slots * c.D;
@@ -144,12 +189,7 @@ void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
 
 void layout_fwd_scratch(const Ctx& c, Arena& ar, FwdScratch& o) {
   layout_partial(c, ar, o.pt);
-  if (c.dt == BF16) {
-    const int64_t R = c.g->R, T = c.g->T;
-    int64_t n = c.d->model == RGNN_HGT ? std::max(R * T * c.Din * 2 * c.D, T * c.Din * c.D)
-                                       : std::max(R, (int64_t)1) * c.Din * c.D;
-    o.bt = ar.take<char>(n * 2);
-  }
+  if (c.dt == BF16) o.bt = ar.take<char>(bt_elems(c) * 2);
   if (c.d->model == RGNN_RGCN) {
     o.P = ar.take<char>(c.g->U * c.D * c.esz);
     if (c.d->norm_kind == RGNN_NORM_CUSTOM) {
@@ -164,11 +204,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   const int64_t U = g->U, N = g->N, E = g->E, R = g->R, T = g->T;
   const int model = c.d->model;
   layout_partial(c, ar, o.pt);
-  if (c.dt == BF16) {
-    int64_t n = model == RGNN_HGT ? std::max(R * T * c.Din * 2 * c.D, T * c.Din * c.D)
-                                  : std::max(R, (int64_t)1) * c.Din * c.D;
-    o.bt = ar.take<char>(n * 2);
-  }
+  if (c.dt == BF16) o.bt = ar.take<char>(bt_elems(c) * 2);
   int64_t width = 0, tiles = 0;
   auto need = [&](const Segs& sg, int64_t k1k2) {
     width = std::max(width, k1k2 * count_tiles(sg, WGRAD_ROWS));
@@ -195,15 +231,36 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     o.nst = ar.take<float4>(N);
     need(seg_pair_rel(g), (int64_t)c.Din * c.D);
     width = std::max(width, (int64_t)c.D * count_tiles(seg_pair_rel(g), WSUM_ROWS));
+    if (rgat_nr(c.d)) {
+      o.dz = ar.take<float>(E);
+      o.dt = ar.take<float>(g->UD);
+      o.dPt = ar.take<char>(g->UD * c.D * c.esz);
+      o.dXd = ar.take<char>(g->UD * c.Din * c.esz);
+      o.dWt = ar.take<float>(R * c.Din * c.D);
+      need(seg_dpair_rel(g), (int64_t)c.Din * c.D);
+      width = std::max(width, (int64_t)c.D * count_tiles(seg_dpair_rel(g), WSUM_ROWS));
+    }
   } else {
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
-    o.dXp = ar.take<char>(U * c.Din * c.esz);
     o.dQ = ar.take<char>(N * c.D * c.esz);
-    o.dF = ar.take<float>(R * T * c.Din * 2 * c.D);
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
     o.nst = ar.take<float4>(N);
-    need(seg_pair_rt(g), (int64_t)c.Din * 2 * c.D);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
+    if (hgt_nr(c.d)) {
+      o.dXp = ar.take<char>(U * 2 * c.D * c.esz);  // per-pair [dK|dV] rows
+      o.dKV32 = ar.take<float>(N * 2 * c.D);
+      o.dKVdt = c.dt == BF16 ? ar.take<char>(N * 2 * c.D * c.esz) : nullptr;
+      o.dXkv = ar.take<float>(N * c.Din);
+      o.dBd = ar.take<float>(R * 4 * c.D * c.D);
+      o.dWkv = ar.take<float>(T * c.Din * 2 * c.D);
+      need(seg_pair_rel(g), (int64_t)4 * c.D * c.D);
+      need(seg_node_type(g), (int64_t)c.Din * 2 * c.D);
+    } else {
+      o.dXp = ar.take<char>(U * c.Din * c.esz);
+      o.dF = ar.take<float>(std::max<int64_t>(g->n_act, 1) * c.Din * 2 * c.D);
+      o.dFu = ar.take<float>(std::max<int64_t>(g->n_act, 1) * c.Din * 2 * c.D);
+      need(seg_pair_rt(g), (int64_t)c.Din * 2 * c.D);
+    }
   }
   o.partial = ar.take<float>(std::max<int64_t>(width, 1));
 }
@@ -270,8 +327,22 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     rgcn_fwd_traverse(g, c.dt, c.D, cn, sc.P, out, c.d->self_loop != 0, sc.pt, c.s);
   } else if (model == RGNN_RGAT) {
     RGNN_CHECK(w->W && w->a && w->b, RGNN_ERR_INVALID_ARG, "RGAT needs W, a, b");
-    rgat_tpath_vectors(g->R, c.Din, c.D, w->W, w->b, c.dt, sv.y, c.s);
+    const bool nr = rgat_nr(c.d);
+    if (!nr) rgat_tpath_vectors(g->R, c.Din, c.D, w->W, w->b, c.dt, sv.y, c.s);
     convert_f32((int64_t)g->R * c.D, w->a, c.dt, sv.a32, c.s);
+    if (nr) {
+      // reordering off: attt = (X[dst] W_rel) . b_rel per (rel, dst) pair (the listing's ht),
+      // then expanded to the CSR entries
+      convert_f32((int64_t)g->R * c.D, w->b, c.dt, sv.b32, c.s);
+      GemmArgs t;
+      t.A = X; t.a_dtype = c.dt; t.K = c.Din; t.gather = g->dpair_dst;
+      t.B = w->W; t.b_dtype = c.dt; t.Y = sv.Pt; t.y_dtype = c.dt; t.N = c.D;
+      t.dotvec = sv.b32; t.dotout = sv.tdp;
+      t.num_w = g->R; t.bt_scratch = sc.bt;
+      t.name = "gemm_dpairs_fwd";
+      gemm(c, seg_dpair_rel(g), t);
+      dpair_expand(g, sv.tdp, sv.te, c.s);
+    }
     GemmArgs a;
     a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
     a.B = w->W; a.b_dtype = c.dt; a.Y = sv.P; a.y_dtype = c.dt; a.N = c.D;
@@ -279,18 +350,35 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.num_w = g->R; a.bt_scratch = sc.bt;
     a.name = "gemm_pairs_fwd";
     gemm(c, seg_pair_rel(g), a);
-    rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, out, sv.stats, sc.pt, c.s);
+    rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nr ? sv.te : nullptr, c.d->leaky_slope, out, sv.stats,
+                      sc.pt, c.s);
   } else {
     RGNN_CHECK(w->Wk && w->Wq && w->Wv && w->Watt && w->Wmsg && w->mu, RGNN_ERR_INVALID_ARG,
                "HGT needs Wk, Wq, Wv, Watt, Wmsg, mu");
-    hgt_fold(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, c.s);
-    GemmArgs a;
-    a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
-    a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
-    a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
-    a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
-    a.name = "gemm_pairs_fwd";
-    gemm(c, seg_pair_rt(g), a);
+    if (hgt_nr(c.d)) {
+      // reordering off: [K|V] = X [Wk|Wv]_type per node, then [K~|M] = [K|V][src] blockdiag(.)_rel per pair
+      hgt_nr_weights(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.Wkv, sv.Bd, c.s);
+      GemmArgs k;
+      k.A = X; k.a_dtype = c.dt; k.K = c.Din; k.B = sv.Wkv; k.b_dtype = c.dt; k.Y = sv.KV; k.y_dtype = c.dt;
+      k.N = 2 * c.D; k.num_w = g->T; k.bt_scratch = sc.bt;
+      k.name = "gemm_nodes_kv";
+      gemm(c, seg_node_type(g), k);
+      GemmArgs a;
+      a.A = sv.KV; a.a_dtype = c.dt; a.K = 2 * c.D; a.gather = g->pair_src;
+      a.B = sv.Bd; a.b_dtype = c.dt; a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
+      a.num_w = g->R; a.bt_scratch = sc.bt;
+      a.name = "gemm_pairs_fwd";
+      gemm(c, seg_pair_rel(g), a);
+    } else {
+      hgt_fold(g, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, c.s);
+      GemmArgs a;
+      a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
+      a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
+      a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
+      a.num_w = std::max(g->n_act, 1); a.bt_scratch = sc.bt;
+      a.name = "gemm_pairs_fwd";
+      gemm(c, seg_pair_rt(g), a);
+    }
     GemmArgs q;
     q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
     q.num_w = g->T; q.bt_scratch = sc.bt;
@@ -301,6 +389,96 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
 }
 
 // ---------------------------------------------------------------- backward
+// HGT with reordering off, after A6/A7 produced dQ and d[K~|M] per pair:
+//   d[K|V] per pair = d[K~|M] Bd_rel^T, summed per source node;  dX = dQ Wq^T + d[K|V] [Wk|Wv]^T;
+//   dBd_r = sum_{pairs of r} [K|V][src]^T d[K~|M];  d[Wk|Wv]_t = X_t^T d[K|V]_t;  dWq as reordered.
+void hgt_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const Saved& sv, float* dX,
+                     const rgnn_weight_grads* dW, const BwdScratch& sc) {
+  rgnn_graph_s* g = c.g;
+  const bool need_kv = dX || dW->dWk || dW->dWv;
+  if (need_kv) {
+    GemmArgs a;
+    a.A = sc.dP; a.a_dtype = c.dt; a.K = 2 * c.D; a.B = sv.Bd; a.b_dtype = c.dt; a.transB = true;
+    a.Y = sc.dXp; a.y_dtype = c.dt; a.N = 2 * c.D;
+    a.num_w = g->R; a.bt_scratch = sc.bt;
+    a.name = "gemm_pairs_dkv";
+    gemm(c, seg_pair_rel(g), a);
+    seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, 2 * c.D, sc.dKV32, false, c.s);
+    if (c.dt == BF16) convert_dt((int64_t)g->N * 2 * c.D, sc.dKV32, sc.dKVdt, BF16, c.s);
+  }
+  const void* dKV = c.dt == BF16 ? sc.dKVdt : (const void*)sc.dKV32;
+  if (dX) {
+    GemmArgs q;
+    q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
+    q.Y = dX; q.y_dtype = F32; q.N = c.Din;
+    q.num_w = g->T; q.bt_scratch = sc.bt;
+    q.name = "gemm_nodes_dx";
+    gemm(c, seg_node_type(g), q);
+    GemmArgs k;
+    k.A = dKV; k.a_dtype = c.dt; k.K = 2 * c.D; k.B = sv.Wkv; k.b_dtype = c.dt; k.transB = true;
+    k.Y = sc.dXkv; k.y_dtype = F32; k.N = c.Din;
+    k.num_w = g->T; k.bt_scratch = sc.bt;
+    k.name = "gemm_nodes_dkv_dx";
+    gemm(c, seg_node_type(g), k);
+    add_f32((int64_t)g->N * c.Din, sc.dXkv, dX, c.s);
+  }
+  if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
+  const bool need_bd = dW->dWatt || dW->dWmsg, need_wkv = dW->dWk || dW->dWv;
+  if (need_bd)
+    do_wgrad(c, seg_pair_rel(g), sv.KV, c.dt, 2 * c.D, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dBd, g->R, sc.partial,
+             "wgrad_pairs");
+  if (need_wkv)
+    do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, dKV, c.dt, 2 * c.D, sc.dWkv, g->T, sc.partial,
+             "wgrad_nodes_kv");
+  if (need_bd || need_wkv)
+    hgt_nr_split(g->R, g->T, c.Din, c.D, need_bd ? sc.dBd : nullptr, need_wkv ? sc.dWkv : nullptr, w->mu, dW->dWk,
+                 dW->dWv, dW->dWatt, dW->dWmsg, c.s);
+}
+
+// RGAT with reordering off: A6/A7 read the per-edge destination term t_e and write dz_e; the
+// destination side is then explicit: dt_j = sum of dz over the (rel, dst) pair j, dPt_j = dt_j b_rel,
+// dX[dst] += dPt W_rel^T, dW_rel += X[dst]^T dPt, db_rel = sum_j dt_j Pt_j.
+void rgat_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const float* out, const Saved& sv,
+                      const float* G, float* dX, const rgnn_weight_grads* dW, const BwdScratch& sc) {
+  rgnn_graph_s* g = c.g;
+  rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, nullptr, sv.te, sc.dz, c.d->leaky_slope, sv.stats, G, out, nullptr,
+               sc.GQ, sc.nst, sc.pt, c.s);
+  rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, nullptr, sv.te, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
+                nullptr, sc.pt, c.s);
+  dpair_sum(g, sc.dz, sc.dt, c.s);
+  const bool dst_side = dX || dW->dW;
+  if (dst_side) dpair_outer(plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s), sc.dt, w->b, c.dt, c.D, sc.dPt, c.s);
+  if (dX) {
+    GemmArgs a;
+    a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
+    a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
+    a.num_w = g->R; a.bt_scratch = sc.bt;
+    a.name = "gemm_pairs_dx";
+    gemm(c, seg_pair_rel(g), a);
+    seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, false, c.s);
+    GemmArgs b = a;
+    b.A = sc.dPt; b.Y = sc.dXd;
+    b.name = "gemm_dpairs_dx";
+    gemm(c, seg_dpair_rel(g), b);
+    ensure_dst_dpairs(g, c.s);
+    seg_reduce_rows(g->N, g->dst_dpair_ptr, g->dst_dpairs, sc.dXd, c.dt, c.Din, dX, true, c.s);
+  }
+  if (dW->dW) {
+    do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
+    do_wgrad(c, seg_dpair_rel(g), X, c.dt, c.Din, g->dpair_dst, sc.dPt, c.dt, c.D, sc.dWt, g->R, sc.partial,
+             "wgrad_dpairs");
+    add_f32((int64_t)g->R * c.Din * c.D, sc.dWt, dW->dW, c.s);
+  }
+  if (dW->db) {
+    const Plan& pd = plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s);
+    seg_wsum(&pd, sc.dt, sv.Pt, c.dt, c.D, nullptr, dW->db, g->R, sc.partial, c.s);
+  }
+  if (dW->da) {
+    const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
+    seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
+  }
+}
+
 void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* out, const Saved& sv,
               const float* G, float* dX, const rgnn_weight_grads* dW, const BwdScratch& sc) {
   rgnn_graph_s* g = c.g;
@@ -338,12 +516,14 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
       do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, Gt, c.dt, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
+  } else if (model == RGNN_RGAT && rgat_nr(c.d)) {
+    rgat_backward_nr(c, X, w, out, sv, G, dX, dW, sc);
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
-    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, c.d->leaky_slope, sv.stats, G, out, dXt, sc.GQ, sc.nst, sc.pt,
-                 c.s);
-    rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum, sc.bx,
-                  sc.pt, c.s);
+    rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nullptr, nullptr, c.d->leaky_slope, sv.stats, G, out, dXt,
+                 sc.GQ, sc.nst, sc.pt, c.s);
+    rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, nullptr, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
+                  sc.bx, sc.pt, c.s);
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
@@ -366,13 +546,17 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   } else {
     hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst, sc.pt, c.s);
     hgt_bwd_pair(g, c.dt, c.D, sv.P, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
+    if (hgt_nr(c.d)) {
+      hgt_backward_nr(c, X, w, sv, dX, dW, sc);
+      return;
+    }
     if (dX) {
       // per-pair rows first, then the node GEMM whose epilogue adds them per source (tcgen05 path)
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = 2 * c.D; a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
       a.transB = true;
       a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
-      a.num_w = g->R * g->T; a.bt_scratch = sc.bt;
+      a.num_w = std::max(g->n_act, 1); a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       gemm(c, seg_pair_rt(g), a);
       GemmArgs q;
@@ -385,8 +569,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     }
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {
-      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, g->R * g->T, sc.partial, "wgrad_pairs");
-      hgt_unfold(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, dW->dWk, dW->dWv,
+      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1), sc.partial, "wgrad_pairs");
+      hgt_unfold(g, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, sc.dFu, dW->dWk, dW->dWv,
                  dW->dWatt, dW->dWmsg, c.s);
     }
   }

@@ -104,7 +104,7 @@ rgnn_status rgnn_segment_gemm(rgnn_segments_t p, int32_t dtype, const void* X, c
                               const void* W, int32_t num_weights, int32_t N, int32_t trans_w, void* Y, int32_t y_dtype,
                               void* scratch, size_t scratch_bytes, void* stream) {
   return guarded([&] {
-    RGNN_CHECK(p && W && Y, RGNN_ERR_INVALID_ARG, "NULL plan, W or Y");
+    RGNN_CHECK(p && W && (Y || p->rows == 0), RGNN_ERR_INVALID_ARG, "NULL plan, W or Y");
     RGNN_CHECK(p->rows == 0 || X, RGNN_ERR_INVALID_ARG, "NULL X");
     RGNN_CHECK(dtype == RGNN_F32 || dtype == RGNN_BF16, RGNN_ERR_INVALID_ARG, "dtype");
     RGNN_CHECK(y_dtype == RGNN_F32 || (y_dtype == RGNN_BF16 && dtype == RGNN_BF16), RGNN_ERR_INVALID_ARG,

@@ -292,13 +292,15 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
 // ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
 // z_e = s_p + x_v . y_r (reordered t-path), l = LeakyReLU(z), out_v = sum softmax(l)_e P_p.
 // Requires d_in == d_out == D (the x_v chunk lives in the same lanes as the row chunk).
-template <class TP, int D, bool GROUP>
+// TE (reordering off, F1 ablation): the destination term t_e = (X_v W_r) . b_r is read per CSR
+// entry from te[] (computed by the dst-pair GEMM) instead of x_v . y_r.
+template <class TP, int D, bool GROUP, bool TE>
 __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
                                                   float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
                                                   const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                   const float* __restrict__ spair, const TP* __restrict__ X,
-                                                  const float* __restrict__ y, float slope, float* __restrict__ out,
-                                                  float2* __restrict__ stats) {
+                                                  const float* __restrict__ y, const float* __restrict__ te,
+                                                  float slope, float* __restrict__ out, float2* __restrict__ stats) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
   const int64_t v = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float x[V];
-  cvt16<TP>(ldg16(X + v * D + c * V), x);
+  if (!TE) cvt16<TP>(ldg16(X + v * D + c * V), x);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
@@ -325,19 +327,23 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
       for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
       if (ok[u]) {
         int64_t p = csr_pair[i];
-        int r = csr_rel[i];
         rp[u] = ldg16(P + p * D + c * V);
         sp[u] = spair[p];
-        ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+        if (TE) yv[u][0] = te[i];
+        else ld_f32<V>(y + (int64_t)csr_rel[i] * D + c * V, yv[u]);
       }
     }
     float l[UNR], mx = m;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       float t = 0.f;
+      if (TE) {
+        t = yv[u][0];
+      } else {
 #pragma unroll
-      for (int k = 0; k < V; ++k) t = fmaf(x[k], yv[u][k], t);
-      t = gsum<LPR>(t, w.mask);
+        for (int k = 0; k < V; ++k) t = fmaf(x[k], yv[u][k], t);
+        t = gsum<LPR>(t, w.mask);
+      }
       float z = sp[u] + t;
       float lz = z > 0.f ? z : slope * z;
       l[u] = ok[u] ? lz : -CUDART_INF_F;
@@ -449,12 +455,15 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
 // dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
 // dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path).  Also writes the node record
 // GX_v = [G_v | X_v] (table dtype) and nst_v = (m_v, 1/sum_v, G_v . out_v, 0) read by the pair pass.
-template <class TP, int D, bool GROUP>
+// TE (reordering off): t_e from te[], no dX t-path here; dz_e is written per CSR entry (dz_out)
+// for the explicit destination-side GEMMs.
+template <class TP, int D, bool GROUP, bool TE>
 __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
-                                                      const float* __restrict__ y, float slope,
+                                                      const float* __restrict__ y, const float* __restrict__ te,
+                                                      float* __restrict__ dz_out, float slope,
                                                       const float2* __restrict__ stats,
                                                       const float* __restrict__ Gr, const float* __restrict__ out,
                                                       float* __restrict__ dX, TP* __restrict__ GX,
@@ -497,10 +506,10 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
         for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
         if (i < e) {
           int64_t p = csr_pair[i];
-          int r = csr_rel[i];
           rp[u] = ldg16(P + p * D + c * V);
           sp[u] = spair[p];
-          ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+          if (TE) yv[u][0] = te[i];
+          else ld_f32<V>(y + (int64_t)csr_rel[i] * D + c * V, yv[u]);
         }
       }
 #pragma unroll
@@ -511,22 +520,27 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
         float t = 0.f, da = 0.f;
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          t = fmaf(x[k], yv[u][k], t);
+          if (!TE) t = fmaf(x[k], yv[u][k], t);
           da = fmaf(gv[k], pv[k], da);
         }
-        t = gsum<LPR>(t, w.mask);
+        t = TE ? yv[u][0] : gsum<LPR>(t, w.mask);
         da = gsum<LPR>(da, w.mask);
         float z = sp[u] + t;
         float l = z > 0.f ? z : slope * z;
         float alpha = __expf(l - st.x) * inv;
         float dz = alpha * (da - go) * (z > 0.f ? 1.f : slope);
         if (i < e) {
+          if (TE) {
+            if (c == 0) dz_out[i] = dz;
+          } else {
 #pragma unroll
-          for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
+            for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
+          }
         }
       }
     }
   }
+  if (TE) return;
   if (!GROUP) sum_groups<LPR, V>(dx);
   if (!w.writer()) return;
   st_f32<V>((slot >= 0 ? pacc + (int64_t)slot * D : dX + v * D) + c * V, dx);
@@ -613,11 +627,14 @@ __global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* _
   }
 }
 
-template <class TP, int D, bool GROUP>
+// TE (reordering off): t_e = te[csc2csr[i]]; no bx (the destination side is done by GEMMs).
+template <class TP, int D, bool GROUP, bool TE>
 __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                           float* __restrict__ pacc, float2* __restrict__ pstat,
                                                           const int32_t* __restrict__ csc_dst,
                                                           const int32_t* __restrict__ csc_rel,
+                                                          const int32_t* __restrict__ csc2csr,
+                                                          const float* __restrict__ te,
                                                           const TP* __restrict__ P, const float* __restrict__ spair,
                                                           const float* __restrict__ y, const TP* __restrict__ avec,
                                                           float slope, const TP* __restrict__ GX,
@@ -632,7 +649,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
   const int r = e > b ? csc_rel[b] : 0;
   float pv[V], yv[V];
   cvt16<TP>(ldg16(P + p * D + c * V), pv);
-  ld_f32<V>(y + (int64_t)r * D + c * V, yv);
+  if (!TE) ld_f32<V>(y + (int64_t)r * D + c * V, yv);
   const float sp = spair[p];
   float acc[V], ax[V], zs = 0.f;
 #pragma unroll
@@ -641,15 +658,18 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
     const int i0 = b + t + w.first;
     uint4 rg[UNR_P], rx[UNR_P];
     float4 ns[UNR_P];
+    float tv[UNR_P];
 #pragma unroll
     for (int u = 0; u < UNR_P; ++u) {
       int i = i0 + u * w.step;
       ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       rg[u] = rx[u] = make_uint4(0, 0, 0, 0);
+      tv[u] = 0.f;
       if (i < e) {
         const int64_t d = csc_dst[i];
         rg[u] = ldg16(GX + d * 2 * D + c * V);
-        rx[u] = ldg16(GX + d * 2 * D + D + c * V);
+        if (TE) tv[u] = te[csc2csr[i]];
+        else rx[u] = ldg16(GX + d * 2 * D + D + c * V);
         ns[u] = __ldg(nst + d);
       }
     }
@@ -657,14 +677,14 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
     for (int u = 0; u < UNR_P; ++u) {
       float gr[V], xd[V];
       cvt16<TP>(rg[u], gr);
-      cvt16<TP>(rx[u], xd);
+      if (!TE) cvt16<TP>(rx[u], xd);
       float tt = 0.f, da = 0.f;
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        tt = fmaf(xd[k], yv[k], tt);
+        if (!TE) tt = fmaf(xd[k], yv[k], tt);
         da = fmaf(gr[k], pv[k], da);
       }
-      tt = gsum<LPR>(tt, w.mask);
+      tt = TE ? tv[u] : gsum<LPR>(tt, w.mask);
       da = gsum<LPR>(da, w.mask);
       const bool ok = i0 + u * w.step < e;
       float z = sp + tt;
@@ -675,7 +695,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
 #pragma unroll
       for (int k = 0; k < V; ++k) {
         acc[k] = fmaf(alpha, gr[k], acc[k]);
-        ax[k] = fmaf(dz, xd[k], ax[k]);
+        if (!TE) ax[k] = fmaf(dz, xd[k], ax[k]);
       }
     }
   }
@@ -698,7 +718,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = fmaf(zs, av[k], acc[k]);
   st_tp<V>(dP + p * D + c * V, acc);
-  st_f32<V>(bx + p * D + c * V, ax);
+  if (!TE) st_f32<V>(bx + p * D + c * V, ax);
   if (c == 0) wsum[p] = zs;
 }
 
@@ -921,7 +941,7 @@ __global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const 
 #pragma unroll
   for (int k = 0; k < 4; ++k) acc[k] = fmaf(zs, to_f(avec[(int64_t)r * D + lane * 4 + k]), acc[k]);
   st4(dP + (int64_t)sp.x * D + lane * 4, acc[0], acc[1], acc[2], acc[3]);
-  st4(bx + (int64_t)sp.x * D + lane * 4, ax[0], ax[1], ax[2], ax[3]);
+  if (bx) st4(bx + (int64_t)sp.x * D + lane * 4, ax[0], ax[1], ax[2], ax[3]);
 }
 
 template <class F>
@@ -992,14 +1012,19 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, c
 }
 
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                       const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s) {
+                       const float* y, const float* te, float slope, float* out, float2* stats, const Partial& pt,
+                       cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_rgat_fwd<TP, DD, false>, k_rgat_fwd<TP, DD, true>,
-                  s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
-                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, out, stats);
+      auto go = [&](auto kw, auto kg) {
+        launch_plan("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
+                    (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair,
+                    static_cast<const TP*>(X), y, te, slope, out, stats);
+      };
+      if (te) go(k_rgat_fwd<TP, DD, false, true>, k_rgat_fwd<TP, DD, true, true>);
+      else go(k_rgat_fwd<TP, DD, false, false>, k_rgat_fwd<TP, DD, true, false>);
     });
     launch("merge_heavy_rows", k_merge_softmax<DD>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
@@ -1026,22 +1051,26 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const 
 }
 
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                  const float* y, float slope, const float2* stats, const float* G, const float* out, float* dX,
-                  void* GX, float4* nst, const Partial& pt, cudaStream_t s) {
+                  const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
+                  const float* out, float* dX, void* GX, float4* nst, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_rgat_bwd_dst<TP, DD, false>,
-                  k_rgat_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
-                  static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, slope, stats, G, out, dX,
-                  static_cast<TP*>(GX), nst);
+      auto go = [&](auto kw, auto kg) {
+        launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, (const int32_t*)g->csr_pair,
+                    (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te,
+                    dz, slope, stats, G, out, dX, static_cast<TP*>(GX), nst);
+      };
+      if (te) go(k_rgat_bwd_dst<TP, DD, false, true>, k_rgat_bwd_dst<TP, DD, true, true>);
+      else go(k_rgat_bwd_dst<TP, DD, false, false>, k_rgat_bwd_dst<TP, DD, true, false>);
       launch("rgat_node_prep", k_rgat_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
              g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(X), out, stats,
              static_cast<TP*>(GX), nst);
     });
-    launch("merge_heavy_rows", k_merge_sum<DD, float>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
-           (const int4*)g->rows.splits, (const float*)pt.acc, dX, false);
+    if (!te)
+      launch("merge_heavy_rows", k_merge_sum<DD, float>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+             (const int4*)g->rows.splits, (const float*)pt.acc, dX, false);
   });
 }
 
@@ -1061,20 +1090,24 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 }
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
-                   const void* a, float slope, const void* GX, const float4* nst, void* dP, float* wsum, float* bx,
-                   const Partial& pt, cudaStream_t s) {
+                   const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
+                   float* wsum, float* bx, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgat_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgat_bwd_pair<TP, DD, false>,
-                  k_rgat_bwd_pair<TP, DD, true>, s, pt.acc, pt.stat, (const int32_t*)g->csc_dst,
-                  (const int32_t*)g->csc_rel, static_cast<const TP*>(P), spair, y, static_cast<const TP*>(a), slope,
-                  static_cast<const TP*>(GX), nst, static_cast<TP*>(dP), wsum, bx);
+      auto go = [&](auto kw, auto kg) {
+        launch_plan("rgat_bwd_pair", g->pairs, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
+                    (const int32_t*)g->csc_dst, (const int32_t*)g->csc_rel, (const int32_t*)g->csc2csr, te,
+                    static_cast<const TP*>(P), spair, y, static_cast<const TP*>(a), slope, static_cast<const TP*>(GX),
+                    nst, static_cast<TP*>(dP), wsum, te ? nullptr : bx);
+      };
+      if (te) go(k_rgat_bwd_pair<TP, DD, false, true>, k_rgat_bwd_pair<TP, DD, true, true>);
+      else go(k_rgat_bwd_pair<TP, DD, false, false>, k_rgat_bwd_pair<TP, DD, true, false>);
       launch("merge_heavy_pairs", k_merge_rgat_pair<TP, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
              (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TP*>(a),
-             static_cast<TP*>(dP), wsum, bx);
+             static_cast<TP*>(dP), wsum, te ? nullptr : bx);
     });
   });
 }

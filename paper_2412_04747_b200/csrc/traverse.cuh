@@ -13,23 +13,27 @@ void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* nor
                        bool accumulate, const Partial& pt, cudaStream_t s);
 void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
                       float2* stats, const Partial& pt, cudaStream_t s);
+// te != NULL (reordering off): the destination logit term per CSR entry instead of X_v . y_r
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                       const float* y, float slope, float* out, float2* stats, const Partial& pt, cudaStream_t s);
+                       const float* y, const float* te, float slope, float* out, float2* stats, const Partial& pt,
+                       cudaStream_t s);
 // also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) of every
 // destination with in-edges (read by hgt_bwd_pair)
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
                  cudaStream_t s);
-// also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0)
+// also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
+// te != NULL (reordering off): t_e read from te, dz_e written per CSR entry into dz, dX untouched.
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
-                  const float* y, float slope, const float2* stats, const float* G, const float* out, float* dX,
-                  void* GX, float4* nst, const Partial& pt, cudaStream_t s);
+                  const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
+                  const float* out, float* dX, void* GX, float4* nst, const Partial& pt, cudaStream_t s);
 // G: upstream gradient rows in the layer dtype (bf16 copy on the bf16 path)
 void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const void* G, void* dP,
                    const Partial& pt, cudaStream_t s);
+// te != NULL (reordering off): t_e = te[csc2csr[i]], bx not computed
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
-                   const void* a, float slope, const void* GX, const float4* nst, void* dP, float* wsum, float* bx,
-                   const Partial& pt, cudaStream_t s);
+                   const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
+                   float* wsum, float* bx, const Partial& pt, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn

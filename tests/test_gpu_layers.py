@@ -16,7 +16,8 @@ from tests.helpers import TOL, prepare, rel_err, to_device
 pytestmark = pytest.mark.gpu
 
 
-def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0, compact=True):
+def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0, compact=True,
+             reorder=True):
     from paper_2412_04747_b200 import Graph, Layer
     inp = prepare(layer_inputs(model, g, d_in, d_out, seed_x=2 + seed, seed_w=3 + seed), dtype)
     Gh = upstream_grad(g.num_nodes, d_out, seed=4 + seed)
@@ -27,7 +28,8 @@ def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_imp
     ref_grads = L.backward(model, g, inp, Gh, **kw)
 
     G = Graph.from_hetero(g, compact=compact)
-    layer = Layer(G, model, d_in, d_out, dtype=dtype, self_loop=self_loop, norm=norm, gemm_impl=gemm_impl)
+    layer = Layer(G, model, d_in, d_out, dtype=dtype, self_loop=self_loop, norm=norm, gemm_impl=gemm_impl,
+                  reorder=reorder)
     dev = to_device(inp, dtype)
     X = dev.pop("X")
     out = layer.forward(X, dev)
@@ -150,3 +152,43 @@ def test_split_heavy_pairs(model, dtype):
 def test_vanilla_materialization(model, dtype):
     """compact=0 (one projected row per edge) gives the same layer (compaction is exact)."""
     run_case(model, config_graph("aifb", seed=2, scale=0.5), 64, 64, dtype, compact=False)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("compact", [True, False])
+def test_hgt_no_reorder(dtype, compact):
+    """F1 ablation: HGT with linear-operator reordering off (K = X Wk per node, K~ = K[src] Watt per
+    pair) computes the same layer (reordering is an exact rewrite) -- same oracle, same bar."""
+    run_case("hgt", config_graph("aifb", seed=2), 64, 64, dtype, compact=compact, reorder=False)
+    run_case("hgt", config_graph("tiny", seed=8, scale=0.5), 32, 32, "f32", compact=compact, reorder=False)
+
+
+@pytest.mark.parametrize("gemm_impl", [1, 2])
+def test_hgt_no_reorder_gemm_impls(gemm_impl):
+    run_case("hgt", config_graph("tiny", seed=9, scale=0.5), 64, 64, "bf16", gemm_impl=gemm_impl, reorder=False)
+    run_case("hgt", config_graph("tiny", seed=9, scale=0.5), 128, 64, "bf16", gemm_impl=gemm_impl, reorder=False)
+
+
+def test_hgt_no_reorder_random():
+    for seed in range(4):
+        g = random_small_graph(500 + seed, allow_multi=True)
+        if g.num_edges:
+            run_case("hgt", g, 16, 16, "f32", seed=seed, reorder=False)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("compact", [True, False])
+def test_rgat_no_reorder(dtype, compact):
+    """F1 ablation: RGAT with reordering off (attt = (X[dst] W_r) . b_r per (rel, dst) pair, the
+    listing's ht) computes the same layer -- same oracle, same bar."""
+    run_case("rgat", config_graph("aifb", seed=2), 64, 64, dtype, compact=compact, reorder=False)
+    run_case("rgat", config_graph("tiny", seed=8, scale=0.5), 32, 32, "f32", compact=compact, reorder=False)
+
+
+def test_rgat_no_reorder_random_and_skewed():
+    for seed in range(4):
+        g = random_small_graph(600 + seed, allow_multi=True)
+        if g.num_edges:
+            run_case("rgat", g, 16, 16, "f32", seed=seed, reorder=False)
+    run_case("rgat", config_graph("mutag", seed=1, scale=0.3, a_dst=1.2), 64, 64, "f32", reorder=False)
+    run_case("rgat", config_graph("tiny", seed=9, scale=0.5), 64, 64, "bf16", gemm_impl=1, reorder=False)
