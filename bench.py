@@ -286,12 +286,12 @@ def main():
     grads["dX"] = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
     out = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
 
-    def step(X_local):
+    def step(X_local, dout_local=None):
         Xf = D.all_gather_rows(X_local, ranges, rank) if world > 1 else X_local
         layer.forward(Xf, w, out=out)
         if args.infer:
             return out
-        gr = layer.backward(Xf, w, out, dout, grads=grads, need=wkeys)
+        gr = layer.backward(Xf, w, out, dout if dout_local is None else dout_local, grads=grads, need=wkeys)
         if world > 1:
             dx_own = D.reduce_scatter_rows(gr["dX"], ranges, rank)
             D.all_reduce_grads(gr, wkeys)
@@ -371,31 +371,49 @@ def main():
         douth = dout.cpu().pin_memory()
         dwh = {k: torch.empty(grads[k].shape, dtype=torch.float32).pin_memory() for k in wkeys}
         outh = torch.empty(out.shape, dtype=torch.float32).pin_memory() if args.infer else None
-        Xd = torch.empty_like(X_own)
-        doutd = dout  # refreshed from host each step
+        # double-buffered: the H2D of step i+1's inputs (copy stream) overlaps step i's kernels
+        Xd = [torch.empty_like(X_own) for _ in range(2)]
+        doutd = [torch.empty_like(dout) for _ in range(2)]
+        cs = torch.cuda.Stream(device=dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
         h2d = Xh.numel() * Xh.element_size() + (0 if args.infer else douth.numel() * douth.element_size())
         d2h = outh.numel() * 4 if args.infer else sum(v.numel() * 4 for v in dwh.values())
 
-        def e2e_step():
-            Xd.copy_(Xh, non_blocking=True)
-            if args.infer:
-                step(Xd)
-                outh.copy_(out, non_blocking=True)
-                return
-            doutd.copy_(douth, non_blocking=True)
-            step(Xd)
-            for k in wkeys:
-                dwh[k].copy_(grads[k], non_blocking=True)
+        def issue_copy(k):
+            with torch.cuda.stream(cs):
+                cs.wait_event(consumed[k])  # the step that last read buffer k has finished
+                Xd[k].copy_(Xh, non_blocking=True)
+                if not args.infer:
+                    doutd[k].copy_(douth, non_blocking=True)
+                copied[k].record(cs)
 
-        e2e_step()
+        def e2e_run(K):
+            s = torch.cuda.current_stream()
+            cs.wait_stream(s)
+            issue_copy(0)
+            for i in range(K):
+                k = i % 2
+                if i + 1 < K:
+                    issue_copy(1 - k)
+                s.wait_event(copied[k])
+                if args.infer:
+                    step(Xd[k])
+                    outh.copy_(out, non_blocking=True)
+                else:
+                    step(Xd[k], doutd[k])
+                    for name in wkeys:
+                        dwh[name].copy_(grads[name], non_blocking=True)
+                consumed[k].record(s)
+
+        e2e_run(2)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         s = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        for _ in range(args.steps):
-            e2e_step()
+        e2e_run(args.steps)
         e1.record(s)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
@@ -405,7 +423,9 @@ def main():
             ems = float(t.item())
         e2e = {"value": g.num_edges * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
-               "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI); per step H2D of X and dout from pinned host memory, D2H of every weight gradient (dX stays on the device for the layer below)"}
+               "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI); per step H2D of X and dout from pinned "
+                       "host memory (double-buffered on a copy stream: step i+1's copy overlaps step i), D2H of every "
+                       "weight gradient (dX stays on the device for the layer below)"}
 
     # ---- roofline of the dominant kernel
     peaks = load_peaks()
@@ -426,8 +446,15 @@ def main():
     if dom is not None:
         ms_k = kernels[dom]["ms_per_step"]
         achieved = alg[dom] / (ms_k / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp) and not args.no_compact and not args.no_reorder and not args.infer and world == 1:
+            tr = json.load(open(tp)).get(args.config, {}).get(dom)
+            traffic = tr["bytes_per_step"] if tr else None
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                    "traffic_note": "ncu dram read+write bytes per step of this label (profiles/ncu_traffic.json)"
+                                    if traffic else None, "peak_source": peaks["source"],
                     "frac_of_8TBps": achieved / 8000.0, "algorithmic_bytes_per_step": int(alg[dom]),
                     "launches_per_step": kernels[dom]["launches_per_step"], "ms_per_step": ms_k,
                     "note": "bytes and time per step of the kernel label (all its launches in one step)"}
