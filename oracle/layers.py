@@ -154,38 +154,56 @@ def rgat_backward(g: HeteroGraph, X, W, a, b, G, slope: float = 0.2) -> Dict[str
 
 
 # ----------------------------------------------------------------- HGT (C5, reading g7)
-def hgt_forward(g: HeteroGraph, X, Wk, Wq, Wv, Watt, Wmsg, mu):
-    """Single-head HGT message passing (reading g7 of fig:rgat_layer):
+def _heads(x: np.ndarray, heads: int) -> np.ndarray:
+    """[E, d] -> [E, heads, d / heads]: head h owns the contiguous columns h*dh .. (h+1)*dh - 1."""
+    return x.reshape(x.shape[0], heads, x.shape[1] // heads)
+
+
+def hgt_forward(g: HeteroGraph, X, Wk, Wq, Wv, Watt, Wmsg, mu, heads: int = 1):
+    """HGT message passing (reading g7 of fig:rgat_layer), H heads (the traversal
+    template's head loop, algo:traversal_template P:926; reading b12: head h owns columns
+    h*dh..(h+1)*dh-1 of K', q and M, dh = d_out / H):
          k = h_s Wk_tau(s) ; v = h_s Wv_tau(s) ; q = h_d Wq_tau(d)
-         K'_e = k Watt_r ; M_e = v Wmsg_r ; l_e = mu_r (K'_e . q) / sqrt(d_out)
-         alpha = edge_softmax ; out_v = sum alpha_e M_e."""
+         K'_e = k Watt_r ; M_e = v Wmsg_r ; l_{e,h} = mu_r (K'_{e,h} . q_{e,h}) / sqrt(dh)
+         alpha_{.,h} = edge_softmax per head ; out_{v,h} = sum alpha_{e,h} M_{e,h}."""
     n = g.num_nodes
     tau = g.node_type_of()
     d_out = Watt.shape[2]
+    dh = d_out // heads
     k = typed_matmul(X[g.src], Wk, tau[g.src])
     v = typed_matmul(X[g.src], Wv, tau[g.src])
     q = typed_matmul(X[g.dst], Wq, tau[g.dst])
     Kp = typed_matmul(k, Watt, g.rel)
     M = typed_matmul(v, Wmsg, g.rel)
-    l = mu[g.rel] * np.sum(Kp * q, axis=1) / np.sqrt(d_out)
-    alpha, m, s = edge_softmax(l, g.dst, n)
-    out = segment_sum(alpha[:, None] * M, g.dst, n)
+    l = mu[g.rel][:, None] * np.sum(_heads(Kp, heads) * _heads(q, heads), axis=2) / np.sqrt(dh)  # [E, H]
+    alpha = np.zeros_like(l)
+    m = np.zeros((n, heads))
+    s = np.zeros((n, heads))
+    for h in range(heads):
+        alpha[:, h], m[:, h], s[:, h] = edge_softmax(l[:, h], g.dst, n)
+    out = segment_sum((alpha[:, :, None] * _heads(M, heads)).reshape(M.shape), g.dst, n)
+    if heads == 1:
+        l, alpha, m, s = l[:, 0], alpha[:, 0], m[:, 0], s[:, 0]
     return out, {"k": k, "v": v, "q": q, "Kp": Kp, "M": M, "logit": l, "alpha": alpha, "m": m, "s": s}
 
 
-def hgt_backward(g: HeteroGraph, X, Wk, Wq, Wv, Watt, Wmsg, mu, G) -> Dict[str, np.ndarray]:
+def hgt_backward(g: HeteroGraph, X, Wk, Wq, Wv, Watt, Wmsg, mu, G, heads: int = 1) -> Dict[str, np.ndarray]:
     n, R, T = g.num_nodes, g.num_rels, g.num_node_types
     tau = g.node_type_of()
     d_out = Watt.shape[2]
-    _, c = hgt_forward(g, X, Wk, Wq, Wv, Watt, Wmsg, mu)
-    k, v, q, Kp, M, alpha = c["k"], c["v"], c["q"], c["Kp"], c["M"], c["alpha"]
+    dh = d_out // heads
+    _, c = hgt_forward(g, X, Wk, Wq, Wv, Watt, Wmsg, mu, heads)
+    k, v, q, Kp, M = c["k"], c["v"], c["q"], c["Kp"], c["M"]
+    alpha = c["alpha"].reshape(-1, heads)
     Gd = G[g.dst]
-    dalpha = np.sum(Gd * M, axis=1)
-    dl = edge_softmax_backward(alpha, dalpha, g.dst, n)
-    scale = mu[g.rel] / np.sqrt(d_out)
-    dM = alpha[:, None] * Gd
-    dKp = (dl * scale)[:, None] * q
-    dq = (dl * scale)[:, None] * Kp
+    dalpha = np.sum(_heads(Gd, heads) * _heads(M, heads), axis=2)  # [E, H]
+    dl = np.zeros_like(dalpha)
+    for h in range(heads):
+        dl[:, h] = edge_softmax_backward(alpha[:, h], dalpha[:, h], g.dst, n)
+    scale = mu[g.rel] / np.sqrt(dh)
+    dM = (alpha[:, :, None] * _heads(Gd, heads)).reshape(Gd.shape)
+    dKp = ((dl * scale[:, None])[:, :, None] * _heads(q, heads)).reshape(q.shape)
+    dq = ((dl * scale[:, None])[:, :, None] * _heads(Kp, heads)).reshape(Kp.shape)
     dWmsg = typed_outer_sum(v, dM, g.rel, R)
     dWatt = typed_outer_sum(k, dKp, g.rel, R)
     dv = typed_matmul(dM, Wmsg, g.rel, transpose=True)
@@ -204,7 +222,7 @@ PARAMS = {"rgcn": ("W", "W0"), "rgat": ("W", "a", "b"), "hgt": ("Wk", "Wq", "Wv"
 
 
 def forward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], *, norm=None, norm_kind: str = "mean",
-            self_loop: bool = True, slope: float = 0.2):
+            self_loop: bool = True, slope: float = 0.2, heads: int = 1):
     if model == "rgcn":
         if norm is None:
             norm = rgcn_edge_norm(g, norm_kind)
@@ -212,12 +230,13 @@ def forward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], *, norm=None
     if model == "rgat":
         return rgat_forward(g, inp["X"], inp["W"], inp["a"], inp["b"], slope)
     if model == "hgt":
-        return hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"])
+        return hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], heads)
     raise ValueError(model)
 
 
 def backward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], G: np.ndarray, *, norm=None,
-             norm_kind: str = "mean", self_loop: bool = True, slope: float = 0.2) -> Dict[str, np.ndarray]:
+             norm_kind: str = "mean", self_loop: bool = True, slope: float = 0.2,
+             heads: int = 1) -> Dict[str, np.ndarray]:
     if model == "rgcn":
         if norm is None:
             norm = rgcn_edge_norm(g, norm_kind)
@@ -225,5 +244,6 @@ def backward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], G: np.ndarr
     if model == "rgat":
         return rgat_backward(g, inp["X"], inp["W"], inp["a"], inp["b"], G, slope)
     if model == "hgt":
-        return hgt_backward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], G)
+        return hgt_backward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], G,
+                            heads)
     raise ValueError(model)

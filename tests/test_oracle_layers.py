@@ -219,3 +219,58 @@ def test_destination_decomposition(model):
         assert np.allclose(out_sub[ch], out_full[ch], atol=1e-12)
     for k in full:
         assert _rel_err(acc[k], full[k]) < 1e-12, k
+
+
+# ----------------------------------------------------------------- multi-head HGT (F2, reading b12)
+@pytest.mark.parametrize("heads", [2, 4])
+@pytest.mark.parametrize("seed", range(4))
+def test_hgt_head_logits_and_softmax(heads, seed):
+    """Per head h: the logit is mu_r K'[:, h] . q[:, h] / sqrt(dh), its softmax sums to one per
+    destination, and out[:, h] is the alpha_h-weighted sum of M[:, h] (brute force per edge)."""
+    g = random_small_graph(300 + seed, allow_multi=True)
+    d = 8
+    inp = layer_inputs("hgt", g, 5, d, seed_x=seed, seed_w=seed + 1)
+    mu = inp["mu"] * 1.3
+    out, c = L.hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], mu, heads=heads)
+    dh = d // heads
+    Kp, q, M = c["Kp"], c["q"], c["M"]
+    for h in range(heads):
+        cs = slice(h * dh, (h + 1) * dh)
+        want = mu[g.rel] * np.sum(Kp[:, cs] * q[:, cs], axis=1) / np.sqrt(dh)
+        np.testing.assert_allclose(c["logit"][:, h], want, rtol=1e-12, atol=1e-12)
+        for v in range(g.num_nodes):
+            es = np.nonzero(g.dst == v)[0]
+            if len(es) == 0:
+                assert np.all(out[v, cs] == 0)
+                continue
+            ex = np.exp(want[es] - want[es].max())
+            a = ex / ex.sum()
+            np.testing.assert_allclose(out[v, cs], (a[:, None] * M[es][:, cs]).sum(0), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("heads", [2, 4])
+def test_hgt_heads_one_relation_reduce_to_single_head(heads):
+    from synth.graphs import HeteroGraph
+    rng = np.random.default_rng(7)
+    n, E = 12, 40
+    g = HeteroGraph(np.array([0, 5, n]), 1, rng.integers(0, n, E).astype(np.int32),
+                    rng.integers(0, n, E).astype(np.int32), np.zeros(E, np.int32))
+    d = 8
+    inp = layer_inputs("hgt", g, 6, d, seed_x=1, seed_w=2)
+    out, _ = L.hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"],
+                           heads=heads)
+    dh = d // heads
+    I = np.eye(dh)[None]
+    for h in range(heads):
+        cs = slice(h * dh, (h + 1) * dh)
+        Wk1 = inp["Wk"] @ inp["Watt"][0][:, cs]
+        Wv1 = inp["Wv"] @ inp["Wmsg"][0][:, cs]
+        o1, _ = L.hgt_forward(g, inp["X"], Wk1, inp["Wq"][:, :, cs], Wv1, I, I, inp["mu"])
+        np.testing.assert_allclose(out[:, cs], o1, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("heads", [2, 4])
+@pytest.mark.parametrize("seed", range(3))
+def test_fd_hgt_heads(heads, seed):
+    g = random_small_graph(400 + seed, allow_multi=True)
+    _fd_check("hgt", g, 5, 8, seed=seed, opts={"heads": heads})
