@@ -46,6 +46,7 @@ BENCH_CONFIGS = {
     # name: graph config, layer, d_in, d_out, dtype, BASELINE.json configs index
     "mag_hgt": dict(graph="mag", model="hgt", d=64, dtype="bf16", baseline=3),
     "mag_hgt_f32": dict(graph="mag", model="hgt", d=64, dtype="f32", baseline=3),
+    "mag_hgt_h8": dict(graph="mag", model="hgt", d=64, dtype="bf16", baseline=3, heads=8),
     "mag_rgat": dict(graph="mag", model="rgat", d=64, dtype="bf16", baseline=3),
     "am_rgat": dict(graph="am", model="rgat", d=64, dtype="bf16", baseline=2),
     "am_hgt": dict(graph="am", model="hgt", d=64, dtype="bf16", baseline=2),
@@ -280,7 +281,8 @@ def main():
     dout = torch.tensor(Gh, dtype=torch.float32, device=dev)
     if world > 1:
         dout = D.masked_rows(dout, lo, hi)
-    layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl, reorder=not args.no_reorder)
+    layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl, reorder=not args.no_reorder,
+                  heads=cfg.get("heads", 1))
     wkeys = {"rgcn": ["dW", "dW0"], "rgat": ["dW", "da", "db"], "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[model]
     grads = {k: torch.empty(w[k[1:]].shape, dtype=torch.float32, device=dev) for k in wkeys}
     grads["dX"] = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
@@ -495,7 +497,7 @@ def main():
                            g.num_edges * 4 * 9 / 1e9),
                        "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
                        "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
-                       "reorder": not args.no_reorder, "mode": "inference (forward only)" if args.infer else "training (forward + backward)",
+                       "reorder": not args.no_reorder, "heads": cfg.get("heads", 1), "mode": "inference (forward only)" if args.infer else "training (forward + backward)",
                        "cuda_graph": bool(use_graph)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "memory": memory, "kernels": kernels,

@@ -176,6 +176,10 @@ typedef struct {
                           destination term as (X[dst] W_r) . b_r per (rel, dst) pair (lst:ir_example's ht,
                           attt) instead of X[dst] . (W_r b_r) (fig:linear_opt).  Ignored for RGCN
                           (no weight-weight product).  0 = the default reordered path. */
+  int32_t num_heads;   /* HGT attention heads H in {0 or 1, 2, 4, 8} (F2; the traversal template's head
+                          loop, algo:traversal_template P:926): head h owns output columns h*dh .. (h+1)*dh-1,
+                          dh = d_out / H (a multiple of 8 for bf16, 4 for f32); l_{e,h} = mu_r K~_{e,h} . q_{v,h}
+                          / sqrt(dh), a softmax per (destination, head).  UNSUPPORTED > 1 for RGCN / RGAT. */
 } rgnn_layer_desc;
 
 /* Layer weights, device pointers in the layer dtype (mu and edge_norm: float).

@@ -279,10 +279,10 @@ __global__ void k_rgat_y(int d_in, int d_out, const TW* W, const TW* b, float* y
 // A2 for HGT: one folded weight per ACTIVE (r, t) combination a (pairs of relation r whose source
 // has type t): F[a] = [mu_r/sqrt(d) Wk_t Watt_r | Wv_t Wmsg_r]  (d_in x 2d).
 template <class TW>
-__global__ void k_hgt_fold(int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt, const TW* Wmsg,
+__global__ void k_hgt_fold(int T, int d_in, int d, int dh, const TW* Wk, const TW* Wv, const TW* Watt, const TW* Wmsg,
                            const float* mu, const int32_t* act_rt, float* F, TW* Fdt) {
   const int a = blockIdx.x, rt = act_rt[a], r = rt / T, t = rt % T;
-  const float c = mu[r] * rsqrtf((float)d);
+  const float c = mu[r] * rsqrtf((float)dh);
   for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < d_in * 2 * d; idx += blockDim.x * gridDim.y) {
     const int k = idx / (2 * d), n2 = idx % (2 * d);
     const bool key = n2 < d;
@@ -302,7 +302,7 @@ __global__ void k_hgt_fold(int T, int d_in, int d, const TW* Wk, const TW* Wv, c
 //   Wkv[t] = [Wk_t | Wv_t]                         (d_in x 2d, node GEMM KV = X Wkv_type)
 //   Bd[r]  = blockdiag(mu_r/sqrt(d) Watt_r, Wmsg_r)  (2d x 2d, pair GEMM [K~|M] = KV[src] Bd_rel)
 template <class TW>
-__global__ void k_hgt_nr_weights(int R, int T, int d_in, int d, const TW* Wk, const TW* Wv, const TW* Watt,
+__global__ void k_hgt_nr_weights(int R, int T, int d_in, int d, int dh, const TW* Wk, const TW* Wv, const TW* Watt,
                                  const TW* Wmsg, const float* mu, TW* Wkv, TW* Bd) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t n1 = (int64_t)T * d_in * 2 * d, n2 = (int64_t)R * 4 * d * d;
@@ -314,7 +314,7 @@ __global__ void k_hgt_nr_weights(int R, int T, int d_in, int d, const TW* Wk, co
     const int64_t j = i - n1;
     const int r = (int)(j / (4 * d * d)), rem = (int)(j % (4 * d * d)), a = rem / (2 * d), b = rem % (2 * d);
     float v = 0.f;
-    if (a < d && b < d) v = mu[r] * rsqrtf((float)d) * to_f(Watt[((size_t)r * d + a) * d + b]);
+    if (a < d && b < d) v = mu[r] * rsqrtf((float)dh) * to_f(Watt[((size_t)r * d + a) * d + b]);
     else if (a >= d && b >= d) v = to_f(Wmsg[((size_t)r * d + a - d) * d + b - d]);
     Bd[j] = from_f<TW>(v);
   }
@@ -322,13 +322,13 @@ __global__ void k_hgt_nr_weights(int R, int T, int d_in, int d, const TW* Wk, co
 
 // The weight gradients of the R-off path from dBd [R][2d][2d] and dWkv [T][d_in][2d] (diagonal
 // blocks and column halves; the off-diagonal blocks of Bd are not parameters).
-__global__ void k_hgt_nr_split(int R, int T, int d_in, int d, const float* dBd, const float* dWkv, const float* mu,
+__global__ void k_hgt_nr_split(int R, int T, int d_in, int d, int dh, const float* dBd, const float* dWkv, const float* mu,
                                float* dWk, float* dWv, float* dWatt, float* dWmsg) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t n1 = (int64_t)R * d * d, n2 = (int64_t)T * d_in * d;
   if (i < n1) {
     const int r = (int)(i / (d * d)), a = (int)(i % (d * d)) / d, b = (int)(i % d);
-    if (dBd && dWatt) dWatt[i] = mu[r] * rsqrtf((float)d) * dBd[((size_t)r * 2 * d + a) * 2 * d + b];
+    if (dBd && dWatt) dWatt[i] = mu[r] * rsqrtf((float)dh) * dBd[((size_t)r * 2 * d + a) * 2 * d + b];
     if (dBd && dWmsg) dWmsg[i] = dBd[((size_t)r * 2 * d + d + a) * 2 * d + d + b];
   } else if (i < n1 + n2) {
     const int64_t j = i - n1, tk = j / d;
@@ -393,7 +393,7 @@ __global__ void k_add_f32(int64_t n, const float* __restrict__ x, float* __restr
 // P[a][k][d+j] = dF[a][k][d:2d] . Wmsg_r[j][:] (the dF row staged in shared memory, weight rows
 // read as 16-byte vectors).  Step 2, block (t, k): the sum of P over the combinations of type t.
 template <class TW>
-__global__ void k_hgt_unfold_node_p(int T, int d_in, int d, const TW* Watt, const TW* Wmsg, const float* mu,
+__global__ void k_hgt_unfold_node_p(int T, int d_in, int d, int dh, const TW* Watt, const TW* Wmsg, const float* mu,
                                     const int32_t* act_rt, const float* dF, float* P) {
   extern __shared__ float fsm[];  // [2d]
   constexpr int V = Vec<TW>::N;
@@ -412,7 +412,7 @@ __global__ void k_hgt_unfold_node_p(int T, int d_in, int d, const TW* Watt, cons
 #pragma unroll
     for (int i = 0; i < V; ++i) acc = fmaf(f[n0 + i], w[i], acc);
   }
-  P[row + tid] = key ? mu[r] * rsqrtf((float)d) * acc : acc;
+  P[row + tid] = key ? mu[r] * rsqrtf((float)dh) * acc : acc;
 }
 
 __global__ void k_hgt_unfold_node_sum(int d_in, int d, const int32_t* t_act_ptr, const int32_t* t_act, const float* P,
@@ -427,7 +427,7 @@ __global__ void k_hgt_unfold_node_sum(int d_in, int d, const int32_t* t_act_ptr,
 //   dWatt[r][j][n] = c_r sum_{a=(r,t)} sum_k Wk[t][k][j] dF[a][k][n],  dWmsg[r][j][n] = sum_a sum_k Wv[t][k][j] dF[a][k][d+n]
 // Block (r, j), 2d threads: thread n < d -> dWatt[r][j][n], thread d + n -> dWmsg[r][j][n] (coalesced dF rows).
 template <class TW>
-__global__ void k_hgt_unfold_rel(int T, int d_in, int d, const TW* Wk, const TW* Wv, const float* mu,
+__global__ void k_hgt_unfold_rel(int T, int d_in, int d, int dh, const TW* Wk, const TW* Wv, const float* mu,
                                  const int32_t* act_rt, const int32_t* r_act_ptr, const float* dF, float* dWatt,
                                  float* dWmsg) {
   const int r = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
@@ -440,7 +440,7 @@ __global__ void k_hgt_unfold_rel(int T, int d_in, int d, const TW* Wk, const TW*
     for (int k = 0; k < d_in; ++k) acc = fmaf(to_f(W[(size_t)k * d]), f[(size_t)k * 2 * d], acc);
   }
   if (key) {
-    if (dWatt) dWatt[((size_t)r * d + j) * d + tid] = mu[r] * rsqrtf((float)d) * acc;
+    if (dWatt) dWatt[((size_t)r * d + j) * d + tid] = mu[r] * rsqrtf((float)dh) * acc;
   } else if (dWmsg) {
     dWmsg[((size_t)r * d + j) * d + tid - d] = acc;
   }
@@ -580,20 +580,20 @@ void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b
            static_cast<const bf16*>(W), static_cast<const bf16*>(b), y);
 }
 
-void hgt_fold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+void hgt_fold(const rgnn_graph_s* g, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt,
               const void* Wmsg, const float* mu, int dtype, float* F, void* Fdt, cudaStream_t s) {
   const dim3 grid(g->n_act, ceil_div(d_in * 2 * d, 256));
   if (dtype == F32)
-    launch("hgt_fold", k_hgt_fold<float>, grid, dim3(256), 0, s, g->T, d_in, d, static_cast<const float*>(Wk),
+    launch("hgt_fold", k_hgt_fold<float>, grid, dim3(256), 0, s, g->T, d_in, d, dh, static_cast<const float*>(Wk),
            static_cast<const float*>(Wv), static_cast<const float*>(Watt), static_cast<const float*>(Wmsg), mu,
            g->act_rt, F, static_cast<float*>(nullptr));
   else
-    launch("hgt_fold", k_hgt_fold<bf16>, grid, dim3(256), 0, s, g->T, d_in, d, static_cast<const bf16*>(Wk),
+    launch("hgt_fold", k_hgt_fold<bf16>, grid, dim3(256), 0, s, g->T, d_in, d, dh, static_cast<const bf16*>(Wk),
            static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt), static_cast<const bf16*>(Wmsg), mu,
            g->act_rt, F, static_cast<bf16*>(Fdt));
 }
 
-void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt,
                 const void* Wmsg, const float* mu, int dtype, const float* dF, float* P, float* dWk, float* dWv,
                 float* dWatt, float* dWmsg, cudaStream_t s) {
   const int R = g->R, T = g->T;
@@ -601,14 +601,14 @@ void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const vo
   auto go = [&](auto* tw) {
     using TW = std::remove_pointer_t<decltype(tw)>;
     if ((dWk || dWv) && g->n_act > 0) {
-      launch("hgt_unfold_node", k_hgt_unfold_node_p<TW>, dim3(g->n_act, d_in), dim3(2 * d), sm, s, T, d_in, d,
+      launch("hgt_unfold_node", k_hgt_unfold_node_p<TW>, dim3(g->n_act, d_in), dim3(2 * d), sm, s, T, d_in, d, dh,
              static_cast<const TW*>(Watt), static_cast<const TW*>(Wmsg), mu, g->act_rt, dF, P);
     }
     if (dWk || dWv)
       launch("hgt_unfold_node", k_hgt_unfold_node_sum, dim3(T, d_in), dim3(2 * d), 0, s, d_in, d, g->t_act_ptr,
              g->t_act, P, dWk, dWv);
     if (dWatt || dWmsg)
-      launch("hgt_unfold_rel", k_hgt_unfold_rel<TW>, dim3(R, d), dim3(2 * d), 0, s, T, d_in, d,
+      launch("hgt_unfold_rel", k_hgt_unfold_rel<TW>, dim3(R, d), dim3(2 * d), 0, s, T, d_in, d, dh,
              static_cast<const TW*>(Wk), static_cast<const TW*>(Wv), mu, g->act_rt, g->r_act_ptr, dF, dWatt, dWmsg);
   };
   if (dtype == F32) go(static_cast<float*>(nullptr));
@@ -625,23 +625,23 @@ void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, 
            static_cast<const bf16*>(W), static_cast<const bf16*>(b), Bsum, dW, db);
 }
 
-void hgt_nr_weights(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+void hgt_nr_weights(int R, int T, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
                     const float* mu, int dtype, void* Wkv, void* Bd, cudaStream_t s) {
   const int64_t n = (int64_t)T * d_in * 2 * d + (int64_t)R * 4 * d * d;
   if (dtype == F32)
-    launch("hgt_nr_weights", k_hgt_nr_weights<float>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d,
+    launch("hgt_nr_weights", k_hgt_nr_weights<float>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d, dh,
            static_cast<const float*>(Wk), static_cast<const float*>(Wv), static_cast<const float*>(Watt),
            static_cast<const float*>(Wmsg), mu, static_cast<float*>(Wkv), static_cast<float*>(Bd));
   else
-    launch("hgt_nr_weights", k_hgt_nr_weights<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d,
+    launch("hgt_nr_weights", k_hgt_nr_weights<bf16>, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d, dh,
            static_cast<const bf16*>(Wk), static_cast<const bf16*>(Wv), static_cast<const bf16*>(Watt),
            static_cast<const bf16*>(Wmsg), mu, static_cast<bf16*>(Wkv), static_cast<bf16*>(Bd));
 }
 
-void hgt_nr_split(int R, int T, int d_in, int d, const float* dBd, const float* dWkv, const float* mu, float* dWk,
+void hgt_nr_split(int R, int T, int d_in, int d, int dh, const float* dBd, const float* dWkv, const float* mu, float* dWk,
                   float* dWv, float* dWatt, float* dWmsg, cudaStream_t s) {
   const int64_t n = (int64_t)R * d * d + (int64_t)T * d_in * d;
-  launch("hgt_nr_split", k_hgt_nr_split, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d, dBd, dWkv, mu, dWk,
+  launch("hgt_nr_split", k_hgt_nr_split, dim3(ceil_div(n, 256)), dim3(256), 0, s, R, T, d_in, d, dh, dBd, dWkv, mu, dWk,
          dWv, dWatt, dWmsg);
 }
 

@@ -59,6 +59,7 @@ struct Ctx {
   int dt, D, Din;
   size_t esz;
   cudaStream_t s;
+  int H = 1;  // attention heads (HGT; F2)
 };
 
 void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
@@ -74,6 +75,12 @@ void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
   RGNN_CHECK(d->norm_kind >= 0 && d->norm_kind <= 3, RGNN_ERR_INVALID_ARG, "unknown norm_kind");
   RGNN_CHECK(d->gemm_impl >= 0 && d->gemm_impl <= 2, RGNN_ERR_INVALID_ARG, "unknown gemm_impl");
   RGNN_CHECK(d->no_reorder == 0 || d->no_reorder == 1, RGNN_ERR_INVALID_ARG, "no_reorder must be 0 or 1");
+  const int H = d->num_heads <= 1 ? 1 : d->num_heads;
+  RGNN_CHECK(d->num_heads >= 0 && (H == 1 || H == 2 || H == 4 || H == 8), RGNN_ERR_UNSUPPORTED,
+             "num_heads must be 0/1, 2, 4 or 8");
+  RGNN_CHECK(H == 1 || d->model == RGNN_HGT, RGNN_ERR_UNSUPPORTED, "num_heads > 1 is implemented for HGT only");
+  RGNN_CHECK((d->d_out / H) % (d->dtype == BF16 ? 8 : 4) == 0, RGNN_ERR_UNSUPPORTED,
+             "head width d_out / num_heads must be a multiple of 8 (bf16) or 4 (f32) elements");
 }
 
 // linear-operator reordering off (F1 ablation)
@@ -121,7 +128,7 @@ void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
     case RGNN_HGT:
       o.P = ar.take<char>(U * 2 * c.D * c.esz);
       o.Q = ar.take<char>(N * c.D * c.esz);
-      o.stats = ar.take<float2>(N);
+      o.stats = ar.take<float2>(N * c.H);
       if (hgt_nr(c.d)) {
         o.KV = ar.take<char>(N * 2 * c.D * c.esz);
         o.Wkv = ar.take<char>(T * c.Din * 2 * c.D * c.esz);
@@ -184,7 +191,7 @@ void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
   const int64_t rows = c.g->rows.n_slots * c.D;
   const int64_t pairs = c.g->pairs.n_slots * (c.d->model == RGNN_RGCN ? c.D : 2 * c.D);
   pt.acc = ar.take<float>(std::max<int64_t>(std::max(rows, pairs), 1));
-  pt.stat = ar.take<float2>(std::max<int64_t>(std::max(c.g->rows.n_slots, c.g->pairs.n_slots), 1));
+  pt.stat = ar.take<float2>(std::max<int64_t>(std::max(c.g->rows.n_slots * c.H, c.g->pairs.n_slots), 1));
 }
 
 void layout_fwd_scratch(const Ctx& c, Arena& ar, FwdScratch& o) {
@@ -244,7 +251,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
     o.dQ = ar.take<char>(N * c.D * c.esz);
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
-    o.nst = ar.take<float4>(N);
+    o.nst = ar.take<float4>(N * c.H);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
     if (hgt_nr(c.d)) {
       o.dXp = ar.take<char>(U * 2 * c.D * c.esz);  // per-pair [dK|dV] rows
@@ -357,7 +364,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
                "HGT needs Wk, Wq, Wv, Watt, Wmsg, mu");
     if (hgt_nr(c.d)) {
       // reordering off: [K|V] = X [Wk|Wv]_type per node, then [K~|M] = [K|V][src] blockdiag(.)_rel per pair
-      hgt_nr_weights(g->R, g->T, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.Wkv, sv.Bd, c.s);
+      hgt_nr_weights(g->R, g->T, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.Wkv, sv.Bd, c.s);
       GemmArgs k;
       k.A = X; k.a_dtype = c.dt; k.K = c.Din; k.B = sv.Wkv; k.b_dtype = c.dt; k.Y = sv.KV; k.y_dtype = c.dt;
       k.N = 2 * c.D; k.num_w = g->T; k.bt_scratch = sc.bt;
@@ -370,7 +377,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
       a.name = "gemm_pairs_fwd";
       gemm(c, seg_pair_rel(g), a);
     } else {
-      hgt_fold(g, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, c.s);
+      hgt_fold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, c.s);
       GemmArgs a;
       a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
       a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
@@ -384,7 +391,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     q.num_w = g->T; q.bt_scratch = sc.bt;
     q.name = "gemm_nodes_fwd";
     gemm(c, seg_node_type(g), q);
-    hgt_fwd_traverse(g, c.dt, c.D, sv.P, sv.Q, out, sv.stats, sc.pt, c.s);
+    hgt_fwd_traverse(g, c.dt, c.D, c.H, sv.P, sv.Q, out, sv.stats, sc.pt, c.s);
   }
 }
 
@@ -431,7 +438,7 @@ void hgt_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const S
     do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, dKV, c.dt, 2 * c.D, sc.dWkv, g->T, sc.partial,
              "wgrad_nodes_kv");
   if (need_bd || need_wkv)
-    hgt_nr_split(g->R, g->T, c.Din, c.D, need_bd ? sc.dBd : nullptr, need_wkv ? sc.dWkv : nullptr, w->mu, dW->dWk,
+    hgt_nr_split(g->R, g->T, c.Din, c.D, c.D / c.H, need_bd ? sc.dBd : nullptr, need_wkv ? sc.dWkv : nullptr, w->mu, dW->dWk,
                  dW->dWv, dW->dWatt, dW->dWmsg, c.s);
 }
 
@@ -544,8 +551,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       seg_wsum(&pp, sc.wsum, sv.P, c.dt, c.D, nullptr, dW->da, g->R, sc.partial, c.s);
     }
   } else {
-    hgt_bwd_dst(g, c.dt, c.D, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst, sc.pt, c.s);
-    hgt_bwd_pair(g, c.dt, c.D, sv.P, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
+    hgt_bwd_dst(g, c.dt, c.D, c.H, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst, sc.pt, c.s);
+    hgt_bwd_pair(g, c.dt, c.D, c.H, sv.P, sc.GQ, sc.nst, sc.dP, sc.pt, c.s);
     if (hgt_nr(c.d)) {
       hgt_backward_nr(c, X, w, sv, dX, dW, sc);
       return;
@@ -570,7 +577,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {
       do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1), sc.partial, "wgrad_pairs");
-      hgt_unfold(g, c.Din, c.D, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, sc.dFu, dW->dWk, dW->dWv,
+      hgt_unfold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, sc.dFu, dW->dWk, dW->dWv,
                  dW->dWatt, dW->dWmsg, c.s);
     }
   }
@@ -579,7 +586,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
 Ctx make_ctx(rgnn_graph_s* g, const rgnn_layer_desc* d, void* stream) {
   check_desc(g, d);
   Ctx c{g, d, d->dtype, d->d_out, d->d_in, d->dtype == F32 ? (size_t)4 : (size_t)2,
-        static_cast<cudaStream_t>(stream)};
+        static_cast<cudaStream_t>(stream), d->num_heads <= 1 ? 1 : d->num_heads};
   return c;
 }
 

@@ -69,19 +69,20 @@ void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const v
 // A2 (linear-operator reordering): weight-weight products.
 void rgat_tpath_vectors(int R, int d_in, int d_out, const void* W, const void* b, int dtype, float* y,
                         cudaStream_t s);
-// F[a] for every active (r, t) combination a of g (graph.cuh): [mu_r/sqrt(d) Wk_t Watt_r | Wv_t Wmsg_r]
-void hgt_fold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+// F[a] for every active (r, t) combination a of g (graph.cuh): [mu_r/sqrt(dh) Wk_t Watt_r | Wv_t Wmsg_r]
+// (dh = head width d / H; the per-head logit scale)
+void hgt_fold(const rgnn_graph_s* g, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt,
               const void* Wmsg, const float* mu, int dtype, float* F32out, void* Fdt, cudaStream_t s);
 // dWk, dWv, dWatt, dWmsg from dF[a] (fully overwritten; NULL outputs are skipped); P: scratch of dF's size
-void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, const void* Wk, const void* Wv, const void* Watt,
+void hgt_unfold(const rgnn_graph_s* g, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt,
                 const void* Wmsg, const float* mu, int dtype, const float* dF, float* P, float* dWk, float* dWv,
                 float* dWatt, float* dWmsg, cudaStream_t s);
 void rgat_tpath_grads(int R, int d_in, int d_out, const void* W, const void* b, int dtype, const float* Bsum,
                       float* dW, float* db, cudaStream_t s);
 // F1 ablation (HGT, reordering off): un-folded weights and the split of their gradients.
-void hgt_nr_weights(int R, int T, int d_in, int d, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
+void hgt_nr_weights(int R, int T, int d_in, int d, int dh, const void* Wk, const void* Wv, const void* Watt, const void* Wmsg,
                     const float* mu, int dtype, void* Wkv, void* Bd, cudaStream_t s);
-void hgt_nr_split(int R, int T, int d_in, int d, const float* dBd, const float* dWkv, const float* mu, float* dWk,
+void hgt_nr_split(int R, int T, int d_in, int d, int dh, const float* dBd, const float* dWkv, const float* mu, float* dWk,
                   float* dWv, float* dWatt, float* dWmsg, cudaStream_t s);
 void add_f32(int64_t n, const float* x, float* y, cudaStream_t s);
 // F1 ablation (RGAT, reordering off): per (rel, dst) pair -> CSR entries, CSR entries -> per pair,

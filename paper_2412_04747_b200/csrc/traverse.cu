@@ -217,18 +217,23 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n, const int4* __restr
 }
 
 // ------------------------------------------------------------------ HGT forward (A3+A4+A5)
-// KM row of pair p = [K~_p | M_p] (2D wide);  l_e = K~_p . q_v;  out_v = sum softmax(l)_e M_p
-template <class TP, int D, bool GROUP>
+// KM row of pair p = [K~_p | M_p] (2D wide);  l_e = K~_p . q_v;  out_v = sum softmax(l)_e M_p.
+// H heads (F2): head h owns columns h*dh..(h+1)*dh-1, i.e. LH = LPR/H consecutive lanes of a group;
+// its logit is reduced over those lanes only and its online-softmax state lives in them, so
+// per-lane state is per-head state; stats / partial stats are [id][H].
+template <class TP, int D, bool GROUP, int H>
 __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
                                                  float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
                                                  const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                  float* __restrict__ out, float2* __restrict__ stats) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
+  static_assert(LPR % H == 0, "a head must own whole 16-byte lane vectors");
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t v = w.item.x;
-  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c, hd = c / LH;
+  const bool hlead = w.has && (c % LH == 0) && (GROUP || w.g == 0);
   float q[V];
   cvt16<TP>(ldg16(Q + v * D + c * V), q);
   float m = -CUDART_INF_F, s = 0.f, acc[V];
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
       float d = 0.f;
 #pragma unroll
       for (int k = 0; k < V; ++k) d = fmaf(kx[k], q[k], d);
-      d = gsum<LPR>(d, w.mask);
+      d = gsum<LH>(d, w.mask);
       l[u] = ok[u] ? d : -CUDART_INF_F;
       mx = fmaxf(mx, l[u]);
     }
@@ -279,14 +284,14 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   if (!GROUP) merge_groups<LPR, V>(m, s, acc);
   if (slot >= 0) {  // chunk of a heavy row: unnormalised state, merged by k_merge_softmax
     if (w.writer()) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
-    if (w.leader()) pstat[slot] = make_float2(m, s);
+    if (hlead) pstat[(int64_t)slot * H + hd] = make_float2(m, s);
     return;
   }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
   if (w.writer()) st_f32<V>(out + v * D + c * V, acc);
-  if (w.leader()) stats[v] = make_float2(m, s);
+  if (hlead) stats[v * H + hd] = make_float2(m, s);
 }
 
 // ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
 // ------------------------------------------------------------------ HGT backward, dst-major (A6)
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
 // dQ_v = sum_e dl_e K~_p   (layer dtype; heavy rows: fp32 partials merged by k_merge_sum)
-template <class TP, int D, bool GROUP>
+template <class TP, int D, bool GROUP, int H>
 __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
@@ -388,11 +393,11 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
                                                      const float* __restrict__ out, TP* __restrict__ dQ,
                                                      TP* __restrict__ GQ, float4* __restrict__ nst) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t v = w.item.x;
-  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c, hd = c / LH;
   float dq[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) dq[k] = 0.f;
@@ -404,13 +409,13 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
     float go = 0.f;
 #pragma unroll
     for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
-    go = gsum<LPR>(go, w.mask);
-    const float2 st = stats[v];
+    go = gsum<LH>(go, w.mask);
+    const float2 st = stats[v * H + hd];
     const float inv = 1.f / st.y;
     if (slot < 0 && e > b && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
       st_tp<V>(GQ + v * 2 * D + c * V, gv);
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
-      if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
+      if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x, inv, go, 0.f);
     }
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
@@ -437,8 +442,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
           l = fmaf(kx[k], q[k], l);
           da = fmaf(gv[k], mv[k], da);
         }
-        l = gsum<LPR>(l, w.mask);
-        da = gsum<LPR>(da, w.mask);
+        l = gsum<LH>(l, w.mask);
+        da = gsum<LH>(da, w.mask);
         float dl = (i < e) ? __expf(l - st.x) * inv * (da - go) : 0.f;
 #pragma unroll
         for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
@@ -727,14 +732,14 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
 // pair:  K~_p and M_p in registers; per edge e of p: l_e = K~_p . Q_d, alpha_e = exp(l_e - m_d)/sum_d,
 //        dalpha_e = G_d . M_p, dl_e = alpha_e (dalpha_e - G_d . out_d);
 //        dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d  ->  dKM_p = [dK~_p | dM_p].
-template <class TP, int D>
+template <class TP, int D, int H>
 __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __restrict__ rows,
                                                        const float* __restrict__ Gr,
                                                        const TP* __restrict__ Q, const float* __restrict__ out,
                                                        const float2* __restrict__ stats, TP* __restrict__ GQ,
                                                        float4* __restrict__ nst) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
   const int64_t j = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EG + g;
   if (j >= n) return;
@@ -746,27 +751,27 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __
   float go = 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
-  go = gsum<LPR>(go, group_mask<LPR>(g));
+  go = gsum<LH>(go, group_mask<LPR>(g));
   st_tp<V>(GQ + v * 2 * D + c * V, gv);
   st_tp<V>(GQ + v * 2 * D + D + c * V, qv);
-  if (c == 0) {
-    float2 st = stats[v];
-    nst[v] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
+  if (c % LH == 0) {
+    float2 st = stats[v * H + c / LH];
+    nst[v * H + c / LH] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
   }
 }
 
 // One lane moves 16 bytes of the G half and 16 bytes of the Q half of a GQ row (V columns each).
-template <class TP, int D, bool GROUP>
+template <class TP, int D, bool GROUP, int H>
 __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csc_dst,
                                                       const TP* __restrict__ KM, const TP* __restrict__ GQ,
                                                       const float4* __restrict__ nst, TP* __restrict__ dKM) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t p = w.item.x;
-  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c, hd = c / LH;
   float kx[V], mv[V];
   cvt16<TP>(ldg16(KM + p * 2 * D + c * V), kx);
   cvt16<TP>(ldg16(KM + p * 2 * D + D + c * V), mv);
@@ -786,7 +791,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
         const int64_t d = csc_dst[i];
         rg[u] = ldg16(GQ + d * 2 * D + c * V);
         rq[u] = ldg16(GQ + d * 2 * D + D + c * V);
-        ns[u] = __ldg(nst + d);
+        ns[u] = __ldg(nst + d * H + hd);
       }
     }
 #pragma unroll
@@ -800,8 +805,8 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
         l = fmaf(kx[k], qv[k], l);
         da = fmaf(gr[k], mv[k], da);
       }
-      l = gsum<LPR>(l, w.mask);
-      da = gsum<LPR>(da, w.mask);
+      l = gsum<LH>(l, w.mask);
+      da = gsum<LH>(da, w.mask);
       float alpha = (i0 + u * w.step < e) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
       float dl = alpha * (da - ns[u].z);
 #pragma unroll
@@ -831,27 +836,28 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
 // One CTA per heavy id: warp w folds chunks w, w+8, ... of the id (lane c owns columns 4c..4c+3
 // of a W-wide row, looping over W in steps of 128); the 8 warp results are then combined in warp
 // order through shared memory.  Fixed orders throughout: deterministic.
-template <int D>
+template <int D, int H>
 __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const int4* __restrict__ splits,
                                                        const float* __restrict__ pacc,
                                                        const float2* __restrict__ pstat, float* __restrict__ out,
                                                        float2* __restrict__ stats) {
-  __shared__ float sm_m[8], sm_s[8];
+  // lane owns columns 4*lane .. 4*lane+3, which belong to head hh = 4*lane / (D / H)
+  __shared__ float sm_m[8][32], sm_s[8][32];
   __shared__ __align__(16) float sm_acc[8][D];
   const int4 sp = splits[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float m = -CUDART_INF_F;
-  for (int i = tid; i < sp.z; i += 256) m = fmaxf(m, pstat[sp.y + i].x);
-  m = warp_max(m);
-  if (lane == 0) sm_m[warp] = m;
-  __syncthreads();
-  m = sm_m[0];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) m = fmaxf(m, sm_m[k]);
-  float s = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
   const bool act = lane * 4 < D;
+  const int hh = act ? lane * 4 / (D / H) : 0;
+  float m = -CUDART_INF_F;
+  for (int i = warp; i < sp.z; i += 8) m = fmaxf(m, pstat[(int64_t)(sp.y + i) * H + hh].x);
+  sm_m[warp][lane] = m;
+  __syncthreads();
+  m = sm_m[0][lane];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) m = fmaxf(m, sm_m[k][lane]);
+  float s = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int i = warp; i < sp.z; i += 8) {
-    float2 st = pstat[sp.y + i];
+    float2 st = pstat[(int64_t)(sp.y + i) * H + hh];
     float wt = safe_exp_diff(st.x, m);
     s = fmaf(st.y, wt, s);
     if (act) {
@@ -860,24 +866,24 @@ __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const in
       acc[2] = fmaf(wt, a.z, acc[2]); acc[3] = fmaf(wt, a.w, acc[3]);
     }
   }
-  __syncthreads();
-  if (lane == 0) sm_s[warp] = s;
+  sm_s[warp][lane] = s;
   if (act) *reinterpret_cast<float4*>(&sm_acc[warp][lane * 4]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
   __syncthreads();
   if (warp == 0) {
     float st = 0.f, a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      st += sm_s[k];
+      st += sm_s[k][lane];
       if (act)
 #pragma unroll
         for (int j = 0; j < 4; ++j) a4[j] += sm_acc[k][lane * 4 + j];
     }
     float inv = st > 0.f ? 1.f / st : 0.f;
-    if (act)
+    if (act) {
       *reinterpret_cast<float4*>(out + (int64_t)sp.x * D + lane * 4) =
           make_float4(a4[0] * inv, a4[1] * inv, a4[2] * inv, a4[3] * inv);
-    if (lane == 0) stats[sp.x] = make_float2(m, st);
+      if ((lane * 4) % (D / H) == 0) stats[(int64_t)sp.x * H + hh] = make_float2(m, st);
+    }
   }
 }
 
@@ -996,18 +1002,39 @@ void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* nor
   });
 }
 
-void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
+// H heads: template dispatch, only where a head owns whole lane vectors (LPR % H == 0)
+template <int LPR, class F>
+void by_heads(int H, F&& f) {
+  auto go = [&](auto hc) {
+    constexpr int HH = decltype(hc)::value;
+    if constexpr (LPR % HH == 0) f(hc);
+    else RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "num_heads: a head must span a multiple of 16 bytes of the row");
+  };
+  switch (H) {
+    case 1: go(std::integral_constant<int, 1>()); break;
+    case 2: go(std::integral_constant<int, 2>()); break;
+    case 4: go(std::integral_constant<int, 4>()); break;
+    case 8: go(std::integral_constant<int, 8>()); break;
+    default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "num_heads must be 1, 2, 4 or 8");
+  }
+}
+
+void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, float* out,
                       float2* stats, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("hgt_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_hgt_fwd<TP, DD, false>, k_hgt_fwd<TP, DD, true>,
-                  s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
-                  static_cast<const TP*>(Q), out, stats);
+      by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
+        constexpr int HH = decltype(hc)::value;
+        launch_plan("hgt_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_hgt_fwd<TP, DD, false, HH>,
+                    k_hgt_fwd<TP, DD, true, HH>, s, pt.acc, pt.stat, (const int32_t*)g->csr_pair,
+                    static_cast<const TP*>(KM), static_cast<const TP*>(Q), out, stats);
+        launch("merge_heavy_rows", k_merge_softmax<DD, HH>, dim3(g->rows.n_split), dim3(256), 0, s,
+               g->rows.n_split, (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out,
+               stats);
+      });
     });
-    launch("merge_heavy_rows", k_merge_softmax<DD>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
-           (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
@@ -1026,24 +1053,28 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
       if (te) go(k_rgat_fwd<TP, DD, false, true>, k_rgat_fwd<TP, DD, true, true>);
       else go(k_rgat_fwd<TP, DD, false, false>, k_rgat_fwd<TP, DD, true, false>);
     });
-    launch("merge_heavy_rows", k_merge_softmax<DD>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
+    launch("merge_heavy_rows", k_merge_softmax<DD, 1>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
            (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out, stats);
   });
 }
 
-void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
                  cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false>,
-                  k_hgt_bwd_dst<TP, DD, true>, s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
-                  static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ), static_cast<TP*>(GQ), nst);
-      launch("hgt_node_prep", k_hgt_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
-             g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
-             static_cast<TP*>(GQ), nst);
+      by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
+        constexpr int HH = decltype(hc)::value;
+        launch_plan("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH>,
+                    k_hgt_bwd_dst<TP, DD, true, HH>, s, pt.acc, (const int32_t*)g->csr_pair,
+                    static_cast<const TP*>(KM), static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
+                    static_cast<TP*>(GQ), nst);
+        launch("hgt_node_prep", k_hgt_node_prep<TP, DD, HH>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256),
+               0, s, g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
+               static_cast<TP*>(GQ), nst);
+      });
       launch("merge_heavy_rows", k_merge_sum<DD, TP>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
              (const int4*)g->rows.splits, (const float*)pt.acc, static_cast<TP*>(dQ), false);
     });
@@ -1112,16 +1143,18 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
   });
 }
 
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false>,
-                  k_hgt_bwd_pair<TP, DD, true>, s,
-                  pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ), nst,
-                  static_cast<TP*>(dKM));
+      by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
+        constexpr int HH = decltype(hc)::value;
+        launch_plan("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false, HH>,
+                    k_hgt_bwd_pair<TP, DD, true, HH>, s, pt.acc, (const int32_t*)g->csc_dst,
+                    static_cast<const TP*>(KM), static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
+      });
       launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
     });

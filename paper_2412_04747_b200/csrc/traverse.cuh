@@ -11,7 +11,8 @@ struct Partial {
 };
 void rgcn_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const float* norm, const void* P, float* out,
                        bool accumulate, const Partial& pt, cudaStream_t s);
-void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, float* out,
+// HGT, H heads (head h = columns h*D/H .. (h+1)*D/H - 1): stats and the node records are [N][H]
+void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, float* out,
                       float2* stats, const Partial& pt, cudaStream_t s);
 // te != NULL (reordering off): the destination logit term per CSR entry instead of X_v . y_r
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
@@ -19,7 +20,7 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
                        cudaStream_t s);
 // also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) of every
 // destination with in-edges (read by hgt_bwd_pair)
-void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* Q, const float2* stats,
+void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
                  cudaStream_t s);
 // also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
@@ -34,6 +35,6 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
                    float* wsum, float* bx, const Partial& pt, cudaStream_t s);
-void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* KM, const void* GQ, const float4* nst,
+void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn

@@ -17,19 +17,21 @@ pytestmark = pytest.mark.gpu
 
 
 def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0, compact=True,
-             reorder=True):
+             reorder=True, heads=1):
     from paper_2412_04747_b200 import Graph, Layer
     inp = prepare(layer_inputs(model, g, d_in, d_out, seed_x=2 + seed, seed_w=3 + seed), dtype)
     Gh = upstream_grad(g.num_nodes, d_out, seed=4 + seed)
     kw = {}
     if model == "rgcn":
         kw = {"norm": L.rgcn_edge_norm(g, norm), "self_loop": self_loop}
+    if heads != 1:
+        kw["heads"] = heads
     ref_out, _ = L.forward(model, g, inp, **kw)
     ref_grads = L.backward(model, g, inp, Gh, **kw)
 
     G = Graph.from_hetero(g, compact=compact)
     layer = Layer(G, model, d_in, d_out, dtype=dtype, self_loop=self_loop, norm=norm, gemm_impl=gemm_impl,
-                  reorder=reorder)
+                  reorder=reorder, heads=heads)
     dev = to_device(inp, dtype)
     X = dev.pop("X")
     out = layer.forward(X, dev)
@@ -192,3 +194,30 @@ def test_rgat_no_reorder_random_and_skewed():
             run_case("rgat", g, 16, 16, "f32", seed=seed, reorder=False)
     run_case("rgat", config_graph("mutag", seed=1, scale=0.3, a_dst=1.2), 64, 64, "f32", reorder=False)
     run_case("rgat", config_graph("tiny", seed=9, scale=0.5), 64, 64, "bf16", gemm_impl=1, reorder=False)
+
+
+# ----------------------------------------------------------------- F2: multi-head HGT
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("heads", [2, 4, 8])
+def test_hgt_heads(dtype, heads):
+    run_case("hgt", config_graph("aifb", seed=3), 64, 64, dtype, heads=heads)
+
+
+@pytest.mark.parametrize("heads", [2, 8])
+def test_hgt_heads_skewed_vanilla_noreorder(heads):
+    # heavy rows (split + per-head merges), vanilla rows, reordering off, a narrower layer
+    run_case("hgt", config_graph("mutag", seed=1, scale=0.3, a_dst=1.2), 64, 64, "f32", heads=heads)
+    run_case("hgt", config_graph("tiny", seed=5, scale=0.5), 64, 64, "bf16", heads=heads, compact=False)
+    run_case("hgt", config_graph("tiny", seed=6, scale=0.5), 64, 64, "bf16", heads=heads, reorder=False)
+    run_case("hgt", config_graph("tiny", seed=7, scale=0.5), 128, 32, "f32", heads=heads)
+
+
+def test_heads_errors():
+    from paper_2412_04747_b200 import Graph, Layer, RGNNError
+    G = Graph.from_hetero(config_graph("tiny", seed=1))
+    with pytest.raises(RGNNError, match="HGT only"):
+        Layer(G, "rgat", 64, 64, heads=2)
+    with pytest.raises(RGNNError, match="num_heads"):
+        Layer(G, "hgt", 64, 64, heads=3)
+    with pytest.raises(RGNNError, match="head width"):
+        Layer(G, "hgt", 16, 16, dtype="bf16", heads=4)
