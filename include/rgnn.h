@@ -180,6 +180,8 @@ typedef struct {
                           loop, algo:traversal_template P:926): head h owns output columns h*dh .. (h+1)*dh-1,
                           dh = d_out / H (a multiple of 8 for bf16, 4 for f32); l_{e,h} = mu_r K~_{e,h} . q_{v,h}
                           / sqrt(dh), a softmax per (destination, head).  UNSUPPORTED > 1 for RGCN / RGAT. */
+  int32_t hgt_tail;    /* 1: HGT layer tail (F2, reading b12): out_v = GELU(h_v) A_type(v) + X_v, where h is
+                          the attention aggregation; needs d_in == d_out and weights.A.  0: out = h. */
 } rgnn_layer_desc;
 
 /* Layer weights, device pointers in the layer dtype (mu and edge_norm: float).
@@ -196,6 +198,7 @@ typedef struct {
   const void* Wmsg;        /* HGT: [R][d_out][d_out] relation message matrix */
   const float* mu;         /* HGT: [R] relation prior (not trained) */
   const float* edge_norm;  /* RGCN, norm_kind CUSTOM: [E] by edge id */
+  const void* A;           /* HGT with hgt_tail: [T][d_out][d_out] target-type output linear (A-linear) */
 } rgnn_weights;
 
 /* Weight gradients, device float pointers, same shapes as rgnn_weights.
@@ -210,6 +213,7 @@ typedef struct {
   float* dWv;
   float* dWatt;
   float* dWmsg;
+  float* dA;
 } rgnn_weight_grads;
 
 /* Bytes of the `saved` buffer (forward -> backward activations) and of the

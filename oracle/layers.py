@@ -217,12 +217,40 @@ def hgt_backward(g: HeteroGraph, X, Wk, Wq, Wv, Watt, Wmsg, mu, G, heads: int = 
     return {"dX": dX, "dWk": dWk, "dWq": dWq, "dWv": dWv, "dWatt": dWatt, "dWmsg": dWmsg}
 
 
+# ----------------------------------------------------------------- HGT layer tail (F2, reading b12)
+_erf = np.vectorize(__import__("math").erf, otypes=[float])
+
+
+def gelu(x: np.ndarray) -> np.ndarray:
+    """GELU(x) = x Phi(x) = x (1 + erf(x / sqrt 2)) / 2 (the exact, erf form)."""
+    return 0.5 * x * (1.0 + _erf(x / np.sqrt(2.0)))
+
+
+def gelu_grad(x: np.ndarray) -> np.ndarray:
+    """d GELU / dx = Phi(x) + x phi(x)."""
+    return 0.5 * (1.0 + _erf(x / np.sqrt(2.0))) + x * np.exp(-0.5 * x * x) / np.sqrt(2.0 * np.pi)
+
+
+def hgt_tail_forward(g: HeteroGraph, h, X, A):
+    """HGT's output transform (the target-type "A-linear" with a residual, reading b12):
+    out_v = GELU(h_v) A_tau(v) + X_v."""
+    return typed_matmul(gelu(h), A, g.node_type_of()) + X
+
+
+def hgt_tail_backward(g: HeteroGraph, h, X, A, G):
+    """Returns (dh, dA); the residual adds G to dX."""
+    tau = g.node_type_of()
+    dA = typed_outer_sum(gelu(h), G, tau, g.num_node_types)
+    dh = typed_matmul(G, A, tau, transpose=True) * gelu_grad(h)
+    return dh, dA
+
+
 # ----------------------------------------------------------------- dispatch
 PARAMS = {"rgcn": ("W", "W0"), "rgat": ("W", "a", "b"), "hgt": ("Wk", "Wq", "Wv", "Watt", "Wmsg")}
 
 
 def forward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], *, norm=None, norm_kind: str = "mean",
-            self_loop: bool = True, slope: float = 0.2, heads: int = 1):
+            self_loop: bool = True, slope: float = 0.2, heads: int = 1, tail: bool = False):
     if model == "rgcn":
         if norm is None:
             norm = rgcn_edge_norm(g, norm_kind)
@@ -230,13 +258,17 @@ def forward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], *, norm=None
     if model == "rgat":
         return rgat_forward(g, inp["X"], inp["W"], inp["a"], inp["b"], slope)
     if model == "hgt":
-        return hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], heads)
+        h, c = hgt_forward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], heads)
+        if tail:
+            c["h"] = h
+            return hgt_tail_forward(g, h, inp["X"], inp["A"]), c
+        return h, c
     raise ValueError(model)
 
 
 def backward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], G: np.ndarray, *, norm=None,
              norm_kind: str = "mean", self_loop: bool = True, slope: float = 0.2,
-             heads: int = 1) -> Dict[str, np.ndarray]:
+             heads: int = 1, tail: bool = False) -> Dict[str, np.ndarray]:
     if model == "rgcn":
         if norm is None:
             norm = rgcn_edge_norm(g, norm_kind)
@@ -244,6 +276,13 @@ def backward(model: str, g: HeteroGraph, inp: Dict[str, np.ndarray], G: np.ndarr
     if model == "rgat":
         return rgat_backward(g, inp["X"], inp["W"], inp["a"], inp["b"], G, slope)
     if model == "hgt":
-        return hgt_backward(g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"], G,
-                            heads)
+        args = (g, inp["X"], inp["Wk"], inp["Wq"], inp["Wv"], inp["Watt"], inp["Wmsg"], inp["mu"])
+        if not tail:
+            return hgt_backward(*args, G, heads)
+        h, _ = hgt_forward(*args, heads)
+        dh, dA = hgt_tail_backward(g, h, inp["X"], inp["A"], G)
+        out = hgt_backward(*args, dh, heads)
+        out["dX"] = out["dX"] + G
+        out["dA"] = dA
+        return out
     raise ValueError(model)

@@ -373,6 +373,28 @@ __global__ void k_dpair_outer(const Tile* __restrict__ tiles, const float* __res
   }
 }
 
+// F2, HGT layer tail: GELU (exact, erf form) of the aggregation, its derivative, and the residual.
+template <class TO>
+__global__ void k_gelu_fwd(int64_t n, const float* __restrict__ h, TO* __restrict__ gh) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = h[i];
+    gh[i] = from_f<TO>(0.5f * x * (1.f + erff(x * 0.70710678118654752f)));
+  }
+}
+__global__ void k_gelu_bwd(int64_t n, const float* __restrict__ h, float* __restrict__ dg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = h[i];
+    const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+    const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+    dg[i] *= cdf + x * pdf;
+  }
+}
+template <class TX>
+__global__ void k_add_dt(int64_t n, const TX* __restrict__ x, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += to_f(x[i]);
+}
+
 // y += x (fp32, 16-byte vectors when aligned)
 __global__ void k_add_f32(int64_t n, const float* __restrict__ x, float* __restrict__ y) {
   const int64_t n4 = n >> 2;
@@ -662,6 +684,24 @@ void dpair_outer(const Plan& p, const float* dt, const void* b, int dtype, int D
   else
     launch("dpair_outer", k_dpair_outer<bf16>, dim3(p.count), dim3(256), 0, s, p.tiles, dt,
            static_cast<const bf16*>(b), D, static_cast<bf16*>(dPt));
+}
+
+namespace {
+inline dim3 ew_grid(int64_t n) { return dim3((unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), 148 * 16)); }
+}  // namespace
+
+void gelu_fwd(int64_t n, const float* h, void* gh, int dtype, cudaStream_t s) {
+  if (dtype == F32) launch("tail_gelu", k_gelu_fwd<float>, ew_grid(n), dim3(256), 0, s, n, h, static_cast<float*>(gh));
+  else launch("tail_gelu", k_gelu_fwd<bf16>, ew_grid(n), dim3(256), 0, s, n, h, static_cast<bf16*>(gh));
+}
+
+void gelu_bwd(int64_t n, const float* h, float* dg, cudaStream_t s) {
+  launch("tail_gelu_bwd", k_gelu_bwd, ew_grid(n), dim3(256), 0, s, n, h, dg);
+}
+
+void add_dt(int64_t n, const void* x, int dtype, float* y, cudaStream_t s) {
+  if (dtype == F32) launch("tail_residual", k_add_dt<float>, ew_grid(n), dim3(256), 0, s, n, static_cast<const float*>(x), y);
+  else launch("tail_residual", k_add_dt<bf16>, ew_grid(n), dim3(256), 0, s, n, static_cast<const bf16*>(x), y);
 }
 
 void add_f32(int64_t n, const float* x, float* y, cudaStream_t s) {

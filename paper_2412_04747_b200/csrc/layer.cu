@@ -79,6 +79,9 @@ void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
   RGNN_CHECK(d->num_heads >= 0 && (H == 1 || H == 2 || H == 4 || H == 8), RGNN_ERR_UNSUPPORTED,
              "num_heads must be 0/1, 2, 4 or 8");
   RGNN_CHECK(H == 1 || d->model == RGNN_HGT, RGNN_ERR_UNSUPPORTED, "num_heads > 1 is implemented for HGT only");
+  RGNN_CHECK(d->hgt_tail == 0 || d->hgt_tail == 1, RGNN_ERR_INVALID_ARG, "hgt_tail must be 0 or 1");
+  RGNN_CHECK(!d->hgt_tail || (d->model == RGNN_HGT && d->d_in == d->d_out), RGNN_ERR_UNSUPPORTED,
+             "hgt_tail needs an HGT layer with d_in == d_out (residual)");
   RGNN_CHECK((d->d_out / H) % (d->dtype == BF16 ? 8 : 4) == 0, RGNN_ERR_UNSUPPORTED,
              "head width d_out / num_heads must be a multiple of 8 (bf16) or 4 (f32) elements");
 }
@@ -104,6 +107,8 @@ struct Saved {
   float* tdp = nullptr;    //   Pt . b_rel per (rel, dst) pair [UD]
   float* te = nullptr;     //   the same per CSR entry [E]
   float* b32 = nullptr;    //   b as fp32 [R][D]
+  float* H32 = nullptr;    // HGT tail: the attention aggregation h [N][D] fp32
+  void* GH = nullptr;      //   GELU(h) [N][D] layer dtype
 };
 
 void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
@@ -129,6 +134,10 @@ void layout_saved(const Ctx& c, Arena& ar, Saved& o) {
       o.P = ar.take<char>(U * 2 * c.D * c.esz);
       o.Q = ar.take<char>(N * c.D * c.esz);
       o.stats = ar.take<float2>(N * c.H);
+      if (c.d->hgt_tail) {
+        o.H32 = ar.take<float>(N * c.D);
+        o.GH = ar.take<char>(N * c.D * c.esz);
+      }
       if (hgt_nr(c.d)) {
         o.KV = ar.take<char>(N * 2 * c.D * c.esz);
         o.Wkv = ar.take<char>(T * c.Din * 2 * c.D * c.esz);
@@ -174,6 +183,8 @@ struct BwdScratch {
   void* dPt = nullptr;     //   dt (x) b_rel [UD][D] layer dtype
   void* dXd = nullptr;     //   dPt W_rel^T [UD][Din] layer dtype
   float* dWt = nullptr;    //   X[dst]^T dPt per relation [R][Din][D]
+  float* dH = nullptr;     // HGT tail: dL/dh [N][D]
+  void* Gdt = nullptr;     //   dout in the layer dtype [N][D]
   float* partial = nullptr;
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
@@ -250,6 +261,10 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   } else {
     o.dP = ar.take<char>(U * 2 * c.D * c.esz);
     o.dQ = ar.take<char>(N * c.D * c.esz);
+    if (c.d->hgt_tail) {
+      o.dH = ar.take<float>(N * c.D);
+      o.Gdt = ar.take<char>(N * c.D * c.esz);
+    }
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
     o.nst = ar.take<float4>(N * c.H);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
@@ -391,7 +406,18 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     q.num_w = g->T; q.bt_scratch = sc.bt;
     q.name = "gemm_nodes_fwd";
     gemm(c, seg_node_type(g), q);
-    hgt_fwd_traverse(g, c.dt, c.D, c.H, sv.P, sv.Q, out, sv.stats, sc.pt, c.s);
+    float* h = c.d->hgt_tail ? sv.H32 : out;
+    hgt_fwd_traverse(g, c.dt, c.D, c.H, sv.P, sv.Q, h, sv.stats, sc.pt, c.s);
+    if (c.d->hgt_tail) {  // out = GELU(h) A_type + X  (F2, reading b12)
+      RGNN_CHECK(w->A, RGNN_ERR_INVALID_ARG, "hgt_tail needs weights.A");
+      gelu_fwd((int64_t)g->N * c.D, h, sv.GH, c.dt, c.s);
+      GemmArgs t;
+      t.A = sv.GH; t.a_dtype = c.dt; t.K = c.D; t.B = w->A; t.b_dtype = c.dt; t.Y = out; t.y_dtype = F32; t.N = c.D;
+      t.num_w = g->T; t.bt_scratch = sc.bt;
+      t.name = "tail_gemm_fwd";
+      gemm(c, seg_node_type(g), t);
+      add_dt((int64_t)g->N * c.D, X, c.dt, out, c.s);
+    }
   }
 }
 
@@ -583,6 +609,31 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   }
 }
 
+// HGT tail backward: dh = (dout A_type^T) * GELU'(h); the attention layer's backward with G = dh and
+// out = h; then dX += dout (residual) and dA_t = sum_{v of type t} GELU(h_v)^T dout_v.
+void tail_backward(const Ctx& c, const void* X, const rgnn_weights* w, const Saved& sv, const float* dout, float* dX,
+                   const rgnn_weight_grads* dW, const BwdScratch& sc) {
+  rgnn_graph_s* g = c.g;
+  RGNN_CHECK(w->A, RGNN_ERR_INVALID_ARG, "hgt_tail needs weights.A");
+  const int64_t n = (int64_t)g->N * c.D;
+  const void* Gt = dout;
+  if (c.dt == BF16) {
+    convert_dt(n, dout, sc.Gdt, BF16, c.s);
+    Gt = sc.Gdt;
+  }
+  GemmArgs t;
+  t.A = Gt; t.a_dtype = c.dt; t.K = c.D; t.B = w->A; t.b_dtype = c.dt; t.transB = true;
+  t.Y = sc.dH; t.y_dtype = F32; t.N = c.D;
+  t.num_w = g->T; t.bt_scratch = sc.bt;
+  t.name = "tail_gemm_dx";
+  gemm(c, seg_node_type(g), t);
+  gelu_bwd(n, sv.H32, sc.dH, c.s);
+  backward(c, X, w, sv.H32, sv, sc.dH, dX, dW, sc);
+  if (dX) add_f32(n, dout, dX, c.s);
+  if (dW && dW->dA)
+    do_wgrad(c, seg_node_type(g), sv.GH, c.dt, c.D, nullptr, Gt, c.dt, c.D, dW->dA, g->T, sc.partial, "tail_wgrad");
+}
+
 Ctx make_ctx(rgnn_graph_s* g, const rgnn_layer_desc* d, void* stream) {
   check_desc(g, d);
   Ctx c{g, d, d->dtype, d->d_out, d->d_in, d->dtype == F32 ? (size_t)4 : (size_t)2,
@@ -649,7 +700,11 @@ rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* d, const 
     Arena b{static_cast<char*>(scratch), xb};
     BwdScratch bs;
     layout_bwd_scratch(c, b, bs);
-    backward(c, X, w, out, sv, dout, dX, dW, bs);
+    if (d->hgt_tail) {
+      tail_backward(c, X, w, sv, dout, dX, dW, bs);
+    } else {
+      backward(c, X, w, out, sv, dout, dX, dW, bs);
+    }
   });
 }
 

@@ -85,6 +85,10 @@ void hgt_nr_weights(int R, int T, int d_in, int d, int dh, const void* Wk, const
 void hgt_nr_split(int R, int T, int d_in, int d, int dh, const float* dBd, const float* dWkv, const float* mu, float* dWk,
                   float* dWv, float* dWatt, float* dWmsg, cudaStream_t s);
 void add_f32(int64_t n, const float* x, float* y, cudaStream_t s);
+// F2 HGT tail: gh = GELU(h) (erf form) in the layer dtype; dg *= GELU'(h); y += x (x in the layer dtype)
+void gelu_fwd(int64_t n, const float* h, void* gh, int dtype, cudaStream_t s);
+void gelu_bwd(int64_t n, const float* h, float* dg, cudaStream_t s);
+void add_dt(int64_t n, const void* x, int dtype, float* y, cudaStream_t s);
 // F1 ablation (RGAT, reordering off): per (rel, dst) pair -> CSR entries, CSR entries -> per pair,
 // and the rank-1 rows dPt[j] = dt[j] b_rel(j) over a dpair_rel plan.
 void dpair_expand(const rgnn_graph_s* g, const float* tdp, float* te, cudaStream_t s);

@@ -50,11 +50,12 @@ class GraphOptsC(C.Structure):
 class LayerDescC(C.Structure):
     _fields_ = [("model", C.c_int32), ("dtype", C.c_int32), ("d_in", C.c_int32), ("d_out", C.c_int32),
                 ("self_loop", C.c_int32), ("norm_kind", C.c_int32), ("leaky_slope", C.c_float),
-                ("gemm_impl", C.c_int32), ("no_reorder", C.c_int32), ("num_heads", C.c_int32)]
+                ("gemm_impl", C.c_int32), ("no_reorder", C.c_int32), ("num_heads", C.c_int32),
+                ("hgt_tail", C.c_int32)]
 
 
-WEIGHT_FIELDS = ["W", "W0", "a", "b", "Wk", "Wq", "Wv", "Watt", "Wmsg", "mu", "edge_norm"]
-GRAD_FIELDS = ["dW", "dW0", "da", "db", "dWk", "dWq", "dWv", "dWatt", "dWmsg"]
+WEIGHT_FIELDS = ["W", "W0", "a", "b", "Wk", "Wq", "Wv", "Watt", "Wmsg", "mu", "edge_norm", "A"]
+GRAD_FIELDS = ["dW", "dW0", "da", "db", "dWk", "dWq", "dWv", "dWatt", "dWmsg", "dA"]
 
 
 class WeightsC(C.Structure):
@@ -234,10 +235,10 @@ class Layer:
 
     def __init__(self, graph: Graph, model: str, d_in: int, d_out: int, dtype: str = "f32", self_loop: bool = True,
                  norm: str = "mean", leaky_slope: float = 0.2, gemm_impl: int = 0, reorder: bool = True,
-                 heads: int = 1):
+                 heads: int = 1, tail: bool = False):
         self.graph = graph
         self.desc = LayerDescC(MODELS[model], DTYPES[dtype], d_in, d_out, int(self_loop), NORMS[norm],
-                               float(leaky_slope), int(gemm_impl), int(not reorder), int(heads))
+                               float(leaky_slope), int(gemm_impl), int(not reorder), int(heads), int(tail))
         self.model, self.dtype_name = model, dtype
         self.torch_dtype = torch.float32 if dtype == "f32" else torch.bfloat16
         sb, xb = C.c_size_t(), C.c_size_t()
@@ -276,7 +277,7 @@ class Layer:
         wc = self._weights(w)
         shapes = {k: tuple(v.shape) for k, v in w.items() if v is not None and k not in ("mu", "edge_norm")}
         default = {"rgcn": ["dW", "dW0"] if self.desc.self_loop else ["dW"], "rgat": ["dW", "da", "db"],
-                   "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[self.model]
+                   "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"] + (["dA"] if self.desc.hgt_tail else [])}[self.model]
         need = default if need is None else need
         grads = dict(grads or {})
         gc = GradsC()

@@ -44,6 +44,7 @@ def layer_inputs(model: str, g: HeteroGraph, d_in: int, d_out: int,
         out["Watt"] = _glorot(rw, (r, d_out, d_out), d_out, d_out)
         out["Wmsg"] = _glorot(rw, (r, d_out, d_out), d_out, d_out)
         out["mu"] = np.ones(r)
+        out["A"] = _glorot(rw, (t, d_out, d_out), d_out, d_out)  # tail A-linear (F2), drawn last
     else:
         raise ValueError(f"unknown model {model!r}")
     return out

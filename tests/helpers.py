@@ -7,7 +7,7 @@ import torch
 from synth import round_bf16
 
 TOL = {"f32": 1e-4, "bf16": 2e-2}   # north_star tolerances, metric g17
-WEIGHT_KEYS = ("W", "W0", "a", "b", "Wk", "Wq", "Wv", "Watt", "Wmsg")
+WEIGHT_KEYS = ("W", "W0", "a", "b", "Wk", "Wq", "Wv", "Watt", "Wmsg", "A")
 
 
 def rel_err(gpu: np.ndarray, ref: np.ndarray) -> float:

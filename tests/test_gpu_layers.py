@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_impl=0, seed=0, compact=True,
-             reorder=True, heads=1):
+             reorder=True, heads=1, tail=False):
     from paper_2412_04747_b200 import Graph, Layer
     inp = prepare(layer_inputs(model, g, d_in, d_out, seed_x=2 + seed, seed_w=3 + seed), dtype)
     Gh = upstream_grad(g.num_nodes, d_out, seed=4 + seed)
@@ -26,12 +26,14 @@ def run_case(model, g, d_in, d_out, dtype, norm="mean", self_loop=True, gemm_imp
         kw = {"norm": L.rgcn_edge_norm(g, norm), "self_loop": self_loop}
     if heads != 1:
         kw["heads"] = heads
+    if tail:
+        kw["tail"] = True
     ref_out, _ = L.forward(model, g, inp, **kw)
     ref_grads = L.backward(model, g, inp, Gh, **kw)
 
     G = Graph.from_hetero(g, compact=compact)
     layer = Layer(G, model, d_in, d_out, dtype=dtype, self_loop=self_loop, norm=norm, gemm_impl=gemm_impl,
-                  reorder=reorder, heads=heads)
+                  reorder=reorder, heads=heads, tail=tail)
     dev = to_device(inp, dtype)
     X = dev.pop("X")
     out = layer.forward(X, dev)
@@ -221,3 +223,20 @@ def test_heads_errors():
         Layer(G, "hgt", 64, 64, heads=3)
     with pytest.raises(RGNNError, match="head width"):
         Layer(G, "hgt", 16, 16, dtype="bf16", heads=4)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("heads", [1, 4])
+def test_hgt_tail(dtype, heads):
+    """F2: out = GELU(h) A_type + X (reading b12) after the attention aggregation h."""
+    run_case("hgt", config_graph("aifb", seed=4), 64, 64, dtype, heads=heads, tail=True)
+    run_case("hgt", config_graph("tiny", seed=11, scale=0.5), 32, 32, dtype, heads=heads, tail=True)
+
+
+def test_hgt_tail_variants():
+    run_case("hgt", config_graph("mutag", seed=2, scale=0.3, a_dst=1.2), 64, 64, "bf16", tail=True, reorder=False)
+    run_case("hgt", config_graph("tiny", seed=12, scale=0.5), 64, 64, "bf16", tail=True, compact=False, gemm_impl=1)
+    from paper_2412_04747_b200 import Graph, Layer, RGNNError
+    G = Graph.from_hetero(config_graph("tiny", seed=1))
+    with pytest.raises(RGNNError, match="hgt_tail"):
+        Layer(G, "hgt", 64, 32, tail=True)

@@ -170,7 +170,7 @@ def _fd_check(model, g, d_in, d_out, seed, n_probe=6, opts=None):
         return L.forward(model, g, p, **opts)[0]
 
     rng = np.random.default_rng(seed)
-    for name in ("X",) + L.PARAMS[model]:
+    for name in ("X",) + L.PARAMS[model] + (("A",) if opts.get("tail") else ()):
         if "d" + name not in grads:
             continue
         arr = inp[name]
@@ -274,3 +274,32 @@ def test_hgt_heads_one_relation_reduce_to_single_head(heads):
 def test_fd_hgt_heads(heads, seed):
     g = random_small_graph(400 + seed, allow_multi=True)
     _fd_check("hgt", g, 5, 8, seed=seed, opts={"heads": heads})
+
+
+# ----------------------------------------------------------------- HGT tail (F2, reading b12)
+def test_gelu_values():
+    """GELU(x) = x Phi(x): Phi(1) = 0.8413447460685429, Phi(-1) = 0.15865525393145707 (normal CDF
+    table values), GELU(0) = 0, GELU(x) -> x for large x and -> 0 for very negative x."""
+    x = np.array([0.0, 1.0, -1.0, 2.0, 8.0, -8.0])
+    want = np.array([0.0, 0.8413447460685429, -0.15865525393145707, 2 * 0.9772498680518208, 8.0, 0.0])
+    np.testing.assert_allclose(L.gelu(x), want, rtol=1e-12, atol=1e-12)
+    # derivative: Phi(x) + x phi(x); at 0 it is 1/2, at 1: 0.8413447 + 0.2419707
+    np.testing.assert_allclose(L.gelu_grad(np.array([0.0, 1.0])), [0.5, 0.8413447460685429 + 0.24197072451914337],
+                               rtol=1e-12)
+
+
+def test_tail_identity_weights():
+    g = random_small_graph(31)
+    rng = np.random.default_rng(1)
+    h = rng.normal(size=(g.num_nodes, 4))
+    I = np.broadcast_to(np.eye(4), (g.num_node_types, 4, 4))
+    np.testing.assert_allclose(L.hgt_tail_forward(g, h, np.zeros_like(h), I), L.gelu(h), rtol=1e-13)
+    X = rng.normal(size=h.shape)
+    np.testing.assert_allclose(L.hgt_tail_forward(g, h, X, I) - X, L.gelu(h), rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("heads", [1, 2])
+@pytest.mark.parametrize("seed", range(3))
+def test_fd_hgt_tail(heads, seed):
+    g = random_small_graph(500 + seed, allow_multi=True)
+    _fd_check("hgt", g, 8, 8, seed=seed, opts={"heads": heads, "tail": True})
