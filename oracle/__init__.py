@@ -15,6 +15,8 @@ Contents
              adjacency, GAT / masked dot-product attention
   gemm.py    A1 typed segment GEMM Y[S] = X[G] x W[T] (GEMM template)
   fd.py      central finite differences of L = sum(out * G) (reading g12)
+  train.py   F4 training step: stacked layers with ReLU, NLL loss vs random labels
+             (P:1062), exact backward through the stack, SGD update
   sample.py  subgraph extraction so that sampled output rows of a large
              graph can be evaluated exactly by the same functions
 

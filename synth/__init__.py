@@ -11,8 +11,8 @@ restated in DESIGN.md "Input recipe".
 """
 from .graphs import (HeteroGraph, g7, load_tsv, dump_tsv, synth_heterograph,
                      config_graph, CONFIGS, random_small_graph)
-from .inputs import layer_inputs, round_bf16, segment_inputs, upstream_grad
+from .inputs import layer_inputs, random_labels, round_bf16, segment_inputs, stack_inputs, upstream_grad
 
 __all__ = ["HeteroGraph", "g7", "load_tsv", "dump_tsv", "synth_heterograph",
            "config_graph", "CONFIGS", "random_small_graph", "layer_inputs",
-           "round_bf16", "segment_inputs", "upstream_grad"]
+           "round_bf16", "segment_inputs", "upstream_grad", "random_labels", "stack_inputs"]

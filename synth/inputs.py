@@ -90,3 +90,25 @@ def segment_inputs(seed: int, seg_lens, K: int, N: int, num_src: int = 0, num_we
         "seg_weight": rng.integers(0, nw, size=S).astype(np.int32) if shuffle_weights else None,
     }
     return out
+
+
+def random_labels(n: int, num_classes: int, seed: int = 5, labelled_frac: float = 1.0) -> np.ndarray:
+    """The "precomputed random label tensor" of the training measurement: int32 class
+    ids uniform in [0, num_classes); a seeded (1 - labelled_frac) share of rows gets -1 (no label)."""
+    rng = np.random.default_rng(seed)
+    y = rng.integers(0, num_classes, size=n).astype(np.int32)
+    if labelled_frac < 1.0:
+        y[rng.random(n) >= labelled_frac] = -1
+    return y
+
+
+def stack_inputs(model: str, g: HeteroGraph, d: int, num_layers: int) -> list:
+    """Weights of `num_layers` stacked layers of width d (layer i drawn with seed 3 + i, D1);
+    X (seed 2) is returned in the first layer's dict."""
+    out = []
+    for i in range(num_layers):
+        p = layer_inputs(model, g, d, d, seed_w=3 + i)
+        if i:
+            p.pop("X")
+        out.append(p)
+    return out
