@@ -55,6 +55,11 @@ BENCH_CONFIGS = {
     "bgs_rgat": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1),
     "wikikg2_rgcn": dict(graph="wikikg2", model="rgcn", d=64, dtype="bf16", baseline=4),
     "tiny_rgcn": dict(graph="tiny", model="rgcn", d=16, dtype="f32", baseline=0),
+    # F4: a whole 2-layer training step (layer, ReLU, layer, NLL loss vs random labels, backward, SGD)
+    "aifb_rgat_train": dict(graph="aifb", model="rgat", d=64, dtype="bf16", baseline=1, layers=2),
+    "bgs_rgat_train": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1, layers=2),
+    "am_rgat_train": dict(graph="am", model="rgat", d=64, dtype="bf16", baseline=2, layers=2),
+    "mag_hgt_train": dict(graph="mag", model="hgt", d=64, dtype="bf16", baseline=3, layers=2),
 }
 
 
@@ -252,6 +257,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
+    if cfg.get("layers", 1) > 1:
+        return run_train(args, cfg, world, rank, local_rank)
 
     import torch
     import torch.distributed as dist
@@ -507,10 +514,243 @@ def main():
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------- F4 training step
+TRAIN_LR = 1e-3
+LABEL_SEED, LABELLED_FRAC = 5, 1.0
+
+
+def train_bytes(model, dtype, N, E, U, R, T, d, layers, num_params):
+    """Algorithmic bytes per training step: every layer kernel once per layer (the dX kernels of
+    layer 1 are pruned: its input is data), plus the F4 kernels."""
+    b = 2 if dtype == "bf16" else 4
+    per = algorithmic_bytes(model, dtype, N, E, U, 0, R, T, d, d)
+    dx = {"gemm_pairs_dx", "gemm_nodes_dx", "seg_reduce_rows", "gemm_selfloop_dx"}
+    out = {k: v * (layers - 1 if k in dx else layers) for k, v in per.items()}
+    out["relu_fwd"] = (layers - 1) * N * d * (4 + b)
+    out["relu_bwd"] = (layers - 1) * N * d * 12
+    out["nll_loss"] = N * d * 8 + N * 4
+    out["sgd_update"] = num_params * (4 + 4 + 4 + (b if b == 2 else 0))
+    return out
+
+
+def cpu_train_sample(cfg, layers, target_s=15.0):
+    """The fp64 oracle's training step (oracle/train.py, as it stands) on the same generator at a
+    reduced scale, grown until one step takes a few seconds; edges/s = layers * E / step time."""
+    from oracle import train as OT
+    from synth import stack_inputs, random_labels
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    trained = {"rgcn": ("W", "W0"), "rgat": ("W", "a", "b"), "hgt": ("Wk", "Wq", "Wv", "Watt", "Wmsg")}[cfg["model"]]
+    scale, tot_t, tot_e = 1e-3, 0.0, 0
+    while True:
+        g = config_graph(cfg["graph"], seed=1, scale=scale)
+        ps = stack_inputs(cfg["model"], g, cfg["d"], layers)
+        X = ps[0].pop("X")
+        y = random_labels(g.num_nodes, cfg["d"], seed=LABEL_SEED)
+        t = time.perf_counter()
+        OT.train_step(cfg["model"], g, X, ps, y, TRAIN_LR, trained)
+        dt = time.perf_counter() - t
+        tot_t += dt
+        tot_e += layers * g.num_edges
+        if tot_t >= 0.5 * target_s or scale >= 1.0:
+            break
+        scale = min(1.0, scale * max(2.0, min(8.0, 0.5 * target_s / max(dt, 1e-3))))
+    return {"value": tot_e / tot_t, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+            "sample": f"fp64 numpy oracle {layers}-layer {cfg['model'].upper()} training step (oracle/train.py) on the "
+                      f"{cfg['graph']} generator at growing scales up to {scale:g} ({g.num_edges} edges); "
+                      f"{tot_e} layer-edges in {tot_t:.1f} s", "seconds": tot_t}
+
+
+def run_train(args, cfg, world, rank, local_rank):
+    """F4: one step = `layers` stacked layers forward (ReLU between), NLL loss vs a random label
+    tensor, backward through the stack, SGD update of every weight.  value = layers * E
+    edges per step / step time (each layer processes every edge forward and backward)."""
+    import torch
+    from paper_2412_04747_b200 import Graph, Stack, rgnn
+    from synth import stack_inputs, random_labels
+    if world > 1:
+        raise SystemExit("training-step configs run on one GPU (the partitioned path is the layer bench)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    layers = cfg["layers"]
+    g = config_graph(cfg["graph"], seed=1)
+    model, d, dtype = cfg["model"], cfg["d"], cfg["dtype"]
+    G = Graph.from_hetero(g, device=dev, compact=not args.no_compact)
+    info = G.info()
+    ps = stack_inputs(model, g, d, layers)
+    Xh64 = ps[0].pop("X")
+    td = torch.float32 if dtype == "f32" else torch.bfloat16
+    st = Stack(G, model, d, [{k: torch.tensor(v) for k, v in p.items()} for p in ps], dtype=dtype,
+               reorder=not args.no_reorder)
+    X = torch.tensor(Xh64.astype(np.float32), device=dev).to(td)
+    y = random_labels(g.num_nodes, d, seed=LABEL_SEED, labelled_frac=LABELLED_FRAC)
+    nl = int((y >= 0).sum())
+    labels = torch.tensor(y, device=dev)
+
+    def step(Xd, yd):
+        return st.train_step(Xd, yd, nl, TRAIN_LR)
+
+    for _ in range(args.warmup):
+        step(X, labels)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.15)
+
+    def timed(K):
+        torch.cuda.synchronize()
+        rgnn.profile_reset()
+        rgnn.profile_enable(True)
+        n0 = rgnn.launch_count()
+        s = torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        t0 = time.time()
+        ev[0].record(s)
+        for i in range(K):
+            step(X, labels)
+            ev[i + 1].record(s)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        launches = rgnn.launch_count() - n0
+        prof = rgnn.profile_read()
+        rgnn.profile_enable(False)
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
+        return ev[0].elapsed_time(ev[K]), per, launches, prof, t0, t1
+
+    ms, per, launches, prof, t0, t1 = timed(args.steps)
+    time.sleep(0.12)
+    clocks = sampler.summary(t0, t1)
+    remeasured = False
+    if set(clocks["reasons"]) & BAD_REASONS:
+        remeasured = True
+        ms, per, launches, prof, t0, t1 = timed(args.steps)
+        time.sleep(0.12)
+        clocks = sampler.summary(t0, t1)
+    sampler.stop()
+    loss_now = float(st.nll.loss.item())
+    ms_per_step = ms / args.steps
+    value = layers * g.num_edges * args.steps / (ms / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        yh = labels.cpu().pin_memory()
+        lossh = torch.empty(1, dtype=torch.float32).pin_memory()
+        Xd = [torch.empty_like(X) for _ in range(2)]
+        yd = [torch.empty_like(labels) for _ in range(2)]
+        cs = torch.cuda.Stream(device=dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def issue_copy(k):
+            with torch.cuda.stream(cs):
+                cs.wait_event(consumed[k])
+                Xd[k].copy_(Xh, non_blocking=True)
+                yd[k].copy_(yh, non_blocking=True)
+                copied[k].record(cs)
+
+        def e2e_run(K):
+            s = torch.cuda.current_stream()
+            cs.wait_stream(s)
+            issue_copy(0)
+            for i in range(K):
+                k = i % 2
+                if i + 1 < K:
+                    issue_copy(1 - k)
+                s.wait_event(copied[k])
+                lossh.copy_(step(Xd[k], yd[k]), non_blocking=True)
+                consumed[k].record(s)
+
+        e2e_run(2)
+        torch.cuda.synchronize()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        e2e_run(args.steps)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        e2e = {"value": layers * g.num_edges * args.steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size() + yh.numel() * 4),
+               "d2h_bytes_per_step": 4, "ms_per_step": ems / args.steps,
+               "path": "paper_2412_04747_b200.Stack.train_step (C-ABI); per step H2D of X and the labels from pinned "
+                       "host memory (double-buffered on a copy stream), D2H of the loss"}
+
+    peaks = load_peaks()
+    U, E = info["num_pairs"], info["num_edges"]
+    nparams = sum(m.numel() for ms_ in st.master for m in ms_.values())
+    alg = train_bytes(model, dtype, g.num_nodes, E, U, g.num_rels, g.num_node_types, d, layers, nparams)
+    tot_ms = sum(x["ms"] for x in prof.values())
+    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                   "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}
+    for k in kernels:
+        if k in alg and alg[k]:
+            kernels[k]["algorithmic_bytes_per_step"] = int(alg[k])
+            kernels[k]["achieved_gbs"] = alg[k] / (kernels[k]["ms_per_step"] / 1e3) / 1e9
+    dom = max((k for k in prof if k in alg), key=lambda k: prof[k]["ms"], default=None)
+    roofline = None
+    if dom is not None:
+        ms_k = kernels[dom]["ms_per_step"]
+        achieved = alg[dom] / (ms_k / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
+                    "algorithmic_bytes_per_step": int(alg[dom]), "launches_per_step": kernels[dom]["launches_per_step"],
+                    "ms_per_step": ms_k, "step_algorithmic_gb": sum(alg.values()) / 1e9,
+                    "step_achieved_gbs": sum(alg.values()) / (ms_per_step / 1e3) / 1e9,
+                    "note": "bytes and time per step of the kernel label (all its launches in one step, both layers)"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_train_sample(cfg, layers, target_s=args.cpu_seconds)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_per_step_median": float(np.median(per)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": f"{cfg['graph']}-shaped {layers}-layer {model.upper()} training step, hidden {d} "
+                               f"(BASELINE.json configs[{cfg['baseline']}]): layers + ReLU + NLL loss vs random labels "
+                               f"+ backward + SGD; value counts E edges per layer",
+                   "graph": cfg["graph"], "layer": model, "layers": layers, "d": d, "nodes": g.num_nodes,
+                   "edges": int(g.num_edges), "pairs": int(U), "relations": g.num_rels,
+                   "node_types": g.num_node_types, "compaction_ratio": info["compaction_ratio"],
+                   "labelled_rows": nl, "lr": TRAIN_LR, "loss_after_timed_steps": loss_now,
+                   "parallelism": "single GPU", "l2": "flush: none; working set %.2f GB %s L2 (126 MB)" % (
+                       sum(alg.values()) / 1e9 / max(1, layers), ">" if sum(alg.values()) > 126e6 * layers else "~"),
+                   "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
+                   "reorder": not args.no_reorder, "mode": "training (2-layer step incl. loss and SGD)"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
+        "memory": {"graph_index_bytes": int(info["device_bytes"]),
+                   "saved_bytes": int(sum(l.saved.numel() for l in st.layers)),
+                   "scratch_bytes": int(sum(l.scratch.numel() for l in st.layers)),
+                   "peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev))},
+    }
+    print(json.dumps(line))
+
+
 def run_reference(args, cfg, world, rank):
     """Reference arm of this tier: the fp64 oracle as it stands on the host cores; each step is
     a bounded sample of the workload (in-edge subgraph of random destinations)."""
     if rank != 0:
+        return
+    if cfg.get("layers", 1) > 1:
+        vals, secs, edges = [], 0.0, 0
+        per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+        for i in range(args.steps):
+            r = cpu_train_sample(cfg, cfg["layers"], target_s=per_step)
+            secs += r["seconds"]
+            edges += r["value"] * r["seconds"]
+        value = edges / secs
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic",
+                          "config": {"workload": f"{cfg['graph']}-shaped {cfg['layers']}-layer {cfg['model'].upper()} "
+                                                 "training step, bounded sample per step", "graph": cfg["graph"]},
+                          "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                                           "sample": r["sample"]},
+                          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
     g = config_graph(cfg["graph"], seed=1)
     model, d = cfg["model"], cfg["d"]

@@ -278,6 +278,56 @@ RGNN_API rgnn_status rgnn_segment_gemm(rgnn_segments_t p, int32_t dtype, const v
                                        const void* W, int32_t num_weights, int32_t N, int32_t trans_w, void* Y,
                                        int32_t y_dtype, void* scratch, size_t scratch_bytes, void* stream);
 
+/* ------------------------------------------------------------------ F4: training step around the layers
+ * a stacked-layer training step.  The paper's training measurement computes
+ * "the negative log-likelihood loss by comparing the output with a precomputed random label
+ * tensor" (§3.4.1); BASELINE.json's AIFB/AM configs stack 2 RGAT layers.  Between layers
+ * the activation is ReLU (DESIGN.md b13), the optimiser plain SGD (b15).
+ * All calls enqueue on `stream` and never synchronise it. */
+
+/* a[i] = max(h[i], 0) converted to `dtype` (the next layer's input X), i in [0, n).
+ * h: device float[n]; a: device [n] in dtype (may alias h only for RGNN_F32).
+ * Errors: INVALID_ARG (NULL with n > 0, bad dtype), CUDA. */
+RGNN_API rgnn_status rgnn_relu_forward(int64_t n, const float* h, void* a, int32_t dtype, void* stream);
+
+/* dh[i] = h[i] > 0 ? da[i] : 0 (ReLU'(0) = 0), i in [0, n).  h, da, dh: device float[n];
+ * dh may alias da (in place).  Errors: INVALID_ARG, CUDA. */
+RGNN_API rgnn_status rgnn_relu_backward(int64_t n, const float* h, const float* da, float* dh, void* stream);
+
+/* Scratch bytes of rgnn_nll_loss for n rows (per-block partial sums; caller-owned device memory). */
+RGNN_API rgnn_status rgnn_nll_loss_workspace(int64_t n, int32_t c, size_t* scratch_bytes);
+
+/* Mean negative log-likelihood of log_softmax over each row of logits (DESIGN.md b14):
+ *   loss = -(1/num_labeled) sum_{v: 0 <= labels[v] < c} log softmax(logits[v])[labels[v]]
+ *   dlogits[v] = (softmax(logits[v]) - onehot(labels[v])) / num_labeled   (labelled rows)
+ *   dlogits[v] = 0                                                        (labels[v] < 0)
+ * logits: device float[n][c], row-major; labels: device int32[n]; c in [1, 1024].
+ * num_labeled: the number of rows with a label in [0, c), known to the caller (it built the
+ * labels).  loss: device float[1], written by the call's last kernel: NaN if the rows the
+ * device counted as labelled differ from num_labeled, or any label is >= c (the device-side
+ * error report; the call itself cannot see device data without a sync).  dlogits: device
+ * float[n][c] or NULL (loss only).  Deterministic: fixed grid, fixed reduction order.
+ * Errors: INVALID_ARG (NULL pointers, c out of range, scratch too small), CUDA. */
+RGNN_API rgnn_status rgnn_nll_loss(int64_t n, int32_t c, const float* logits, const int32_t* labels,
+                                   int64_t num_labeled, float* loss, float* dlogits, void* scratch,
+                                   size_t scratch_bytes, void* stream);
+
+/* One parameter tensor of an SGD update: master -= lr * grad (float, device, n elements);
+ * then, when shadow != NULL, shadow = master converted to shadow_dtype (the copy the layers read,
+ * e.g. bf16 weights of the tensor-core path).  For an f32 layer, master is the weight itself. */
+typedef struct {
+  float* master;
+  const float* grad;
+  void* shadow;
+  int64_t n;
+} rgnn_sgd_tensor;
+
+/* Plain SGD (theta <- theta - lr dL/dtheta, no momentum / weight decay; reading b15) over
+ * `count` tensors (host array) in one launch per 32 tensors.  shadow_dtype: rgnn_dtype.
+ * Errors: INVALID_ARG (NULL pointers, negative n, bad dtype), CUDA. */
+RGNN_API rgnn_status rgnn_sgd_update(int32_t count, const rgnn_sgd_tensor* tensors, float lr,
+                                     int32_t shadow_dtype, void* stream);
+
 /* ------------------------------------------------------------------ profiling
  * When enabled, every kernel the library launches is bracketed by CUDA events
  * on its launch stream.  rgnn_profile_read synchronises those events and

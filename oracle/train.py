@@ -7,7 +7,9 @@ loss by comparing the output with a precomputed random label tensor" (P:1062
 §3.4.1); the BASELINE.json AIFB/AM configs are "RGAT 2 layers hidden 64".
 
 Readings (DESIGN.md b13-b15):
-  * between stacked layers: ReLU (SURVEY.md §8(c) C2 g2), h_{l+1} input = max(h_l, 0);
+  * between stacked layers: ReLU, h_{l+1} input = max(h_l, 0); on the bf16
+    path the next layer reads the bf16 rounding of max(h_l, 0), so the oracle of that path
+    applies the same rounding (`act_round`), as C7 rounds the first layer's X;
   * loss: L = -(1/|V_lab|) sum_{v in V_lab} log softmax(out_v)[y_v] over the rows with a
     label y_v in [0, C) (rows with y_v < 0 carry no label), the negative log-likelihood of
     log_softmax outputs, mean reduction;
@@ -20,7 +22,7 @@ exact backward in reverse order, then the update.
 """
 from __future__ import annotations
 
-from typing import Dict, List, Sequence, Tuple
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -63,8 +65,16 @@ def _layer_inp(params: Dict[str, np.ndarray], X: np.ndarray) -> Dict[str, np.nda
     return d
 
 
+Round = Optional[Callable[[np.ndarray], np.ndarray]]
+
+
+def _act(h: np.ndarray, act_round: Round) -> np.ndarray:
+    a = relu(h)
+    return act_round(a) if act_round is not None else a
+
+
 def stack_forward(model: str, g: HeteroGraph, X: np.ndarray, params: Sequence[Dict[str, np.ndarray]],
-                  labels: np.ndarray, **kw) -> Tuple[float, List[np.ndarray]]:
+                  labels: np.ndarray, act_round: Round = None, **kw) -> Tuple[float, List[np.ndarray]]:
     """Forward of len(params) stacked layers with ReLU between them, then the NLL loss.
     Returns (loss, [h_1, ..., h_n]) (pre-activation layer outputs)."""
     hs: List[np.ndarray] = []
@@ -72,20 +82,22 @@ def stack_forward(model: str, g: HeteroGraph, X: np.ndarray, params: Sequence[Di
     for i, p in enumerate(params):
         h, _ = L.forward(model, g, _layer_inp(p, x), **kw)
         hs.append(h)
-        x = relu(h) if i + 1 < len(params) else h
+        x = _act(h, act_round) if i + 1 < len(params) else h
     loss, _ = nll_loss(hs[-1], labels)
     return loss, hs
 
 
 def stack_backward(model: str, g: HeteroGraph, X: np.ndarray, params: Sequence[Dict[str, np.ndarray]],
-                   labels: np.ndarray, **kw) -> Tuple[float, List[Dict[str, np.ndarray]]]:
+                   labels: np.ndarray, act_round: Round = None, **kw) -> Tuple[float, List[Dict[str, np.ndarray]]]:
     """Loss and the weight gradients of every layer (list of dicts in layer order).
-    Layer 1's dX (the input features) is dropped: the input is data, not a parameter."""
-    loss, hs = stack_forward(model, g, X, params, labels, **kw)
+    Layer 1's dX (the input features) is dropped: the input is data, not a parameter.
+    With act_round the rounding is treated as the identity in the backward (straight through:
+    the gradient flows to max(h, 0) unchanged, as on the device)."""
+    loss, hs = stack_forward(model, g, X, params, labels, act_round, **kw)
     _, G = nll_loss(hs[-1], labels)
     grads: List[Dict[str, np.ndarray]] = [None] * len(params)  # type: ignore[list-item]
     for i in range(len(params) - 1, -1, -1):
-        x = X if i == 0 else relu(hs[i - 1])
+        x = X if i == 0 else _act(hs[i - 1], act_round)
         gi = L.backward(model, g, _layer_inp(params[i], x), G, **kw)
         if i > 0:
             G = gi["dX"] * (hs[i - 1] > 0)   # ReLU' (0 at h = 0)
@@ -107,7 +119,7 @@ def sgd(params: Sequence[Dict[str, np.ndarray]], grads: Sequence[Dict[str, np.nd
 
 
 def train_step(model: str, g: HeteroGraph, X: np.ndarray, params: Sequence[Dict[str, np.ndarray]],
-               labels: np.ndarray, lr: float, trained: Sequence[str], **kw):
+               labels: np.ndarray, lr: float, trained: Sequence[str], act_round: Round = None, **kw):
     """One training step: returns (loss before the update, grads, updated params)."""
-    loss, grads = stack_backward(model, g, X, params, labels, **kw)
+    loss, grads = stack_backward(model, g, X, params, labels, act_round, **kw)
     return loss, grads, sgd(params, grads, lr, trained)

@@ -4,6 +4,8 @@ The compute lives in librgnn.so (csrc/, C-ABI in include/rgnn.h); `rgnn` is its
 ctypes binding.  Build with `python -m paper_2412_04747_b200.build`.
 """
 from . import rgnn
-from .rgnn import Graph, Layer, RGNNError, SegmentPlan, lib, segment_gemm, version
+from .rgnn import Graph, Layer, NllLoss, RGNNError, SegmentPlan, lib, segment_gemm, version
+from .train import Stack
 
-__all__ = ["rgnn", "Graph", "Layer", "RGNNError", "SegmentPlan", "lib", "segment_gemm", "version"]
+__all__ = ["rgnn", "Graph", "Layer", "NllLoss", "RGNNError", "SegmentPlan", "Stack", "lib", "segment_gemm",
+           "version"]

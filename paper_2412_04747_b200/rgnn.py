@@ -30,7 +30,8 @@ EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_b
             "rgnn_graph_array_size", "rgnn_graph_destroy", "rgnn_layer_workspace", "rgnn_layer_forward",
             "rgnn_layer_backward", "rgnn_profile_enable", "rgnn_profile_reset", "rgnn_profile_read",
             "rgnn_launch_count", "rgnn_segment_plan_create", "rgnn_segment_plan_destroy",
-            "rgnn_segment_gemm_workspace", "rgnn_segment_gemm"]
+            "rgnn_segment_gemm_workspace", "rgnn_segment_gemm", "rgnn_relu_forward", "rgnn_relu_backward",
+            "rgnn_nll_loss_workspace", "rgnn_nll_loss", "rgnn_sgd_update"]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -64,6 +65,10 @@ class WeightsC(C.Structure):
 
 class GradsC(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in GRAD_FIELDS]
+
+
+class SgdTensorC(C.Structure):
+    _fields_ = [("master", C.c_void_p), ("grad", C.c_void_p), ("shadow", C.c_void_p), ("n", C.c_int64)]
 
 
 class RGNNError(RuntimeError):
@@ -115,6 +120,12 @@ def lib() -> C.CDLL:
         L.rgnn_segment_gemm.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_size_t, C.c_void_p]
+        L.rgnn_relu_forward.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        L.rgnn_relu_backward.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.rgnn_nll_loss_workspace.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
+        L.rgnn_nll_loss.argtypes = [C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_size_t, C.c_void_p]
+        L.rgnn_sgd_update.argtypes = [C.c_int32, C.POINTER(SgdTensorC), C.c_float, C.c_int32, C.c_void_p]
         L.rgnn_profile_enable.argtypes = [C.c_int32]
         L.rgnn_profile_read.argtypes = [C.c_char_p, C.c_size_t]
         _lib = L
@@ -346,6 +357,63 @@ def segment_gemm(plan: SegmentPlan, X: torch.Tensor, W: torch.Tensor, gather: Op
                                    {torch.float32: F32, torch.bfloat16: BF16}[out.dtype], _ptr(scratch),
                                    scratch.numel(), _stream()))
     return out
+
+
+# ----------------------------------------------------------------- F4 training-step primitives
+def relu_forward(h: torch.Tensor, out: Optional[torch.Tensor] = None, dtype: Optional[torch.dtype] = None) -> torch.Tensor:
+    """out = max(h, 0) in `dtype` (the next layer's input; rgnn_relu_forward)."""
+    if h.dtype != torch.float32:
+        raise TypeError("h must be float32")
+    if out is None:
+        out = torch.empty(h.shape, dtype=dtype or torch.float32, device=h.device)
+    _check(lib().rgnn_relu_forward(h.numel(), _ptr(h), _ptr(out), {torch.float32: F32, torch.bfloat16: BF16}[out.dtype],
+                                   _stream()))
+    return out
+
+
+def relu_backward(h: torch.Tensor, da: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """dh = da where h > 0 else 0 (rgnn_relu_backward; out may be da)."""
+    if out is None:
+        out = torch.empty_like(da)
+    if not (h.dtype == da.dtype == out.dtype == torch.float32) or h.numel() != da.numel() or da.numel() != out.numel():
+        raise TypeError("h, da, out: float32 tensors of one size")
+    _check(lib().rgnn_relu_backward(h.numel(), _ptr(h), _ptr(da), _ptr(out), _stream()))
+    return out
+
+
+class NllLoss:
+    """Mean NLL of log_softmax rows against int32 labels (rows with label < 0 are unlabelled);
+    rgnn_nll_loss.  The loss stays on the device (a float32 scalar tensor)."""
+
+    def __init__(self, n: int, c: int, device="cuda"):
+        sb = C.c_size_t()
+        _check(lib().rgnn_nll_loss_workspace(int(n), int(c), C.byref(sb)))
+        self.n, self.c = int(n), int(c)
+        self.scratch = torch.empty(max(sb.value, 1), dtype=torch.uint8, device=device)
+        self.loss = torch.empty(1, dtype=torch.float32, device=device)
+
+    def __call__(self, logits: torch.Tensor, labels: torch.Tensor, num_labeled: int,
+                 dlogits: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if logits.dtype != torch.float32 or tuple(logits.shape) != (self.n, self.c):
+            raise TypeError(f"logits must be float32 [{self.n}, {self.c}]")
+        if labels.dtype != torch.int32 or labels.numel() != self.n:
+            raise TypeError("labels must be int32 [n]")
+        _check(lib().rgnn_nll_loss(self.n, self.c, _ptr(logits), _ptr(labels), int(num_labeled), _ptr(self.loss),
+                                   _ptr(dlogits), _ptr(self.scratch), self.scratch.numel(), _stream()))
+        return self.loss
+
+
+def sgd_update(tensors, lr: float, shadow_dtype: torch.dtype = torch.float32) -> None:
+    """theta -= lr * grad for each (master, grad, shadow-or-None) triple (rgnn_sgd_update, one launch)."""
+    arr = (SgdTensorC * max(len(tensors), 1))()
+    for i, (m, g, sh) in enumerate(tensors):
+        if m.dtype != torch.float32 or g.dtype != torch.float32 or m.numel() != g.numel():
+            raise TypeError("master and grad must be float32 of one size")
+        if sh is not None and (sh.numel() != m.numel() or sh.dtype != shadow_dtype):
+            raise TypeError("shadow must match master's size and shadow_dtype")
+        arr[i] = SgdTensorC(_ptr(m), _ptr(g), _ptr(sh), m.numel())
+    _check(lib().rgnn_sgd_update(len(tensors), arr, float(lr), {torch.float32: F32, torch.bfloat16: BF16}[shadow_dtype],
+                                 _stream()))
 
 
 def profile_enable(on: bool = True) -> None:

@@ -112,3 +112,4 @@ def stack_inputs(model: str, g: HeteroGraph, d: int, num_layers: int) -> list:
             p.pop("X")
         out.append(p)
     return out
+

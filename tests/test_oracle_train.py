@@ -137,3 +137,17 @@ def test_sgd_first_order_decrease(model):
                 assert np.array_equal(q[k], p[k] - lr * gr["d" + k])
             else:
                 assert q[k] is p[k]
+
+
+def test_act_round_identity_and_effect():
+    """act_round = identity reproduces the unrounded stack; bf16 rounding changes the loss by
+    O(2^-9) only (it rounds the second layer's input, C7)."""
+    from synth import round_bf16
+    g = random_small_graph(5, max_nodes=16, max_edges=60)
+    X, ps = _stack("rgat", g, 8, 2)
+    y = random_labels(g.num_nodes, 8, seed=1)
+    l0, g0 = T.stack_backward("rgat", g, X, ps, y)
+    l1, g1 = T.stack_backward("rgat", g, X, ps, y, act_round=lambda a: a)
+    assert l0 == l1 and all(np.array_equal(a["dW"], b["dW"]) for a, b in zip(g0, g1))
+    l2, _ = T.stack_backward("rgat", g, X, ps, y, act_round=round_bf16)
+    assert l2 != l0 and abs(l2 - l0) <= 1e-2 * abs(l0)
