@@ -55,6 +55,9 @@ BENCH_CONFIGS = {
     "bgs_rgat": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1),
     "wikikg2_rgcn": dict(graph="wikikg2", model="rgcn", d=64, dtype="bf16", baseline=4),
     "tiny_rgcn": dict(graph="tiny", model="rgcn", d=16, dtype="f32", baseline=0),
+    "mutag_rgat": dict(graph="mutag", model="rgat", d=64, dtype="bf16", baseline=1),
+    "fb15k_rgcn": dict(graph="fb15k", model="rgcn", d=64, dtype="bf16", baseline=4),
+    "biokg_hgt": dict(graph="biokg", model="hgt", d=64, dtype="bf16", baseline=3),
     # F4: a whole 2-layer training step (layer, ReLU, layer, NLL loss vs random labels, backward, SGD)
     "aifb_rgat_train": dict(graph="aifb", model="rgat", d=64, dtype="bf16", baseline=1, layers=2),
     "bgs_rgat_train": dict(graph="bgs", model="rgat", d=64, dtype="bf16", baseline=1, layers=2),
@@ -220,10 +223,32 @@ def cpu_oracle_sample(g, model, inp, Gh, target_s=15.0, seed=0):
         if elapsed >= 0.5 * target_s or n_dst >= g.num_nodes:
             break
         n_dst = int(min(g.num_nodes, n_dst * max(2.0, 0.6 * target_s / max(dt, 1e-3))))
-    return {"value": edges / elapsed, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+    return {"value": edges / elapsed, "unit": UNIT, "cores": int(threads), "kind": "oracle", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
             "sample": f"fp64 numpy oracle, vanilla per-edge {model.upper()} fwd+bwd on in-edge subgraphs of random "
                       f"destinations: {edges} edges in {elapsed:.1f} s (last sample {last[0]} dst / {last[1]} edges)",
             "seconds": elapsed}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def single_thread(fn, target_s):
+    """the oracle timed a second time on one host thread (BLAS limited to 1)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        return None
+    with threadpool_limits(limits=1):
+        r = fn(target_s)
+    return {"value": r["value"], "unit": r["unit"], "cores": 1, "sample": r["sample"]}
 
 
 # ----------------------------------------------------------------- main
@@ -245,6 +270,9 @@ def main():
                     help="vanilla materialization (one projected row per edge): the C ablation of tab:optimizations")
     ap.add_argument("--no-reorder", action="store_true",
                     help="linear-operator reordering off (HGT): the R ablation of tab:optimizations")
+    ap.add_argument("--a-dst", type=float, default=None,
+                    help="destination Zipf exponent of the generator (SURVEY.md §8(d) D1 load-balance sensitivity "
+                         "points: 0 = uniform in-degrees, 1.2 = heavier skew; default the config's 0.8)")
     ap.add_argument("--infer", action="store_true",
                     help="inference: a step is the forward pass only (the 'Inference' columns of tab:optimizations)")
     args = ap.parse_args()
@@ -270,7 +298,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    g = config_graph(cfg["graph"], seed=1)
+    g = config_graph(cfg["graph"], seed=1, a_dst=args.a_dst)
     model, d, dtype = cfg["model"], cfg["d"], cfg["dtype"]
     ranges = D.partition_ranges(g.dst, g.num_nodes, world)
     lo, hi = ranges[rank]
@@ -484,6 +512,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.infer:
         cpu = cpu_oracle_sample(g, model, inp, Gh, target_s=args.cpu_seconds)
+        cpu["single_thread"] = single_thread(lambda t: cpu_oracle_sample(g, model, inp, Gh, target_s=t),
+                                             args.cpu_seconds / 3)
 
     if rank == 0:
         line = {
@@ -505,7 +535,7 @@ def main():
                        "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
                        "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
                        "reorder": not args.no_reorder, "heads": cfg.get("heads", 1), "mode": "inference (forward only)" if args.infer else "training (forward + backward)",
-                       "cuda_graph": bool(use_graph)},
+                       "cuda_graph": bool(use_graph), "a_dst": args.a_dst if args.a_dst is not None else 0.8},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "memory": memory, "kernels": kernels,
         }
@@ -558,7 +588,8 @@ def cpu_train_sample(cfg, layers, target_s=15.0):
         if tot_t >= 0.5 * target_s or scale >= 1.0:
             break
         scale = min(1.0, scale * max(2.0, min(8.0, 0.5 * target_s / max(dt, 1e-3))))
-    return {"value": tot_e / tot_t, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+    return {"value": tot_e / tot_t, "unit": UNIT, "cores": int(threads), "kind": "oracle", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
             "sample": f"fp64 numpy oracle {layers}-layer {cfg['model'].upper()} training step (oracle/train.py) on the "
                       f"{cfg['graph']} generator at growing scales up to {scale:g} ({g.num_edges} edges); "
                       f"{tot_e} layer-edges in {tot_t:.1f} s", "seconds": tot_t}
@@ -576,7 +607,7 @@ def run_train(args, cfg, world, rank, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     layers = cfg["layers"]
-    g = config_graph(cfg["graph"], seed=1)
+    g = config_graph(cfg["graph"], seed=1, a_dst=args.a_dst)
     model, d, dtype = cfg["model"], cfg["d"], cfg["dtype"]
     G = Graph.from_hetero(g, device=dev, compact=not args.no_compact)
     info = G.info()
@@ -596,21 +627,35 @@ def run_train(args, cfg, world, rank, local_rank):
     for _ in range(args.warmup):
         step(X, labels)
     torch.cuda.synchronize()
+    graph = None
+    if args.cuda_graph:  # launch-bound small graphs: replay one captured training step
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            step(X, labels)
+        torch.cuda.current_stream().wait_stream(cs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(X, labels)
+        torch.cuda.synchronize()
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.15)
 
-    def timed(K):
+    def timed(K, use_graph=False):
         torch.cuda.synchronize()
         rgnn.profile_reset()
-        rgnn.profile_enable(True)
+        rgnn.profile_enable(not use_graph)
         n0 = rgnn.launch_count()
         s = torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
         t0 = time.time()
         ev[0].record(s)
         for i in range(K):
-            step(X, labels)
+            if use_graph:
+                graph.replay()
+            else:
+                step(X, labels)
             ev[i + 1].record(s)
         torch.cuda.synchronize()
         t1 = time.time()
@@ -620,15 +665,18 @@ def run_train(args, cfg, world, rank, local_rank):
         per = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
         return ev[0].elapsed_time(ev[K]), per, launches, prof, t0, t1
 
-    ms, per, launches, prof, t0, t1 = timed(args.steps)
+    use_graph = graph is not None
+    ms, per, launches, prof, t0, t1 = timed(args.steps, use_graph)
     time.sleep(0.12)
     clocks = sampler.summary(t0, t1)
     remeasured = False
     if set(clocks["reasons"]) & BAD_REASONS:
         remeasured = True
-        ms, per, launches, prof, t0, t1 = timed(args.steps)
+        ms, per, launches, prof, t0, t1 = timed(args.steps, use_graph)
         time.sleep(0.12)
         clocks = sampler.summary(t0, t1)
+    if use_graph:  # launches inside the graph: counted and profiled on an un-captured pass
+        _, _, launches, prof, _, _ = timed(args.steps, False)
     sampler.stop()
     loss_now = float(st.nll.loss.item())
     ms_per_step = ms / args.steps
@@ -704,6 +752,7 @@ def run_train(args, cfg, world, rank, local_rank):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_train_sample(cfg, layers, target_s=args.cpu_seconds)
+        cpu["single_thread"] = single_thread(lambda t: cpu_train_sample(cfg, layers, target_s=t), args.cpu_seconds / 3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_per_step_median": float(np.median(per)),
@@ -718,7 +767,8 @@ def run_train(args, cfg, world, rank, local_rank):
                    "parallelism": "single GPU", "l2": "flush: none; working set %.2f GB %s L2 (126 MB)" % (
                        sum(alg.values()) / 1e9 / max(1, layers), ">" if sum(alg.values()) > 126e6 * layers else "~"),
                    "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
-                   "reorder": not args.no_reorder, "mode": "training (2-layer step incl. loss and SGD)"},
+                   "reorder": not args.no_reorder, "mode": "training (2-layer step incl. loss and SGD)",
+                   "cuda_graph": use_graph, "a_dst": args.a_dst if args.a_dst is not None else 0.8},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks, "remeasured_for_clocks": remeasured, "kernels": kernels,
         "memory": {"graph_index_bytes": int(info["device_bytes"]),
