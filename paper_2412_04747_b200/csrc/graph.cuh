@@ -13,6 +13,8 @@ namespace rgnn {
 constexpr int SPLIT_THRESH = 1024;  // heavy: more edges than this -> chunks of SPLIT_CHUNK, one warp each,
 constexpr int SPLIT_CHUNK = 512;    //        partial states merged afterwards
 constexpr int LIGHT_MAX = 64;       // light: at most this many edges -> one lane group each; else one warp
+constexpr int SHORT_MAX = 4;        // short: light items with at most this many edges (a suffix of the sorted
+                                    //        light list) -> KI items per lane group, gathered together
 
 // Edge-balanced work list over "ids" (destination rows or pairs) whose edges are the
 // contiguous range [begin, begin + deg) of the CSR (rows) or CSC (pairs).
@@ -20,6 +22,7 @@ struct WorkPlan {
   int4* items = nullptr;   // (id, edge begin, edge end, partial slot or -1)
   int64_t n_warp = 0;      // items [0, n_warp): heavy chunks then medium ids, one warp per item
   int64_t n_items = 0;     // items [n_warp, n_items): light ids, one lane group per item
+  int64_t n_short = 0;     // items [n_short, n_items): short light ids (<= SHORT_MAX edges; n_warp <= n_short)
   int4* splits = nullptr;  // (id, first slot, number of slots, 0) for every heavy id
   int64_t n_split = 0;
   int64_t n_slots = 0;

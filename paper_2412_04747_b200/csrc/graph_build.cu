@@ -255,6 +255,8 @@ void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std
   heavy.insert(heavy.end(), medium.begin(), medium.end());
   heavy.insert(heavy.end(), light.begin(), light.end());
   wp.n_items = (int64_t)heavy.size();
+  wp.n_short = wp.n_items;  // light items are sorted longest first: the short ones are a suffix
+  while (wp.n_short > wp.n_warp && heavy[wp.n_short - 1].z - heavy[wp.n_short - 1].y <= SHORT_MAX) --wp.n_short;
   wp.n_split = (int64_t)splits.size();
   wp.n_slots = slots;
   wp.items = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(wp.n_items, 1), s));

@@ -20,6 +20,8 @@
 // pair p the edges are contiguous in the CSC -> dP_p / [dK~_p | dM_p].  No float atomics.
 #include <math_constants.h>
 
+#include <cstdlib>
+#include <tuple>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -28,7 +30,13 @@
 namespace rgnn {
 namespace {
 
-constexpr int UNR = 4;    // edges per group loaded ahead (dst-major and pair kernels)
+#ifndef RGNN_UNR_D
+#define RGNN_UNR_D 4
+#endif
+#ifndef RGNN_PF_D
+#define RGNN_PF_D 0
+#endif
+constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and pair kernels)
 #ifndef RGNN_UNR_P
 #define RGNN_UNR_P 2
 #endif
@@ -78,6 +86,15 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
 __device__ __forceinline__ void st4(bf16* p, float a, float b, float c, float d) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
   *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+// 16-byte shared-memory load the compiler may not hoist (lane-private staging slots are re-read
+// per edge instead of occupying registers)
+__device__ __forceinline__ uint4 lds16(const uint4* p) {
+  uint4 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
 }
 
 // sum over the LPR lanes of one group (mask = the lanes executing this call)
@@ -162,6 +179,34 @@ struct Work {
   static constexpr unsigned mask = 0xffffffffu;
 };
 
+// Short items (<= SHORT_MAX edges, graph.cuh): each lane group owns KI items of the sorted list
+// (group g of warp w: items w*EG*KI + g + EG*k, k < KI) and gathers edge t of all of them in
+// the same step, so one dependent load chain (item -> index -> row) serves KI items instead of
+// one.  Trip count = the longest of the warp's items (warp-uniform; the list is sorted).
+template <int LPR, int KI>
+struct WorkK {
+  static constexpr int EG = 32 / LPR;
+  int lane, g, c, span;
+  int4 it[KI];
+  __device__ __forceinline__ bool init(int64_t n, const int4* __restrict__ items) {
+    lane = threadIdx.x & 31;
+    g = lane / LPR;
+    c = lane % LPR;
+    const int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (int64_t)(EG * KI);
+    if (base >= n) return false;
+    int mx = 0;
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      const int64_t j = base + g + (int64_t)EG * k;
+      it[k] = j < n ? items[j] : make_int4(-1, 0, 0, -1);
+      mx = max(mx, it[k].z - it[k].y);
+    }
+    span = __reduce_max_sync(0xffffffffu, mx);
+    return true;
+  }
+  static constexpr unsigned mask = 0xffffffffu;
+};
+
 // ------------------------------------------------------------------ RGCN forward (A5)
 // out_v (+)= sum_e norm_e P[pair_e]     (Eq. 3.1; self-loop X W_0 already in out when accumulate)
 template <class TP, int D, bool GROUP>
@@ -239,6 +284,14 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
+#if RGNN_PF_D
+  int pp[UNR];  // pair ids of the next UNR edges, loaded one iteration ahead
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int i = b + w.first + u * w.step;
+    pp[u] = i < e ? csr_pair[i] : 0;
+  }
+#endif
   for (int t = 0; t < w.span; t += w.step * UNR) {
     const int i0 = b + t + w.first;
     uint4 rk[UNR], rm[UNR];
@@ -249,11 +302,22 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
       ok[u] = i < e;
       rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
       if (ok[u]) {
+#if RGNN_PF_D
+        int64_t p = pp[u];
+#else
         int64_t p = csr_pair[i];
+#endif
         rk[u] = ldg16(KM + p * 2 * D + c * V);
         rm[u] = ldg16(KM + p * 2 * D + D + c * V);
       }
     }
+#if RGNN_PF_D
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = i0 + (UNR + u) * w.step;
+      pp[u] = i < e ? csr_pair[i] : 0;
+    }
+#endif
     float l[UNR], mx = m;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -292,6 +356,71 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   for (int k = 0; k < V; ++k) acc[k] *= inv;
   if (w.writer()) st_f32<V>(out + v * D + c * V, acc);
   if (hlead) stats[v * H + hd] = make_float2(m, s);
+}
+
+// Short rows (<= SHORT_MAX in-edges, incl. empty rows), KI per lane group.
+template <class TP, int D, int H, int KI>
+__global__ void __launch_bounds__(256) k_hgt_fwd_k(int64_t n, const int4* __restrict__ items,
+                                                   const int32_t* __restrict__ csr_pair, const TP* __restrict__ KM,
+                                                   const TP* __restrict__ Q, float* __restrict__ out,
+                                                   float2* __restrict__ stats) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
+  WorkK<LPR, KI> w;
+  if (!w.init(n, items)) return;
+  const int c = w.c, hd = c / LH;
+  uint4 qr[KI];
+  float m[KI], sm[KI], acc[KI][V];
+#pragma unroll
+  for (int k = 0; k < KI; ++k) {
+    qr[k] = w.it[k].z > w.it[k].y ? ldg16(Q + (int64_t)w.it[k].x * D + c * V) : make_uint4(0, 0, 0, 0);
+    m[k] = -CUDART_INF_F;
+    sm[k] = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[k][j] = 0.f;
+  }
+  for (int t = 0; t < w.span; ++t) {
+    uint4 rk[KI], rm[KI];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      const int i = w.it[k].y + t;
+      rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
+      if (i < w.it[k].z) {
+        const int64_t p = csr_pair[i];
+        rk[k] = ldg16(KM + p * 2 * D + c * V);
+        rm[k] = ldg16(KM + p * 2 * D + D + c * V);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      float kx[V], q[V];
+      cvt16<TP>(rk[k], kx);
+      cvt16<TP>(qr[k], q);
+      float d = 0.f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) d = fmaf(kx[j], q[j], d);
+      d = gsum<LH>(d, w.mask);
+      const float l = (w.it[k].y + t < w.it[k].z) ? d : -CUDART_INF_F;
+      const float mx = fmaxf(m[k], l);
+      const float sc = safe_exp_diff(m[k], mx), wt = safe_exp_diff(l, mx);
+      sm[k] = sm[k] * sc + wt;
+      float mv[V];
+      cvt16<TP>(rm[k], mv);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[k][j] = fmaf(wt, mv[j], acc[k][j] * sc);
+      m[k] = mx;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KI; ++k) {
+    if (w.it[k].x < 0) continue;
+    const int64_t v = w.it[k].x;
+    const float inv = sm[k] > 0.f ? 1.f / sm[k] : 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[k][j] *= inv;
+    st_f32<V>(out + v * D + c * V, acc[k]);
+    if (c % LH == 0) stats[v * H + hd] = make_float2(m[k], sm[k]);
+  }
 }
 
 // ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
@@ -415,8 +544,16 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
     if (slot < 0 && e > b && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
       st_tp<V>(GQ + v * 2 * D + c * V, gv);
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
-      if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x, inv, go, 0.f);
+      if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
+#if RGNN_PF_D
+    int pp[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = b + w.first + u * w.step;
+      pp[u] = i < e ? csr_pair[i] : 0;
+    }
+#endif
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
       uint4 rk[UNR], rm[UNR];
@@ -425,11 +562,22 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
         int i = i0 + u * w.step;
         rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
         if (i < e) {
+#if RGNN_PF_D
+          int64_t p = pp[u];
+#else
           int64_t p = csr_pair[i];
+#endif
           rk[u] = ldg16(KM + p * 2 * D + c * V);
           rm[u] = ldg16(KM + p * 2 * D + D + c * V);
         }
       }
+#if RGNN_PF_D
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = i0 + (UNR + u) * w.step;
+        pp[u] = i < e ? csr_pair[i] : 0;
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
@@ -456,10 +604,98 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
   else st_tp<V>(dQ + v * D + c * V, dq);
 }
 
+// Short rows (<= SHORT_MAX in-edges, incl. empty rows), KI per lane group; also the node records.
+template <class TP, int D, int H, int KI>
+__global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __restrict__ items,
+                                                       const int32_t* __restrict__ csr_pair,
+                                                       const TP* __restrict__ KM, const TP* __restrict__ Q,
+                                                       const float2* __restrict__ stats, const float* __restrict__ Gr,
+                                                       const float* __restrict__ out, TP* __restrict__ dQ,
+                                                       TP* __restrict__ GQ, float4* __restrict__ nst) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
+  __shared__ uint4 sg[KI][256];  // G_v chunk (table dtype) of each item, lane-private
+  WorkK<LPR, KI> w;
+  if (!w.init(n, items)) return;
+  const int c = w.c, hd = c / LH;
+  uint4 qr[KI];
+  float go[KI], lse[KI], dq[KI][V];
+#pragma unroll
+  for (int k = 0; k < KI; ++k) {
+    const bool has = w.it[k].z > w.it[k].y;
+    const int64_t v = has ? w.it[k].x : 0;
+    qr[k] = make_uint4(0, 0, 0, 0);
+    go[k] = 0.f;
+    lse[k] = CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < V; ++j) dq[k][j] = 0.f;
+    if (has) {
+      float gv[V], ov[V], q[V];
+      qr[k] = ldg16(Q + v * D + c * V);
+      ld_f32<V>(Gr + v * D + c * V, gv);
+      ld_f32<V>(out + v * D + c * V, ov);
+      float x = 0.f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) x = fmaf(gv[j], ov[j], x);
+      go[k] = x;
+      const float2 st = stats[v * H + hd];
+      lse[k] = st.x + logf(st.y);
+      cvt16<TP>(qr[k], q);
+      st_tp<V>(GQ + v * 2 * D + c * V, gv);
+      st_tp<V>(GQ + v * 2 * D + D + c * V, q);
+      uint4 gpk;
+      if constexpr (sizeof(TP) == 2) {
+        store16(reinterpret_cast<bf16*>(&gpk), gv);
+        sg[k][threadIdx.x] = gpk;
+      } else {
+        sg[k][threadIdx.x] = *reinterpret_cast<uint4*>(gv);
+      }
+    }
+    go[k] = gsum<LH>(go[k], w.mask);
+    if (has && c % LH == 0) nst[v * H + hd] = make_float4(lse[k], go[k], 0.f, 0.f);
+  }
+  for (int t = 0; t < w.span; ++t) {
+    uint4 rk[KI], rm[KI];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      const int i = w.it[k].y + t;
+      rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
+      if (i < w.it[k].z) {
+        const int64_t p = csr_pair[i];
+        rk[k] = ldg16(KM + p * 2 * D + c * V);
+        rm[k] = ldg16(KM + p * 2 * D + D + c * V);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      float kx[V], x[V];
+      cvt16<TP>(rk[k], kx);
+      cvt16<TP>(qr[k], x);
+      float l = 0.f, da = 0.f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) l = fmaf(kx[j], x[j], l);
+      cvt16<TP>(rm[k], x);
+      float gv[V];
+      cvt16<TP>(lds16(&sg[k][threadIdx.x]), gv);
+#pragma unroll
+      for (int j = 0; j < V; ++j) da = fmaf(gv[j], x[j], da);
+      l = gsum<LH>(l, w.mask);
+      da = gsum<LH>(da, w.mask);
+      const float dl = (w.it[k].y + t < w.it[k].z) ? __expf(l - lse[k]) * (da - go[k]) : 0.f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) dq[k][j] = fmaf(dl, kx[j], dq[k][j]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KI; ++k)
+    if (w.it[k].x >= 0) st_tp<V>(dQ + (int64_t)w.it[k].x * D + c * V, dq[k]);
+}
+
 // ------------------------------------------------------------------ RGAT backward, dst-major (A6)
 // dalpha_e = G_v . P_p ; dl_e = alpha_e (dalpha_e - G_v . out_v) ; dz_e = dl_e (z_e > 0 ? 1 : slope)
 // dX_v = sum_e dz_e y_{r_e}  (destination side of the reordered t-path).  Also writes the node record
-// GX_v = [G_v | X_v] (table dtype) and nst_v = (m_v, 1/sum_v, G_v . out_v, 0) read by the pair pass.
+// GX_v = [G_v | X_v] (table dtype) and nst_v = (lse_v = m_v + log sum_v, G_v . out_v, 0, 0) read by the
+// pair pass (alpha_e = exp(l_e - lse_v); 8 bytes per edge gathered instead of 16).
 // TE (reordering off): t_e from te[], no dX t-path here; dz_e is written per CSR entry (dz_out)
 // for the explicit destination-side GEMMs.
 template <class TP, int D, bool GROUP, bool TE>
@@ -496,7 +732,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
     if (slot < 0 && e > b && w.writer()) {  // node record (heavy rows: k_rgat_node_prep)
       st_tp<V>(GX + v * 2 * D + c * V, gv);
       st_tp<V>(GX + v * 2 * D + D + c * V, x);
-      if (w.leader()) nst[v] = make_float4(st.x, inv, go, 0.f);
+      if (w.leader()) nst[v] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
@@ -599,9 +835,50 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair(int64_t n, const int4* __
   else st_tp<V>(dP + p * D + c * V, acc);
 }
 
+template <class TP, int D, int KI>
+__global__ void __launch_bounds__(256) k_rgcn_bwd_pair_k(int64_t n, const int4* __restrict__ items,
+                                                         const int32_t* __restrict__ csc_dst,
+                                                         const float* __restrict__ csc_norm,
+                                                         const TP* __restrict__ Gr, TP* __restrict__ dP) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
+  WorkK<LPR, KI> w;
+  if (!w.init(n, items)) return;
+  const int c = w.c;
+  float acc[KI][V];
+#pragma unroll
+  for (int k = 0; k < KI; ++k)
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[k][j] = 0.f;
+  for (int t = 0; t < w.span; ++t) {
+    uint4 gr[KI];
+    float wt[KI];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      const int i = w.it[k].y + t;
+      gr[k] = make_uint4(0, 0, 0, 0);
+      wt[k] = 0.f;
+      if (i < w.it[k].z) {
+        wt[k] = csc_norm[i];
+        gr[k] = ldg16(Gr + (int64_t)csc_dst[i] * D + c * V);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      float x[V];
+      cvt16<TP>(gr[k], x);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[k][j] = fmaf(wt[k], x[j], acc[k][j]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KI; ++k)
+    if (w.it[k].x >= 0) st_tp<V>(dP + (int64_t)w.it[k].x * D + c * V, acc[k]);
+}
+
 // RGAT, recomputing the edge terms from the destination's node record (no per-edge buffer):
 // per pair p (relation r): P_p, y_r, s_p in registers; per edge e of p:
-//   z_e = s_p + X_d . y_r, alpha_e = exp(LeakyReLU(z_e) - m_d)/sum_d, dalpha_e = G_d . P_p,
+//   z_e = s_p + X_d . y_r, alpha_e = exp(LeakyReLU(z_e) - lse_d), dalpha_e = G_d . P_p,
 //   dz_e = alpha_e (dalpha_e - G_d . out_d) (z_e > 0 ? 1 : slope);
 // dP_p = sum alpha_e G_d + (sum dz_e) a_r, wsum_p = sum dz_e (-> da_r), bx_p = sum dz_e X_d (-> B_r).
 template <class TP, int D>
@@ -628,7 +905,7 @@ __global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* _
   st_tp<V>(GX + v * 2 * D + D + c * V, xv);
   if (c == 0) {
     float2 st = stats[v];
-    nst[v] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
+    nst[v] = make_float4(st.y > 0.f ? st.x + logf(st.y) : CUDART_INF_F, go, 0.f, 0.f);
   }
 }
 
@@ -662,12 +939,12 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
   for (int t = 0; t < w.span; t += w.step * UNR_P) {
     const int i0 = b + t + w.first;
     uint4 rg[UNR_P], rx[UNR_P];
-    float4 ns[UNR_P];
+    float2 ns[UNR_P];
     float tv[UNR_P];
 #pragma unroll
     for (int u = 0; u < UNR_P; ++u) {
       int i = i0 + u * w.step;
-      ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      ns[u] = make_float2(0.f, 0.f);
       rg[u] = rx[u] = make_uint4(0, 0, 0, 0);
       tv[u] = 0.f;
       if (i < e) {
@@ -675,7 +952,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
         rg[u] = ldg16(GX + d * 2 * D + c * V);
         if (TE) tv[u] = te[csc2csr[i]];
         else rx[u] = ldg16(GX + d * 2 * D + D + c * V);
-        ns[u] = __ldg(nst + d);
+        ns[u] = __ldg(reinterpret_cast<const float2*>(nst + d));
       }
     }
 #pragma unroll
@@ -694,8 +971,8 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
       const bool ok = i0 + u * w.step < e;
       float z = sp + tt;
       float l = z > 0.f ? z : slope * z;
-      float alpha = ok ? __expf(l - ns[u].x) * ns[u].y : 0.f;
-      float dz = alpha * (da - ns[u].z) * (z > 0.f ? 1.f : slope);
+      float alpha = ok ? __expf(l - ns[u].x) : 0.f;
+      float dz = alpha * (da - ns[u].y) * (z > 0.f ? 1.f : slope);
       zs += dz;
 #pragma unroll
       for (int k = 0; k < V; ++k) {
@@ -728,8 +1005,8 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
 }
 
 // HGT, recomputing alpha per edge from a per-node record (no per-edge buffer):
-// prep:  GQ_v = [G_v | Q_v] in the table dtype, nst_v = (m_v, 1/sum_v, G_v . out_v, 0);
-// pair:  K~_p and M_p in registers; per edge e of p: l_e = K~_p . Q_d, alpha_e = exp(l_e - m_d)/sum_d,
+// prep:  GQ_v = [G_v | Q_v] in the table dtype, nst_v = (lse_v = m_v + log sum_v, G_v . out_v, 0, 0);
+// pair:  K~_p and M_p in registers; per edge e of p: l_e = K~_p . Q_d, alpha_e = exp(l_e - lse_d),
 //        dalpha_e = G_d . M_p, dl_e = alpha_e (dalpha_e - G_d . out_d);
 //        dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d  ->  dKM_p = [dK~_p | dM_p].
 template <class TP, int D, int H>
@@ -756,7 +1033,7 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __
   st_tp<V>(GQ + v * 2 * D + D + c * V, qv);
   if (c % LH == 0) {
     float2 st = stats[v * H + c / LH];
-    nst[v * H + c / LH] = make_float4(st.x, st.y > 0.f ? 1.f / st.y : 0.f, go, 0.f);
+    nst[v * H + c / LH] = make_float4(st.y > 0.f ? st.x + logf(st.y) : CUDART_INF_F, go, 0.f, 0.f);
   }
 }
 
@@ -781,17 +1058,17 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
   for (int t = 0; t < w.span; t += w.step * UNR_P) {
     const int i0 = b + t + w.first;
     uint4 rg[UNR_P], rq[UNR_P];
-    float4 ns[UNR_P];
+    float2 ns[UNR_P];
 #pragma unroll
     for (int u = 0; u < UNR_P; ++u) {
       int i = i0 + u * w.step;
-      ns[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      ns[u] = make_float2(0.f, 0.f);
       rg[u] = rq[u] = make_uint4(0, 0, 0, 0);
       if (i < e) {
         const int64_t d = csc_dst[i];
         rg[u] = ldg16(GQ + d * 2 * D + c * V);
         rq[u] = ldg16(GQ + d * 2 * D + D + c * V);
-        ns[u] = __ldg(nst + d * H + hd);
+        ns[u] = __ldg(reinterpret_cast<const float2*>(nst + d * H + hd));
       }
     }
 #pragma unroll
@@ -807,8 +1084,8 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
       }
       l = gsum<LH>(l, w.mask);
       da = gsum<LH>(da, w.mask);
-      float alpha = (i0 + u * w.step < e) ? __expf(l - ns[u].x) * ns[u].y : 0.f;
-      float dl = alpha * (da - ns[u].z);
+      float alpha = (i0 + u * w.step < e) ? __expf(l - ns[u].x) : 0.f;
+      float dl = alpha * (da - ns[u].y);
 #pragma unroll
       for (int k = 0; k < V; ++k) {
         ak[k] = fmaf(dl, qv[k], ak[k]);
@@ -829,6 +1106,177 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair(int64_t n,
     TP* o = dKM + p * 2 * D;
     st_tp<V>(o + c * V, ak);
     st_tp<V>(o + D + c * V, am);
+  }
+}
+
+// Group mode of the HGT pair pass with the pair's K~_p / M_p chunks staged in shared memory
+// (lane-private slots, re-read per edge) instead of 16 registers: the freed registers carry
+// U edges' gathers in flight per group (U = 4 vs UNR_P = 2), i.e. twice the memory-level
+// parallelism of the register-resident version at the same occupancy.
+
+#ifndef RGNN_UNR_S
+#define RGNN_UNR_S 1
+#endif
+#ifndef RGNN_PF
+#define RGNN_PF 1
+#endif
+
+template <class TP, int D, int H, int U>
+__global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_s(int64_t n, const int4* __restrict__ items,
+                                                                        float* __restrict__ pacc,
+                                                                        const int32_t* __restrict__ csc_dst,
+                                                                        const TP* __restrict__ KM,
+                                                                        const TP* __restrict__ GQ,
+                                                                        const float4* __restrict__ nst,
+                                                                        TP* __restrict__ dKM) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
+  __shared__ uint4 skm[2][256];
+  Work<true, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c, hd = c / LH;
+  uint4* const sk = &skm[0][threadIdx.x];
+  uint4* const sm = &skm[1][threadIdx.x];
+  *sk = w.has ? ldg16(KM + p * 2 * D + c * V) : make_uint4(0, 0, 0, 0);
+  *sm = w.has ? ldg16(KM + p * 2 * D + D + c * V) : make_uint4(0, 0, 0, 0);
+  float ak[V], am[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
+#if RGNN_PF
+  int di[U];  // destination ids of the next U edges, loaded one iteration ahead
+#pragma unroll
+  for (int u = 0; u < U; ++u) di[u] = b + u < e ? csc_dst[b + u] : 0;
+#endif
+  for (int t = 0; t < w.span; t += U) {
+    const int i0 = b + t;
+    uint4 rg[U], rq[U];
+    float2 ns[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u;
+      ns[u] = make_float2(CUDART_INF_F, 0.f);
+      rg[u] = rq[u] = make_uint4(0, 0, 0, 0);
+      if (i < e) {
+#if RGNN_PF
+        const int64_t d = di[u];
+#else
+        const int64_t d = csc_dst[i];
+#endif
+        rg[u] = ldg16(GQ + d * 2 * D + c * V);
+        rq[u] = ldg16(GQ + d * 2 * D + D + c * V);
+        ns[u] = __ldg(reinterpret_cast<const float2*>(nst + d * H + hd));
+      }
+    }
+#if RGNN_PF
+#pragma unroll
+    for (int u = 0; u < U; ++u) di[u] = i0 + U + u < e ? csc_dst[i0 + U + u] : 0;
+#endif
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float gr[V], qv[V], x[V];
+      cvt16<TP>(rg[u], gr);
+      cvt16<TP>(rq[u], qv);
+      float l = 0.f, da = 0.f;
+      cvt16<TP>(lds16(sk), x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) l = fmaf(x[k], qv[k], l);
+      cvt16<TP>(lds16(sm), x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) da = fmaf(gr[k], x[k], da);
+      l = gsum<LH>(l, w.mask);
+      da = gsum<LH>(da, w.mask);
+      const float alpha = __expf(l - ns[u].x);  // 0 for padding (lse = +inf)
+      const float dl = alpha * (da - ns[u].y);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        ak[k] = fmaf(dl, qv[k], ak[k]);
+        am[k] = fmaf(alpha, gr[k], am[k]);
+      }
+    }
+  }
+  if (!w.writer()) return;
+  if (slot >= 0) {
+    float* o = pacc + (int64_t)slot * 2 * D;
+    st_f32<V>(o + c * V, ak);
+    st_f32<V>(o + D + c * V, am);
+  } else {
+    TP* o = dKM + p * 2 * D;
+    st_tp<V>(o + c * V, ak);
+    st_tp<V>(o + D + c * V, am);
+  }
+}
+
+// Short pairs (<= SHORT_MAX edges), KI per lane group; K~_p / M_p of each item staged in shared memory.
+template <class TP, int D, int H, int KI>
+__global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t n, const int4* __restrict__ items,
+                                                                        const int32_t* __restrict__ csc_dst,
+                                                                        const TP* __restrict__ KM,
+                                                                        const TP* __restrict__ GQ,
+                                                                        const float4* __restrict__ nst,
+                                                                        TP* __restrict__ dKM) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
+  __shared__ uint4 skm[2 * KI][256];
+  WorkK<LPR, KI> w;
+  if (!w.init(n, items)) return;
+  const int c = w.c, hd = c / LH;
+#pragma unroll
+  for (int k = 0; k < KI; ++k) {
+    const bool ok = w.it[k].x >= 0;
+    const int64_t p = ok ? w.it[k].x : 0;
+    skm[2 * k][threadIdx.x] = ok ? ldg16(KM + p * 2 * D + c * V) : make_uint4(0, 0, 0, 0);
+    skm[2 * k + 1][threadIdx.x] = ok ? ldg16(KM + p * 2 * D + D + c * V) : make_uint4(0, 0, 0, 0);
+  }
+  float ak[KI][V], am[KI][V];
+#pragma unroll
+  for (int k = 0; k < KI; ++k)
+#pragma unroll
+    for (int j = 0; j < V; ++j) ak[k][j] = am[k][j] = 0.f;
+  for (int t = 0; t < w.span; ++t) {
+    uint4 rg[KI], rq[KI];
+    float2 ns[KI];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      const int i = w.it[k].y + t;
+      ns[k] = make_float2(CUDART_INF_F, 0.f);
+      rg[k] = rq[k] = make_uint4(0, 0, 0, 0);
+      if (i < w.it[k].z) {
+        const int64_t d = csc_dst[i];
+        rg[k] = ldg16(GQ + d * 2 * D + c * V);
+        rq[k] = ldg16(GQ + d * 2 * D + D + c * V);
+        ns[k] = __ldg(reinterpret_cast<const float2*>(nst + d * H + hd));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      float gr[V], qv[V], x[V];
+      cvt16<TP>(rg[k], gr);
+      cvt16<TP>(rq[k], qv);
+      float l = 0.f, da = 0.f;
+      cvt16<TP>(lds16(&skm[2 * k][threadIdx.x]), x);
+#pragma unroll
+      for (int j = 0; j < V; ++j) l = fmaf(x[j], qv[j], l);
+      cvt16<TP>(lds16(&skm[2 * k + 1][threadIdx.x]), x);
+#pragma unroll
+      for (int j = 0; j < V; ++j) da = fmaf(gr[j], x[j], da);
+      l = gsum<LH>(l, w.mask);
+      da = gsum<LH>(da, w.mask);
+      const float alpha = __expf(l - ns[k].x);
+      const float dl = alpha * (da - ns[k].y);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        ak[k][j] = fmaf(dl, qv[j], ak[k][j]);
+        am[k][j] = fmaf(alpha, gr[j], am[k][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KI; ++k) {
+    if (w.it[k].x < 0) continue;
+    TP* o = dKM + (int64_t)w.it[k].x * 2 * D;
+    st_tp<V>(o + c * V, ak[k]);
+    st_tp<V>(o + D + c * V, am[k]);
   }
 }
 
@@ -967,6 +1415,15 @@ void by_dtype(int dtype, F&& f) {
   else f((bf16*)nullptr);
 }
 
+// RGNN_STAGE=0 selects the register-resident group-mode pair kernel (A/B switch for the staged one)
+inline bool stage_pair_rows() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_STAGE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 inline dim3 warps(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
 inline dim3 groups(int64_t n, int lpr) { return dim3(ceil_div(ceil_div(n, 32 / lpr) * (int64_t)32, 256)); }
 
@@ -982,6 +1439,40 @@ void launch_plan(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, cu
          (const int4*)wp.items, args...);
   launch(intern(std::string(name) + "/group"), kg, groups(nl, lpr), dim3(256), 0, side, nl,
          (const int4*)(wp.items + wp.n_warp), args...);
+  join_side(s);
+  profile_end(slot, s);
+}
+
+// RGNN_SHORT=0 turns the short-item kernels off (A/B switch)
+inline bool use_short() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_SHORT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// As launch_plan, plus the short items [n_short, n_items) on the main stream after the warp half with
+// KI items per lane group (ks takes the short-kernel argument list `sargs`, a tuple).
+template <int KI, class KW, class KG, class KS, class... Args, class... SArgs>
+void launch_plan_short(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, KS ks,
+                       std::tuple<SArgs...> sargs, cudaStream_t s, Args... args) {
+  if (!use_short()) {
+    launch_plan(name, wp, lpr, kw, kg, s, args...);
+    return;
+  }
+  const int64_t ng = wp.n_short - wp.n_warp, ns = wp.n_items - wp.n_short;
+  int slot = -1;
+  profile_begin(name, s, &slot);
+  cudaStream_t side = fork_side(s);
+  launch(intern(std::string(name) + "/group"), kg, groups(ng, lpr), dim3(256), 0, side, ng,
+         (const int4*)(wp.items + wp.n_warp), args...);
+  launch(intern(std::string(name) + "/warp"), kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp,
+         (const int4*)wp.items, args...);
+  std::apply([&](auto... a) {
+    launch(intern(std::string(name) + "/short"), ks, groups(ceil_div(ns, KI), lpr), dim3(256), 0, s, ns,
+           (const int4*)(wp.items + wp.n_short), a...);
+  }, sargs);
   join_side(s);
   profile_end(slot, s);
 }
@@ -1027,9 +1518,12 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, int H, const void
       using TP = std::remove_pointer_t<decltype(tp)>;
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
-        launch_plan("hgt_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_hgt_fwd<TP, DD, false, HH>,
-                    k_hgt_fwd<TP, DD, true, HH>, s, pt.acc, pt.stat, (const int32_t*)g->csr_pair,
-                    static_cast<const TP*>(KM), static_cast<const TP*>(Q), out, stats);
+        launch_plan_short<2>("hgt_fwd_traverse", g->rows, Geo<TP, DD>::LPR, k_hgt_fwd<TP, DD, false, HH>,
+                             k_hgt_fwd<TP, DD, true, HH>, k_hgt_fwd_k<TP, DD, HH, 2>,
+                             std::make_tuple((const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                                             static_cast<const TP*>(Q), out, stats),
+                             s, pt.acc, pt.stat, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                             static_cast<const TP*>(Q), out, stats);
         launch("merge_heavy_rows", k_merge_softmax<DD, HH>, dim3(g->rows.n_split), dim3(256), 0, s,
                g->rows.n_split, (const int4*)g->rows.splits, (const float*)pt.acc, (const float2*)pt.stat, out,
                stats);
@@ -1067,10 +1561,14 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM,
       using TP = std::remove_pointer_t<decltype(tp)>;
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
-        launch_plan("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH>,
-                    k_hgt_bwd_dst<TP, DD, true, HH>, s, pt.acc, (const int32_t*)g->csr_pair,
-                    static_cast<const TP*>(KM), static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
-                    static_cast<TP*>(GQ), nst);
+        launch_plan_short<2>("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH>,
+                             k_hgt_bwd_dst<TP, DD, true, HH>, k_hgt_bwd_dst_k<TP, DD, HH, 2>,
+                             std::make_tuple((const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                                             static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
+                                             static_cast<TP*>(GQ), nst),
+                             s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
+                             static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
+                             static_cast<TP*>(GQ), nst);
         launch("hgt_node_prep", k_hgt_node_prep<TP, DD, HH>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256),
                0, s, g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
                static_cast<TP*>(GQ), nst);
@@ -1111,9 +1609,12 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
-      launch_plan("rgcn_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgcn_bwd_pair<TP, DD, false>,
-                  k_rgcn_bwd_pair<TP, DD, true>, s, pt.acc, (const int32_t*)g->csc_dst, csc_norm,
-                  static_cast<const TP*>(G), static_cast<TP*>(dP));
+      launch_plan_short<4>("rgcn_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgcn_bwd_pair<TP, DD, false>,
+                           k_rgcn_bwd_pair<TP, DD, true>, k_rgcn_bwd_pair_k<TP, DD, 4>,
+                           std::make_tuple((const int32_t*)g->csc_dst, csc_norm, static_cast<const TP*>(G),
+                                           static_cast<TP*>(dP)),
+                           s, pt.acc, (const int32_t*)g->csc_dst, csc_norm, static_cast<const TP*>(G),
+                           static_cast<TP*>(dP));
       launch("merge_heavy_pairs", k_merge_sum<DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s, g->pairs.n_split,
              (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dP), false);
     });
@@ -1151,9 +1652,16 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
       using TP = std::remove_pointer_t<decltype(tp)>;
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
-        launch_plan("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false, HH>,
-                    k_hgt_bwd_pair<TP, DD, true, HH>, s, pt.acc, (const int32_t*)g->csc_dst,
-                    static_cast<const TP*>(KM), static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
+        auto go = [&](auto kg) {
+          launch_plan_short<2>("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false, HH>, kg,
+                               k_hgt_bwd_pair_k<TP, DD, HH, 2>,
+                               std::make_tuple((const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
+                                               static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM)),
+                               s, pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
+                               static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
+        };
+        if (stage_pair_rows()) go(k_hgt_bwd_pair_s<TP, DD, HH, RGNN_UNR_S>);
+        else go(k_hgt_bwd_pair<TP, DD, true, HH>);
       });
       launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
