@@ -1004,6 +1004,143 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
   if (c == 0) wsum[p] = zs;
 }
 
+// Group mode of the RGAT pair pass (reordered path): P_p and y_r chunks staged in shared memory
+// (lane-private), one edge per step with the next destination id prefetched (as k_hgt_bwd_pair_s).
+template <class TP, int D>
+__global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair_s(
+    int64_t n, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
+    const int32_t* __restrict__ csc_dst, const int32_t* __restrict__ csc_rel, const int32_t* __restrict__ csc2csr,
+    const float* __restrict__ te, const TP* __restrict__ P, const float* __restrict__ spair,
+    const float* __restrict__ y, const TP* __restrict__ avec, float slope, const TP* __restrict__ GX,
+    const float4* __restrict__ nst, TP* __restrict__ dP, float* __restrict__ wsum, float* __restrict__ bx) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
+  static_assert(V % 4 == 0, "y chunk as 16-byte fp32 vectors");
+  __shared__ uint4 sst[1 + V / 4][256];  // [P chunk (table dtype) | y_r chunk (fp32, V/4 vectors)]
+  Work<true, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  const int r = e > b ? csc_rel[b] : 0;
+  sst[0][threadIdx.x] = w.has ? ldg16(P + p * D + c * V) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < V / 4; ++j)
+    sst[1 + j][threadIdx.x] = w.has ? __ldg(reinterpret_cast<const uint4*>(y + (int64_t)r * D + c * V) + j)
+                                    : make_uint4(0, 0, 0, 0);
+  const float sp = w.has ? spair[p] : 0.f;
+  float acc[V], ax[V], zs = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = ax[k] = 0.f;
+  int dn = b < e ? csc_dst[b] : 0;
+  for (int t = 0; t < w.span; ++t) {
+    const int i = b + t;
+    const bool ok = i < e;
+    uint4 rg = make_uint4(0, 0, 0, 0), rx = make_uint4(0, 0, 0, 0);
+    float2 ns = make_float2(CUDART_INF_F, 0.f);
+    if (ok) {
+      const int64_t d = dn;
+      rg = ldg16(GX + d * 2 * D + c * V);
+      rx = ldg16(GX + d * 2 * D + D + c * V);
+      ns = __ldg(reinterpret_cast<const float2*>(nst + d));
+    }
+    dn = i + 1 < e ? csc_dst[i + 1] : 0;
+    float gr[V], xd[V], x[V];
+    cvt16<TP>(rg, gr);
+    cvt16<TP>(rx, xd);
+    float tt = 0.f, da = 0.f;
+#pragma unroll
+    for (int j = 0; j < V / 4; ++j) {
+      const uint4 yv = lds16(&sst[1 + j][threadIdx.x]);
+      tt = fmaf(xd[4 * j], __uint_as_float(yv.x), tt);
+      tt = fmaf(xd[4 * j + 1], __uint_as_float(yv.y), tt);
+      tt = fmaf(xd[4 * j + 2], __uint_as_float(yv.z), tt);
+      tt = fmaf(xd[4 * j + 3], __uint_as_float(yv.w), tt);
+    }
+    cvt16<TP>(lds16(&sst[0][threadIdx.x]), x);
+#pragma unroll
+    for (int k = 0; k < V; ++k) da = fmaf(gr[k], x[k], da);
+    tt = gsum<LPR>(tt, w.mask);
+    da = gsum<LPR>(da, w.mask);
+    const float z = sp + tt;
+    const float l = z > 0.f ? z : slope * z;
+    const float alpha = ok ? __expf(l - ns.x) : 0.f;
+    const float dz = alpha * (da - ns.y) * (z > 0.f ? 1.f : slope);
+    zs += dz;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      acc[k] = fmaf(alpha, gr[k], acc[k]);
+      ax[k] = fmaf(dz, xd[k], ax[k]);
+    }
+  }
+  if (!w.writer()) return;
+  if (slot >= 0) {
+    st_f32<V>(pacc + (int64_t)slot * 2 * D + c * V, acc);
+    st_f32<V>(pacc + (int64_t)slot * 2 * D + D + c * V, ax);
+    if (c == 0) pstat[slot] = make_float2(zs, 0.f);
+    return;
+  }
+  float av[V];
+  cvt16<TP>(ldg16(avec + (int64_t)r * D + c * V), av);
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = fmaf(zs, av[k], acc[k]);
+  st_tp<V>(dP + p * D + c * V, acc);
+  st_f32<V>(bx + p * D + c * V, ax);
+  if (c == 0) wsum[p] = zs;
+}
+
+// RGCN pair pass, group mode: U edges per step with their (destination, norm) prefetched a step ahead.
+#ifndef RGNN_UNR_R
+#define RGNN_UNR_R 2
+#endif
+template <class TP, int D, int U>
+__global__ void __launch_bounds__(256) k_rgcn_bwd_pair_p(int64_t n, const int4* __restrict__ items,
+                                                         float* __restrict__ pacc,
+                                                         const int32_t* __restrict__ csc_dst,
+                                                         const float* __restrict__ csc_norm,
+                                                         const TP* __restrict__ Gr, TP* __restrict__ dP) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR;
+  Work<true, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  int dn[U];
+  float wn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    dn[u] = b + u < e ? csc_dst[b + u] : 0;
+    wn[u] = b + u < e ? csc_norm[b + u] : 0.f;
+  }
+  for (int t = 0; t < w.span; t += U) {
+    uint4 gr[U];
+    float wt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      gr[u] = b + t + u < e ? ldg16(Gr + (int64_t)dn[u] * D + c * V) : make_uint4(0, 0, 0, 0);
+      wt[u] = wn[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = b + t + U + u;
+      dn[u] = i < e ? csc_dst[i] : 0;
+      wn[u] = i < e ? csc_norm[i] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float x[V];
+      cvt16<TP>(gr[u], x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = fmaf(wt[u], x[k], acc[k]);
+    }
+  }
+  if (!w.writer()) return;
+  if (slot >= 0) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
+  else st_tp<V>(dP + p * D + c * V, acc);
+}
+
 // HGT, recomputing alpha per edge from a per-node record (no per-edge buffer):
 // prep:  GQ_v = [G_v | Q_v] in the table dtype, nst_v = (lse_v = m_v + log sum_v, G_v . out_v, 0, 0);
 // pair:  K~_p and M_p in registers; per edge e of p: l_e = K~_p . Q_d, alpha_e = exp(l_e - lse_d),
@@ -1610,7 +1747,7 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       launch_plan_short<4>("rgcn_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_rgcn_bwd_pair<TP, DD, false>,
-                           k_rgcn_bwd_pair<TP, DD, true>, k_rgcn_bwd_pair_k<TP, DD, 4>,
+                           k_rgcn_bwd_pair_p<TP, DD, RGNN_UNR_R>, k_rgcn_bwd_pair_k<TP, DD, 4>,
                            std::make_tuple((const int32_t*)g->csc_dst, csc_norm, static_cast<const TP*>(G),
                                            static_cast<TP*>(dP)),
                            s, pt.acc, (const int32_t*)g->csc_dst, csc_norm, static_cast<const TP*>(G),
@@ -1635,6 +1772,7 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
                     nst, static_cast<TP*>(dP), wsum, te ? nullptr : bx);
       };
       if (te) go(k_rgat_bwd_pair<TP, DD, false, true>, k_rgat_bwd_pair<TP, DD, true, true>);
+      else if (stage_pair_rows()) go(k_rgat_bwd_pair<TP, DD, false, false>, k_rgat_bwd_pair_s<TP, DD>);
       else go(k_rgat_bwd_pair<TP, DD, false, false>, k_rgat_bwd_pair<TP, DD, true, false>);
       launch("merge_heavy_pairs", k_merge_rgat_pair<TP, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
