@@ -39,6 +39,14 @@ __global__ void k_gather3(int64_t E, const int32_t* idx, const int32_t* a, const
   oa[i] = a[j]; ob[i] = b[j]; oc[i] = c[j];
 }
 
+__global__ void k_short_first(int64_t n, int4* items, const int32_t* idx) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int4 it = items[j];
+  it.w = it.z > it.y ? -2 - idx[it.y] : -1;
+  items[j] = it;
+}
+
 __global__ void k_iota(int64_t n, int32_t* out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = (int32_t)i;
@@ -284,6 +292,13 @@ void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
   }
   build_work_plan(g, rb, rd, g->rows, s);
   build_work_plan(g, pb, pd, g->pairs, s);
+  // short items carry their first edge's gather index (rows: csr_pair, pairs: csc_dst) as
+  // w = -2 - index (negative: never a partial slot), saving the short kernels one dependent load
+  const int64_t nr = g->rows.n_items - g->rows.n_short, np = g->pairs.n_items - g->pairs.n_short;
+  launch("graph_short_first", k_short_first, dim3(std::max<unsigned>(ceil_div(nr, TB), 1)), dim3(TB), 0, s, nr,
+         g->rows.items + g->rows.n_short, (const int32_t*)g->csr_pair);
+  launch("graph_short_first", k_short_first, dim3(std::max<unsigned>(ceil_div(np, TB), 1)), dim3(TB), 0, s, np,
+         g->pairs.items + g->pairs.n_short, (const int32_t*)g->csc_dst);
 }
 
 // The (rel, dst) pairs grouped by destination (ascending rel within a destination; stable sort of

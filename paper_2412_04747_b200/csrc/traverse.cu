@@ -205,6 +205,10 @@ struct WorkK {
     return true;
   }
   static constexpr unsigned mask = 0xffffffffu;
+  // gather index of edge t of item k: the first edge's is carried in the item (w = -2 - index)
+  __device__ __forceinline__ int64_t index(int k, int t, const int32_t* __restrict__ idx) const {
+    return t == 0 ? (int64_t)(-2 - it[k].w) : (int64_t)idx[it[k].y + t];
+  }
 };
 
 // ------------------------------------------------------------------ RGCN forward (A5)
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(256) k_hgt_fwd_k(int64_t n, const int4* __rest
       const int i = w.it[k].y + t;
       rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t p = csr_pair[i];
+        const int64_t p = w.index(k, t, csr_pair);
         rk[k] = ldg16(KM + p * 2 * D + c * V);
         rm[k] = ldg16(KM + p * 2 * D + D + c * V);
       }
@@ -661,7 +665,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       const int i = w.it[k].y + t;
       rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t p = csr_pair[i];
+        const int64_t p = w.index(k, t, csr_pair);
         rk[k] = ldg16(KM + p * 2 * D + c * V);
         rm[k] = ldg16(KM + p * 2 * D + D + c * V);
       }
@@ -860,7 +864,7 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair_k(int64_t n, const int4* 
       wt[k] = 0.f;
       if (i < w.it[k].z) {
         wt[k] = csc_norm[i];
-        gr[k] = ldg16(Gr + (int64_t)csc_dst[i] * D + c * V);
+        gr[k] = ldg16(Gr + w.index(k, t, csc_dst) * D + c * V);
       }
     }
 #pragma unroll
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t 
       ns[k] = make_float2(CUDART_INF_F, 0.f);
       rg[k] = rq[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t d = csc_dst[i];
+        const int64_t d = w.index(k, t, csc_dst);
         rg[k] = ldg16(GQ + d * 2 * D + c * V);
         rq[k] = ldg16(GQ + d * 2 * D + D + c * V);
         ns[k] = __ldg(reinterpret_cast<const float2*>(nst + d * H + hd));
