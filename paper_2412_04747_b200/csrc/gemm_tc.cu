@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
                                                  TY* __restrict__ Y, const float* __restrict__ dotvec,
                                                  float* __restrict__ dotout, const int32_t* __restrict__ red_ptr,
                                                  const int32_t* __restrict__ red_list,
-                                                 const float* __restrict__ red_rows) {
+                                                 const void* __restrict__ red_rows, int red_bf16) {
   constexpr int K = KB * 64;
   constexpr int NCOLS = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   constexpr uint32_t A_BYTES = 128 * 128;  // per K block
@@ -251,13 +251,29 @@ __global__ void __launch_bounds__(128) k_gemm_tc(const Tile* __restrict__ tiles,
 #pragma unroll
       for (int i = 0; i < NV; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * N + c0 + i), dot);
     }
-    if (red_ptr && valid) {  // fused per-row reduction of gathered fp32 rows
+    if (red_ptr && valid) {  // fused per-row reduction of gathered rows (fp32 or bf16)
       for (int j = red_ptr[row], je = red_ptr[row + 1]; j < je; ++j) {
-        const float* rr = red_rows + (int64_t)red_list[j] * N + c0;
+        if (red_bf16) {
+          const bf16* rr = static_cast<const bf16*>(red_rows) + (int64_t)red_list[j] * N + c0;
+          if constexpr (NV % 8 == 0) {
 #pragma unroll
-        for (int i = 0; i < NV; i += 4) {
-          float4 x = __ldg(reinterpret_cast<const float4*>(rr + i));
-          v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
+            for (int i = 0; i < NV; i += 8) {
+              float x[8];
+              load16(rr + i, x);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) v[i + q] += x[q];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) v[i] += __bfloat162float(rr[i]);
+          }
+        } else {
+          const float* rr = static_cast<const float*>(red_rows) + (int64_t)red_list[j] * N + c0;
+#pragma unroll
+          for (int i = 0; i < NV; i += 4) {
+            float4 x = __ldg(reinterpret_cast<const float4*>(rr + i));
+            v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
+          }
         }
       }
     }
@@ -665,7 +681,7 @@ void launch_tc(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
     attr_set = true;
   }
   launch(a.name, k, dim3(a.ntiles), dim3(128), smem, s, a.tiles, static_cast<const bf16*>(a.A), a.gather, Bt,
-         static_cast<TY*>(a.Y), a.dotvec, a.dotout, a.red_ptr, a.red_list, a.red_rows);
+         static_cast<TY*>(a.Y), a.dotvec, a.dotout, a.red_ptr, a.red_list, a.red_rows, (int)(a.red_dtype == BF16));
 }
 
 template <class TY, int KB>

@@ -287,6 +287,17 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
   o.partial = ar.take<float>(std::max<int64_t>(width, 1));
 }
 
+// The per-source reduction of the pair dX rows is fused into the node GEMM's epilogue when sources
+// have few pairs on average (RGNN_FUSE_RED = 0 / 1 forces it off / on).
+bool fuse_pair_reduce(const rgnn_graph_s* g) {
+  static const int mode = [] {
+    const char* v = getenv("RGNN_FUSE_RED");
+    return v ? atoi(v) : -1;
+  }();
+  if (mode >= 0) return mode == 1;
+  return g->N > 0 && 2 * g->U <= 9 * g->N;  // U/N <= 4.5 (mag 1.6, AM 4.1)
+}
+
 // ---------------------------------------------------------------- GEMM selection
 // Returns true when the tcgen05 kernel ran (it honours the fused row reduction; SIMT does not).
 bool gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
@@ -597,8 +608,13 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       q.Y = dX; q.y_dtype = F32; q.N = c.Din;
       q.num_w = g->T; q.bt_scratch = sc.bt;
       q.name = "gemm_nodes_dx";
-      gemm(c, seg_node_type(g), q);
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
+      // few pairs per source (U/N small): the node GEMM's epilogue adds each row's per-pair dX rows
+      // (one thread per row, whole 16-byte vectors), saving dX's write + re-read by seg_reduce_rows
+      if (fuse_pair_reduce(g)) {
+        q.red_ptr = g->src_pair_ptr; q.red_list = g->src_pairs; q.red_rows = sc.dXp; q.red_dtype = c.dt;
+      }
+      if (!gemm(c, seg_node_type(g), q) || q.red_ptr == nullptr)
+        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
     }
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
     if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {

@@ -26,10 +26,11 @@ struct GemmArgs {
   float* dotout = nullptr;
   const char* name = "gemm";      // profiling label of the launch
   // optional fused row reduction (tcgen05 path only): Y[row] += sum_{i in [red_ptr[row], red_ptr[row+1])}
-  // red_rows[red_list[i]][:]  (fp32 rows of width N; used for dX += sum of per-pair dX rows by source)
+  // red_rows[red_list[i]][:]  (rows of width N in red_dtype; used for dX += sum of per-pair dX rows by source)
   const int32_t* red_ptr = nullptr;
   const int32_t* red_list = nullptr;
-  const float* red_rows = nullptr;
+  const void* red_rows = nullptr;
+  int red_dtype = F32;
   int num_w = 0;                  // number of weight matrices in B (tcgen05 path: K-major image size)
   void* bt_scratch = nullptr;     // tcgen05 path: device buffer for num_w*K*N bf16 (K-major B image)
 };

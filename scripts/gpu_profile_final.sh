@@ -2,6 +2,7 @@
 # ncu --set full of the traversal kernels (mag HGT + AM RGAT + wikikg2 RGCN)
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -2
 mkdir -p gpurun_out/fin
+timeout 1500 python -m pytest tests -q -x -m gpu 2>&1 | tail -2 > gpurun_out/fin/pytest_gpu.txt
 python bench.py 2>&1 | tail -1 > gpurun_out/fin/bench_mag_hgt.json
 for c in mag_hgt_f32 mag_hgt_h8 mag_rgat am_rgat am_hgt bgs_rgat wikikg2_rgcn biokg_hgt; do
   python bench.py --config $c --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/fin/bench_$c.json
@@ -18,4 +19,12 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_
 timeout 1200 ncu --set full --clock-control none -k regex:'k_gemm|k_wgrad|k_seg_reduce' --launch-skip 21 --launch-count 7 -o gpurun_out/fin/ncu_gemm_mag_hgt python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/fin/ncu_gemm_mag_hgt.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:'k_rgat_(fwd|bwd)' --launch-skip 18 --launch-count 6 -o gpurun_out/fin/ncu_trav_am_rgat python bench.py --config am_rgat --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/fin/ncu_trav_am_rgat.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:'k_rgcn_(fwd|bwd)' --launch-skip 15 --launch-count 5 -o gpurun_out/fin/ncu_trav_wikikg2_rgcn python bench.py --config wikikg2_rgcn --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/fin/ncu_trav_wikikg2_rgcn.log 2>&1
-ls -la gpurun_out/fin
+# reports -> text (details + raw csv); keep only the mag HGT traversal report (gpurun_out is capped at 64 MiB)
+for r in ncu_trav_mag_hgt ncu_gemm_mag_hgt ncu_trav_am_rgat ncu_trav_wikikg2_rgcn; do
+  if [ -f gpurun_out/fin/$r.ncu-rep ]; then
+    ncu -i gpurun_out/fin/$r.ncu-rep --page details --csv > gpurun_out/fin/$r.details.csv 2>/dev/null
+    ncu -i gpurun_out/fin/$r.ncu-rep --page raw --csv > gpurun_out/fin/$r.raw.csv 2>/dev/null
+    [ "$r" != ncu_trav_mag_hgt ] && rm -f gpurun_out/fin/$r.ncu-rep
+  fi
+done
+ls -la gpurun_out/fin; du -sh gpurun_out
