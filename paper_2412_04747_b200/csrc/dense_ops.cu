@@ -522,6 +522,8 @@ void gemm_simt(const GemmArgs& a, cudaStream_t s) {
   else RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "gemm: unsupported dtype combination");
 }
 
+SegPartialReduceFn seg_partial_reduce_kernel() { return k_seg_partial_reduce; }
+
 void wgrad(const WgradArgs& a, cudaStream_t s) {
   const Plan& p = *a.plan;
   RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));

@@ -441,6 +441,165 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
          static_cast<const bf16*>(a.Bm), a.partial);
 }
 
+// ------------------------------------------------------------------ fused pair-side backward (A8)
+// One pass over the pair gradient rows dP (= dKM for HGT) of a 2048-row weight-gradient tile
+// computes both products that read them:
+//   partial[tile] = sum_{rows} X[gather(row)]^T dP[row]        (as k_wgrad_tc: D_w[m = k2][n = k1])
+//   Y[row]        = dP[row] W_w^T   (W_w: [K1][K2] row-major, i.e. already K-major for this MMA)
+// The staged dP sub-tile is read by the tensor cores twice: MN-major (weight gradient) and
+// K-major (dX rows) -- the 128B-swizzled lines are the same bytes in both views.  The dX
+// accumulator is double-buffered in TMEM; its epilogue (thread = row, bf16 row store) for
+// sub-tile s runs while the MMAs of s+1 execute.  Saves one full read of dP versus the two
+// separate kernels.
+template <int K1, int K2>
+__global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ tiles, const bf16* __restrict__ A,
+                                                     const int32_t* __restrict__ gather, const bf16* __restrict__ Bm,
+                                                     const bf16* __restrict__ Wm, bf16* __restrict__ Y,
+                                                     float* __restrict__ partial) {
+  constexpr int ROWS = 128;
+  constexpr int KB1 = K1 / 64, KB2 = K2 / 64;
+  constexpr uint32_t BLK = ROWS * 128;
+  constexpr uint32_t STAGE = (KB1 + KB2) * BLK;
+  constexpr uint32_t WBLK = K1 * 128;  // one 64-wide K block of the K1 weight rows
+  constexpr int NCOLS = K1 <= 64 ? 256 : 512;  // D_w (K1) + 2 x D_x (K1)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE + KB2 * WBLK);  // free[2], xready[2], done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Tile t = tiles[blockIdx.x];
+  const int nsub = (t.row1 - t.row0 + ROWS - 1) / ROWS;
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t s_w = s_base + 2 * STAGE;
+
+  if (warp == 0) tmem_alloc<NCOLS>(tslot);
+  if (tid == 32) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // the segment's weight W_w (K1 rows of K2) into KB2 swizzled K blocks
+  for (int idx = tid; idx < K1 * 8 * KB2; idx += 128) {
+    const int kb = idx / (K1 * 8), rem = idx % (K1 * 8), n = rem >> 3, c = rem & 7;
+    cp_async16(s_w + kb * WBLK + n * 128 + ((c ^ (n & 7)) << 4), Wm + ((int64_t)t.w * K1 + n) * K2 + kb * 64 + c * 8);
+  }
+  auto load = [&](int sub, int stage) {
+    const uint32_t sb = s_base + stage * STAGE;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      int idx = it * 128 + tid;
+      int r = idx >> 3, c = idx & 7;
+      int row = t.row0 + sub * ROWS + r;
+      bool ok = row < t.row1;
+      int rr = ok ? row : t.row0;
+      int64_t xa = gather ? (int64_t)gather[rr] : (int64_t)rr;
+      uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+#pragma unroll
+      for (int j = 0; j < KB2; ++j) cp_async16_zfill(sb + j * BLK + off, Bm + (int64_t)rr * K2 + j * 64 + c * 8, ok);
+#pragma unroll
+      for (int j = 0; j < KB1; ++j)
+        cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  load(0, 0);  // (the weight copies join this commit group)
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t idesc_w = umma_idesc_bf16_mn(K1);
+  const uint32_t idesc_x = umma_idesc_bf16(K1);
+
+  auto epilogue_x = [&](int sb_i) {
+    const int b = sb_i & 1;
+    mbar_wait(&bars[2 + b], (sb_i >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int r = warp * 32 + lane;
+    const int64_t row = (int64_t)t.row0 + sb_i * ROWS + r;
+    const bool ok = row < t.row1;
+#pragma unroll
+    for (int c0 = 0; c0 < K1; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + K1 + b * K1 + c0, v);
+      if (ok) {
+        bf16* yp = Y + row * K1 + c0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) store16(yp + 8 * q, v + 8 * q);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  };
+
+  for (int sub = 0; sub < nsub; ++sub) {
+    const int st = sub & 1;
+    if (sub + 1 < nsub) {
+      if (sub + 1 >= 2) mbar_wait(&bars[(sub + 1) & 1], ((sub - 1) >> 1) & 1);
+      load(sub + 1, (sub + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t sb = s_base + st * STAGE;
+#pragma unroll
+      for (int k = 0; k < ROWS / 16; ++k) {  // weight gradient: D_w += dP^T X (both MN-major)
+        uint64_t da = umma_desc_mn_sw128(sb + k * 2048, KB2 == 2 ? BLK : 0);
+        uint64_t db = umma_desc_mn_sw128(sb + KB2 * BLK + k * 2048, BLK);
+        umma_bf16(tmem, da, db, idesc_w, (sub | k) ? 1u : 0u);
+      }
+#pragma unroll
+      for (int kb = 0; kb < KB2; ++kb)  // dX rows: D_x[st] = dP W^T (both K-major)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint64_t da = umma_desc_sw128(sb + kb * BLK + k * 32);
+          uint64_t db = umma_desc_sw128(s_w + kb * WBLK + k * 32);
+          umma_bf16(tmem + K1 + st * K1, da, db, idesc_x, (kb | k) ? 1u : 0u);
+        }
+      umma_commit(&bars[st]);
+      umma_commit(&bars[2 + st]);
+      if (sub == nsub - 1) umma_commit(&bars[4]);
+    }
+    if (sub >= 1) epilogue_x(sub - 1);
+  }
+  if (nsub > 0) epilogue_x(nsub - 1);
+  mbar_wait(&bars[4], 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  float* out = partial + (size_t)blockIdx.x * K1 * K2;
+  if (warp * 32 < K2) {
+#pragma unroll
+    for (int c0 = 0; c0 < K1; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      const int m = warp * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) out[(size_t)(c0 + i) * K2 + m] = v[i];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<NCOLS>(tmem);
+}
+
+template <int K1, int K2>
+void launch_pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s) {
+  constexpr uint32_t STAGE = (K1 / 64 + K2 / 64) * 128 * 128;
+  size_t smem = 1024 + 2 * STAGE + (K2 / 64) * K1 * 128 + 64;
+  // at most two CTAs per SM: TMEM 2 x 256 columns (K1 = 64)
+  smem = std::max(smem, (size_t)(232448 / 3) + 1);
+  auto k = k_pair_bwd_tc<K1, K2>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  launch(a.name, k, dim3(a.plan->count), dim3(128), smem, s, a.plan->tiles, static_cast<const bf16*>(a.X), a.gather,
+         static_cast<const bf16*>(a.dP), static_cast<const bf16*>(a.W), static_cast<bf16*>(a.Y), a.partial);
+}
+
 // ------------------------------------------------------------------ persistent warp-specialized GEMM
 // One CTA per SM loops over work items (tile, n-block) in static round robin; an item is a
 // 128-row tile of one weight segment times an NT-column block of that segment's weight.
@@ -707,6 +866,20 @@ bool use_ws(const GemmArgs& a) {
 }
 
 }  // namespace
+
+bool pair_bwd_tc_supported(int K1, int K2) { return K1 == 64 && (K2 == 64 || K2 == 128); }
+
+void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s) {
+  RGNN_CHECK(pair_bwd_tc_supported(a.K1, a.K2), RGNN_ERR_UNSUPPORTED, "fused pair backward: K1 = 64, K2 = 64 / 128");
+  RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));
+  if (a.plan->count == 0) return;
+  if (a.K2 == 64) launch_pair_bwd_tc<64, 64>(a, s);
+  else launch_pair_bwd_tc<64, 128>(a, s);
+  const Plan& p = *a.plan;
+  const int64_t width = (int64_t)a.K1 * a.K2;
+  launch("wgrad_reduce", seg_partial_reduce_kernel(), dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
+         p.seg_tile_ptr, p.seg_w, (const float*)a.partial, width, a.out);
+}
 
 bool wgrad_tc_supported(const WgradArgs& a) {
   return a.a_dtype == BF16 && a.b_dtype == BF16 && (a.K1 == 64 || a.K1 == 128) && (a.K2 == 64 || a.K2 == 128);

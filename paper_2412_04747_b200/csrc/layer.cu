@@ -298,6 +298,25 @@ bool fuse_pair_reduce(const rgnn_graph_s* g) {
   return g->N > 0 && 2 * g->U <= 9 * g->N;  // U/N <= 4.5 (mag 1.6, AM 4.1)
 }
 
+// A8 fused (bf16, tcgen05): the per-pair dX rows dP W^T and the pair weight gradient X[src]^T dP
+// from one read of dP (k_pair_bwd_tc).  RGNN_FUSE_PAIR=0 runs the two kernels separately.
+bool fused_pair_bwd(const Ctx& c, const Segs& sg, const void* X, const void* dP, int K2, const void* W, void* dXp,
+                    float* dWout, int num_w, float* partial) {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_FUSE_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  if (!on || c.dt != BF16 || c.d->gemm_impl == 1 || !pair_bwd_tc_supported(c.Din, K2)) return false;
+  PairBwdArgs a;
+  a.plan = &plan(c.g, sg, WGRAD_ROWS, c.s);
+  a.X = X; a.gather = c.g->pair_src; a.K1 = c.Din;
+  a.dP = dP; a.K2 = K2; a.W = W; a.Y = dXp;
+  a.out = dWout; a.num_w = num_w; a.partial = partial;
+  a.name = "pair_bwd_fused";
+  pair_bwd_tc(a, c.s);
+  return true;
+}
+
 // ---------------------------------------------------------------- GEMM selection
 // Returns true when the tcgen05 kernel ran (it honours the fused row reduction; SIMT does not).
 bool gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
@@ -540,13 +559,15 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       Gt = sc.Gt;
     }
     rgcn_bwd_pair(g, c.dt, c.D, xn, Gt, sc.dP, sc.pt, c.s);
+    const bool fused = dX && dW->dW &&
+                       fused_pair_bwd(c, seg_pair_rel(g), X, sc.dP, c.D, w->W, sc.dXp, dW->dW, g->R, sc.partial);
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
-      gemm(c, seg_pair_rel(g), a);
+      if (!fused) gemm(c, seg_pair_rel(g), a);
       if (c.d->self_loop) {  // dX = G W0^T, then + the per-source sum of the pair rows
         GemmArgs b;
         b.A = Gt; b.a_dtype = c.dt; b.K = c.D; b.B = w->W0; b.b_dtype = c.dt; b.transB = true;
@@ -557,7 +578,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       }
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, c.d->self_loop != 0, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
+    if (dW->dW && !fused)
+      do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
       do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, Gt, c.dt, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
   } else if (model == RGNN_RGAT && rgat_nr(c.d)) {
@@ -568,20 +590,23 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
                  sc.GQ, sc.nst, sc.pt, c.s);
     rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, nullptr, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
                   sc.bx, sc.pt, c.s);
+    const bool fused = dX && dW->dW &&
+                       fused_pair_bwd(c, seg_pair_rel(g), X, sc.dP, c.D, w->W, sc.dXp, dW->dW, g->R, sc.partial);
     if (dX) {
       GemmArgs a;
       a.A = sc.dP; a.a_dtype = c.dt; a.K = c.D; a.B = w->W; a.b_dtype = c.dt; a.transB = true;
       a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
-      gemm(c, seg_pair_rel(g), a);
+      if (!fused) gemm(c, seg_pair_rel(g), a);
       seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
     }
     if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
       const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
       seg_wsum(&pp, nullptr, sc.bx, F32, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
     }
-    if (dW->dW) do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
+    if (dW->dW && !fused)
+      do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW || dW->db) rgat_tpath_grads(g->R, c.Din, c.D, w->W, w->b, c.dt, sc.Bsum, dW->dW, dW->db, c.s);
     if (dW->da) {
       const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
@@ -594,6 +619,10 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       hgt_backward_nr(c, X, w, sv, dX, dW, sc);
       return;
     }
+    const bool needF = dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg;
+    const bool fused = dX && needF &&
+                       fused_pair_bwd(c, seg_pair_rt(g), X, sc.dP, 2 * c.D, sv.Fdt, sc.dXp, sc.dF,
+                                      std::max(g->n_act, 1), sc.partial);
     if (dX) {
       // per-pair rows first, then the node GEMM whose epilogue adds them per source (tcgen05 path)
       GemmArgs a;
@@ -602,7 +631,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       a.Y = sc.dXp; a.y_dtype = c.dt; a.N = c.Din;
       a.num_w = std::max(g->n_act, 1); a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
-      gemm(c, seg_pair_rt(g), a);
+      if (!fused) gemm(c, seg_pair_rt(g), a);
       GemmArgs q;
       q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
       q.Y = dX; q.y_dtype = F32; q.N = c.Din;
@@ -617,8 +646,10 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
         seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
     }
     if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
-    if (dW->dWk || dW->dWv || dW->dWatt || dW->dWmsg) {
-      do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1), sc.partial, "wgrad_pairs");
+    if (needF) {
+      if (!fused)
+        do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1),
+                 sc.partial, "wgrad_pairs");
       hgt_unfold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, sc.dFu, dW->dWk, dW->dWv,
                  dW->dWatt, dW->dWmsg, c.s);
     }

@@ -59,6 +59,29 @@ void wgrad(const WgradArgs& a, cudaStream_t s);
 bool wgrad_tc_supported(const WgradArgs& a);
 void wgrad_tc(const WgradArgs& a, cudaStream_t s);
 
+// Fused pair-side backward (tcgen05, bf16): over the tiles of one plan (per-segment weight w),
+//   Y[row] = dP[row] W_w^T  (W: [num_w][K1][K2] bf16; Y: [rows][K1] bf16)
+//   out[w] = sum_{rows of w} X[gather(row)]^T dP[row]  (fp32 [num_w][K1][K2], two-level, deterministic)
+struct PairBwdArgs {
+  const Plan* plan = nullptr;
+  const void* X = nullptr;
+  const int32_t* gather = nullptr;
+  int K1 = 0;
+  const void* dP = nullptr;
+  int K2 = 0;
+  const void* W = nullptr;
+  void* Y = nullptr;
+  float* out = nullptr;
+  int num_w = 0;
+  float* partial = nullptr;  // scratch [ntiles][K1][K2]
+  const char* name = "pair_bwd";
+};
+bool pair_bwd_tc_supported(int K1, int K2);
+void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s);
+// the second level of the deterministic weight-gradient reduction (dense_ops.cu)
+using SegPartialReduceFn = void (*)(int, const int32_t*, const int32_t*, const float*, int64_t, float*);
+SegPartialReduceFn seg_partial_reduce_kernel();
+
 // out[w][k] = sum_{rows of w} wt[row] * A[gather(row)][k]  (fp32 out; same two-level scheme)
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather,
               float* out, int num_w, float* partial, cudaStream_t s);
