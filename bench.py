@@ -122,7 +122,20 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
             out["from_f32"] = N * d * (4 + b)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
         out["wgrad_selfloop"] = N * (d_in * b + d * b)
+    # A8 fused (k_pair_bwd_tc): per pair the X[src] gather, the dP row read once, the dX row written
+    k2 = 2 * d if model == "hgt" else d
+    out["pair_bwd_fused"] = U * (4 + 2 * d_in * b + k2 * b)
     return out
+
+
+def adjust_for_fusions(alg, prof, U, N, d_in, b):
+    """Kernel labels that absorbed another kernel's work carry its bytes: when the per-source
+    reduction of the pair dX rows runs in the HGT node GEMM's epilogue (no seg_reduce_rows launch),
+    gemm_nodes_dx also gathers the pair rows (U rows + list) and skips dX's write + re-read."""
+    if "gemm_nodes_dx" in prof and "seg_reduce_rows" not in prof and "gemm_nodes_dx" in alg:
+        alg = dict(alg)
+        alg["gemm_nodes_dx"] += U * (4 + d_in * b) + N * 4
+    return alg
 
 
 # ----------------------------------------------------------------- clocks
@@ -469,6 +482,7 @@ def main():
     gi = G.info()
     U, E = gi["num_pairs"], gi["num_edges"]
     alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
+    alg = adjust_for_fusions(alg, prof, U, g.num_nodes, d, 2 if dtype == "bf16" else 4)
     # per-step view of each kernel label (a label may cover several launches per step, e.g. the
     # warp-mode and group-mode launches of one traversal); bytes are per step as well
     tot_ms = sum(x["ms"] for x in prof.values())
@@ -554,7 +568,7 @@ def train_bytes(model, dtype, N, E, U, R, T, d, layers, num_params):
     layer 1 are pruned: its input is data), plus the F4 kernels."""
     b = 2 if dtype == "bf16" else 4
     per = algorithmic_bytes(model, dtype, N, E, U, 0, R, T, d, d)
-    dx = {"gemm_pairs_dx", "gemm_nodes_dx", "seg_reduce_rows", "gemm_selfloop_dx"}
+    dx = {"gemm_pairs_dx", "gemm_nodes_dx", "seg_reduce_rows", "gemm_selfloop_dx", "pair_bwd_fused"}
     out = {k: v * (layers - 1 if k in dx else layers) for k, v in per.items()}
     out["relu_fwd"] = (layers - 1) * N * d * (4 + b)
     out["relu_bwd"] = (layers - 1) * N * d * 12
@@ -731,6 +745,7 @@ def run_train(args, cfg, world, rank, local_rank):
     U, E = info["num_pairs"], info["num_edges"]
     nparams = sum(m.numel() for ms_ in st.master for m in ms_.values())
     alg = train_bytes(model, dtype, g.num_nodes, E, U, g.num_rels, g.num_node_types, d, layers, nparams)
+    alg = adjust_for_fusions(alg, prof, U * (layers - 1), g.num_nodes * (layers - 1), d, 2 if dtype == "bf16" else 4)
     tot_ms = sum(x["ms"] for x in prof.values())
     kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                    "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}
