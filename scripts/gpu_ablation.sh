@@ -12,4 +12,4 @@ for c in ${CONFIGS:-mag_hgt am_hgt aifb_hgt am_rgat aifb_rgat mag_rgat}; do
     python bench.py --config $c $mode --no-compact --no-reorder --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/abl/${tag}_U.json
   done
 done
-timeout 1500 python -m pytest tests -q -x -m "gpu and not slow" 2>&1 | tail -3
+echo ablation-done

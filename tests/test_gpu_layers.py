@@ -58,6 +58,14 @@ def test_tiny_config(model, dtype):
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+def test_am_shape_single_edge_pairs(model, dtype):
+    # configs[2] shape at 1 %: ~70 % of the (rel, src) pairs have one edge, so most pair-gradient rows
+    # come from the destination-major pass (single-edge pairs) and the short-item kernels
+    run_case(model, config_graph("am", seed=1, scale=0.01), 64, 64, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
 def test_aifb_shape_d64(model, dtype):
     # configs[1] shape (AIFB-like: 104 relations, few edges each), hidden 64
     run_case(model, config_graph("aifb", seed=1), 64, 64, dtype)
