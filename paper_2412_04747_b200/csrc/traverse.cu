@@ -33,6 +33,9 @@ namespace {
 #ifndef RGNN_UNR_D
 #define RGNN_UNR_D 4
 #endif
+#ifndef RGNN_PF_D
+#define RGNN_PF_D 0
+#endif
 constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and pair kernels)
 #ifndef RGNN_UNR_P
 #define RGNN_UNR_P 2
@@ -202,18 +205,9 @@ struct WorkK {
     return true;
   }
   static constexpr unsigned mask = 0xffffffffu;
-  // gather index of edge t of item k, one step ahead: first() before the loop (the first edge's
-  // index is carried in the item, w = -2 - index), next() right after a step's row loads
-  __device__ __forceinline__ void first(int* nx) const {
-#pragma unroll
-    for (int k = 0; k < KI; ++k) nx[k] = it[k].z > it[k].y ? -2 - it[k].w : 0;
-  }
-  __device__ __forceinline__ void next(int* nx, int t, const int32_t* __restrict__ idx) const {
-#pragma unroll
-    for (int k = 0; k < KI; ++k) {
-      const int j = it[k].y + t + 1;
-      nx[k] = j < it[k].z ? idx[j] : 0;
-    }
+  // gather index of edge t of item k: the first edge's is carried in the item (w = -2 - index)
+  __device__ __forceinline__ int64_t index(int k, int t, const int32_t* __restrict__ idx) const {
+    return t == 0 ? (int64_t)(-2 - it[k].w) : (int64_t)idx[it[k].y + t];
   }
 };
 
@@ -294,6 +288,14 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
+#if RGNN_PF_D
+  int pp[UNR];  // pair ids of the next UNR edges, loaded one iteration ahead
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int i = b + w.first + u * w.step;
+    pp[u] = i < e ? csr_pair[i] : 0;
+  }
+#endif
   for (int t = 0; t < w.span; t += w.step * UNR) {
     const int i0 = b + t + w.first;
     uint4 rk[UNR], rm[UNR];
@@ -304,11 +306,22 @@ __global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restri
       ok[u] = i < e;
       rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
       if (ok[u]) {
+#if RGNN_PF_D
+        int64_t p = pp[u];
+#else
         int64_t p = csr_pair[i];
+#endif
         rk[u] = ldg16(KM + p * 2 * D + c * V);
         rm[u] = ldg16(KM + p * 2 * D + D + c * V);
       }
     }
+#if RGNN_PF_D
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = i0 + (UNR + u) * w.step;
+      pp[u] = i < e ? csr_pair[i] : 0;
+    }
+#endif
     float l[UNR], mx = m;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -370,8 +383,6 @@ __global__ void __launch_bounds__(256) k_hgt_fwd_k(int64_t n, const int4* __rest
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[k][j] = 0.f;
   }
-  int nx[KI];
-  w.first(nx);
   for (int t = 0; t < w.span; ++t) {
     uint4 rk[KI], rm[KI];
 #pragma unroll
@@ -379,12 +390,11 @@ __global__ void __launch_bounds__(256) k_hgt_fwd_k(int64_t n, const int4* __rest
       const int i = w.it[k].y + t;
       rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t p = (int64_t)nx[k];
+        const int64_t p = w.index(k, t, csr_pair);
         rk[k] = ldg16(KM + p * 2 * D + c * V);
         rm[k] = ldg16(KM + p * 2 * D + D + c * V);
       }
     }
-    w.next(nx, t, csr_pair);
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
       float kx[V], q[V];
@@ -540,6 +550,14 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
       if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
+#if RGNN_PF_D
+    int pp[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = b + w.first + u * w.step;
+      pp[u] = i < e ? csr_pair[i] : 0;
+    }
+#endif
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
       uint4 rk[UNR], rm[UNR];
@@ -548,11 +566,22 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __re
         int i = i0 + u * w.step;
         rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
         if (i < e) {
+#if RGNN_PF_D
+          int64_t p = pp[u];
+#else
           int64_t p = csr_pair[i];
+#endif
           rk[u] = ldg16(KM + p * 2 * D + c * V);
           rm[u] = ldg16(KM + p * 2 * D + D + c * V);
         }
       }
+#if RGNN_PF_D
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = i0 + (UNR + u) * w.step;
+        pp[u] = i < e ? csr_pair[i] : 0;
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
@@ -629,8 +658,6 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
     go[k] = gsum<LH>(go[k], w.mask);
     if (has && c % LH == 0) nst[v * H + hd] = make_float4(lse[k], go[k], 0.f, 0.f);
   }
-  int nx[KI];
-  w.first(nx);
   for (int t = 0; t < w.span; ++t) {
     uint4 rk[KI], rm[KI];
 #pragma unroll
@@ -638,12 +665,11 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       const int i = w.it[k].y + t;
       rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t p = (int64_t)nx[k];
+        const int64_t p = w.index(k, t, csr_pair);
         rk[k] = ldg16(KM + p * 2 * D + c * V);
         rm[k] = ldg16(KM + p * 2 * D + D + c * V);
       }
     }
-    w.next(nx, t, csr_pair);
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
       float kx[V], x[V];
@@ -828,8 +854,6 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair_k(int64_t n, const int4* 
   for (int k = 0; k < KI; ++k)
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[k][j] = 0.f;
-  int nx[KI];
-  w.first(nx);
   for (int t = 0; t < w.span; ++t) {
     uint4 gr[KI];
     float wt[KI];
@@ -840,10 +864,9 @@ __global__ void __launch_bounds__(256) k_rgcn_bwd_pair_k(int64_t n, const int4* 
       wt[k] = 0.f;
       if (i < w.it[k].z) {
         wt[k] = csc_norm[i];
-        gr[k] = ldg16(Gr + (int64_t)nx[k] * D + c * V);
+        gr[k] = ldg16(Gr + w.index(k, t, csc_dst) * D + c * V);
       }
     }
-    w.next(nx, t, csc_dst);
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
       float x[V];
@@ -1351,8 +1374,6 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t 
   for (int k = 0; k < KI; ++k)
 #pragma unroll
     for (int j = 0; j < V; ++j) ak[k][j] = am[k][j] = 0.f;
-  int nx[KI];
-  w.first(nx);
   for (int t = 0; t < w.span; ++t) {
     uint4 rg[KI], rq[KI];
     float2 ns[KI];
@@ -1362,13 +1383,12 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t 
       ns[k] = make_float2(CUDART_INF_F, 0.f);
       rg[k] = rq[k] = make_uint4(0, 0, 0, 0);
       if (i < w.it[k].z) {
-        const int64_t d = (int64_t)nx[k];
+        const int64_t d = w.index(k, t, csc_dst);
         rg[k] = ldg16(GQ + d * 2 * D + c * V);
         rq[k] = ldg16(GQ + d * 2 * D + D + c * V);
         ns[k] = __ldg(reinterpret_cast<const float2*>(nst + d * H + hd));
       }
     }
-    w.next(nx, t, csc_dst);
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
       float gr[V], qv[V], x[V];
