@@ -59,9 +59,27 @@ def test_tiny_config(model, dtype):
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
 def test_am_shape_single_edge_pairs(model, dtype):
-    # configs[2] shape at 1 %: ~70 % of the (rel, src) pairs have one edge, so most pair-gradient rows
-    # come from the destination-major pass (single-edge pairs) and the short-item kernels
-    run_case(model, config_graph("am", seed=1, scale=0.01), 64, 64, dtype)
+    # configs[2] shape at 1 %: ~70 % of the (rel, src) pairs have one edge (short-item kernels).
+    g = config_graph("am", seed=1, scale=0.01)
+    seed = 0
+    if model == "rgat":  # the LeakyReLU branch is an integer decision taken from a float (see _kink_free_seed)
+        seed = _kink_free_seed(g, 64)
+    run_case(model, g, 64, 64, dtype, seed=seed)
+
+
+def _kink_free_seed(g, d, rel_band=1e-5):
+    """First input seed whose RGAT logits z_e all lie outside the fp32 rounding band of LeakyReLU's kink
+    (|z_e| > rel_band * median |z|): at the kink the derivative (1 or the slope) is decided by the sign
+    of a float both sides round differently, so such draws are skipped (reading g6's convention only
+    fixes z = 0 exactly).  Oracle-side, from the seeded inputs only."""
+    for seed in range(20):
+        inp = layer_inputs("rgat", g, d, d, seed_x=2 + seed, seed_w=3 + seed)
+        X, W, a, b = inp["X"], inp["W"], inp["a"], inp["b"]
+        z = (np.sum(L.typed_matmul(X[g.src], W, g.rel) * a[g.rel], axis=1) +
+             np.sum(L.typed_matmul(X[g.dst], W, g.rel) * b[g.rel], axis=1))
+        if np.min(np.abs(z)) > rel_band * np.median(np.abs(z)):
+            return seed
+    raise AssertionError("no kink-free draw")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
