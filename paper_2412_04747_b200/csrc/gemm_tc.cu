@@ -451,7 +451,7 @@ void launch_wgrad_tc(const WgradArgs& a, cudaStream_t s) {
 // accumulator is double-buffered in TMEM; its epilogue (thread = row, bf16 row store) for
 // sub-tile s runs while the MMAs of s+1 execute.  Saves one full read of dP versus the two
 // separate kernels.
-template <int K1, int K2>
+template <int K1, int K2, int S>
 __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ tiles, const bf16* __restrict__ A,
                                                      const int32_t* __restrict__ gather, const bf16* __restrict__ Bm,
                                                      const bf16* __restrict__ Wm, bf16* __restrict__ Y,
@@ -464,18 +464,21 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
   constexpr int NCOLS = K1 <= 64 ? 256 : 512;  // D_w (K1) + 2 x D_x (K1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE + KB2 * WBLK);  // free[2], xready[2], done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  // barriers: free[S] (stage s consumed by its MMAs), xready[2] (dX accumulator b written), done
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * STAGE + KB2 * WBLK);
+  uint64_t* xready = bars + S;
+  uint64_t* done = bars + S + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + S + 3);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Tile t = tiles[blockIdx.x];
   const int nsub = (t.row1 - t.row0 + ROWS - 1) / ROWS;
   const uint32_t s_base = smem_u32(smem);
-  const uint32_t s_w = s_base + 2 * STAGE;
+  const uint32_t s_w = s_base + S * STAGE;
 
   if (warp == 0) tmem_alloc<NCOLS>(tslot);
   if (tid == 32) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < S + 3; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the segment's weight W_w (K1 rows of K2) into KB2 swizzled K blocks
@@ -483,27 +486,33 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
     const int kb = idx / (K1 * 8), rem = idx % (K1 * 8), n = rem >> 3, c = rem & 7;
     cp_async16(s_w + kb * WBLK + n * 128 + ((c ^ (n & 7)) << 4), Wm + ((int64_t)t.w * K1 + n) * K2 + kb * 64 + c * 8);
   }
-  auto load = [&](int sub, int stage) {
-    const uint32_t sb = s_base + stage * STAGE;
+  // sub-tile `sub` into stage sub % S; every call commits one cp.async group (empty past the end)
+  auto load = [&](int sub) {
+    if (sub < nsub) {
+      const uint32_t sb = s_base + (sub % S) * STAGE;
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      int idx = it * 128 + tid;
-      int r = idx >> 3, c = idx & 7;
-      int row = t.row0 + sub * ROWS + r;
-      bool ok = row < t.row1;
-      int rr = ok ? row : t.row0;
-      int64_t xa = gather ? (int64_t)gather[rr] : (int64_t)rr;
-      uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+      for (int it = 0; it < 8; ++it) {
+        int idx = it * 128 + tid;
+        int r = idx >> 3, c = idx & 7;
+        int row = t.row0 + sub * ROWS + r;
+        bool ok = row < t.row1;
+        int rr = ok ? row : t.row0;
+        int64_t xa = gather ? (int64_t)gather[rr] : (int64_t)rr;
+        uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
 #pragma unroll
-      for (int j = 0; j < KB2; ++j) cp_async16_zfill(sb + j * BLK + off, Bm + (int64_t)rr * K2 + j * 64 + c * 8, ok);
+        for (int j = 0; j < KB2; ++j)
+          cp_async16_zfill(sb + j * BLK + off, Bm + (int64_t)rr * K2 + j * 64 + c * 8, ok);
 #pragma unroll
-      for (int j = 0; j < KB1; ++j)
-        cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+        for (int j = 0; j < KB1; ++j)
+          cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  load(0, 0);  // (the weight copies join this commit group)
+  // prologue: S-1 sub-tiles in flight (the weight copies join the first group)
+#pragma unroll
+  for (int i = 0; i < S - 1; ++i) load(i);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
@@ -512,7 +521,7 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
 
   auto epilogue_x = [&](int sb_i) {
     const int b = sb_i & 1;
-    mbar_wait(&bars[2 + b], (sb_i >> 1) & 1);
+    mbar_wait(&xready[b], (sb_i >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const int r = warp * 32 + lane;
     const int64_t row = (int64_t)t.row0 + sb_i * ROWS + r;
@@ -531,14 +540,11 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
   };
 
   for (int sub = 0; sub < nsub; ++sub) {
-    const int st = sub & 1;
-    if (sub + 1 < nsub) {
-      if (sub + 1 >= 2) mbar_wait(&bars[(sub + 1) & 1], ((sub - 1) >> 1) & 1);
-      load(sub + 1, (sub + 1) & 1);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
+    const int st = sub % S;
+    // refill the stage last used by sub-1 (its MMAs must have consumed it) with sub + S - 1
+    if (sub >= 1 && sub + S - 1 < nsub) mbar_wait(&bars[(sub - 1) % S], ((sub - 1) / S) & 1);
+    load(sub + S - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1) : "memory");  // sub-tile `sub` landed
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -552,21 +558,22 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
         umma_bf16(tmem, da, db, idesc_w, (sub | k) ? 1u : 0u);
       }
 #pragma unroll
-      for (int kb = 0; kb < KB2; ++kb)  // dX rows: D_x[st] = dP W^T (both K-major)
+      for (int kb = 0; kb < KB2; ++kb)  // dX rows: D_x[sub & 1] = dP W^T (both K-major)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           uint64_t da = umma_desc_sw128(sb + kb * BLK + k * 32);
           uint64_t db = umma_desc_sw128(s_w + kb * WBLK + k * 32);
-          umma_bf16(tmem + K1 + st * K1, da, db, idesc_x, (kb | k) ? 1u : 0u);
+          umma_bf16(tmem + K1 + (sub & 1) * K1, da, db, idesc_x, (kb | k) ? 1u : 0u);
         }
       umma_commit(&bars[st]);
-      umma_commit(&bars[2 + st]);
-      if (sub == nsub - 1) umma_commit(&bars[4]);
+      umma_commit(&xready[sub & 1]);
+      if (sub == nsub - 1) umma_commit(done);
     }
     if (sub >= 1) epilogue_x(sub - 1);
   }
   if (nsub > 0) epilogue_x(nsub - 1);
-  mbar_wait(&bars[4], 0);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   float* out = partial + (size_t)blockIdx.x * K1 * K2;
   if (warp * 32 < K2) {
@@ -584,13 +591,18 @@ __global__ void __launch_bounds__(128) k_pair_bwd_tc(const Tile* __restrict__ ti
   if (warp == 0) tmem_dealloc<NCOLS>(tmem);
 }
 
+#ifndef RGNN_PAIR_BWD_STAGES
+#define RGNN_PAIR_BWD_STAGES 2
+#endif
+
 template <int K1, int K2>
 void launch_pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s) {
+  constexpr int S = RGNN_PAIR_BWD_STAGES;
   constexpr uint32_t STAGE = (K1 / 64 + K2 / 64) * 128 * 128;
-  size_t smem = 1024 + 2 * STAGE + (K2 / 64) * K1 * 128 + 64;
+  size_t smem = 1024 + S * STAGE + (K2 / 64) * K1 * 128 + 128;
   // at most two CTAs per SM: TMEM 2 x 256 columns (K1 = 64)
   smem = std::max(smem, (size_t)(232448 / 3) + 1);
-  auto k = k_pair_bwd_tc<K1, K2>;
+  auto k = k_pair_bwd_tc<K1, K2, S>;
   static bool attr_set = false;
   if (!attr_set) {
     RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
