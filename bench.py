@@ -105,11 +105,11 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
         # A6 also writes the node record [G_v | X_v] (2d*b) + 16 B
         out["rgat_bwd_dst"] = E * (8 + d * b + 4) + N * (16 + d_in * b + 12 * d + 8 + 2 * d * b + 16)
         # A7 per edge: CSC dst, the destination's [G|X] row and 16-B record; per pair: P row, s, dP, wsum, bx
-        out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + 4 * d)
+        out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + d * b)
         out["gemm_pairs_dx"] = U * (d * b + d_in * b)
         out["seg_reduce_rows"] = U * (4 + d_in * b) + N * (4 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
-        out["seg_wsum"] = U * (4 * d) + U * (4 + d * b)
+        out["seg_wsum"] = U * (d * b) + U * (4 + d * b)
     else:
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b)
         out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)

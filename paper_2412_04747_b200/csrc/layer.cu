@@ -166,7 +166,7 @@ struct BwdScratch {
   void* dXp = nullptr;    // [U][Din] layer dtype
   void* dQ = nullptr;     // HGT [N][D] layer dtype; RGAT dX fallback [N][D] fp32
   float* wsum = nullptr;  // RGAT [U]
-  float* bx = nullptr;    // RGAT [U][D]  sum_e dz_e X_d per pair
+  void* bx = nullptr;     // RGAT [U][D]  sum_e dz_e X_d per pair, layer dtype (bf16 path: b7)
   float* Bsum = nullptr;  // RGAT [R][Din]
   float* dF = nullptr;    // HGT [n_act][Din][2D]
   float* dFu = nullptr;   // HGT [n_act][Din][2D] per-combination unfold products
@@ -243,7 +243,7 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     o.dXp = ar.take<char>(U * c.Din * c.esz);
     o.dQ = ar.take<float>(N * c.D);
     o.wsum = ar.take<float>(U);
-    o.bx = ar.take<float>(U * c.D);
+    o.bx = ar.take<char>(U * c.D * c.esz);
     o.Bsum = ar.take<float>(R * c.Din);
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
     o.nst = ar.take<float4>(N);
@@ -603,7 +603,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     }
     if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
       const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
-      seg_wsum(&pp, nullptr, sc.bx, F32, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
+      seg_wsum(&pp, nullptr, sc.bx, c.dt, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
     }
     if (dW->dW && !fused)
       do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");

@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
                                                           const float* __restrict__ y, const TP* __restrict__ avec,
                                                           float slope, const TP* __restrict__ GX,
                                                           const float4* __restrict__ nst, TP* __restrict__ dP,
-                                                          float* __restrict__ wsum, float* __restrict__ bx) {
+                                                          float* __restrict__ wsum, TP* __restrict__ bx) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair(int64_t n
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = fmaf(zs, av[k], acc[k]);
   st_tp<V>(dP + p * D + c * V, acc);
-  if (!TE) st_f32<V>(bx + p * D + c * V, ax);
+  if (!TE) st_tp<V>(bx + p * D + c * V, ax);
   if (c == 0) wsum[p] = zs;
 }
 
@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair_s(
     const int32_t* __restrict__ csc_dst, const int32_t* __restrict__ csc_rel, const int32_t* __restrict__ csc2csr,
     const float* __restrict__ te, const TP* __restrict__ P, const float* __restrict__ spair,
     const float* __restrict__ y, const TP* __restrict__ avec, float slope, const TP* __restrict__ GX,
-    const float4* __restrict__ nst, TP* __restrict__ dP, float* __restrict__ wsum, float* __restrict__ bx) {
+    const float4* __restrict__ nst, TP* __restrict__ dP, float* __restrict__ wsum, TP* __restrict__ bx) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   static_assert(V % 4 == 0, "y chunk as 16-byte fp32 vectors");
@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_rgat_bwd_pair_s(
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = fmaf(zs, av[k], acc[k]);
   st_tp<V>(dP + p * D + c * V, acc);
-  st_f32<V>(bx + p * D + c * V, ax);
+  st_tp<V>(bx + p * D + c * V, ax);
   if (c == 0) wsum[p] = zs;
 }
 
@@ -1516,7 +1516,7 @@ __global__ void __launch_bounds__(256) k_merge_rgat_pair(int64_t n_split, const 
                                                          const int32_t* __restrict__ pair_csc_beg,
                                                          const int32_t* __restrict__ csc_rel,
                                                          const TW* __restrict__ avec, TW* __restrict__ dP,
-                                                         float* __restrict__ wsum, float* __restrict__ bx) {
+                                                         float* __restrict__ wsum, TW* __restrict__ bx) {
   const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (j >= n_split) return;
   const int lane = threadIdx.x & 31;
@@ -1764,7 +1764,7 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, float* bx, const Partial& pt, cudaStream_t s) {
+                   float* wsum, void* bx, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
@@ -1773,7 +1773,7 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
         launch_plan("rgat_bwd_pair", g->pairs, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
                     (const int32_t*)g->csc_dst, (const int32_t*)g->csc_rel, (const int32_t*)g->csc2csr, te,
                     static_cast<const TP*>(P), spair, y, static_cast<const TP*>(a), slope, static_cast<const TP*>(GX),
-                    nst, static_cast<TP*>(dP), wsum, te ? nullptr : bx);
+                    nst, static_cast<TP*>(dP), wsum, te ? nullptr : static_cast<TP*>(bx));
       };
       if (te) go(k_rgat_bwd_pair<TP, DD, false, true>, k_rgat_bwd_pair<TP, DD, true, true>);
       else if (stage_pair_rows()) go(k_rgat_bwd_pair<TP, DD, false, false>, k_rgat_bwd_pair_s<TP, DD>);
@@ -1781,7 +1781,7 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
       launch("merge_heavy_pairs", k_merge_rgat_pair<TP, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
              g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
              (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TP*>(a),
-             static_cast<TP*>(dP), wsum, te ? nullptr : bx);
+             static_cast<TP*>(dP), wsum, te ? nullptr : static_cast<TP*>(bx));
     });
   });
 }

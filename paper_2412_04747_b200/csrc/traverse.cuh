@@ -34,7 +34,7 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 // te != NULL (reordering off): t_e = te[csc2csr[i]], bx not computed
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, float* bx, const Partial& pt, cudaStream_t s);
+                   float* wsum, void* bx, const Partial& pt, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn
