@@ -131,6 +131,91 @@ __global__ void __launch_bounds__(kNllThreads) k_nll_rows(int64_t n, int c, cons
   }
 }
 
+// C in {64, 128, 256}: L = C / 8 lanes per row (8 values = two 16-byte vectors per lane), 32 / L
+// rows per warp at once; the same per-block partials as k_nll_rows.
+template <int C>
+__global__ void __launch_bounds__(kNllThreads) k_nll_rows_v(int64_t n, const float* __restrict__ z,
+                                                           const int32_t* __restrict__ y, float inv_count,
+                                                           float* __restrict__ dz, NllPartial* __restrict__ part) {
+  constexpr int L = C / 8, RPW = 32 / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, c = lane % L;
+  const unsigned gmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (g * L));
+  double wloss = 0.0;
+  long long wcount = 0;
+  int wbad = 0;
+  const int64_t stride = (int64_t)gridDim.x * kNllWarps * RPW;
+  for (int64_t row = ((int64_t)blockIdx.x * kNllWarps + warp) * RPW + g; row - g < n; row += stride) {
+    const bool has = row < n;
+    float v[8];
+    if (has) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(z + row * C + c * 8));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(z + row * C + c * 8 + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0.f;
+    }
+    const int lab = has ? __ldg(y + row) : -1;
+    float m = v[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) m = fmaxf(m, v[k]);
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const bool labelled = lab >= 0 && lab < C;
+    if (lab >= C) wbad = 1;
+    float zy = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (labelled && c * 8 + k == lab) zy = v[k];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = expf(v[k] - m);
+      s += v[k];
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      zy += __shfl_xor_sync(0xffffffffu, zy, o);
+    }
+    if (labelled && c == 0) {
+      wloss -= (double)(zy - m) - (double)logf(s);
+      wcount += 1;
+    }
+    if (dz && has) {
+      const float scale = labelled ? inv_count / s : 0.f;
+      float o8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o8[k] = v[k] * scale - ((labelled && c * 8 + k == lab) ? inv_count : 0.f);
+      float* dr = dz + row * C + c * 8;
+      *reinterpret_cast<float4*>(dr) = make_float4(o8[0], o8[1], o8[2], o8[3]);
+      *reinterpret_cast<float4*>(dr + 4) = make_float4(o8[4], o8[5], o8[6], o8[7]);
+    }
+    (void)gmask;
+  }
+  // warp totals in lane order (fixed), then the block's warps in order
+  double wl = wloss;
+  long long wc = wcount;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wl += __shfl_xor_sync(0xffffffffu, wl, o);
+    wc += __shfl_xor_sync(0xffffffffu, wc, o);
+  }
+  __shared__ NllPartial sp[kNllWarps];
+  const int anybad = __any_sync(0xffffffffu, wbad);
+  if (lane == 0) sp[warp] = NllPartial{wl, wc, anybad ? 1 : 0, 0};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    NllPartial p{0.0, 0, 0, 0};
+    for (int w = 0; w < kNllWarps; ++w) {
+      p.loss += sp[w].loss;
+      p.count += sp[w].count;
+      p.bad |= sp[w].bad;
+    }
+    part[blockIdx.x] = p;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_nll_final(int nparts, const NllPartial* __restrict__ part,
                                                    long long num_labeled, float* __restrict__ loss) {
   __shared__ double sl[256];
@@ -163,7 +248,7 @@ __global__ void __launch_bounds__(256) k_nll_final(int nparts, const NllPartial*
 }
 
 int nll_blocks(int64_t n) {
-  return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, kNllWarps), 1), kSMs * 8);
+  return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, kNllWarps), 1), kSMs * 64);  // tens of rows per warp, many rows in flight
 }
 
 // ------------------------------------------------------------------ SGD
@@ -273,7 +358,13 @@ rgnn_status rgnn_nll_loss(int64_t n, int32_t c, const float* logits, const int32
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     NllPartial* part = static_cast<NllPartial*>(scratch);
     const float inv = num_labeled ? 1.f / (float)num_labeled : 0.f;
-    if (n > 0) {
+    const bool vec = (c == 64 || c == 128 || c == 256) &&
+                     ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) & 15) == 0;
+    if (n > 0 && vec) {
+      if (c == 64) launch("nll_loss", k_nll_rows_v<64>, dim3(nb), dim3(kNllThreads), 0, s, n, logits, labels, inv, dlogits, part);
+      else if (c == 128) launch("nll_loss", k_nll_rows_v<128>, dim3(nb), dim3(kNllThreads), 0, s, n, logits, labels, inv, dlogits, part);
+      else launch("nll_loss", k_nll_rows_v<256>, dim3(nb), dim3(kNllThreads), 0, s, n, logits, labels, inv, dlogits, part);
+    } else if (n > 0) {
       const int per = (c + 31) / 32;
       auto go = [&](auto kern) {
         launch("nll_loss", kern, dim3(nb), dim3(kNllThreads), 0, s, n, (int)c, logits, labels, inv, dlogits, part);

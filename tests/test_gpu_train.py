@@ -26,7 +26,8 @@ from tests.helpers import TOL, prepare, rel_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,c", [(1, 1), (37, 4), (1001, 33), (5000, 64), (777, 100), (129, 1024), (3, 64)])
+@pytest.mark.parametrize("n,c", [(1, 1), (37, 4), (1001, 33), (5000, 64), (777, 100), (129, 1024), (3, 64), (1, 64),
+                                 (513, 128), (77, 256), (100003, 64)])
 def test_nll_loss(n, c):
     from paper_2412_04747_b200 import NllLoss
     rng = np.random.default_rng(n + c)
