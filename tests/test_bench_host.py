@@ -1,0 +1,59 @@
+"""Host-side logic of bench.py (no GPU): the algorithmic-byte model of DESIGN.md §6 and the
+training-step accounting.  The formulas are the method's own data movement, so they are checked
+against hand-counted cases and structural identities rather than against measurements."""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_hgt_bytes_hand_counted():
+    # one edge, one pair, one node, d = 8, bf16
+    b = bench.algorithmic_bytes("hgt", "bf16", N=1, E=1, U=1, UD=0, R=1, T=1, d_in=8, d=8)
+    # forward traversal: per edge the pair index + the [K~|M] row; per node the stats (8 B), the
+    # q row (bf16) and the fp32 output row, plus 8 B of softmax statistics
+    assert b["hgt_fwd_traverse"] == (4 + 2 * 8 * 2) + (8 + 8 * 2 + 4 * 8 + 8)
+    # pair GEMM: index + gathered X row + [K~|M] row written
+    assert b["gemm_pairs_fwd"] == 4 + 8 * 2 + 2 * 8 * 2
+    # fused A8: index + X row + dKM row read + dX row written
+    assert b["pair_bwd_fused"] == 4 + 2 * 8 * 2 + 2 * 8 * 2
+
+
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_bytes_scale_linearly(model, dtype):
+    """Doubling E, U and N doubles every kernel's bytes (no hidden constants)."""
+    a = bench.algorithmic_bytes(model, dtype, N=100, E=1000, U=300, UD=0, R=4, T=2, d_in=64, d=64)
+    b = bench.algorithmic_bytes(model, dtype, N=200, E=2000, U=600, UD=0, R=4, T=2, d_in=64, d=64)
+    assert set(a) == set(b)
+    for k in a:
+        assert b[k] == 2 * a[k], k
+    # bf16 tables never cost more than fp32 ones
+    if dtype == "bf16":
+        f = bench.algorithmic_bytes(model, "f32", N=100, E=1000, U=300, UD=0, R=4, T=2, d_in=64, d=64)
+        for k in set(a) & set(f):  # (RGCN's bf16 path adds the bf16 copy of G, "from_f32")
+            assert a[k] <= f[k], k
+
+
+def test_fusion_adjustment():
+    alg = bench.algorithmic_bytes("hgt", "bf16", N=10, E=100, U=30, UD=0, R=2, T=2, d_in=64, d=64)
+    prof_fused = {"gemm_nodes_dx": {}, "pair_bwd_fused": {}}
+    adj = bench.adjust_for_fusions(alg, prof_fused, 30, 10, 64, 2)
+    assert adj["gemm_nodes_dx"] == alg["gemm_nodes_dx"] + 30 * (4 + 64 * 2) + 10 * 4
+    assert bench.adjust_for_fusions(alg, {"gemm_nodes_dx": {}, "seg_reduce_rows": {}}, 30, 10, 64, 2) == alg
+
+
+def test_train_bytes_layers():
+    one = bench.algorithmic_bytes("rgat", "bf16", N=50, E=500, U=200, UD=0, R=3, T=1, d_in=64, d=64)
+    two = bench.train_bytes("rgat", "bf16", N=50, E=500, U=200, R=3, T=1, d=64, layers=2, num_params=1000)
+    # layer kernels twice, except the dX kernels (layer 1's input is data)
+    assert two["rgat_fwd_traverse"] == 2 * one["rgat_fwd_traverse"]
+    assert two["gemm_pairs_dx"] == one["gemm_pairs_dx"]
+    assert two["nll_loss"] == 50 * 64 * 8 + 50 * 4
+    assert two["relu_fwd"] == 50 * 64 * (4 + 2)
+    assert two["sgd_update"] == 1000 * (12 + 2)
