@@ -40,6 +40,17 @@ constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and 
 #ifndef RGNN_UNR_P
 #define RGNN_UNR_P 2
 #endif
+// launch bounds of the HGT destination-major kernels (tuning knobs: -DRGNN_FWD_MINB=n / -DRGNN_DST_MINB=n)
+#ifdef RGNN_FWD_MINB
+#define RGNN_FWD_LB __launch_bounds__(256, RGNN_FWD_MINB)
+#else
+#define RGNN_FWD_LB __launch_bounds__(256)
+#endif
+#ifdef RGNN_DST_MINB
+#define RGNN_DST_LB __launch_bounds__(256, RGNN_DST_MINB)
+#else
+#define RGNN_DST_LB __launch_bounds__(256)
+#endif
 #ifndef RGNN_PAIR_MINB
 #define RGNN_PAIR_MINB 4
 #endif
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(256) k_rgcn_fwd(int64_t n, const int4* __restr
 // its logit is reduced over those lanes only and its online-softmax state lives in them, so
 // per-lane state is per-head state; stats / partial stats are [id][H].
 template <class TP, int D, bool GROUP, int H>
-__global__ void __launch_bounds__(256) k_hgt_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
+__global__ void RGNN_FWD_LB k_hgt_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
                                                  float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
                                                  const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                  float* __restrict__ out, float2* __restrict__ stats) {
@@ -519,7 +530,7 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
 // dQ_v = sum_e dl_e K~_p   (layer dtype; heavy rows: fp32 partials merged by k_merge_sum)
 template <class TP, int D, bool GROUP, int H>
-__global__ void __launch_bounds__(256) k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
+__global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
