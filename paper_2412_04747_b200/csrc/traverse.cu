@@ -77,6 +77,17 @@ __device__ __forceinline__ void st_f32(float* p, const float* v) {
 #pragma unroll
   for (int i = 0; i < V; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
+// Round values to the table dtype and back (identity for fp32).  The softmax backward uses the
+// upstream gradient G_v in both dalpha_e = G_v . M and the row term G_v . out_v; the pair-major
+// pass reads G_v from the bf16 node record, so every pass rounds it the same way and the two
+// terms cancel exactly where they should (e.g. a single-edge softmax, alpha = 1: dl = 0).
+template <class TP, int V>
+__device__ __forceinline__ void round_tp(float* v) {
+  if constexpr (sizeof(TP) == 2) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = __bfloat162float(__float2bfloat16_rn(v[k]));
+  }
+}
 // 4 consecutive elements of a table row as floats (8 B for bf16, 16 B for fp32)
 __device__ __forceinline__ void ld4(const float* p, float* o) {
   float4 x = __ldg(reinterpret_cast<const float4*>(p));
@@ -549,6 +560,7 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
     float q[V], gv[V], ov[V];
     cvt16<TP>(ldg16(Q + v * D + c * V), q);
     ld_f32<V>(Gr + v * D + c * V, gv);
+    round_tp<TP, V>(gv);  // G_v in the table precision everywhere (dalpha and the row term G_v . out_v)
     ld_f32<V>(out + v * D + c * V, ov);
     float go = 0.f;
 #pragma unroll
@@ -648,6 +660,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       float gv[V], ov[V], q[V];
       qr[k] = ldg16(Q + v * D + c * V);
       ld_f32<V>(Gr + v * D + c * V, gv);
+      round_tp<TP, V>(gv);
+    round_tp<TP, V>(gv);  // G_v in the table precision everywhere (dalpha and the row term G_v . out_v)
       ld_f32<V>(out + v * D + c * V, ov);
       float x = 0.f;
 #pragma unroll
@@ -737,6 +751,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
     float x[V], gv[V], ov[V];
     cvt16<TP>(ldg16(X + v * D + c * V), x);
     ld_f32<V>(Gr + v * D + c * V, gv);
+    round_tp<TP, V>(gv);  // G_v in the table precision everywhere (dalpha and the row term G_v . out_v)
     ld_f32<V>(out + v * D + c * V, ov);
     float go = 0.f;
 #pragma unroll
@@ -910,6 +925,7 @@ __global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* _
   const int64_t v = rows[j].x;
   float gv[V], ov[V], xv[V];
   ld_f32<V>(Gr + v * D + c * V, gv);
+  round_tp<TP, V>(gv);
   ld_f32<V>(out + v * D + c * V, ov);
   cvt16<TP>(ldg16(X + v * D + c * V), xv);
   float go = 0.f;
@@ -1175,6 +1191,7 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __
   const int64_t v = rows[j].x;
   float gv[V], ov[V], qv[V];
   ld_f32<V>(Gr + v * D + c * V, gv);
+  round_tp<TP, V>(gv);
   ld_f32<V>(out + v * D + c * V, ov);
   cvt16<TP>(ldg16(Q + v * D + c * V), qv);
   float go = 0.f;

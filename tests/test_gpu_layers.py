@@ -266,3 +266,54 @@ def test_hgt_tail_variants():
     G = Graph.from_hetero(config_graph("tiny", seed=1))
     with pytest.raises(RGNNError, match="hgt_tail"):
         Layer(G, "hgt", 64, 32, tail=True)
+
+
+def _degenerate_graphs():
+    """Edge cases of the work plans: no edges at all; one (rel, src) pair with 3,000 edges to
+    distinct destinations (a heavy pair split in chunks, every row a single edge -> short
+    items); one destination with 3,000 in-edges from distinct sources over 3 relations (a heavy
+    row; every pair a single edge); a self-loop-only graph."""
+    from synth.graphs import HeteroGraph
+    i32 = lambda a: np.asarray(a, np.int32)  # noqa: E731
+    n = 4000
+    ptr2 = np.array([0, 1000, n], np.int64)
+    out = {"no_edges": HeteroGraph(ptr2, 3, i32([]), i32([]), i32([]))}
+    k = np.arange(1, 3001)
+    out["heavy_pair"] = HeteroGraph(ptr2, 2, i32(np.zeros(3000)), i32(k), i32(np.ones(3000)))
+    out["heavy_row"] = HeteroGraph(ptr2, 3, i32(k), i32(np.zeros(3000)), i32(k % 3))
+    s = np.arange(0, n, 7)
+    out["self_loops"] = HeteroGraph(ptr2, 1, i32(s), i32(s), i32(np.zeros(len(s))))
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
+@pytest.mark.parametrize("name", ["no_edges", "heavy_pair", "heavy_row", "self_loops"])
+def test_degenerate_graphs(name, model, dtype):
+    """Tensors the oracle gives as exactly zero (e.g. the attention weights' gradients when every
+    softmax has a single edge, alpha = 1) are compared in absolute terms (inputs are O(1))."""
+    from paper_2412_04747_b200 import Graph, Layer
+    g = _degenerate_graphs()[name]
+    seed = _kink_free_seed(g, 64) if (model == "rgat" and g.num_edges) else 0
+    d = 64
+    inp = prepare(layer_inputs(model, g, d, d, seed_x=2 + seed, seed_w=3 + seed), dtype)
+    Gh = upstream_grad(g.num_nodes, d, seed=4 + seed)
+    kw = {"norm": L.rgcn_edge_norm(g, "mean")} if model == "rgcn" else {}
+    ref_out, _ = L.forward(model, g, inp, **kw)
+    ref = L.backward(model, g, inp, Gh, **kw)
+    G = Graph.from_hetero(g)
+    layer = Layer(G, model, d, d, dtype=dtype)
+    dev = to_device(inp, dtype)
+    X = dev.pop("X")
+    out = layer.forward(X, dev)
+    grads = layer.backward(X, dev, out, torch.tensor(Gh, dtype=torch.float32, device="cuda"))
+    torch.cuda.synchronize()
+    tol = TOL[dtype]
+    ref["out"] = ref_out
+    grads["out"] = out
+    errs = {}
+    for k, v in ref.items():
+        gpu = grads[k].cpu().numpy()
+        errs[k] = rel_err(gpu, v) if np.abs(v).max() > 0 else float(np.abs(gpu).max())
+    bad = {k: e for k, e in errs.items() if not e <= tol}
+    assert not bad, (name, model, dtype, errs)
