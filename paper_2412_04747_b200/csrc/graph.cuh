@@ -12,7 +12,10 @@ namespace rgnn {
 // Work classes of destination rows and compact pairs (by their number of edges):
 constexpr int SPLIT_THRESH = 1024;  // heavy: more edges than this -> chunks of SPLIT_CHUNK, one warp each,
 constexpr int SPLIT_CHUNK = 512;    //        partial states merged afterwards
-constexpr int LIGHT_MAX = 64;       // light: at most this many edges -> one lane group each; else one warp
+#ifndef RGNN_LIGHT_MAX
+#define RGNN_LIGHT_MAX 64
+#endif
+constexpr int LIGHT_MAX = RGNN_LIGHT_MAX;  // light: at most this many edges -> one lane group each; else one warp
 constexpr int SHORT_MAX = 4;        // short: light items with at most this many edges (a suffix of the sorted
                                     //        light list) -> KI items per lane group, gathered together
 
