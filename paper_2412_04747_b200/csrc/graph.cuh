@@ -26,6 +26,7 @@ struct WorkPlan {
   int64_t n_warp = 0;      // items [0, n_warp): heavy chunks then medium ids, one warp per item
   int64_t n_items = 0;     // items [n_warp, n_items): light ids, one lane group per item
   int64_t n_short = 0;     // items [n_short, n_items): short light ids (<= SHORT_MAX edges; n_warp <= n_short)
+  int64_t n_multi = 0;     // items [n_multi, n_items) have exactly one edge (a suffix of the short ones)
   int4* splits = nullptr;  // (id, first slot, number of slots, 0) for every heavy id
   int64_t n_split = 0;
   int64_t n_slots = 0;
@@ -67,6 +68,7 @@ struct rgnn_graph_s {
   int32_t* csr_rel = nullptr;
   int32_t* csr_eid = nullptr;
   int32_t* csr_pair = nullptr;
+  uint8_t* csr_single = nullptr;  // [E] 1 when the CSR entry's pair has exactly one edge
   int32_t* col_ptr = nullptr;  // [N+1]
   int32_t* csc_dst = nullptr;
   int32_t* csc_rel = nullptr;

@@ -39,6 +39,11 @@ __global__ void k_gather3(int64_t E, const int32_t* idx, const int32_t* a, const
   oa[i] = a[j]; ob[i] = b[j]; oc[i] = c[j];
 }
 
+__global__ void k_csr_single(int64_t E, const int32_t* csr_pair, const int32_t* pair_deg, uint8_t* single) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < E) single[i] = pair_deg[csr_pair[i]] == 1 ? 1 : 0;
+}
+
 __global__ void k_short_first(int64_t n, int4* items, const int32_t* idx) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -265,6 +270,8 @@ void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std
   wp.n_items = (int64_t)heavy.size();
   wp.n_short = wp.n_items;  // light items are sorted longest first: the short ones are a suffix
   while (wp.n_short > wp.n_warp && heavy[wp.n_short - 1].z - heavy[wp.n_short - 1].y <= SHORT_MAX) --wp.n_short;
+  wp.n_multi = wp.n_items;
+  while (wp.n_multi > wp.n_warp && heavy[wp.n_multi - 1].z - heavy[wp.n_multi - 1].y <= 1) --wp.n_multi;
   wp.n_split = (int64_t)splits.size();
   wp.n_slots = slots;
   wp.items = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<int64_t>(wp.n_items, 1), s));
@@ -481,6 +488,9 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
   launch("graph_pos_pair", k_pos_pair, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, run_incl, rank_of_run, g->csc_pair);
   launch("graph_scatter", k_scatter, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csc_eid, g->csc_pair, g->edge_pair);
   launch("graph_gather1", k_gather, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, g->csr_eid, g->edge_pair, g->csr_pair);
+  g->csr_single = reinterpret_cast<uint8_t*>(g->dev_i32((E + 3) / 4, s));
+  launch("graph_single", k_csr_single, dim3(ceil_div(E, TB)), dim3(TB), 0, s, E, (const int32_t*)g->csr_pair,
+         (const int32_t*)g->pair_deg, g->csr_single);
   // csc2csr
   int32_t* csr_pos_of_eid = tmp.get<int32_t>(E);
   g->csc2csr = g->dev_i32(E, s);

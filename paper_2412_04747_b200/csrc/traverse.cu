@@ -20,6 +20,7 @@
 // pair p the edges are contiguous in the CSC -> dP_p / [dK~_p | dM_p].  No float atomics.
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <tuple>
 #include <type_traits>
@@ -32,9 +33,6 @@ namespace {
 
 #ifndef RGNN_UNR_D
 #define RGNN_UNR_D 4
-#endif
-#ifndef RGNN_PF_D
-#define RGNN_PF_D 0
 #endif
 constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and pair kernels)
 #ifndef RGNN_UNR_P
@@ -310,14 +308,6 @@ __global__ void RGNN_FWD_LB k_hgt_fwd(int64_t n, const int4* __restrict__ items,
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-#if RGNN_PF_D
-  int pp[UNR];  // pair ids of the next UNR edges, loaded one iteration ahead
-#pragma unroll
-  for (int u = 0; u < UNR; ++u) {
-    const int i = b + w.first + u * w.step;
-    pp[u] = i < e ? csr_pair[i] : 0;
-  }
-#endif
   for (int t = 0; t < w.span; t += w.step * UNR) {
     const int i0 = b + t + w.first;
     uint4 rk[UNR], rm[UNR];
@@ -328,22 +318,11 @@ __global__ void RGNN_FWD_LB k_hgt_fwd(int64_t n, const int4* __restrict__ items,
       ok[u] = i < e;
       rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
       if (ok[u]) {
-#if RGNN_PF_D
-        int64_t p = pp[u];
-#else
         int64_t p = csr_pair[i];
-#endif
         rk[u] = ldg16(KM + p * 2 * D + c * V);
         rm[u] = ldg16(KM + p * 2 * D + D + c * V);
       }
     }
-#if RGNN_PF_D
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int i = i0 + (UNR + u) * w.step;
-      pp[u] = i < e ? csr_pair[i] : 0;
-    }
-#endif
     float l[UNR], mx = m;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -540,13 +519,14 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
 // ------------------------------------------------------------------ HGT backward, dst-major (A6)
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
 // dQ_v = sum_e dl_e K~_p   (layer dtype; heavy rows: fp32 partials merged by k_merge_sum)
-template <class TP, int D, bool GROUP, int H>
+template <class TP, int D, bool GROUP, int H, bool SGL>
 __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
                                                      const float* __restrict__ out, TP* __restrict__ dQ,
-                                                     TP* __restrict__ GQ, float4* __restrict__ nst) {
+                                                     TP* __restrict__ GQ, float4* __restrict__ nst,
+                                                     const uint8_t* __restrict__ single, TP* __restrict__ dKM) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   Work<GROUP, LPR> w;
@@ -573,38 +553,22 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
       if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
-#if RGNN_PF_D
-    int pp[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int i = b + w.first + u * w.step;
-      pp[u] = i < e ? csr_pair[i] : 0;
-    }
-#endif
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
       uint4 rk[UNR], rm[UNR];
+      int pid[UNR];  // SGL: the pair id when it has a single edge (its dKM row is written here), else -1
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
         rk[u] = rm[u] = make_uint4(0, 0, 0, 0);
+        pid[u] = -1;
         if (i < e) {
-#if RGNN_PF_D
-          int64_t p = pp[u];
-#else
           int64_t p = csr_pair[i];
-#endif
           rk[u] = ldg16(KM + p * 2 * D + c * V);
           rm[u] = ldg16(KM + p * 2 * D + D + c * V);
+          if (SGL && single[i]) pid[u] = (int)p;
         }
       }
-#if RGNN_PF_D
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int i = i0 + (UNR + u) * w.step;
-        pp[u] = i < e ? csr_pair[i] : 0;
-      }
-#endif
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
@@ -622,6 +586,16 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
         float dl = (i < e) ? __expf(l - st.x) * inv * (da - go) : 0.f;
 #pragma unroll
         for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
+        if (SGL && pid[u] >= 0) {  // single-edge pair: dKM_p = [dl q_v | alpha G_v]
+          const float alpha = __expf(l - st.x) * inv;
+          float o[V];
+#pragma unroll
+          for (int k = 0; k < V; ++k) o[k] = dl * q[k];
+          st_tp<V>(dKM + (int64_t)pid[u] * 2 * D + c * V, o);
+#pragma unroll
+          for (int k = 0; k < V; ++k) o[k] = alpha * gv[k];
+          st_tp<V>(dKM + (int64_t)pid[u] * 2 * D + D + c * V, o);
+        }
       }
     }
   }
@@ -632,13 +606,14 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
 }
 
 // Short rows (<= SHORT_MAX in-edges, incl. empty rows), KI per lane group; also the node records.
-template <class TP, int D, int H, int KI>
+template <class TP, int D, int H, int KI, bool SGL>
 __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __restrict__ items,
                                                        const int32_t* __restrict__ csr_pair,
                                                        const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                        const float2* __restrict__ stats, const float* __restrict__ Gr,
                                                        const float* __restrict__ out, TP* __restrict__ dQ,
-                                                       TP* __restrict__ GQ, float4* __restrict__ nst) {
+                                                       TP* __restrict__ GQ, float4* __restrict__ nst,
+                                                       const uint8_t* __restrict__ single, TP* __restrict__ dKM) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   __shared__ uint4 sg[KI][256];  // G_v chunk (table dtype) of each item, lane-private
@@ -685,14 +660,17 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
   }
   for (int t = 0; t < w.span; ++t) {
     uint4 rk[KI], rm[KI];
+    int pid[KI];
 #pragma unroll
     for (int k = 0; k < KI; ++k) {
       const int i = w.it[k].y + t;
       rk[k] = rm[k] = make_uint4(0, 0, 0, 0);
+      pid[k] = -1;
       if (i < w.it[k].z) {
         const int64_t p = w.index(k, t, csr_pair);
         rk[k] = ldg16(KM + p * 2 * D + c * V);
         rm[k] = ldg16(KM + p * 2 * D + D + c * V);
+        if (SGL && single[i]) pid[k] = (int)p;
       }
     }
 #pragma unroll
@@ -713,6 +691,17 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       const float dl = (w.it[k].y + t < w.it[k].z) ? __expf(l - lse[k]) * (da - go[k]) : 0.f;
 #pragma unroll
       for (int j = 0; j < V; ++j) dq[k][j] = fmaf(dl, kx[j], dq[k][j]);
+      if (SGL && pid[k] >= 0) {  // single-edge pair: dKM_p = [dl q_v | alpha G_v]
+        const float alpha = __expf(l - lse[k]);
+        float o[V], q[V];
+        cvt16<TP>(qr[k], q);
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = dl * q[j];
+        st_tp<V>(dKM + (int64_t)pid[k] * 2 * D + c * V, o);
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = alpha * gv[j];
+        st_tp<V>(dKM + (int64_t)pid[k] * 2 * D + D + c * V, o);
+      }
     }
   }
 #pragma unroll
@@ -1722,22 +1711,27 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
 }
 
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
-                 cudaStream_t s) {
+                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const uint8_t* single, void* dKM,
+                 const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
-        launch_plan_short<2>("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH>,
-                             k_hgt_bwd_dst<TP, DD, true, HH>, k_hgt_bwd_dst_k<TP, DD, HH, 2>,
+        auto go = [&](auto sc) {
+          constexpr bool SG = decltype(sc)::value;
+          launch_plan_short<2>("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH, SG>,
+                             k_hgt_bwd_dst<TP, DD, true, HH, SG>, k_hgt_bwd_dst_k<TP, DD, HH, 2, SG>,
                              std::make_tuple((const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
                                              static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
-                                             static_cast<TP*>(GQ), nst),
+                                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM)),
                              s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
                              static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
-                             static_cast<TP*>(GQ), nst);
+                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM));
+        };
+        if (single) go(std::true_type());
+        else go(std::false_type());
         launch("hgt_node_prep", k_hgt_node_prep<TP, DD, HH>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256),
                0, s, g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
                static_cast<TP*>(GQ), nst);
@@ -1815,7 +1809,12 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
 }
 
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
-                  void* dKM, const Partial& pt, cudaStream_t s) {
+                  void* dKM, bool skip_single, const Partial& pt, cudaStream_t s) {
+  WorkPlan wp = g->pairs;  // single-edge pairs were resolved by the destination-major pass
+  if (skip_single) {
+    wp.n_items = wp.n_multi;
+    wp.n_short = std::min(wp.n_short, wp.n_multi);
+  }
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
@@ -1823,7 +1822,7 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
         auto go = [&](auto kg) {
-          launch_plan_short<2>("hgt_bwd_pair", g->pairs, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false, HH>, kg,
+          launch_plan_short<2>("hgt_bwd_pair", wp, Geo<TP, DD>::LPR, k_hgt_bwd_pair<TP, DD, false, HH>, kg,
                                k_hgt_bwd_pair_k<TP, DD, HH, 2>,
                                std::make_tuple((const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
                                                static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM)),

@@ -20,9 +20,11 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
                        cudaStream_t s);
 // also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) of every
 // destination with in-edges (read by hgt_bwd_pair)
+// single != NULL: the dKM rows of single-edge pairs (graph csr_single) are written here, and
+// hgt_bwd_pair then runs with skip_single (its pair-major pass covers pairs with >= 2 edges)
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
-                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const Partial& pt,
-                 cudaStream_t s);
+                 const float* G, const float* out, void* dQ, void* GQ, float4* nst, const uint8_t* single, void* dKM,
+                 const Partial& pt, cudaStream_t s);
 // also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
 // te != NULL (reordering off): t_e read from te, dz_e written per CSR entry into dz, dX untouched.
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
@@ -36,5 +38,5 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
                    float* wsum, void* bx, const Partial& pt, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
-                  void* dKM, const Partial& pt, cudaStream_t s);
+                  void* dKM, bool skip_single, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn
