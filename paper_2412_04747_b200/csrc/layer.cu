@@ -518,9 +518,9 @@ void rgat_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const 
                       const float* G, float* dX, const rgnn_weight_grads* dW, const BwdScratch& sc) {
   rgnn_graph_s* g = c.g;
   rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, nullptr, sv.te, sc.dz, c.d->leaky_slope, sv.stats, G, out, nullptr,
-               sc.GQ, sc.nst, sc.pt, c.s);
+               sc.GQ, sc.nst, nullptr, nullptr, nullptr, nullptr, nullptr, sc.pt, c.s);
   rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, nullptr, sv.te, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
-                nullptr, sc.pt, c.s);
+                nullptr, false, sc.pt, c.s);
   dpair_sum(g, sc.dz, sc.dt, c.s);
   const bool dst_side = dX || dW->dW;
   if (dst_side) dpair_outer(plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s), sc.dt, w->b, c.dt, c.D, sc.dPt, c.s);
@@ -599,10 +599,11 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     rgat_backward_nr(c, X, w, out, sv, G, dX, dW, sc);
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
+    const bool single = single_in_dst(g);
     rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nullptr, nullptr, c.d->leaky_slope, sv.stats, G, out, dXt,
-                 sc.GQ, sc.nst, sc.pt, c.s);
+                 sc.GQ, sc.nst, single ? g->csr_single : nullptr, w->a, sc.dP, sc.bx, sc.wsum, sc.pt, c.s);
     rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, nullptr, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
-                  sc.bx, sc.pt, c.s);
+                  sc.bx, single, sc.pt, c.s);
     const bool fused = dX && dW->dW &&
                        fused_pair_bwd(c, seg_pair_rel(g), X, sc.dP, c.D, w->W, sc.dXp, dW->dW, g->R, sc.partial);
     if (dX) {

@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
 // pair pass (alpha_e = exp(l_e - lse_v); 8 bytes per edge gathered instead of 16).
 // TE (reordering off): t_e from te[], no dX t-path here; dz_e is written per CSR entry (dz_out)
 // for the explicit destination-side GEMMs.
-template <class TP, int D, bool GROUP, bool TE>
+template <class TP, int D, bool GROUP, bool TE, bool SGL>
 __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
@@ -726,7 +726,9 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
                                                       const float2* __restrict__ stats,
                                                       const float* __restrict__ Gr, const float* __restrict__ out,
                                                       float* __restrict__ dX, TP* __restrict__ GX,
-                                                      float4* __restrict__ nst) {
+                                                      float4* __restrict__ nst, const uint8_t* __restrict__ single,
+                                                      const TP* __restrict__ avec, TP* __restrict__ dP,
+                                                      TP* __restrict__ bx, float* __restrict__ wsum) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
   Work<GROUP, LPR> w;
@@ -757,19 +759,30 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
       const int i0 = b + t + w.first;
       uint4 rp[UNR];
       float sp[UNR], yv[UNR][V];
+      int pid[UNR], rel[UNR];  // SGL: single-edge pair id (else -1) and its relation
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         int i = i0 + u * w.step;
         rp[u] = make_uint4(0, 0, 0, 0);
         sp[u] = 0.f;
+        pid[u] = -1;
+        rel[u] = 0;
 #pragma unroll
         for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
         if (i < e) {
           int64_t p = csr_pair[i];
           rp[u] = ldg16(P + p * D + c * V);
           sp[u] = spair[p];
-          if (TE) yv[u][0] = te[i];
-          else ld_f32<V>(y + (int64_t)csr_rel[i] * D + c * V, yv[u]);
+          if (TE) {
+            yv[u][0] = te[i];
+          } else {
+            const int r = csr_rel[i];
+            ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+            if (SGL && single[i]) {
+              pid[u] = (int)p;
+              rel[u] = r;
+            }
+          }
         }
       }
 #pragma unroll
@@ -795,6 +808,17 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
           } else {
 #pragma unroll
             for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
+            if (SGL && pid[u] >= 0) {  // single-edge pair: dP_p = alpha G_v + dz a_r, bx_p = dz X_v, wsum_p = dz
+              float av[V], o[V];
+              cvt16<TP>(ldg16(avec + (int64_t)rel[u] * D + c * V), av);
+#pragma unroll
+              for (int k = 0; k < V; ++k) o[k] = fmaf(dz, av[k], alpha * gv[k]);
+              st_tp<V>(dP + (int64_t)pid[u] * D + c * V, o);
+#pragma unroll
+              for (int k = 0; k < V; ++k) o[k] = dz * x[k];
+              st_tp<V>(bx + (int64_t)pid[u] * D + c * V, o);
+              if (c == 0) wsum[pid[u]] = dz;
+            }
           }
         }
       }
@@ -1744,7 +1768,8 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM,
 
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
-                  const float* out, float* dX, void* GX, float4* nst, const Partial& pt, cudaStream_t s) {
+                  const float* out, float* dX, void* GX, float4* nst, const uint8_t* single, const void* a, void* dP,
+                  void* bx, float* wsum, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
@@ -1752,10 +1777,12 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
       auto go = [&](auto kw, auto kg) {
         launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, (const int32_t*)g->csr_pair,
                     (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te,
-                    dz, slope, stats, G, out, dX, static_cast<TP*>(GX), nst);
+                    dz, slope, stats, G, out, dX, static_cast<TP*>(GX), nst, single, static_cast<const TP*>(a),
+                    static_cast<TP*>(dP), static_cast<TP*>(bx), wsum);
       };
-      if (te) go(k_rgat_bwd_dst<TP, DD, false, true>, k_rgat_bwd_dst<TP, DD, true, true>);
-      else go(k_rgat_bwd_dst<TP, DD, false, false>, k_rgat_bwd_dst<TP, DD, true, false>);
+      if (te) go(k_rgat_bwd_dst<TP, DD, false, true, false>, k_rgat_bwd_dst<TP, DD, true, true, false>);
+      else if (single) go(k_rgat_bwd_dst<TP, DD, false, false, true>, k_rgat_bwd_dst<TP, DD, true, false, true>);
+      else go(k_rgat_bwd_dst<TP, DD, false, false, false>, k_rgat_bwd_dst<TP, DD, true, false, false>);
       launch("rgat_node_prep", k_rgat_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
              g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(X), out, stats,
              static_cast<TP*>(GX), nst);
@@ -1786,13 +1813,18 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, void* bx, const Partial& pt, cudaStream_t s) {
+                   float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s) {
+  WorkPlan wp = g->pairs;  // single-edge pairs resolved by the destination-major pass (reordered path)
+  if (skip_single && !te) {
+    wp.n_items = wp.n_multi;
+    wp.n_short = std::min(wp.n_short, wp.n_multi);
+  }
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       auto go = [&](auto kw, auto kg) {
-        launch_plan("rgat_bwd_pair", g->pairs, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
+        launch_plan("rgat_bwd_pair", wp, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
                     (const int32_t*)g->csc_dst, (const int32_t*)g->csc_rel, (const int32_t*)g->csc2csr, te,
                     static_cast<const TP*>(P), spair, y, static_cast<const TP*>(a), slope, static_cast<const TP*>(GX),
                     nst, static_cast<TP*>(dP), wsum, te ? nullptr : static_cast<TP*>(bx));

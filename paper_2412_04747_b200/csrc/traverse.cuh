@@ -29,14 +29,15 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM,
 // te != NULL (reordering off): t_e read from te, dz_e written per CSR entry into dz, dX untouched.
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
-                  const float* out, float* dX, void* GX, float4* nst, const Partial& pt, cudaStream_t s);
+                  const float* out, float* dX, void* GX, float4* nst, const uint8_t* single, const void* a, void* dP,
+                  void* bx, float* wsum, const Partial& pt, cudaStream_t s);
 // G: upstream gradient rows in the layer dtype (bf16 copy on the bf16 path)
 void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const void* G, void* dP,
                    const Partial& pt, cudaStream_t s);
 // te != NULL (reordering off): t_e = te[csc2csr[i]], bx not computed
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, void* bx, const Partial& pt, cudaStream_t s);
+                   float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s);
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, bool skip_single, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn
