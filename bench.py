@@ -128,6 +128,30 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
     return out
 
 
+def single_edge_pairs(g):
+    """Number of (rel, src) pairs with exactly one edge (host count; the library resolves them in
+    the destination-major backward pass when they are >= 30 % of the pairs, layer.cu single_in_dst)."""
+    key = g.rel.astype(np.int64) * g.num_nodes + g.src
+    _, cnt = np.unique(key, return_counts=True)
+    return int((cnt == 1).sum())
+
+
+def adjust_for_single(alg, model, E, U, U1, d, b):
+    """Move the single-edge pairs' bytes from the pair-major label to the destination-major one:
+    the pair pass no longer gathers their node records; the dst pass reads a 1-byte flag per edge
+    and writes their gradient rows (HGT [dK~ | dM]; RGAT dP, bx, wsum and reads a_r)."""
+    if model not in ("hgt", "rgat") or 10 * U1 < 3 * U:
+        return alg
+    alg = dict(alg)
+    if model == "hgt":
+        alg["hgt_bwd_pair"] -= U1 * (4 + 2 * d * b + 16) + U1 * (16 + 2 * d * b + 2 * d * b)
+        alg["hgt_bwd_dst"] += E * 1 + U1 * (2 * d * b)
+    else:
+        alg["rgat_bwd_pair"] -= U1 * (4 + 2 * d * b + 16) + U1 * (16 + 4 + d * b + 4 + d * b + 4 + d * b)
+        alg["rgat_bwd_dst"] += E * 1 + U1 * (d * b + d * b + d * b + 4)
+    return alg
+
+
 def adjust_for_fusions(alg, prof, U, N, d_in, b):
     """Kernel labels that absorbed another kernel's work carry its bytes: when the per-source
     reduction of the pair dX rows runs in the HGT node GEMM's epilogue (no seg_reduce_rows launch),
@@ -487,6 +511,8 @@ def main():
     U, E = gi["num_pairs"], gi["num_edges"]
     alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
     alg = adjust_for_fusions(alg, prof, U, g.num_nodes, d, 2 if dtype == "bf16" else 4)
+    if world == 1 and not args.no_compact and model in ("hgt", "rgat"):
+        alg = adjust_for_single(alg, model, E, U, single_edge_pairs(g), d, 2 if dtype == "bf16" else 4)
     # per-step view of each kernel label (a label may cover several launches per step, e.g. the
     # warp-mode and group-mode launches of one traversal); bytes are per step as well
     tot_ms = sum(x["ms"] for x in prof.values())
@@ -752,6 +778,10 @@ def run_train(args, cfg, world, rank, local_rank):
     nparams = sum(m.numel() for ms_ in st.master for m in ms_.values())
     alg = train_bytes(model, dtype, g.num_nodes, E, U, g.num_rels, g.num_node_types, d, layers, nparams)
     alg = adjust_for_fusions(alg, prof, U * (layers - 1), g.num_nodes * (layers - 1), d, 2 if dtype == "bf16" else 4)
+    if not args.no_compact and model in ("hgt", "rgat"):
+        one = adjust_for_single({k: 0 for k in alg}, model, E, U, single_edge_pairs(g), d,
+                                2 if dtype == "bf16" else 4)
+        alg = {k: v + layers * one.get(k, 0) for k, v in alg.items()}
     tot_ms = sum(x["ms"] for x in prof.values())
     kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                    "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}

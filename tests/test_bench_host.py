@@ -57,3 +57,22 @@ def test_train_bytes_layers():
     assert two["nll_loss"] == 50 * 64 * 8 + 50 * 4
     assert two["relu_fwd"] == 50 * 64 * (4 + 2)
     assert two["sgd_update"] == 1000 * (12 + 2)
+
+
+def test_single_edge_adjustment():
+    a = bench.algorithmic_bytes("hgt", "bf16", N=100, E=1000, U=700, UD=0, R=3, T=1, d_in=64, d=64)
+    # below the 30 % threshold nothing moves
+    assert bench.adjust_for_single(a, "hgt", 1000, 700, 100, 64, 2) == a
+    b = bench.adjust_for_single(a, "hgt", 1000, 700, 500, 64, 2)
+    assert b["hgt_bwd_pair"] < a["hgt_bwd_pair"] and b["hgt_bwd_dst"] > a["hgt_bwd_dst"]
+    # the pair pass keeps exactly the bytes of the multi-edge pairs
+    rest = bench.algorithmic_bytes("hgt", "bf16", N=100, E=500, U=200, UD=0, R=3, T=1, d_in=64, d=64)
+    assert b["hgt_bwd_pair"] == rest["hgt_bwd_pair"]
+    assert bench.adjust_for_single(a, "rgcn", 1000, 700, 500, 64, 2) == a
+
+
+def test_single_edge_pairs_count():
+    from synth import g7
+    g = g7()
+    # G7 pairs (rel, src): edges per pair [2, 2, 1, 1, 1] (tests/golden/g7_build.json edge_pair)
+    assert bench.single_edge_pairs(g) == 3
