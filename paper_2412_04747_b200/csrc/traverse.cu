@@ -44,6 +44,14 @@ constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and 
 #else
 #define RGNN_FWD_LB __launch_bounds__(256)
 #endif
+#ifndef RGNN_UNR_SGL
+#define RGNN_UNR_SGL 2
+#endif
+#ifdef RGNN_RGAT_DST_MINB
+#define RGNN_RGAT_DST_LB __launch_bounds__(256, RGNN_RGAT_DST_MINB)
+#else
+#define RGNN_RGAT_DST_LB __launch_bounds__(256)
+#endif
 #ifdef RGNN_DST_MINB
 #define RGNN_DST_LB __launch_bounds__(256, RGNN_DST_MINB)
 #else
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
 // TE (reordering off): t_e from te[], no dX t-path here; dz_e is written per CSR entry (dz_out)
 // for the explicit destination-side GEMMs.
 template <class TP, int D, bool GROUP, bool TE, bool SGL>
-__global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
+__global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
@@ -731,6 +739,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
                                                       TP* __restrict__ bx, float* __restrict__ wsum) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
+  constexpr int UN = SGL ? RGNN_UNR_SGL : UNR;  // the single-edge stores need registers: fewer edges per step
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t v = w.item.x;
@@ -755,13 +764,13 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
       st_tp<V>(GX + v * 2 * D + D + c * V, x);
       if (w.leader()) nst[v] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
-    for (int t = 0; t < w.span; t += w.step * UNR) {
+    for (int t = 0; t < w.span; t += w.step * UN) {
       const int i0 = b + t + w.first;
-      uint4 rp[UNR];
-      float sp[UNR], yv[UNR][V];
-      int pid[UNR], rel[UNR];  // SGL: single-edge pair id (else -1) and its relation
+      uint4 rp[UN];
+      float sp[UN], yv[UN][V];
+      int pid[UN], rel[UN];  // SGL: single-edge pair id (else -1) and its relation
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < UN; ++u) {
         int i = i0 + u * w.step;
         rp[u] = make_uint4(0, 0, 0, 0);
         sp[u] = 0.f;
@@ -786,7 +795,7 @@ __global__ void __launch_bounds__(256) k_rgat_bwd_dst(int64_t n, const int4* __r
         }
       }
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
+      for (int u = 0; u < UN; ++u) {
         int i = i0 + u * w.step;
         float pv[V];
         cvt16<TP>(rp[u], pv);
