@@ -162,6 +162,98 @@ def adjust_for_fusions(alg, prof, U, N, d_in, b):
     return alg
 
 
+def d4_bytes(model, dtype, N, E, U, d):
+    """what the method itself must move per fwd and bwd (fused design, int32
+    indices, fp32 gradients, b = stored feature bytes), plus the D4 term of each traversal row
+    (A3-A5 forward, A6 dst-major, A7 pair-major) for the dominant-kernel comparison."""
+    b = 2 if dtype == "bf16" else 4
+    db = d * b
+    if model == "rgcn":
+        fwd = U * 2 * db + E * (8 + db) + N * (2 * db + 8 * d + 4)
+        bwd = E * (8 + 4 * d) + U * (8 * d + db) + N * (8 * d + db)
+        rows = {"rgcn_fwd_traverse": E * (8 + db) + N * (8 * d + 4), "rgcn_bwd_pair": E * (8 + 4 * d)}
+    elif model == "rgat":
+        fwd = U * (2 * db + 4) + E * (10 + db) + N * (db + 4 * d + 12)
+        bwd = E * (18 + db) + E * (12 + 4 * d) + U * (8 * d + db) + N * (8 * d + db + 4)
+        rows = {"rgat_fwd_traverse": E * (10 + db) + N * (db + 4 * d + 12), "rgat_bwd_dst": E * (18 + db),
+                "rgat_bwd_pair": E * (12 + 4 * d)}
+    else:
+        fwd = U * 3 * db + N * 3 * db + E * (4 + 2 * db) + N * (4 * d + 12)
+        bwd = E * (12 + 2 * db) + E * (12 + 4 * d + db) + U * (12 * d + db) + N * (16 * d + db + 4)
+        rows = {"hgt_fwd_traverse": E * (4 + 2 * db) + N * (4 * d + 12), "hgt_bwd_dst": E * (12 + 2 * db),
+                "hgt_bwd_pair": E * (12 + 4 * d + db)}
+    return {"fwd": fwd, "bwd": bwd, "rows": rows}
+
+
+# kernel-name regex of each traversal label (every launch of the label: warp, group and short halves)
+LABEL_KERNELS = {"hgt_bwd_pair": "k_hgt_bwd_pair", "hgt_bwd_dst": "k_hgt_bwd_dst", "hgt_fwd_traverse": "k_hgt_fwd",
+                 "rgat_bwd_pair": "k_rgat_bwd_pair", "rgat_bwd_dst": "k_rgat_bwd_dst",
+                 "rgat_fwd_traverse": "k_rgat_fwd", "rgcn_bwd_pair": "k_rgcn_bwd_pair",
+                 "rgcn_fwd_traverse": "k_rgcn_fwd", "pair_bwd_fused": "k_pair_bwd_tc"}
+
+
+def source_hash() -> str:
+    """sha1 over the library sources (csrc + include): ties an ncu capture to the build it measured."""
+    import glob
+    import hashlib
+    h = hashlib.sha1()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2412_04747_b200", "csrc", "*")) +
+                   glob.glob(os.path.join(ROOT, "include", "*.h")))
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:12]
+
+
+def parse_ncu_dram(csv_text: str, pattern: str):
+    """Sum dram__bytes_read.sum + dram__bytes_write.sum over the launches whose name contains
+    `pattern` in an `ncu --csv` (--page raw or metric list) log; returns (bytes, launches)."""
+    import csv
+    import io
+    lines = [l for l in csv_text.splitlines() if l.startswith('"')]
+    if not lines:
+        return None, 0
+    rows = list(csv.reader(io.StringIO("\n".join(lines))))
+    h = rows[0]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    if "Metric Name" in h:  # long format: one row per (launch, metric)
+        ki, ii, mi, ui, vi = (h.index("Kernel Name"), h.index("ID"), h.index("Metric Name"), h.index("Metric Unit"),
+                              h.index("Metric Value"))
+        tot, ids = 0.0, set()
+        for r in rows[1:]:
+            if pattern in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                tot += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+                ids.add(r[ii])
+        return (tot if ids else None), len(ids)
+    return None, 0
+
+
+def ncu_traffic_in_run(args, label):
+    """DRAM bytes per step of `label`, measured now on this build: ncu (two DRAM counters, cold-cache
+    serialised replays) over a child bench run of the same config (3 warm-up + 1 step), bytes
+    summed over the label's launches and divided by the 4 steps run.  None when ncu is absent."""
+    import shutil
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    pat = LABEL_KERNELS.get(label)
+    if ncu is None or pat is None:
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--csv",
+           "-k", f"regex:{pat}", sys.executable, os.path.abspath(__file__), "--config", args.config, "--steps", "1",
+           "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-ncu"]
+    if args.a_dst is not None:
+        cmd += ["--a-dst", str(args.a_dst)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=args.ncu_timeout)
+    except (subprocess.TimeoutExpired, OSError):
+        return None
+    tot, n = parse_ncu_dram(r.stdout, pat)
+    if tot is None:
+        return None
+    return {"bytes_per_step": tot / 4.0, "launches": n, "steps": 4, "source_hash": source_hash(),
+            "how": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:{pat} "
+                   f"over bench.py --config {args.config} --steps 1 --warmup 3 (this build, this run)"}
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 50 ms (B200_PROFILING.md clocks line)."""
@@ -288,6 +380,47 @@ def single_thread(fn, target_s):
     return {"value": r["value"], "unit": r["unit"], "cores": 1, "sample": r["sample"]}
 
 
+def roofline_block(alg, prof, steps, ms_per_step, peaks, model, dtype, N, E, U, d, t_fwd, t_bwd, infer):
+    """Per-kernel view + the dominant label's roofline, three ways: its algorithmic bytes (the
+    kernel-level model), the SURVEY.md §8(d) D4 term of its row, and (filled in by the
+    caller) ncu DRAM bytes.  Step-level bytes count only the labels that launched in this run."""
+    hbm = peaks["hbm_gbs"]
+    tot_ms = sum(x["ms"] for x in prof.values())
+    kernels = {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["ms"] / steps,
+                   "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}
+    for k in kernels:
+        if alg.get(k):
+            kernels[k]["algorithmic_bytes_per_step"] = int(alg[k])
+            kernels[k]["achieved_gbs"] = alg[k] / (kernels[k]["ms_per_step"] / 1e3) / 1e9
+    ran = {k: v for k, v in alg.items() if k in prof}
+    d4 = d4_bytes(model, dtype, N, E, U, d)
+    d4_step = d4["fwd"] + (0 if infer else d4["bwd"])
+    out = {"bound": "hbm", "peak": hbm, "unit": "GB/s", "peak_source": peaks["source"],
+           "step_algorithmic_gb": sum(ran.values()) / 1e9,
+           "step_achieved_gbs": sum(ran.values()) / (ms_per_step / 1e3) / 1e9,
+           "step_frac": sum(ran.values()) / (ms_per_step / 1e3) / 1e9 / hbm,
+           "step_d4_gb": d4_step / 1e9, "step_d4_frac": d4_step / (ms_per_step / 1e3) / 1e9 / hbm,
+           "d4_fwd_gb": d4["fwd"] / 1e9, "d4_bwd_gb": d4["bwd"] / 1e9,
+           "t_fwd_ms": t_fwd, "t_bwd_ms": t_bwd,
+           "fwd_d4_frac": d4["fwd"] / (t_fwd / 1e3) / 1e9 / hbm if t_fwd else None,
+           "bwd_d4_frac": d4["bwd"] / (t_bwd / 1e3) / 1e9 / hbm if t_bwd else None,
+           "kernel": None, "traffic": None, "_kernels": kernels}
+    dom = max((k for k in prof if alg.get(k)), key=lambda k: prof[k]["ms"], default=None)
+    if dom is None:
+        return out
+    ms_k = kernels[dom]["ms_per_step"]
+    achieved = alg[dom] / (ms_k / 1e3) / 1e9
+    out.update({"kernel": dom, "achieved": achieved, "frac": achieved / hbm, "frac_of_8TBps": achieved / 8000.0,
+                "algorithmic_bytes_per_step": int(alg[dom]), "launches_per_step": kernels[dom]["launches_per_step"],
+                "ms_per_step": ms_k,
+                "note": "bytes and time per step of the kernel label (all its launches in one step); frac uses the "
+                        "kernel-level byte model, d4_frac the SURVEY.md §8(d) D4 term of the label's row"})
+    if dom in d4["rows"]:
+        out["d4_bytes_per_step"] = int(d4["rows"][dom])
+        out["d4_frac"] = d4["rows"][dom] / (ms_k / 1e3) / 1e9 / hbm
+    return out
+
+
 # ----------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -310,6 +443,11 @@ def main():
     ap.add_argument("--a-dst", type=float, default=None,
                     help="destination Zipf exponent of the generator (SURVEY.md §8(d) D1 load-balance sensitivity "
                          "points: 0 = uniform in-degrees, 1.2 = heavier skew; default the config's 0.8)")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the in-run ncu DRAM-traffic capture of the dominant kernel (roofline.traffic)")
+    ap.add_argument("--ncu-timeout", type=float, default=300.0)
+    ap.add_argument("--comm", action="store_true",
+                    help="N=1: run through a world-1 library communicator (the multi-GPU code path on one GPU)")
     ap.add_argument("--infer", action="store_true",
                     help="inference: a step is the forward pass only (the 'Inference' columns of tab:optimizations)")
     args = ap.parse_args()
@@ -348,11 +486,19 @@ def main():
     td = torch.float32 if dtype == "f32" else torch.bfloat16
     w = {k: torch.tensor(np.asarray(v, np.float32), device=dev).to(torch.float32 if k == "mu" else td)
          for k, v in inp.items() if k != "X"}
+    # X: a full [N, d] buffer per rank; this rank fills its own rows, the library's forward
+    # all-gathers the others into it (NCCL, in place) when N > 1
     X_full = torch.tensor(np.asarray(inp["X"], np.float32), device=dev).to(td)
-    X_own = X_full[lo:hi].contiguous()
-    dout = torch.tensor(Gh, dtype=torch.float32, device=dev)
     if world > 1:
-        dout = D.masked_rows(dout, lo, hi)
+        X_full[:lo] = float("nan")
+        X_full[hi:] = float("nan")
+    X_own = X_full[lo:hi]
+    dout = torch.tensor(Gh, dtype=torch.float32, device=dev)  # the layer reads the owned rows only
+    comm = None
+    if world > 1:
+        comm = D.make_comm(ranges)
+    elif args.comm:  # exercise the library-owned exchange path on one GPU (a world-1 NCCL communicator)
+        comm = rgnn.Comm(0, 1, D.node_ptr(ranges), rgnn.comm_unique_id())
     layer = Layer(G, model, d, d, dtype=dtype, gemm_impl=args.gemm_impl, reorder=not args.no_reorder,
                   heads=cfg.get("heads", 1))
     wkeys = {"rgcn": ["dW", "dW0"], "rgat": ["dW", "da", "db"], "hgt": ["dWk", "dWq", "dWv", "dWatt", "dWmsg"]}[model]
@@ -360,31 +506,31 @@ def main():
     grads["dX"] = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
     out = torch.empty(g.num_nodes, d, dtype=torch.float32, device=dev)
 
-    def step(X_local, dout_local=None):
-        Xf = D.all_gather_rows(X_local, ranges, rank) if world > 1 else X_local
-        layer.forward(Xf, w, out=out)
+    def step(Xb, dout_b=None, mid=None, bufs=None):
+        """One layer forward + backward through the public API; with N > 1 the exchange (X
+        all-gather, dX reduce onto the owners, dW all-reduce) runs inside the library calls."""
+        o, gs = (out, grads) if bufs is None else bufs
+        layer.forward(Xb, w, out=o, comm=comm)
+        if mid is not None:
+            mid()
         if args.infer:
-            return out
-        gr = layer.backward(Xf, w, out, dout if dout_local is None else dout_local, grads=grads, need=wkeys)
-        if world > 1:
-            dx_own = D.reduce_scatter_rows(gr["dX"], ranges, rank)
-            D.all_reduce_grads(gr, wkeys)
-            return dx_own
+            return o
+        gr = layer.backward(Xb, w, o, dout if dout_b is None else dout_b, grads=gs, need=wkeys, comm=comm)
         return gr["dX"]
 
     for _ in range(args.warmup):
-        step(X_own)
+        step(X_full)
     torch.cuda.synchronize()
     graph = None
     if args.cuda_graph and world == 1:
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            step(X_own)  # warm the capture stream
+            step(X_full)  # warm the capture stream
         torch.cuda.current_stream().wait_stream(cs)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step(X_own)
+            step(X_full)
         torch.cuda.synchronize()
 
     sampler = ClockSampler(local_rank)
@@ -400,13 +546,14 @@ def main():
         n0 = rgnn.launch_count()
         s = torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        evm = [torch.cuda.Event(enable_timing=True) for _ in range(K)]  # after each step's forward
         t0 = time.time()
         ev[0].record(s)
         for i in range(K):
             if use_graph:
                 graph.replay()
             else:
-                step(X_own)
+                step(X_full, mid=lambda i=i: evm[i].record(s))
             ev[i + 1].record(s)
         torch.cuda.synchronize()
         t1 = time.time()
@@ -417,10 +564,13 @@ def main():
         rgnn.profile_enable(False)
         ms = ev[0].elapsed_time(ev[K])
         per_step[:] = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
+        if not use_graph:
+            fwd_bwd[:] = [(ev[i].elapsed_time(evm[i]), evm[i].elapsed_time(ev[i + 1])) for i in range(K)]
         return ms, launches, prof, t0, t1
 
     use_graph = graph is not None
     per_step = []  # per-step device times of the last timed() call (D2: median and mean)
+    fwd_bwd = []   # per-step (t_fwd, t_bwd) of the last un-captured timed() call (D2)
     ms, launches, prof, t0, t1 = timed(args.steps, use_graph)
     per_step_timed = list(per_step)
     time.sleep(0.12)
@@ -435,6 +585,8 @@ def main():
     if use_graph:  # launches inside the graph: counted and profiled on an un-captured pass
         _, launches, prof, _, _ = timed(args.steps, False)
     sampler.stop()
+    t_fwd = float(np.median([f for f, _ in fwd_bwd])) if fwd_bwd else None
+    t_bwd = float(np.median([b_ for _, b_ in fwd_bwd])) if fwd_bwd and not args.infer else None
     if world > 1:
         tms = torch.tensor([ms], device=dev)
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
@@ -445,25 +597,32 @@ def main():
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        Xh = X_own.cpu().pin_memory()
-        douth = dout.cpu().pin_memory()
+        Xh = X_own.cpu().pin_memory()            # the owned rows of X and dout, per step H2D
+        douth = dout[lo:hi].cpu().pin_memory()
         dwh = {k: torch.empty(grads[k].shape, dtype=torch.float32).pin_memory() for k in wkeys}
-        outh = torch.empty(out.shape, dtype=torch.float32).pin_memory() if args.infer else None
+        outh = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        own_rows = slice(lo, hi) if world > 1 else slice(0, g.num_nodes)
+        dxh = None if args.infer else torch.empty(hi - lo, d, dtype=torch.float32).pin_memory()
+        ds = torch.cuda.Stream(device=dev)  # D2H of the results (second copy engine)
+        # results double-buffered too: step i+1 computes into the other buffers while step i's are read
+        rbufs = [(out, grads), (torch.empty_like(out), {k: torch.empty_like(v) for k, v in grads.items()})]
+        results_ready = [torch.cuda.Event() for _ in range(2)]
+        results_read = [torch.cuda.Event() for _ in range(2)]
         # double-buffered: the H2D of step i+1's inputs (copy stream) overlaps step i's kernels
-        Xd = [torch.empty_like(X_own) for _ in range(2)]
-        doutd = [torch.empty_like(dout) for _ in range(2)]
+        Xd = [X_full.clone() for _ in range(2)]
+        doutd = [dout.clone() for _ in range(2)]
         cs = torch.cuda.Stream(device=dev)
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
         h2d = Xh.numel() * Xh.element_size() + (0 if args.infer else douth.numel() * douth.element_size())
-        d2h = outh.numel() * 4 if args.infer else sum(v.numel() * 4 for v in dwh.values())
+        d2h = (hi - lo) * d * 4 * (1 if args.infer else 2) + (0 if args.infer else sum(v.numel() * 4 for v in dwh.values()))
 
         def issue_copy(k):
             with torch.cuda.stream(cs):
                 cs.wait_event(consumed[k])  # the step that last read buffer k has finished
-                Xd[k].copy_(Xh, non_blocking=True)
+                Xd[k][lo:hi].copy_(Xh, non_blocking=True)
                 if not args.infer:
-                    doutd[k].copy_(douth, non_blocking=True)
+                    doutd[k][lo:hi].copy_(douth, non_blocking=True)
                 copied[k].record(cs)
 
         def e2e_run(K):
@@ -475,14 +634,20 @@ def main():
                 if i + 1 < K:
                     issue_copy(1 - k)
                 s.wait_event(copied[k])
-                if args.infer:
-                    step(Xd[k])
-                    outh.copy_(out, non_blocking=True)
-                else:
-                    step(Xd[k], doutd[k])
-                    for name in wkeys:
-                        dwh[name].copy_(grads[name], non_blocking=True)
+                s.wait_event(results_read[k])  # results of step i-2 have left buffer set k
+                o, gs = rbufs[k]
+                r = step(Xd[k], bufs=rbufs[k]) if args.infer else step(Xd[k], doutd[k], bufs=rbufs[k])
                 consumed[k].record(s)
+                results_ready[k].record(s)
+                with torch.cuda.stream(ds):
+                    ds.wait_event(results_ready[k])
+                    outh[own_rows].copy_(o[own_rows], non_blocking=True)
+                    if not args.infer:
+                        dxh.copy_(r[own_rows], non_blocking=True)
+                        for name in wkeys:
+                            dwh[name].copy_(gs[name], non_blocking=True)
+                    results_read[k].record(ds)
+            s.wait_stream(ds)
 
         e2e_run(2)
         torch.cuda.synchronize()
@@ -502,46 +667,32 @@ def main():
         e2e = {"value": g.num_edges * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps,
                "path": "paper_2412_04747_b200.Layer forward/backward (C-ABI); per step H2D of X and dout from pinned "
-                       "host memory (double-buffered on a copy stream: step i+1's copy overlaps step i), D2H of every "
-                       "weight gradient (dX stays on the device for the layer below)"}
+                       "host memory (double-buffered on a copy stream: step i+1's copy overlaps step i), D2H of the "
+                       "step's results (the owned output rows, the owned dX rows and every weight gradient) on a "
+                       "second copy stream; the next step waits until the results have been read"}
 
     # ---- roofline of the dominant kernel
     peaks = load_peaks()
     gi = G.info()
     U, E = gi["num_pairs"], gi["num_edges"]
+    bsz = 2 if dtype == "bf16" else 4
     alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
-    alg = adjust_for_fusions(alg, prof, U, g.num_nodes, d, 2 if dtype == "bf16" else 4)
+    alg = adjust_for_fusions(alg, prof, U, g.num_nodes, d, bsz)
     if world == 1 and not args.no_compact and model in ("hgt", "rgat"):
-        alg = adjust_for_single(alg, model, E, U, single_edge_pairs(g), d, 2 if dtype == "bf16" else 4)
-    # per-step view of each kernel label (a label may cover several launches per step, e.g. the
-    # warp-mode and group-mode launches of one traversal); bytes are per step as well
-    tot_ms = sum(x["ms"] for x in prof.values())
-    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
-                   "share": v["ms"] / max(tot_ms, 1e-9)} for k, v in prof.items()}
-    for k in kernels:
-        if k in alg:
-            kernels[k]["algorithmic_bytes_per_step"] = int(alg[k])
-            kernels[k]["achieved_gbs"] = alg[k] / (kernels[k]["ms_per_step"] / 1e3) / 1e9
-    dom = max((k for k in prof if k in alg), key=lambda k: prof[k]["ms"], default=None)
-    roofline = None
-    if dom is not None:
-        ms_k = kernels[dom]["ms_per_step"]
-        achieved = alg[dom] / (ms_k / 1e3) / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp) and not args.no_compact and not args.no_reorder and not args.infer and world == 1:
-            tr = json.load(open(tp)).get(args.config, {}).get(dom)
-            traffic = tr["bytes_per_step"] if tr else None
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                    "traffic_note": "ncu dram read+write bytes per step of this label (profiles/ncu_traffic.json)"
-                                    if traffic else None, "peak_source": peaks["source"],
-                    "frac_of_8TBps": achieved / 8000.0, "algorithmic_bytes_per_step": int(alg[dom]),
-                    "launches_per_step": kernels[dom]["launches_per_step"], "ms_per_step": ms_k,
-                    "note": "bytes and time per step of the kernel label (all its launches in one step)"}
-        step_bytes = sum(alg.values())
-        roofline["step_algorithmic_gb"] = step_bytes / 1e9
-        roofline["step_achieved_gbs"] = step_bytes / (ms_per_step / 1e3) / 1e9
+        alg = adjust_for_single(alg, model, E, U, single_edge_pairs(g), d, bsz)
+    roofline = roofline_block(alg, prof, args.steps, ms_per_step, peaks, model, dtype, g.num_nodes, E, U, d,
+                              t_fwd, t_bwd, args.infer)
+    kernels = roofline.pop("_kernels")
+    if roofline.get("kernel") and world == 1 and not args.no_ncu and not args.cuda_graph:
+        tr = ncu_traffic_in_run(args, roofline["kernel"])
+        if tr is not None:
+            ms_k = roofline["ms_per_step"]
+            roofline["traffic"] = int(tr["bytes_per_step"])
+            roofline["traffic_frac"] = tr["bytes_per_step"] / (ms_k / 1e3) / 1e9 / peaks["hbm_gbs"]
+            roofline["traffic_note"] = ("ncu DRAM read+write bytes per step of this label, cold-cache serialised "
+                                        "replays; traffic_frac = these bytes / the live event time / peak")
+            roofline["traffic_how"] = tr["how"]
+            roofline["traffic_source_hash"] = tr["source_hash"]
 
     gi = G.info()
     memory = {"graph_index_bytes": int(gi["device_bytes"]), "saved_bytes": int(layer.saved.numel()),
@@ -559,6 +710,13 @@ def main():
         cpu["single_thread"] = single_thread(lambda t: cpu_oracle_sample(g, model, inp, Gh, target_s=t),
                                              args.cpu_seconds / 3)
 
+    exchange = None
+    if world > 1:  # bytes of variant X vs variant P per rank, and the one run
+        u_glob = int(np.unique(g.rel.astype(np.int64) * g.num_nodes + g.src).size)
+        exchange = rgnn.exchange_bytes(model, dtype, d, d, g.num_nodes, u_glob, cfg.get("heads", 1))
+        exchange["how"] = ("library-owned NCCL (rgnn_comm): in-place all-gather of X by owner broadcasts on the "
+                           "library's stream, chunk-pipelined with the pair GEMM; dX reduced onto the owners, dW "
+                           "all-reduced, inside rgnn_layer_forward / rgnn_layer_backward")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -581,11 +739,14 @@ def main():
                        "gemm_impl": ["auto (bf16 -> tcgen05)", "simt", "tcgen05"][args.gemm_impl],
                        "materialization": "vanilla (row per edge)" if args.no_compact else "compact (row per (rel, src) pair)",
                        "reorder": not args.no_reorder, "heads": cfg.get("heads", 1), "mode": "inference (forward only)" if args.infer else "training (forward + backward)",
-                       "cuda_graph": bool(use_graph), "a_dst": args.a_dst if args.a_dst is not None else 0.8},
+                       "cuda_graph": bool(use_graph), "a_dst": args.a_dst if args.a_dst is not None else 0.8,
+                       "exchange": exchange},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "memory": memory, "kernels": kernels,
         }
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -794,11 +955,12 @@ def run_train(args, cfg, world, rank, local_rank):
     if dom is not None:
         ms_k = kernels[dom]["ms_per_step"]
         achieved = alg[dom] / (ms_k / 1e3) / 1e9
+        ran = sum(v for k, v in alg.items() if k in prof)  # only the labels that launched
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
                     "algorithmic_bytes_per_step": int(alg[dom]), "launches_per_step": kernels[dom]["launches_per_step"],
-                    "ms_per_step": ms_k, "step_algorithmic_gb": sum(alg.values()) / 1e9,
-                    "step_achieved_gbs": sum(alg.values()) / (ms_per_step / 1e3) / 1e9,
+                    "ms_per_step": ms_k, "step_algorithmic_gb": ran / 1e9,
+                    "step_achieved_gbs": ran / (ms_per_step / 1e3) / 1e9,
                     "note": "bytes and time per step of the kernel label (all its launches in one step, both layers)"}
     cpu = None
     if not args.no_cpu_baseline:

@@ -54,7 +54,7 @@ typedef enum {
   RGNN_ERR_UNSUPPORTED = 3,   /* shape not supported (e.g. d_out not in {16,32,64,128}) */
   RGNN_ERR_OOM = 4,           /* the allocator callback returned NULL */
   RGNN_ERR_CUDA = 5,          /* a CUDA runtime error (message has the CUDA error string) */
-  RGNN_ERR_NCCL = 6           /* reserved for library-owned collectives */
+  RGNN_ERR_NCCL = 6           /* NCCL missing or an NCCL call failed (library-owned collectives) */
 } rgnn_status;
 
 /* Thread-local description of the last failure on this thread ("" if none). */
@@ -223,23 +223,77 @@ typedef struct {
 RGNN_API rgnn_status rgnn_layer_workspace(rgnn_graph_t g, const rgnn_layer_desc* desc, size_t* saved_bytes,
                                  size_t* scratch_bytes);
 
-/* Forward: out[N][d_out] (float, device) = the layer output for every node
- * (rows of destinations outside [dst_lo, dst_hi) and zero in-degree rows hold
- * only the self-loop term for RGCN, zero otherwise; reading g10).
- * X: device [N][d_in] in the layer dtype.  saved: written, needed by backward.
- * Errors: INVALID_ARG (NULL pointers for the model, bad desc), UNSUPPORTED, CUDA. */
+/* ------------------------------------------------------------------ communicator (multi-GPU)
+ * Destination-partitioned multi-GPU layer (north_star: "the graph is partitioned by
+ * destination-node range ... projected source features are exchanged with NCCL all-gather"; the
+ * paper itself is single-GPU, §3.6.2).  One process per GPU.  Rank k owns the node rows
+ * [node_ptr[k], node_ptr[k+1]) (features, outputs, dX) and builds its graph with dst_lo = node_ptr[k],
+ * dst_hi = node_ptr[k+1]: the in-edges of its destinations, with sources anywhere.  The layer calls
+ * take the communicator and then:
+ *   forward : all-gather X in place (rank k's rows are read, the other rows of X are overwritten),
+ *             one ncclBroadcast per owner on a library-owned high-priority stream, each chunk
+ *             signalled by an event so the pair GEMM of the sources already present runs while
+ *             the next chunk is in flight; node-side projections (HGT Q, RGCN self-loop, tail)
+ *             run on the owned rows only; out rows outside the owned range are left untouched.
+ *   backward: reads dout rows of the owned range only; the pair-side dX contributions of every
+ *             source are summed onto their owners (one in-place ncclReduce per owner: a
+ *             reduce-scatter with uneven counts), so dX rows [node_ptr[k], node_ptr[k+1]) hold the
+ *             full gradient on rank k (other rows: this rank's partial contributions); every
+ *             requested weight gradient is summed on all ranks (ncclAllReduce).
+ * The exchanged tensor is X (variant X): N * d_in * b bytes per layer, against U_global * k * d_out *
+ * b for the projected per-pair rows (variant P); with d_in = d_out and U > N (every BASELINE
+ * config) X is the smaller, rgnn_comm_exchange_bytes reports both.
+ * NCCL is loaded at run time (libnccl.so.2; in a PyTorch process the NCCL torch loaded).
+ * Results are deterministic for a fixed world size (NCCL's fixed reduction order), not across sizes. */
+#define RGNN_COMM_ID_BYTES 128
+typedef struct rgnn_comm_s* rgnn_comm_t;
+
+/* A fresh NCCL unique id (RGNN_COMM_ID_BYTES bytes into id_out, host).  Call on one rank and
+ * distribute the bytes to the others out of band (e.g. torch.distributed broadcast).
+ * Errors: INVALID_ARG (NULL), NCCL (libnccl.so.2 missing or ncclGetUniqueId failed). */
+RGNN_API rgnn_status rgnn_comm_unique_id(void* id_out);
+
+/* Create this rank's communicator on the current CUDA device (collective: every rank must call it
+ * with the same id, world and node_ptr).  node_ptr: host int64[world+1], node_ptr[0] = 0,
+ * non-decreasing, node_ptr[world] = N: the owned node rows of every rank.
+ * Errors: INVALID_ARG (bad rank / world / node_ptr), NCCL, CUDA. */
+RGNN_API rgnn_status rgnn_comm_create(int32_t rank, int32_t world, const void* unique_id, const int64_t* node_ptr,
+                                      rgnn_comm_t* out);
+/* Destroy (synchronises the comm stream).  NULL is a no-op. */
+RGNN_API rgnn_status rgnn_comm_destroy(rgnn_comm_t comm);
+RGNN_API rgnn_status rgnn_comm_info(rgnn_comm_t comm, int32_t* rank, int32_t* world);
+/* Bytes one layer forward would exchange per rank under variant X (all-gather of X) and variant P
+ * (all-gather of the projected per-(rel, src) rows of the whole graph, num_pairs_global rows of k
+ * projections: 2 for HGT [K~|M], 1 otherwise), and the variant the library runs (0 = X).
+ * Errors: INVALID_ARG. */
+RGNN_API rgnn_status rgnn_comm_exchange_bytes(const rgnn_layer_desc* desc, int64_t num_nodes, int64_t num_pairs_global,
+                                              int64_t* bytes_x, int64_t* bytes_p, int32_t* variant);
+
+/* Forward: out[N][d_out] (float, device) = the layer output of every destination row in the
+ * graph's owned range [dst_lo, dst_hi) (all rows on one GPU); zero in-degree rows hold only the
+ * self-loop term for RGCN, zero otherwise (reading g10).  Rows outside the owned range are not
+ * written.  X: device [N][d_in] in the layer dtype (read-only without a communicator; with one,
+ * rows outside the owned range are overwritten by the all-gather, see above).
+ * saved: written, needed by backward.  comm: NULL on one GPU; otherwise a communicator whose
+ * node_ptr[rank], node_ptr[rank+1] equal the graph's dst_lo, dst_hi.
+ * Errors: INVALID_ARG (NULL pointers for the model, bad desc, graph range != comm range),
+ * UNSUPPORTED, CUDA, NCCL. */
 RGNN_API rgnn_status rgnn_layer_forward(rgnn_graph_t g, const rgnn_layer_desc* desc, const void* X, const rgnn_weights* w,
-                               float* out, void* saved, void* scratch, void* stream);
+                               float* out, void* saved, void* scratch, rgnn_comm_t comm, void* stream);
 
 /* Backward of L = sum(out * dout) (reading g12).  `out` is the forward output
  * (read by RGAT/HGT for the softmax backward row term G_v . out_v), `saved` the
- * buffer written by the matching forward.  dX: device float [N][d_in] (NULL = not
- * computed), dW: per-field device float (NULL = pruned).  Every requested output
- * is fully overwritten (no accumulation into caller data).
+ * buffer written by the matching forward.  dout rows of the owned range are read.
+ * dX: device float [N][d_in] (NULL = not computed): every row is written — the full
+ * gradient on one GPU; on a partitioned graph without a communicator, this range's
+ * contributions (their sum over the ranges is the gradient); with a communicator, the owned
+ * rows hold the full gradient after the call.  dW: per-field device float (NULL = pruned),
+ * summed over the ranks with a communicator.  Every requested output is fully overwritten
+ * (no accumulation into caller data).  X: as written by the forward.
  * Errors: as for forward. */
 RGNN_API rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* desc, const void* X, const rgnn_weights* w,
                                 const float* out, const void* saved, const float* dout, float* dX,
-                                const rgnn_weight_grads* dW, void* scratch, void* stream);
+                                const rgnn_weight_grads* dW, void* scratch, rgnn_comm_t comm, void* stream);
 
 /* ------------------------------------------------------------------ A1 primitive: typed segment GEMM
  * The paper's GEMM template Y[S] = X[G] x W[T] (§3.3.3, algo:gemm_template P:901-918),

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) k_seg_wsum(const Tile* __restrict__ tiles
 template <class TY, int K>
 __global__ void __launch_bounds__(256) k_seg_reduce_rows(int64_t n, const int32_t* __restrict__ ptr,
                                                          const int32_t* __restrict__ list, const TY* __restrict__ Y,
-                                                         float* __restrict__ out, bool accumulate) {
+                                                         float* __restrict__ out, bool accumulate, int64_t ld) {
   constexpr int V = Vec<TY>::N, LPR = K / V, EG = 32 / LPR, UN = 4;
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) k_seg_reduce_rows(int64_t n, const int32_
 #pragma unroll
     for (int q = 0; q < UN; ++q) {
       raw[q] = make_uint4(0, 0, 0, 0);
-      if (b + t + q < e) raw[q] = ldg16(Y + (int64_t)list[b + t + q] * K + c * V);
+      if (b + t + q < e) raw[q] = ldg16(Y + (int64_t)list[b + t + q] * ld + c * V);
     }
 #pragma unroll
     for (int q = 0; q < UN; ++q) {
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(256) k_seg_reduce_rows(int64_t n, const int32_
     }
   }
   if (!has) return;
-  float* o = out + u * K + c * V;
+  float* o = out + u * ld + c * V;
 #pragma unroll
   for (int k = 0; k < V; k += 4) {
     float4 prev = accumulate ? *reinterpret_cast<const float4*>(o + k) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -574,11 +574,16 @@ void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const v
     using TY = std::remove_pointer_t<decltype(ty)>;
     constexpr int KK = decltype(kc)::value;
     constexpr int LPR = KK / Vec<TY>::N;
-    if constexpr (LPR >= 1 && LPR <= 32)
+    if constexpr (LPR >= 1 && LPR <= 32) {
       launch("seg_reduce_rows", k_seg_reduce_rows<TY, KK>, dim3(ceil_div(ceil_div(n, 32 / LPR) * 32, 256)),
-             dim3(256), 0, s, n, ptr, list, static_cast<const TY*>(Y), out, accumulate);
-    else
-      RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "seg_reduce_rows: fp32 rows wider than 128");
+             dim3(256), 0, s, n, ptr, list, static_cast<const TY*>(Y), out, accumulate, (int64_t)KK);
+    } else {  // fp32 rows of 256: two column halves of 128 (row stride 256)
+      constexpr int KH = KK / 2;
+      for (int h = 0; h < 2; ++h)
+        launch("seg_reduce_rows", k_seg_reduce_rows<TY, KH>, dim3(ceil_div(ceil_div(n, 32 / (KH / Vec<TY>::N)) * 32, 256)),
+               dim3(256), 0, s, n, ptr, list, static_cast<const TY*>(Y) + h * KH, out + h * KH, accumulate,
+               (int64_t)KK);
+    }
   };
   auto by_k = [&](auto* ty) {
     switch (K) {

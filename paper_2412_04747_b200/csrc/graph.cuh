@@ -30,7 +30,19 @@ struct WorkPlan {
   int4* splits = nullptr;  // (id, first slot, number of slots, 0) for every heavy id
   int64_t n_split = 0;
   int64_t n_slots = 0;
+  // Edge-stream chunks (pairs only; the gather-ring kernels): contiguous CSC ranges (begin, end,
+  // slot, 0) that start and end at id boundaries, about STREAM_CHUNK edges each (an id longer than
+  // that alone; heavy ids as their split chunks with slots), longest first.  `_multi` leaves out
+  // the single-edge ids (resolved by the destination-major pass when single_in_dst).
+  int4* chunks = nullptr;
+  int64_t n_chunks = 0;
+  int4* chunks_multi = nullptr;
+  int64_t n_chunks_multi = 0;
 };
+#ifndef RGNN_STREAM_CHUNK
+#define RGNN_STREAM_CHUNK 48
+#endif
+constexpr int STREAM_CHUNK = RGNN_STREAM_CHUNK;
 
 // A contiguous row range [row0, row1) of one segment (weight index w).
 struct Tile {
@@ -60,6 +72,7 @@ struct rgnn_graph_s {
   std::vector<int32_t> pair_rel_ptr_h;   // host [R+1]
   std::vector<int32_t> pair_rt_ptr_h;    // host [R*T+1] : pairs sorted by (rel, src type)
   std::vector<int32_t> dpair_rel_ptr_h;  // host [R+1]
+  std::vector<int32_t> pair_src_h;       // host [U], copied on first use by a chunked (multi-GPU) pair GEMM
 
   // device index arrays (int32)
   int32_t* etype_ptr = nullptr;  // [R+1]
@@ -70,6 +83,7 @@ struct rgnn_graph_s {
   int32_t* csr_pair = nullptr;
   uint8_t* csr_single = nullptr;  // [E] 1 when the CSR entry's pair has exactly one edge
   int32_t* col_ptr = nullptr;  // [N+1]
+  int32_t* col_ptr_full = nullptr;  // [N+1] out-degree prefix over ALL input edges (partitioned builds only)
   int32_t* csc_dst = nullptr;
   int32_t* csc_rel = nullptr;
   int32_t* csc_eid = nullptr;

@@ -61,7 +61,8 @@ void compute_norms(rgnn_graph_s* g, int kind, const float* custom, cudaStream_t 
              g->dpair_cnt, csr_norm);
       break;
     case RGNN_NORM_SYM:
-      launch("norm_sym", k_norm_sym, dim3(ceil_div(g->N, TB)), dim3(TB), 0, s, g->N, g->row_ptr, g->col_ptr,
+      launch("norm_sym", k_norm_sym, dim3(ceil_div(g->N, TB)), dim3(TB), 0, s, g->N, g->row_ptr,
+             g->col_ptr_full ? g->col_ptr_full : g->col_ptr,
              g->csr_src, csr_norm);
       break;
     case RGNN_NORM_NONE:
@@ -106,7 +107,7 @@ const Plan& get_plan(rgnn_graph_s* g, const std::string& key, const std::vector<
   std::vector<int32_t> ptr(1, 0), sw;
   for (int i = 0; i < nseg; ++i) {
     int32_t w = w_of_seg.empty() ? (int32_t)i : w_of_seg[i];
-    for (int64_t r = seg_ptr[i]; r < seg_ptr[i + 1]; r += rows)
+    for (int64_t r = seg_ptr[i]; w >= 0 && r < seg_ptr[i + 1]; r += rows)  // w < 0: a gap, no tiles
       tiles.push_back(Tile{(int32_t)r, (int32_t)std::min<int64_t>(r + rows, seg_ptr[i + 1]), w, (int32_t)i});
     ptr.push_back((int32_t)tiles.size());
     sw.push_back(w);

@@ -155,7 +155,8 @@ __global__ void k_rt_bounds(int32_t R, int32_t T, const int64_t* ntp, int nb, co
   if (i > R * T) return;
   if (i == R * T) { out[i] = (int32_t)U; return; }
   int r = i / T, t = i % T;
-  uint64_t target = ((uint64_t)r << nb) | (uint64_t)ntp[t];
+  // addition, not OR: ntp[t] may equal N = 1 << nb (empty trailing type) and must carry into r + 1
+  uint64_t target = ((uint64_t)r << nb) + (uint64_t)ntp[t];
   int64_t lo = 0, hi = U;
   while (lo < hi) {
     int64_t mid = (lo + hi) / 2;
@@ -242,10 +243,11 @@ void hist_prefix(Tmp& tmp, const int32_t* v, int64_t n, int64_t nbins, int32_t* 
 
 // Edge-balanced work list (graph.cuh WorkPlan) from per-id (begin, degree); one-off host pass.
 void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std::vector<int32_t>& deg,
-                     WorkPlan& wp, cudaStream_t s) {
+                     WorkPlan& wp, cudaStream_t s, int64_t id_lo = 0, int64_t id_hi = -1) {
   std::vector<int4> heavy, medium, light, splits;
   int64_t slots = 0;
-  for (size_t id = 0; id < beg.size(); ++id) {
+  if (id_hi < 0) id_hi = (int64_t)beg.size();
+  for (size_t id = (size_t)id_lo; id < (size_t)id_hi; ++id) {
     int32_t b = beg[id], e = beg[id] + deg[id];
     if (deg[id] > SPLIT_THRESH) {
       int32_t n = 0;
@@ -283,6 +285,51 @@ void build_work_plan(rgnn_graph_s* g, const std::vector<int32_t>& beg, const std
   RGNN_CUDA(cudaStreamSynchronize(s));  // host staging goes out of scope
 }
 
+// Edge-stream chunks of the pair pass (graph.cuh WorkPlan::chunks) from the pairs in CSC order.
+void build_stream_chunks(rgnn_graph_s* g, const std::vector<int32_t>& pb, const std::vector<int32_t>& pd,
+                         WorkPlan& wp, cudaStream_t s) {
+  const int64_t U = g->U;
+  std::vector<int32_t> order(U);  // pairs by (src, rel) = CSC order
+  if (U) RGNN_CUDA(cudaMemcpyAsync(order.data(), g->src_pairs, U * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  std::vector<int4> heavy(std::max<int64_t>(wp.n_warp, 0));
+  if (wp.n_warp)
+    RGNN_CUDA(cudaMemcpyAsync(heavy.data(), wp.items, wp.n_warp * sizeof(int4), cudaMemcpyDeviceToHost, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+  for (int multi = 0; multi < 2; ++multi) {
+    std::vector<int4> ch;
+    for (const int4& it : heavy)
+      if (it.w >= 0) ch.push_back(make_int4(it.y, it.z, it.w, 0));  // split chunks of heavy pairs (slots)
+    int32_t cb = -1, ce = -1;
+    auto close = [&] {
+      if (cb >= 0 && ce > cb) ch.push_back(make_int4(cb, ce, -1, 0));
+      cb = ce = -1;
+    };
+    for (int64_t j = 0; j < U; ++j) {
+      const int32_t p = order[j], b = pb[p], n = pd[p];
+      if (n > SPLIT_THRESH || (multi && n == 1)) {  // heavy (above) or resolved elsewhere: a gap
+        close();
+        continue;
+      }
+      if (n > STREAM_CHUNK) {
+        close();
+        ch.push_back(make_int4(b, b + n, -1, 0));
+        continue;
+      }
+      if (cb < 0) cb = b;
+      ce = b + n;
+      if (ce - cb >= STREAM_CHUNK) close();
+    }
+    close();
+    std::stable_sort(ch.begin() + (int64_t)std::count_if(heavy.begin(), heavy.end(), [](const int4& it) { return it.w >= 0; }),
+                     ch.end(), [](const int4& a, const int4& b) { return a.y - a.x > b.y - b.x; });
+    int4*& dst = multi ? wp.chunks_multi : wp.chunks;
+    (multi ? wp.n_chunks_multi : wp.n_chunks) = (int64_t)ch.size();
+    dst = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<size_t>(ch.size(), 1), s));
+    if (!ch.empty()) RGNN_CUDA(cudaMemcpyAsync(dst, ch.data(), ch.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+    RGNN_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
 void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
   const int64_t N = g->N, U = g->U;
   std::vector<int32_t> rp(N + 1), pb(U), pd(U);
@@ -292,13 +339,17 @@ void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
     RGNN_CUDA(cudaMemcpyAsync(pd.data(), g->pair_deg, U * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   }
   RGNN_CUDA(cudaStreamSynchronize(s));
-  std::vector<int32_t> rb(N), rd(N);
-  for (int64_t v = 0; v < N; ++v) {
+  // destination rows: only the owned range [dst_lo, dst_hi) (a partitioned build has no in-edges
+  // elsewhere; its traversals must not touch the other ranks' output rows)
+  const int64_t lo = g->dst_lo, hi = g->dst_hi;
+  std::vector<int32_t> rb(N, 0), rd(N, 0);
+  for (int64_t v = lo; v < hi; ++v) {
     rb[v] = rp[v];
     rd[v] = rp[v + 1] - rp[v];
   }
-  build_work_plan(g, rb, rd, g->rows, s);
+  build_work_plan(g, rb, rd, g->rows, s, lo, hi);
   build_work_plan(g, pb, pd, g->pairs, s);
+  build_stream_chunks(g, pb, pd, g->pairs, s);
   // short items carry their first edge's gather index (rows: csr_pair, pairs: csc_dst) as
   // w = -2 - index (negative: never a partial slot), saving the short kernels one dependent load
   const int64_t nr = g->rows.n_items - g->rows.n_short, np = g->pairs.n_items - g->pairs.n_short;
@@ -389,6 +440,12 @@ void build_graph(rgnn_graph_s* g, const int32_t* src_in, const int32_t* dst_in, 
     RGNN_FAIL(RGNN_ERR_OUT_OF_RANGE, "node or relation id out of range at edge " + std::to_string(h_bad));
   const int64_t E = h_kept;
   g->E = E;
+  // GCN 'sym' norms need every source's out-degree over the whole graph, not over
+  // the kept (owned-destination) edges only
+  if (g->dst_lo != 0 || g->dst_hi != N) {
+    g->col_ptr_full = g->dev_i32(N + 1, s);
+    hist_prefix(tmp, src_in, E_in, N, g->col_ptr_full, s);
+  }
 
   int32_t* src = tmp.get<int32_t>(E);
   int32_t* dst = tmp.get<int32_t>(E);

@@ -9,6 +9,7 @@
 // dW = X[pair_src]^T dP per segment, two-level deterministic), then A2 unfolding.
 #include <algorithm>
 
+#include "comm.cuh"
 #include "ops.cuh"
 #include "traverse.cuh"
 
@@ -43,6 +44,47 @@ Segs seg_dpair_rel(const rgnn_graph_s* g) {
   return {"dpair_rel", std::vector<int64_t>(g->dpair_rel_ptr_h.begin(), g->dpair_rel_ptr_h.end()), {}};
 }
 
+// A destination-partitioned graph (multi-GPU) owns the rows [dst_lo, dst_hi): its
+// destination-side node work (HGT Q and its gradients, the RGCN self-loop, the HGT tail) runs on
+// those rows only.
+bool partitioned(const rgnn_graph_s* g) { return g->dst_lo != 0 || g->dst_hi != g->N; }
+Segs seg_node_type_own(const rgnn_graph_s* g) {
+  if (!partitioned(g)) return seg_node_type(g);
+  std::vector<int64_t> p(g->node_type_ptr);
+  for (auto& x : p) x = std::min(std::max(x, g->dst_lo), g->dst_hi);
+  return {"node_type_own", p, {}};
+}
+Segs seg_own_nodes(const rgnn_graph_s* g) {
+  if (!partitioned(g)) return seg_all_nodes(g);
+  return {"own_nodes", {g->dst_lo, g->dst_hi}, {0}};
+}
+
+// The pairs of segmentation `sg` whose source lies in rank k's node rows (sources ascend within
+// every pair segment: pairs sort by (rel, src)); the gaps between the segments' sub-ranges are
+// segments of weight -1 (no tiles), so the tile plan covers exactly the chunk.
+Segs seg_chunk(rgnn_graph_s* g, const Segs& sg, const rgnn_comm_s* cm, int k) {
+  if (g->pair_src_h.size() != (size_t)g->U) {
+    g->pair_src_h.resize(g->U);
+    if (g->U)
+      RGNN_CUDA(cudaMemcpy(g->pair_src_h.data(), g->pair_src, g->U * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  const int64_t lo = cm->node_ptr[k], hi = cm->node_ptr[k + 1];
+  Segs out{sg.key + "/chunk" + std::to_string(k) + "of" + std::to_string(cm->world) + "@" + std::to_string(lo), {}, {}};
+  const int nseg = (int)sg.ptr.size() - 1;
+  const int32_t* ps = g->pair_src_h.data();
+  for (int i = 0; i < nseg; ++i) {
+    const int32_t* b = ps + sg.ptr[i];
+    const int32_t* e = ps + sg.ptr[i + 1];
+    const int64_t a0 = std::lower_bound(b, e, (int32_t)lo) - ps, a1 = std::lower_bound(b, e, (int32_t)hi) - ps;
+    if (!out.ptr.empty()) out.w.push_back(-1);  // gap up to this sub-range
+    out.ptr.push_back(a0);
+    out.ptr.push_back(a1);
+    out.w.push_back(sg.w.empty() ? i : sg.w[i]);
+  }
+  if (out.ptr.empty()) out.ptr = {0, 0}, out.w = {-1};
+  return out;
+}
+
 int64_t count_tiles(const Segs& sg, int rows) {
   int64_t n = 0;
   for (size_t i = 0; i + 1 < sg.ptr.size(); ++i) n += (sg.ptr[i + 1] - sg.ptr[i] + rows - 1) / rows;
@@ -60,6 +102,7 @@ struct Ctx {
   size_t esz;
   cudaStream_t s;
   int H = 1;  // attention heads (HGT; F2)
+  rgnn_comm_s* comm = nullptr;  // multi-GPU exchange (NULL on one GPU)
 };
 
 void check_desc(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
@@ -348,6 +391,35 @@ bool gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
   return false;
 }
 
+// The source-side pair GEMM.  With a communicator it runs chunk by chunk of source owners: the own
+// rows first (present at once), then each other owner's pairs after the event of that owner's
+// broadcast, so the all-gather of chunk k+1 overlaps the GEMM of chunk k.
+void pair_gemm(const Ctx& c, const Segs& sg, const GemmArgs& a) {
+  if (!c.comm) {
+    gemm(c, sg, a);
+    return;
+  }
+  for (int j = 0; j <= c.comm->world; ++j) {
+    const int k = j == 0 ? c.comm->rank : j - 1;
+    if (j > 0 && k == c.comm->rank) continue;
+    comm_wait_chunk(c.comm, k, c.s);
+    gemm(c, seg_chunk(c.g, sg, c.comm, k), a);
+  }
+}
+
+// dX[u] (+)= sum of the per-pair rows of source u, for every source row (pairs reach sources outside
+// the owned range).  Owned rows accumulate when `own_acc` (their node-side term was written first)
+// or are skipped when `skip_own` (a GEMM epilogue already added them); other rows are overwritten.
+void reduce_pair_rows(const Ctx& c, const void* rows, int K, float* dX, bool own_acc, bool skip_own = false) {
+  const rgnn_graph_s* g = c.g;
+  const int64_t lo = partitioned(g) ? g->dst_lo : 0, hi = partitioned(g) ? g->dst_hi : g->N;
+  if (lo > 0) seg_reduce_rows(lo, g->src_pair_ptr, g->src_pairs, rows, c.dt, K, dX, false, c.s);
+  if (!skip_own && hi > lo)
+    seg_reduce_rows(hi - lo, g->src_pair_ptr + lo, g->src_pairs, rows, c.dt, K, dX + lo * K, own_acc, c.s);
+  if (hi < g->N)
+    seg_reduce_rows(g->N - hi, g->src_pair_ptr + hi, g->src_pairs, rows, c.dt, K, dX + hi * K, false, c.s);
+}
+
 void do_wgrad(const Ctx& c, const Segs& sg, const void* A, int a_dt, int K1, const int32_t* gather, const void* Bm,
               int b_dt, int K2, float* out, int num_w, float* partial, const char* name) {
   WgradArgs w;
@@ -379,14 +451,14 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.B = w->W; a.b_dtype = c.dt; a.Y = sc.P; a.y_dtype = c.dt; a.N = c.D;
     a.num_w = g->R; a.bt_scratch = sc.bt;
     a.name = "gemm_pairs_fwd";
-    gemm(c, seg_pair_rel(g), a);
-    if (c.d->self_loop) {
+    if (c.d->self_loop) {  // owned rows only; first, while the other owners' rows are in flight
       GemmArgs b;
       b.A = X; b.a_dtype = c.dt; b.K = c.Din; b.B = w->W0; b.b_dtype = c.dt; b.Y = out; b.y_dtype = F32; b.N = c.D;
       b.num_w = 1; b.bt_scratch = sc.bt;
       b.name = "gemm_selfloop_fwd";
-      gemm(c, seg_all_nodes(g), b);
+      gemm(c, seg_own_nodes(g), b);
     }
+    pair_gemm(c, seg_pair_rel(g), a);
     float *cn = sc.csr_norm, *xn = sc.csc_norm;
     graph_norms(g, c.d->norm_kind, w->edge_norm, c.s, &cn, &xn);
     rgcn_fwd_traverse(g, c.dt, c.D, cn, sc.P, out, c.d->self_loop != 0, sc.pt, c.s);
@@ -414,7 +486,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
     a.dotvec = sv.a32; a.dotout = sv.spair;
     a.num_w = g->R; a.bt_scratch = sc.bt;
     a.name = "gemm_pairs_fwd";
-    gemm(c, seg_pair_rel(g), a);
+    pair_gemm(c, seg_pair_rel(g), a);
     rgat_fwd_traverse(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nr ? sv.te : nullptr, c.d->leaky_slope, out, sv.stats,
                       sc.pt, c.s);
   } else {
@@ -422,6 +494,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
                "HGT needs Wk, Wq, Wv, Watt, Wmsg, mu");
     if (hgt_nr(c.d)) {
       // reordering off: [K|V] = X [Wk|Wv]_type per node, then [K~|M] = [K|V][src] blockdiag(.)_rel per pair
+      if (c.comm) comm_wait_all(c.comm, c.s);  // every node's K, V (source side)
       hgt_nr_weights(g->R, g->T, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.Wkv, sv.Bd, c.s);
       GemmArgs k;
       k.A = X; k.a_dtype = c.dt; k.K = c.Din; k.B = sv.Wkv; k.b_dtype = c.dt; k.Y = sv.KV; k.y_dtype = c.dt;
@@ -442,24 +515,32 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
       a.Y = sv.P; a.y_dtype = c.dt; a.N = 2 * c.D;
       a.num_w = std::max(g->n_act, 1); a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_fwd";
-      gemm(c, seg_pair_rt(g), a);
+      GemmArgs q;  // Q of the owned destinations: first, it needs only this rank's rows of X
+      q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
+      q.num_w = g->T; q.bt_scratch = sc.bt;
+      q.name = "gemm_nodes_fwd";
+      gemm(c, seg_node_type_own(g), q);
+      pair_gemm(c, seg_pair_rt(g), a);
     }
-    GemmArgs q;
-    q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
-    q.num_w = g->T; q.bt_scratch = sc.bt;
-    q.name = "gemm_nodes_fwd";
-    gemm(c, seg_node_type(g), q);
+    if (hgt_nr(c.d)) {
+      GemmArgs q;
+      q.A = X; q.a_dtype = c.dt; q.K = c.Din; q.B = w->Wq; q.b_dtype = c.dt; q.Y = sv.Q; q.y_dtype = c.dt; q.N = c.D;
+      q.num_w = g->T; q.bt_scratch = sc.bt;
+      q.name = "gemm_nodes_fwd";
+      gemm(c, seg_node_type_own(g), q);
+    }
     float* h = c.d->hgt_tail ? sv.H32 : out;
     hgt_fwd_traverse(g, c.dt, c.D, c.H, sv.P, sv.Q, h, sv.stats, sc.pt, c.s);
     if (c.d->hgt_tail) {  // out = GELU(h) A_type + X  (F2, reading b12)
       RGNN_CHECK(w->A, RGNN_ERR_INVALID_ARG, "hgt_tail needs weights.A");
-      gelu_fwd((int64_t)g->N * c.D, h, sv.GH, c.dt, c.s);
+      const int64_t o0 = g->dst_lo * c.D, on = (g->dst_hi - g->dst_lo) * c.D;  // owned rows
+      gelu_fwd(on, h + o0, static_cast<char*>(sv.GH) + o0 * c.esz, c.dt, c.s);
       GemmArgs t;
       t.A = sv.GH; t.a_dtype = c.dt; t.K = c.D; t.B = w->A; t.b_dtype = c.dt; t.Y = out; t.y_dtype = F32; t.N = c.D;
       t.num_w = g->T; t.bt_scratch = sc.bt;
       t.name = "tail_gemm_fwd";
-      gemm(c, seg_node_type(g), t);
-      add_dt((int64_t)g->N * c.D, X, c.dt, out, c.s);
+      gemm(c, seg_node_type_own(g), t);
+      add_dt(on, static_cast<const char*>(X) + o0 * c.esz, c.dt, out + o0, c.s);
     }
   }
 }
@@ -484,21 +565,25 @@ void hgt_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const S
   }
   const void* dKV = c.dt == BF16 ? sc.dKVdt : (const void*)sc.dKV32;
   if (dX) {
-    GemmArgs q;
-    q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
-    q.Y = dX; q.y_dtype = F32; q.N = c.Din;
-    q.num_w = g->T; q.bt_scratch = sc.bt;
-    q.name = "gemm_nodes_dx";
-    gemm(c, seg_node_type(g), q);
+    // source side (every node): dX = d[K|V] [Wk|Wv]^T; then the owned rows add dQ Wq^T
     GemmArgs k;
     k.A = dKV; k.a_dtype = c.dt; k.K = 2 * c.D; k.B = sv.Wkv; k.b_dtype = c.dt; k.transB = true;
-    k.Y = sc.dXkv; k.y_dtype = F32; k.N = c.Din;
+    k.Y = dX; k.y_dtype = F32; k.N = c.Din;
     k.num_w = g->T; k.bt_scratch = sc.bt;
     k.name = "gemm_nodes_dkv_dx";
     gemm(c, seg_node_type(g), k);
-    add_f32((int64_t)g->N * c.Din, sc.dXkv, dX, c.s);
+    GemmArgs q;
+    q.A = sc.dQ; q.a_dtype = c.dt; q.K = c.D; q.B = w->Wq; q.b_dtype = c.dt; q.transB = true;
+    q.Y = sc.dXkv; q.y_dtype = F32; q.N = c.Din;
+    q.num_w = g->T; q.bt_scratch = sc.bt;
+    q.name = "gemm_nodes_dx";
+    gemm(c, seg_node_type_own(g), q);
+    const int64_t o0 = g->dst_lo * c.Din;
+    add_f32((g->dst_hi - g->dst_lo) * c.Din, sc.dXkv + o0, dX + o0, c.s);
   }
-  if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
+  if (dW->dWq)
+    do_wgrad(c, seg_node_type_own(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial,
+             "wgrad_nodes");
   const bool need_bd = dW->dWatt || dW->dWmsg, need_wkv = dW->dWk || dW->dWv;
   if (need_bd)
     do_wgrad(c, seg_pair_rel(g), sv.KV, c.dt, 2 * c.D, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dBd, g->R, sc.partial,
@@ -567,8 +652,9 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     // upstream gradient in the table dtype: bf16 copy on the bf16 path (gathered per edge and the
     // A operand of the self-loop tcgen05 GEMMs), G itself on the fp32 path
     const void* Gt = G;
-    if (c.dt == BF16) {
-      convert_dt((int64_t)g->N * c.D, G, sc.Gt, BF16, c.s);
+    if (c.dt == BF16) {  // owned rows: the only rows of G the layer reads
+      const int64_t o0 = g->dst_lo * c.D;
+      convert_dt((g->dst_hi - g->dst_lo) * c.D, G + o0, static_cast<char*>(sc.Gt) + o0 * c.esz, BF16, c.s);
       Gt = sc.Gt;
     }
     rgcn_bwd_pair(g, c.dt, c.D, xn, Gt, sc.dP, sc.pt, c.s);
@@ -587,14 +673,14 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
         b.Y = dX; b.y_dtype = F32; b.N = c.Din;
         b.num_w = 1; b.bt_scratch = sc.bt;
         b.name = "gemm_selfloop_dx";
-        gemm(c, seg_all_nodes(g), b);
+        gemm(c, seg_own_nodes(g), b);
       }
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, c.d->self_loop != 0, c.s);
+      reduce_pair_rows(c, sc.dXp, c.Din, dX, c.d->self_loop != 0);
     }
     if (dW->dW && !fused)
       do_wgrad(c, seg_pair_rel(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, c.D, dW->dW, g->R, sc.partial, "wgrad_pairs");
     if (dW->dW0 && c.d->self_loop)
-      do_wgrad(c, seg_all_nodes(g), X, c.dt, c.Din, nullptr, Gt, c.dt, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
+      do_wgrad(c, seg_own_nodes(g), X, c.dt, c.Din, nullptr, Gt, c.dt, c.D, dW->dW0, 1, sc.partial, "wgrad_selfloop");
   } else if (model == RGNN_RGAT && rgat_nr(c.d)) {
     rgat_backward_nr(c, X, w, out, sv, G, dX, dW, sc);
   } else if (model == RGNN_RGAT) {
@@ -613,7 +699,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       a.num_w = g->R; a.bt_scratch = sc.bt;
       a.name = "gemm_pairs_dx";
       if (!fused) gemm(c, seg_pair_rel(g), a);
-      seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
+      reduce_pair_rows(c, sc.dXp, c.Din, dX, true);  // owned rows hold the t-path term of the dst pass
     }
     if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
       const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
@@ -658,10 +744,12 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       if (fuse_pair_reduce(g)) {
         q.red_ptr = g->src_pair_ptr; q.red_list = g->src_pairs; q.red_rows = sc.dXp; q.red_dtype = c.dt;
       }
-      if (!gemm(c, seg_node_type(g), q) || q.red_ptr == nullptr)
-        seg_reduce_rows(g->N, g->src_pair_ptr, g->src_pairs, sc.dXp, c.dt, c.Din, dX, true, c.s);
+      const bool reduced_own = gemm(c, seg_node_type_own(g), q) && q.red_ptr != nullptr;
+      reduce_pair_rows(c, sc.dXp, c.Din, dX, true, reduced_own);
     }
-    if (dW->dWq) do_wgrad(c, seg_node_type(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial, "wgrad_nodes");
+    if (dW->dWq)
+      do_wgrad(c, seg_node_type_own(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial,
+               "wgrad_nodes");
     if (needF) {
       if (!fused)
         do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1),
@@ -678,10 +766,10 @@ void tail_backward(const Ctx& c, const void* X, const rgnn_weights* w, const Sav
                    const rgnn_weight_grads* dW, const BwdScratch& sc) {
   rgnn_graph_s* g = c.g;
   RGNN_CHECK(w->A, RGNN_ERR_INVALID_ARG, "hgt_tail needs weights.A");
-  const int64_t n = (int64_t)g->N * c.D;
+  const int64_t o0 = g->dst_lo * c.D, n = (g->dst_hi - g->dst_lo) * c.D;  // owned rows
   const void* Gt = dout;
   if (c.dt == BF16) {
-    convert_dt(n, dout, sc.Gdt, BF16, c.s);
+    convert_dt(n, dout + o0, static_cast<char*>(sc.Gdt) + o0 * c.esz, BF16, c.s);
     Gt = sc.Gdt;
   }
   GemmArgs t;
@@ -689,19 +777,47 @@ void tail_backward(const Ctx& c, const void* X, const rgnn_weights* w, const Sav
   t.Y = sc.dH; t.y_dtype = F32; t.N = c.D;
   t.num_w = g->T; t.bt_scratch = sc.bt;
   t.name = "tail_gemm_dx";
-  gemm(c, seg_node_type(g), t);
-  gelu_bwd(n, sv.H32, sc.dH, c.s);
+  gemm(c, seg_node_type_own(g), t);
+  gelu_bwd(n, sv.H32 + o0, sc.dH + o0, c.s);
   backward(c, X, w, sv.H32, sv, sc.dH, dX, dW, sc);
-  if (dX) add_f32(n, dout, dX, c.s);
+  if (dX) add_f32(n, dout + o0, dX + o0, c.s);  // residual (d_in == d_out)
   if (dW && dW->dA)
-    do_wgrad(c, seg_node_type(g), sv.GH, c.dt, c.D, nullptr, Gt, c.dt, c.D, dW->dA, g->T, sc.partial, "tail_wgrad");
+    do_wgrad(c, seg_node_type_own(g), sv.GH, c.dt, c.D, nullptr, Gt, c.dt, c.D, dW->dA, g->T, sc.partial,
+             "tail_wgrad");
 }
 
-Ctx make_ctx(rgnn_graph_s* g, const rgnn_layer_desc* d, void* stream) {
+Ctx make_ctx(rgnn_graph_s* g, const rgnn_layer_desc* d, void* stream, rgnn_comm_s* comm = nullptr) {
   check_desc(g, d);
   Ctx c{g, d, d->dtype, d->d_out, d->d_in, d->dtype == F32 ? (size_t)4 : (size_t)2,
-        static_cast<cudaStream_t>(stream), d->num_heads <= 1 ? 1 : d->num_heads};
+        static_cast<cudaStream_t>(stream), d->num_heads <= 1 ? 1 : d->num_heads, comm};
+  if (comm) {
+    RGNN_CHECK((int64_t)comm->node_ptr.size() == comm->world + 1 && comm->node_ptr[comm->world] == g->N,
+               RGNN_ERR_INVALID_ARG, "communicator node_ptr[world] != the graph's number of nodes");
+    RGNN_CHECK(comm->node_ptr[comm->rank] == g->dst_lo && comm->node_ptr[comm->rank + 1] == g->dst_hi,
+               RGNN_ERR_INVALID_ARG, "the graph's destination range differs from the communicator's rows of this rank");
+  }
   return c;
+}
+
+// every requested weight gradient with its element count (the backward's all-reduce list)
+std::vector<std::pair<float*, size_t>> grad_list(const Ctx& c, const rgnn_weight_grads* dW) {
+  std::vector<std::pair<float*, size_t>> v;
+  if (!dW) return v;
+  const size_t R = c.g->R, T = c.g->T, Din = c.Din, D = c.D;
+  v.push_back({dW->dW, R * Din * D});
+  v.push_back({c.d->self_loop ? dW->dW0 : nullptr, Din * D});
+  v.push_back({dW->da, R * D});
+  v.push_back({dW->db, R * D});
+  v.push_back({dW->dWk, T * Din * D});
+  v.push_back({dW->dWq, T * Din * D});
+  v.push_back({dW->dWv, T * Din * D});
+  v.push_back({dW->dWatt, R * D * D});
+  v.push_back({dW->dWmsg, R * D * D});
+  v.push_back({c.d->hgt_tail ? dW->dA : nullptr, T * D * D});
+  if (c.d->model == RGNN_RGCN) v.resize(2);
+  else if (c.d->model == RGNN_RGAT) v = {v[0], v[2], v[3]};
+  else v = {v[4], v[5], v[6], v[7], v[8], v[9]};
+  return v;
 }
 
 }  // namespace
@@ -732,9 +848,9 @@ rgnn_status rgnn_layer_workspace(rgnn_graph_t g, const rgnn_layer_desc* d, size_
 }
 
 rgnn_status rgnn_layer_forward(rgnn_graph_t g, const rgnn_layer_desc* d, const void* X, const rgnn_weights* w,
-                               float* out, void* saved, void* scratch, void* stream) {
+                               float* out, void* saved, void* scratch, rgnn_comm_t comm, void* stream) {
   return guarded([&] {
-    Ctx c = make_ctx(g, d, stream);
+    Ctx c = make_ctx(g, d, stream, comm);
     RGNN_CHECK(X && w && out && saved && scratch, RGNN_ERR_INVALID_ARG, "NULL argument");
     size_t sb = 0, xb = 0;
     RGNN_CHECK(rgnn_layer_workspace(g, d, &sb, &xb) == RGNN_OK, RGNN_ERR_INVALID_ARG, "workspace query failed");
@@ -744,15 +860,18 @@ rgnn_status rgnn_layer_forward(rgnn_graph_t g, const rgnn_layer_desc* d, const v
     Arena f{static_cast<char*>(scratch), xb};
     FwdScratch fs;
     layout_fwd_scratch(c, f, fs);
+    if (comm)  // in-place all-gather of X by owner chunks, overlapped with the pair GEMM (pair_gemm)
+      comm_allgather_rows_begin(comm, const_cast<void*>(X), (size_t)c.Din * c.esz, c.s);
     forward(c, X, w, out, sv, fs);
+    if (comm) comm_wait_all(comm, c.s);  // X complete on return (the backward reads it)
   });
 }
 
 rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* d, const void* X, const rgnn_weights* w,
                                 const float* out, const void* saved, const float* dout, float* dX,
-                                const rgnn_weight_grads* dW, void* scratch, void* stream) {
+                                const rgnn_weight_grads* dW, void* scratch, rgnn_comm_t comm, void* stream) {
   return guarded([&] {
-    Ctx c = make_ctx(g, d, stream);
+    Ctx c = make_ctx(g, d, stream, comm);
     RGNN_CHECK(X && w && saved && dout && scratch, RGNN_ERR_INVALID_ARG, "NULL argument");
     RGNN_CHECK(d->model == RGNN_RGCN || out, RGNN_ERR_INVALID_ARG, "RGAT/HGT backward needs the forward output");
     size_t sb = 0, xb = 0;
@@ -768,7 +887,20 @@ rgnn_status rgnn_layer_backward(rgnn_graph_t g, const rgnn_layer_desc* d, const 
     } else {
       backward(c, X, w, out, sv, dout, dX, dW, bs);
     }
+    if (comm) comm_reduce_grads(comm, dX, c.Din, grad_list(c, dW), c.s);
   });
 }
 
 }  // extern "C"
+
+extern "C" rgnn_status rgnn_comm_exchange_bytes(const rgnn_layer_desc* d, int64_t num_nodes, int64_t num_pairs_global,
+                                                int64_t* bytes_x, int64_t* bytes_p, int32_t* variant) {
+  return guarded([&] {
+    RGNN_CHECK(d && bytes_x && bytes_p && variant && num_nodes >= 0 && num_pairs_global >= 0, RGNN_ERR_INVALID_ARG,
+               "bad argument");
+    const int64_t b = d->dtype == RGNN_BF16 ? 2 : 4, k = d->model == RGNN_HGT ? 2 : 1;
+    *bytes_x = num_nodes * d->d_in * b;
+    *bytes_p = num_pairs_global * k * d->d_out * b;
+    *variant = 0;  // X (the only variant implemented; the smaller one whenever U_global * k * d_out >= N * d_in)
+  });
+}

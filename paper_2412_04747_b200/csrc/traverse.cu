@@ -643,8 +643,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       float gv[V], ov[V], q[V];
       qr[k] = ldg16(Q + v * D + c * V);
       ld_f32<V>(Gr + v * D + c * V, gv);
-      round_tp<TP, V>(gv);
-    round_tp<TP, V>(gv);  // G_v in the table precision everywhere (dalpha and the row term G_v . out_v)
+      round_tp<TP, V>(gv);  // G_v in the table precision everywhere (dalpha and the row term G_v . out_v)
       ld_f32<V>(out + v * D + c * V, ov);
       float x = 0.f;
 #pragma unroll
@@ -1471,6 +1470,161 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t 
   }
 }
 
+// ------------------------------------------------------------------ gather-ring pair pass (HGT A7)
+// The pair-major pass as an edge stream: one lane group walks a chunk of the src-CSC (a contiguous
+// run of whole pairs, WorkPlan::chunks) edge by edge, and every gathered node record ([G_d | Q_d]
+// and the (lse_d, G_d . out_d) record) travels global -> shared memory by cp.async into a
+// lane-private S-stage ring, issued S-1 edges ahead of its use.  Only the issuing lane reads a slot
+// (wait_group, no barrier), so the in-flight gathers cost no registers: S-1 edges per group are
+// outstanding at all times, across pair boundaries (short pairs no longer drain the pipeline).  The
+// destination and pair ids of the next LPR edges arrive as one coalesced load per group (lane c holds
+// edge base + c) and are shuffled to the issuing step; the pair's K~_p / M_p ride in the stage of its
+// first edge.  Per pair: dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d (as k_hgt_bwd_pair), written
+// when the stream leaves the pair (heavy pairs: their split chunk's fp32 partial into its slot).
+__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ float2 lds8(const float2* p) {
+  float2 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
+struct RingStage {  // one lane's slice of one gathered edge (80 B)
+  uint4 g, q, k, m;
+  float2 ns, pad;
+};
+
+#ifndef RGNN_RING_S
+#define RGNN_RING_S 4
+#endif
+constexpr int RING_TB = 128;
+
+template <class TP, int D, int H, int S>
+__global__ void __launch_bounds__(RING_TB) k_hgt_bwd_pair_ring(int64_t nch, const int4* __restrict__ chunks,
+                                                               float* __restrict__ pacc,
+                                                               const int32_t* __restrict__ csc_dst,
+                                                               const int32_t* __restrict__ csc_pair,
+                                                               const TP* __restrict__ KM, const TP* __restrict__ GQ,
+                                                               const float4* __restrict__ nst, TP* __restrict__ dKM) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H;
+  __shared__ RingStage ring[S][RING_TB];
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR, hd = c / LH;
+  const int64_t gid = ((blockIdx.x * (int64_t)RING_TB + threadIdx.x) >> 5) * EG + g;
+  if (((blockIdx.x * (int64_t)RING_TB + threadIdx.x) >> 5) * EG >= nch) return;  // whole warp idle
+  const int4 ch = gid < nch ? chunks[gid] : make_int4(0, 0, -1, 0);
+  const int a = ch.x, L = ch.y - ch.x, slot = ch.z;
+  const int span = __reduce_max_sync(0xffffffffu, L);
+  const int src0 = g * LPR;  // first lane of this group
+  // ids of the edges [base, base + LPR) of the stream: lane c holds edge base + c
+  int d_cur, p_cur, d_nxt, p_nxt;
+  auto ld_ids = [&](int base, int& dd, int& pp) {
+    const int i = base + c;
+    dd = i < L ? __ldg(csc_dst + a + i) : 0;
+    pp = i < L ? __ldg(csc_pair + a + i) : -1;
+  };
+  ld_ids(0, d_cur, p_cur);
+  ld_ids(LPR, d_nxt, p_nxt);
+  int last_issued = -1;
+  int rp[S];      // pair id of the edge in each stage (-2: past the end)
+  bool rf[S];     // the edge is its pair's first in this stream
+#pragma unroll
+  for (int i = 0; i < S; ++i) rp[i] = -2, rf[i] = false;
+  RingStage* const my = &ring[0][threadIdx.x];
+  // issue edge q of the stream into stage st
+  auto issue = [&](int q, int st) {
+    if (q > 0 && q % LPR == 0) {  // warp-uniform: next id batch
+      d_cur = d_nxt;
+      p_cur = p_nxt;
+      ld_ids(q + LPR, d_nxt, p_nxt);
+    }
+    const int d = __shfl_sync(0xffffffffu, d_cur, src0 + q % LPR);
+    const int pp = __shfl_sync(0xffffffffu, p_cur, src0 + q % LPR);
+    const bool valid = q < L;
+    const bool first = valid && pp != last_issued;
+    RingStage* sl = my + st * RING_TB;
+    if (valid) {
+      const TP* gq = GQ + (int64_t)d * 2 * D + c * V;
+      cp_async16_ca(&sl->g, gq);
+      cp_async16_ca(&sl->q, gq + D);
+      cp_async8_ca(&sl->ns, nst + (int64_t)d * H + hd);
+      if (first) {
+        const TP* km = KM + (int64_t)pp * 2 * D + c * V;
+        cp_async16_ca(&sl->k, km);
+        cp_async16_ca(&sl->m, km + D);
+      }
+      last_issued = pp;
+    }
+    cp_async_commit();
+    rp[st] = valid ? pp : -2;
+    rf[st] = first;
+  };
+#pragma unroll
+  for (int q = 0; q < S - 1; ++q) issue(q, q);
+  uint4 kpk = make_uint4(0, 0, 0, 0), mpk = kpk;
+  float ak[V], am[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
+  for (int q0 = 0; q0 < span; q0 += S) {
+#pragma unroll
+    for (int st = 0; st < S; ++st) {
+      const int q = q0 + st;
+      issue(q + S - 1, (st + S - 1) % S);
+      cp_async_wait<S - 1>();  // stage st (edge q) has landed for this lane
+      const RingStage* sl = my + st * RING_TB;
+      const bool valid = rp[st] != -2;
+      if (rf[st]) {
+        kpk = lds16(&sl->k);
+        mpk = lds16(&sl->m);
+      }
+      float gr[V], qv[V], x[V];
+      cvt16<TP>(valid ? lds16(&sl->g) : make_uint4(0, 0, 0, 0), gr);
+      cvt16<TP>(valid ? lds16(&sl->q) : make_uint4(0, 0, 0, 0), qv);
+      const float2 ns = valid ? lds8(&sl->ns) : make_float2(CUDART_INF_F, 0.f);
+      float l = 0.f, da = 0.f;
+      cvt16<TP>(kpk, x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) l = fmaf(x[k], qv[k], l);
+      cvt16<TP>(mpk, x);
+#pragma unroll
+      for (int k = 0; k < V; ++k) da = fmaf(gr[k], x[k], da);
+      l = gsum<LH>(l, 0xffffffffu);
+      da = gsum<LH>(da, 0xffffffffu);
+      const float alpha = __expf(l - ns.x);  // 0 past the end (lse = +inf)
+      const float dl = alpha * (da - ns.y);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        ak[k] = fmaf(dl, qv[k], ak[k]);
+        am[k] = fmaf(alpha, gr[k], am[k]);
+      }
+      if (valid && rp[(st + 1) % S] != rp[st]) {  // the stream leaves pair rp[st]: write its rows
+        if (slot >= 0) {
+          float* o = pacc + (int64_t)slot * 2 * D;
+          st_f32<V>(o + c * V, ak);
+          st_f32<V>(o + D + c * V, am);
+        } else {
+          TP* o = dKM + (int64_t)rp[st] * 2 * D;
+          st_tp<V>(o + c * V, ak);
+          st_tp<V>(o + D + c * V, am);
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ heavy-id merges
 // One CTA per heavy id: warp w folds chunks w, w+8, ... of the id (lane c owns columns 4c..4c+3
 // of a W-wide row, looping over W in steps of 128); the 8 warp results are then combined in warp
@@ -1849,8 +2003,38 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
   });
 }
 
+// RGNN_RING=0 selects the work-plan pair kernels (warp / staged group / short) instead of the gather ring
+inline bool use_ring() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_RING");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   void* dKM, bool skip_single, const Partial& pt, cudaStream_t s) {
+  if (use_ring()) {
+    const int64_t nch = skip_single ? g->pairs.n_chunks_multi : g->pairs.n_chunks;
+    const int4* ch = skip_single ? g->pairs.chunks_multi : g->pairs.chunks;
+    by_width(D, [&](auto Dc) {
+      constexpr int DD = decltype(Dc)::value;
+      by_dtype(dtype, [&](auto* tp) {
+        using TP = std::remove_pointer_t<decltype(tp)>;
+        constexpr int LPR = Geo<TP, DD>::LPR;
+        by_heads<LPR>(H, [&](auto hc) {
+          constexpr int HH = decltype(hc)::value;
+          launch("hgt_bwd_pair", k_hgt_bwd_pair_ring<TP, DD, HH, RGNN_RING_S>,
+                 dim3(ceil_div(ceil_div(nch, 32 / LPR) * (int64_t)32, RING_TB)), dim3(RING_TB), 0, s, nch, ch,
+                 pt.acc, (const int32_t*)g->csc_dst, (const int32_t*)g->csc_pair, static_cast<const TP*>(KM),
+                 static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
+        });
+        launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
+               g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
+      });
+    });
+    return;
+  }
   WorkPlan wp = g->pairs;  // single-edge pairs were resolved by the destination-major pass
   if (skip_single) {
     wp.n_items = wp.n_multi;

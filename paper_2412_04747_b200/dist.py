@@ -1,18 +1,19 @@
-"""Destination-partitioned multi-GPU layer; host logic + torch.distributed plumbing.
+"""Destination-partitioned multi-GPU layer: host logic + torch.distributed plumbing.
 
-Partition: rank k owns the destination range [lo_k, hi_k), chosen so every rank
-receives about E / P in-edges (contiguous prefix over the in-degree counts).  It
-builds the graph of the in-edges of its range (rgnn_graph_build with dst_lo/dst_hi),
-so every destination-side step (logits, softmax, aggregation) is local.  The same
-ranges partition the source rows of X: rank k owns X[lo_k:hi_k].
+Partition: rank k owns the node rows [lo_k, hi_k), chosen so every rank receives about E / P
+in-edges (contiguous prefix over the in-degree counts).  It builds the graph of the in-edges of
+its range (rgnn_graph_build with dst_lo/dst_hi), so every destination-side step (logits, softmax,
+aggregation, Q, the self-loop) is local, and the same ranges partition the rows of X, out and dX.
 
-Exchange (variant X of §8(e)):
-  forward   X_full = all_gather(X_own)                    (NCCL over NVLink)
-  backward  the loss decomposes over destinations, so each rank back-propagates
-            G masked to its own rows; dX_own = reduce_scatter(dX_partial) and
-            dW = all_reduce(dW_partial).
-Exactness of the decomposition is the property pinned by
-tests/test_oracle_layers.py::test_destination_decomposition.
+The exchange itself is library-owned (include/rgnn.h "communicator"): `make_comm` shares one
+NCCL unique id over the torch process group (the only use of torch.distributed on the data path
+is this bootstrap) and creates the rgnn communicator; rgnn_layer_forward then all-gathers X in
+owner chunks on the library's stream, overlapped with the pair GEMM, and rgnn_layer_backward
+reduces dX onto the owners and all-reduces the weight gradients.
+
+`allgather_rows_reference` / `reduce_rows_reference` restate that exchange schedule with
+torch.distributed (one broadcast / reduce per owner, in place) for the world-size-2 gloo tests
+on CPU, which check that the per-rank decomposition reproduces the single-process oracle.
 """
 from __future__ import annotations
 
@@ -41,42 +42,60 @@ def partition_ranges(dst: np.ndarray, num_nodes: int, world: int) -> List[Tuple[
     return [(cuts[k], cuts[k + 1]) for k in range(world)]
 
 
-def pad_ranges(ranges: Sequence[Tuple[int, int]]) -> int:
-    """Row count each rank contributes to the fixed-size collectives (max range length)."""
-    return max(hi - lo for lo, hi in ranges)
+def node_ptr(ranges: Sequence[Tuple[int, int]]) -> List[int]:
+    """[world+1] row boundaries of contiguous ranges (rgnn_comm_create's node_ptr)."""
+    out = [int(ranges[0][0])] + [int(hi) for _, hi in ranges]
+    if out[0] != 0 or any(ranges[k][1] != ranges[k + 1][0] for k in range(len(ranges) - 1)):
+        raise ValueError("ranges must be contiguous and start at 0")
+    return out
 
 
-def all_gather_rows(local: torch.Tensor, ranges, rank: int, group=None) -> torch.Tensor:
-    """Concatenate the owned row blocks of every rank (variable sizes, padded collective)."""
-    world = len(ranges)
-    m = pad_ranges(ranges)
-    buf = torch.zeros((m,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    buf[: local.shape[0]] = local
-    out = torch.empty((world * m,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
-    return torch.cat([out[k * m: k * m + (hi - lo)] for k, (lo, hi) in enumerate(ranges)], dim=0)
+def share_unique_id(make_id, group=None) -> bytes:
+    """Rank 0 draws the id (make_id()), every rank returns the same bytes (torch.distributed
+    broadcast of a byte tensor; works over gloo and nccl process groups)."""
+    rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    raw = make_id() if rank == 0 else None
+    n = torch.tensor([len(raw) if raw is not None else 0], dtype=torch.int64, device=dev)
+    dist.broadcast(n, src=0, group=group)
+    buf = torch.zeros(int(n.item()), dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.cpu().numpy().tobytes())
 
 
-def reduce_scatter_rows(full: torch.Tensor, ranges, rank: int, group=None) -> torch.Tensor:
-    """Sum the full-size partial over ranks and return the owned rows of this rank."""
-    world = len(ranges)
-    m = pad_ranges(ranges)
-    send = torch.zeros((world * m,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+def make_comm(ranges: Sequence[Tuple[int, int]], group=None):
+    """The library communicator of this rank for the given row partition (collective)."""
+    from .rgnn import Comm, comm_unique_id
+    uid = share_unique_id(comm_unique_id, group)
+    return Comm(dist.get_rank(group), dist.get_world_size(group), node_ptr(ranges), uid)
+
+
+# ----------------------------------------------------------------- CPU restatement (gloo tests)
+def allgather_rows_reference(rows: torch.Tensor, ranges, group=None) -> None:
+    """In-place all-gather by owner: the rows of each rank are broadcast from it (the library's
+    forward schedule, one broadcast per owner)."""
     for k, (lo, hi) in enumerate(ranges):
-        send[k * m: k * m + (hi - lo)] = full[lo:hi]
-    recv = torch.empty((m,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
-    dist.reduce_scatter_tensor(recv, send, group=group)
-    lo, hi = ranges[rank]
-    return recv[: hi - lo]
+        if hi > lo:
+            chunk = rows[lo:hi].contiguous()
+            dist.broadcast(chunk, src=k, group=group)
+            rows[lo:hi] = chunk
+
+
+def reduce_rows_reference(partial: torch.Tensor, ranges, group=None) -> None:
+    """In-place reduce onto the owners: after the call rank k's rows [lo_k, hi_k) hold the sum over
+    ranks (the library's backward schedule, one reduce per owner)."""
+    for k, (lo, hi) in enumerate(ranges):
+        if hi > lo:
+            chunk = partial[lo:hi].contiguous()
+            dist.reduce(chunk, dst=k, group=group)
+            if dist.get_rank(group) == k:
+                partial[lo:hi] = chunk
 
 
 def all_reduce_grads(grads: Dict[str, torch.Tensor], keys, group=None) -> None:
     for k in keys:
         if k in grads:
             dist.all_reduce(grads[k], group=group)
-
-
-def masked_rows(G: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
-    Gm = torch.zeros_like(G)
-    Gm[lo:hi] = G[lo:hi]
-    return Gm

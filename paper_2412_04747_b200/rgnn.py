@@ -31,7 +31,9 @@ EXPORTED = ["rgnn_last_error", "rgnn_version", "rgnn_graph_build", "rgnn_graph_b
             "rgnn_layer_backward", "rgnn_profile_enable", "rgnn_profile_reset", "rgnn_profile_read",
             "rgnn_launch_count", "rgnn_segment_plan_create", "rgnn_segment_plan_destroy",
             "rgnn_segment_gemm_workspace", "rgnn_segment_gemm", "rgnn_relu_forward", "rgnn_relu_backward",
-            "rgnn_nll_loss_workspace", "rgnn_nll_loss", "rgnn_sgd_update"]
+            "rgnn_nll_loss_workspace", "rgnn_nll_loss", "rgnn_sgd_update", "rgnn_comm_unique_id", "rgnn_comm_create",
+            "rgnn_comm_destroy", "rgnn_comm_info", "rgnn_comm_exchange_bytes"]
+COMM_ID_BYTES = 128
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -108,10 +110,16 @@ def lib() -> C.CDLL:
         L.rgnn_layer_workspace.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.POINTER(C.c_size_t),
                                            C.POINTER(C.c_size_t)]
         L.rgnn_layer_forward.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.c_void_p, C.POINTER(WeightsC),
-                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.rgnn_layer_backward.argtypes = [C.c_void_p, C.POINTER(LayerDescC), C.c_void_p, C.POINTER(WeightsC),
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GradsC),
-                                          C.c_void_p, C.c_void_p]
+                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        L.rgnn_comm_unique_id.argtypes = [C.c_void_p]
+        L.rgnn_comm_create.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]
+        L.rgnn_comm_destroy.argtypes = [C.c_void_p]
+        L.rgnn_comm_info.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.rgnn_comm_exchange_bytes.argtypes = [C.POINTER(LayerDescC), C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                                               C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         L.rgnn_segment_plan_create.argtypes = [C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32), ALLOC_FN,
                                                FREE_FN, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
         L.rgnn_segment_plan_destroy.argtypes = [C.c_void_p]
@@ -142,13 +150,15 @@ def _stream(stream: Optional[torch.cuda.Stream] = None) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
-def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+def _ptr(t: Optional[torch.Tensor], align: int = 4) -> Optional[int]:
     if t is None:
         return None
     if not t.is_cuda:
         raise ValueError("expected a CUDA tensor")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
+    if t.data_ptr() % align:
+        raise ValueError(f"tensor data must be {align}-byte aligned (the kernels use vector loads)")
     return t.data_ptr()
 
 
@@ -205,6 +215,7 @@ class Graph:
                                            self._alloc.alloc_cb, self._alloc.free_cb, None, _stream(), C.byref(h)))
         self.handle = h
         self.node_type_ptr = [int(x) for x in node_type_ptr]
+        self.num_input_edges = e
 
     @classmethod
     def from_hetero(cls, g, dst_range=None, device="cuda", compact: bool = True) -> "Graph":
@@ -259,32 +270,76 @@ class Layer:
         self.n = graph.info()["num_nodes"]
         self.d_in, self.d_out = d_in, d_out
 
+    def weight_shapes(self) -> Dict[str, tuple]:
+        """Expected shape of every weight the model reads (include/rgnn.h rgnn_weights)."""
+        i = self.graph.info()
+        R, T, di, do = int(i["num_rels"]), int(i["num_node_types"]), self.d_in, self.d_out
+        if self.model == "rgcn":
+            sh = {"W": (R, di, do)}
+            if self.desc.self_loop:
+                sh["W0"] = (di, do)
+        elif self.model == "rgat":
+            sh = {"W": (R, di, do), "a": (R, do), "b": (R, do)}
+        else:
+            sh = {"Wk": (T, di, do), "Wq": (T, di, do), "Wv": (T, di, do), "Watt": (R, do, do),
+                  "Wmsg": (R, do, do), "mu": (R,)}
+            if self.desc.hgt_tail:
+                sh["A"] = (T, do, do)
+        return sh
+
     def _weights(self, w: Dict[str, torch.Tensor]) -> WeightsC:
+        """Check dtype, shape and 16-byte alignment of every weight before its pointer crosses
+        the C-ABI (the library takes raw pointers and cannot see a wrong shape)."""
         wc = WeightsC()
+        shapes = self.weight_shapes()
+        for f, want_shape in shapes.items():
+            if f == "mu" and w.get(f) is None:
+                continue  # NULL mu => mu_r = 1
+            if w.get(f) is None:
+                raise ValueError(f"{self.model} layer needs weight {f} of shape {want_shape}")
         for f in WEIGHT_FIELDS:
             t = w.get(f)
             if t is not None:
                 want = torch.float32 if f in ("mu", "edge_norm") else self.torch_dtype
                 if t.dtype != want:
                     raise TypeError(f"weight {f} must be {want}, got {t.dtype}")
-                setattr(wc, f, _ptr(t))
+                if f in shapes and tuple(t.shape) != shapes[f]:
+                    raise ValueError(f"weight {f} must have shape {shapes[f]}, got {tuple(t.shape)}")
+                if f == "edge_norm" and t.numel() != self.graph.num_input_edges:
+                    raise ValueError(f"edge_norm must have one value per input edge ({self.graph.num_input_edges})")
+                setattr(wc, f, _ptr(t, align=4 if f in ("mu", "edge_norm") else 16))
         return wc
 
-    def forward(self, X: torch.Tensor, w: Dict[str, torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        if X.dtype != self.torch_dtype:
-            raise TypeError(f"X must be {self.torch_dtype}")
+    def _rows(self, name: str, t: torch.Tensor, width: int, dtype: torch.dtype) -> None:
+        if t.dtype != dtype:
+            raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+        if tuple(t.shape) != (self.n, width):
+            raise ValueError(f"{name} must have shape ({self.n}, {width}), got {tuple(t.shape)}")
+
+    def forward(self, X: torch.Tensor, w: Dict[str, torch.Tensor], out: Optional[torch.Tensor] = None,
+                comm: Optional["Comm"] = None) -> torch.Tensor:
+        """out = layer(X).  With a communicator (multi-GPU), X is the full [N, d_in] buffer whose own
+        rows this rank filled; the library all-gathers the other rows into it (in place) and writes
+        the owned output rows."""
+        self._rows("X", X, self.d_in, self.torch_dtype)
         if out is None:
             out = torch.empty(self.n, self.d_out, dtype=torch.float32, device=X.device)
+        self._rows("out", out, self.d_out, torch.float32)
         self._wc = self._weights(w)
-        _check(lib().rgnn_layer_forward(self.graph.handle, C.byref(self.desc), _ptr(X), C.byref(self._wc), _ptr(out),
-                                        _ptr(self.saved), _ptr(self.scratch), _stream()))
+        _check(lib().rgnn_layer_forward(self.graph.handle, C.byref(self.desc), _ptr(X, 16), C.byref(self._wc),
+                                        _ptr(out, 16), _ptr(self.saved, 16), _ptr(self.scratch, 16),
+                                        comm.handle if comm is not None else None, _stream()))
         return out
 
     def backward(self, X: torch.Tensor, w: Dict[str, torch.Tensor], out: torch.Tensor, dout: torch.Tensor,
                  need_dX: bool = True, grads: Optional[Dict[str, torch.Tensor]] = None,
-                 need: Optional[list] = None) -> Dict[str, torch.Tensor]:
+                 need: Optional[list] = None, comm: Optional["Comm"] = None) -> Dict[str, torch.Tensor]:
         """Gradients of sum(out * dout).  `need` lists weight-gradient names to compute
-        (default: all for the model); missing ones are pruned."""
+        (default: all for the model); missing ones are pruned.  With a communicator the owned
+        rows of dX hold the full gradient and every weight gradient is summed over the ranks."""
+        self._rows("X", X, self.d_in, self.torch_dtype)
+        self._rows("out", out, self.d_out, torch.float32)
+        self._rows("dout", dout, self.d_out, torch.float32)
         wc = self._weights(w)
         shapes = {k: tuple(v.shape) for k, v in w.items() if v is not None and k not in ("mu", "edge_norm")}
         default = {"rgcn": ["dW", "dW0"] if self.desc.self_loop else ["dW"], "rgat": ["dW", "da", "db"],
@@ -295,13 +350,68 @@ class Layer:
         for name in need:
             if name not in grads:
                 grads[name] = torch.empty(shapes[name[1:]], dtype=torch.float32, device=X.device)
-            setattr(gc, name, _ptr(grads[name]))
+            g = grads[name]
+            if g.dtype != torch.float32 or tuple(g.shape) != shapes[name[1:]]:
+                raise ValueError(f"gradient {name} must be float32 of shape {shapes[name[1:]]}")
+            setattr(gc, name, _ptr(g, 16))
         if need_dX and "dX" not in grads:
             grads["dX"] = torch.empty(self.n, self.d_in, dtype=torch.float32, device=X.device)
-        _check(lib().rgnn_layer_backward(self.graph.handle, C.byref(self.desc), _ptr(X), C.byref(wc), _ptr(out),
-                                         _ptr(self.saved), _ptr(dout), _ptr(grads.get("dX")) if need_dX else None,
-                                         C.byref(gc), _ptr(self.scratch), _stream()))
+        if need_dX:
+            self._rows("dX", grads["dX"], self.d_in, torch.float32)
+        _check(lib().rgnn_layer_backward(self.graph.handle, C.byref(self.desc), _ptr(X, 16), C.byref(wc),
+                                         _ptr(out, 16), _ptr(self.saved, 16), _ptr(dout, 16),
+                                         _ptr(grads.get("dX"), 16) if need_dX else None, C.byref(gc),
+                                         _ptr(self.scratch, 16), comm.handle if comm is not None else None,
+                                         _stream()))
         return grads
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (rgnn_comm_unique_id) to be shared with the other ranks."""
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    _check(lib().rgnn_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """Library-owned NCCL communicator of one rank (rgnn_comm_create): the layer's multi-GPU exchange
+    (all-gather of X in owner chunks, reduce of dX onto the owners, all-reduce of dW) runs inside
+    rgnn_layer_forward / rgnn_layer_backward on the library's own stream.  node_ptr: [world+1] owned
+    node rows of every rank.  unique_id: the bytes of comm_unique_id() from one rank (share_unique_id)."""
+
+    def __init__(self, rank: int, world: int, node_ptr, unique_id: bytes):
+        if len(unique_id) != COMM_ID_BYTES:
+            raise ValueError(f"unique_id must be {COMM_ID_BYTES} bytes")
+        ptr = [int(x) for x in node_ptr]
+        if len(ptr) != world + 1:
+            raise ValueError("node_ptr needs world + 1 entries")
+        h = C.c_void_p()
+        _check(lib().rgnn_comm_create(int(rank), int(world), C.create_string_buffer(unique_id, COMM_ID_BYTES),
+                                      (C.c_int64 * len(ptr))(*ptr), C.byref(h)))
+        self.handle = h
+        self.rank, self.world, self.node_ptr = int(rank), int(world), ptr
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().rgnn_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def exchange_bytes(model: str, dtype: str, d_in: int, d_out: int, num_nodes: int, num_pairs_global: int,
+                   heads: int = 1) -> Dict[str, int]:
+    """Per-rank bytes of one forward exchange under variant X (all-gather of X) and variant P
+    (all-gather of the projected per-pair rows), and the variant the library runs."""
+    desc = LayerDescC(MODELS[model], DTYPES[dtype], d_in, d_out, 1, 0, 0.2, 0, 0, heads, 0)
+    bx, bp, v = C.c_int64(), C.c_int64(), C.c_int32()
+    _check(lib().rgnn_comm_exchange_bytes(C.byref(desc), int(num_nodes), int(num_pairs_global), C.byref(bx),
+                                          C.byref(bp), C.byref(v)))
+    return {"bytes_x": bx.value, "bytes_p": bp.value, "variant": "XP"[v.value]}
 
 
 class SegmentPlan:

@@ -78,3 +78,26 @@ def test_segment_plan_argument_errors(lib):
     assert st == 1 and "negative weight" in lib.rgnn_last_error().decode()
     assert lib.rgnn_segment_gemm(None, 1, None, None, 64, None, 1, 64, 0, None, 1, None, 0, None) == 1
     assert lib.rgnn_segment_plan_destroy(None) == 0
+
+
+def test_comm_argument_errors(lib):
+    """Communicator entry points validate their arguments before touching NCCL or a device."""
+    from paper_2412_04747_b200 import rgnn
+    out = C.c_void_p()
+    ptr = (C.c_int64 * 3)(0, 5, 10)
+    uid = C.create_string_buffer(rgnn.COMM_ID_BYTES)
+    assert lib.rgnn_comm_create(2, 2, uid, ptr, C.byref(out)) == 1          # rank outside [0, world)
+    assert "rank" in lib.rgnn_last_error().decode()
+    bad = (C.c_int64 * 3)(0, 6, 5)
+    assert lib.rgnn_comm_create(0, 2, uid, bad, C.byref(out)) == 1          # decreasing node_ptr
+    assert lib.rgnn_comm_create(0, 2, None, ptr, C.byref(out)) == 1
+    assert lib.rgnn_comm_destroy(None) == 0
+
+
+def test_exchange_bytes():
+    """Variant X moves N d_in b bytes, variant P U_global k d_out b (k = 2 for HGT's [K~|M])."""
+    from paper_2412_04747_b200 import rgnn
+    e = rgnn.exchange_bytes("hgt", "bf16", 64, 64, num_nodes=1000, num_pairs_global=3000)
+    assert e == {"bytes_x": 1000 * 64 * 2, "bytes_p": 3000 * 2 * 64 * 2, "variant": "X"}
+    e = rgnn.exchange_bytes("rgcn", "f32", 64, 64, num_nodes=1000, num_pairs_global=3000)
+    assert e["bytes_p"] == 3000 * 64 * 4

@@ -76,3 +76,38 @@ def test_single_edge_pairs_count():
     g = g7()
     # G7 pairs (rel, src): edges per pair [2, 2, 1, 1, 1] (tests/golden/g7_build.json edge_pair)
     assert bench.single_edge_pairs(g) == 3
+
+
+def test_d4_terms():
+    """SURVEY.md §8(d) D4 evaluated by hand: mag HGT bf16 A7 term E (12 + 4d + db) = 8.36 GB, and the
+    per-edge dominant terms 28 + 5db + 4d (HGT), 40 + 2db + 4d (RGAT), 16 + db + 4d (RGCN)."""
+    E, N, U, d = 21_111_007, 1_939_743, 3_186_438, 64
+    h = bench.d4_bytes("hgt", "bf16", N, E, U, d)
+    assert h["rows"]["hgt_bwd_pair"] == E * 396
+    assert abs(h["rows"]["hgt_bwd_pair"] / 1e9 - 8.36) < 0.01
+    for model, per_edge in (("hgt", 28 + 5 * 128 + 256), ("rgat", 40 + 2 * 128 + 256), ("rgcn", 16 + 128 + 256)):
+        a = bench.d4_bytes(model, "bf16", N=0, E=1, U=0, d=64)
+        assert a["fwd"] + a["bwd"] == per_edge, model
+
+
+def test_roofline_counts_only_launched_labels():
+    alg = {"a": 1000, "b": 3000, "never": 5000}
+    prof = {"a": {"launches": 2, "ms": 2.0}, "b": {"launches": 2, "ms": 4.0}}
+    peaks = {"hbm_gbs": 1.0, "source": "t"}
+    r = bench.roofline_block(alg, prof, 2, 3.0, peaks, "hgt", "bf16", 1, 1, 1, 64, 1.0, 2.0, False)
+    assert r["step_algorithmic_gb"] == 4000 / 1e9
+    assert r["kernel"] == "b" and r["ms_per_step"] == 2.0
+
+
+def test_parse_ncu_dram():
+    csv = "\n".join([
+        '==PROF== Connected to process',
+        '"ID","Process ID","Process Name","Host Name","Kernel Name","Context","Stream","Block Size","Grid Size",'
+        '"Device","CC","Section Name","Metric Name","Metric Unit","Metric Value"',
+        '"0","1","p","h","void k_hgt_bwd_pair_s<1>(int)","1","7","(256,1,1)","(1,1,1)","0","10.0","","dram__bytes_read.sum","Mbyte","1,000.5"',
+        '"0","1","p","h","void k_hgt_bwd_pair_s<1>(int)","1","7","(256,1,1)","(1,1,1)","0","10.0","","dram__bytes_write.sum","Kbyte","500"',
+        '"1","1","p","h","void k_hgt_bwd_pair_k<1>(int)","1","7","(256,1,1)","(1,1,1)","0","10.0","","dram__bytes_read.sum","Gbyte","1"',
+        '"2","1","p","h","void k_other(int)","1","7","(256,1,1)","(1,1,1)","0","10.0","","dram__bytes_read.sum","Gbyte","9"',
+    ])
+    tot, n = bench.parse_ncu_dram(csv, "k_hgt_bwd_pair")
+    assert n == 2 and abs(tot - (1000.5e6 + 500e3 + 1e9)) < 1

@@ -1,8 +1,10 @@
 """World-size-2 gloo test of the destination-partitioned multi-GPU bookkeeping
-(paper_2412_04747_b200/dist.py) on CPU: partition ranges, all-gather of owned
-rows, masked-G backward, reduce-scatter of dX and all-reduce of dW reproduce
-the single-process oracle exactly (the per-rank compute is the oracle on the
-rank's in-edge subgraph, i.e. what each GPU computes)."""
+(paper_2412_04747_b200/dist.py) on CPU: partition ranges, the library's exchange schedule
+restated with torch.distributed (in-place all-gather of X by owner broadcasts, reduce of the
+partial dX onto the owners, all-reduce of dW), and the owned-rows-only dout reproduce the
+single-process oracle exactly (the per-rank compute is the oracle on the rank's in-edge
+subgraph, i.e. what each GPU computes); plus the NCCL unique-id bootstrap over the process
+group (the only torch.distributed call the GPU path makes)."""
 import os
 import socket
 
@@ -36,19 +38,32 @@ def _worker(rank, world, port, model, q):
         Gh = upstream_grad(g.num_nodes, 8)
         ranges = D.partition_ranges(g.dst, g.num_nodes, world)
         lo, hi = ranges[rank]
-        # forward exchange: all-gather the owned source rows of X
-        X_full = D.all_gather_rows(torch.from_numpy(inp["X"][lo:hi]), ranges, rank).numpy()
+        # forward exchange: rows of other ranks are garbage until the owner broadcasts arrive
+        X = torch.full(inp["X"].shape, float("nan"), dtype=torch.float64)
+        X[lo:hi] = torch.from_numpy(inp["X"][lo:hi])
+        D.allgather_rows_reference(X, ranges)
+        X_full = X.numpy()
         assert np.array_equal(X_full, inp["X"])
         sub, eids = S.in_edge_subgraph(g, np.arange(lo, hi))
         kw = {"norm": L.rgcn_edge_norm(g, "mean")[eids]} if model == "rgcn" else {}
         local = dict(inp, X=X_full)
         out, _ = L.forward(model, sub, local, **kw)
-        out_full = D.all_gather_rows(torch.from_numpy(out[lo:hi]), ranges, rank).numpy()
-        grads = L.backward(model, sub, local, S.masked_grad(Gh, np.arange(lo, hi)), **kw)
-        dX_own = D.reduce_scatter_rows(torch.from_numpy(grads.pop("dX")), ranges, rank)
-        dX_full = D.all_gather_rows(dX_own, ranges, rank).numpy()
+        out_t = torch.from_numpy(np.ascontiguousarray(out))
+        D.allgather_rows_reference(out_t, ranges)   # only to compare the whole output on rank 0
+        out_full = out_t.numpy()
+        # dout: only the owned rows are read (the rest is never touched on a rank)
+        Gown = np.full_like(Gh, np.nan)
+        Gown[lo:hi] = Gh[lo:hi]
+        grads = L.backward(model, sub, local, np.where(np.isnan(Gown), 0.0, Gown), **kw)
+        dX = torch.from_numpy(np.ascontiguousarray(grads.pop("dX")))
+        D.reduce_rows_reference(dX, ranges)
+        D.allgather_rows_reference(dX, ranges)      # only to compare the whole dX on rank 0
+        dX_full = dX.numpy()
         tg = {k: torch.from_numpy(v) for k, v in grads.items()}
         D.all_reduce_grads(tg, list(tg))
+        # the NCCL-id bootstrap: rank 0's bytes reach every rank unchanged
+        uid = D.share_unique_id(lambda: bytes(range(128)))
+        assert uid == bytes(range(128))
         if rank == 0:
             ref_out, _ = L.forward(model, g, inp)
             ref = L.backward(model, g, inp, Gh)
@@ -74,6 +89,13 @@ def test_two_rank_partition_matches_oracle(model):
         assert p.exitcode == 0
     assert ranges[0][0] == 0 and ranges[-1][1] > ranges[0][1]
     assert max(err.values()) < 1e-12, err
+
+
+def test_node_ptr():
+    from paper_2412_04747_b200.dist import node_ptr
+    assert node_ptr([(0, 3), (3, 3), (3, 10)]) == [0, 3, 3, 10]
+    with pytest.raises(ValueError):
+        node_ptr([(0, 3), (4, 10)])
 
 
 def test_partition_ranges_balance():

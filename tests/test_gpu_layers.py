@@ -283,12 +283,20 @@ def _degenerate_graphs():
     out["heavy_row"] = HeteroGraph(ptr2, 3, i32(k), i32(np.zeros(3000)), i32(k % 3))
     s = np.arange(0, n, 7)
     out["self_loops"] = HeteroGraph(ptr2, 1, i32(s), i32(s), i32(np.zeros(len(s))))
+    # N a power of two and an empty trailing node type (its first id is N = 1 << bits): the
+    # (relation, source type) bounds of the pairs must stay monotone for every relation
+    m = 4096
+    rng = np.random.default_rng(9)
+    src = rng.integers(0, m, size=6000)
+    rel = (src >= 2048).astype(np.int64) + 2 * rng.integers(0, 2, size=6000)   # rels 0..3, odd ones too
+    out["empty_last_type_pow2"] = HeteroGraph(np.array([0, 2048, m, m], np.int64), 4, i32(src),
+                                              i32(rng.integers(0, m, size=6000)), i32(rel))
     return out
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("model", ["rgcn", "rgat", "hgt"])
-@pytest.mark.parametrize("name", ["no_edges", "heavy_pair", "heavy_row", "self_loops"])
+@pytest.mark.parametrize("name", ["no_edges", "heavy_pair", "heavy_row", "self_loops", "empty_last_type_pow2"])
 def test_degenerate_graphs(name, model, dtype):
     """Tensors the oracle gives as exactly zero (e.g. the attention weights' gradients when every
     softmax has a single edge, alpha = 1) are compared in absolute terms (inputs are O(1))."""
@@ -317,3 +325,36 @@ def test_degenerate_graphs(name, model, dtype):
         errs[k] = rel_err(gpu, v) if np.abs(v).max() > 0 else float(np.abs(gpu).max())
     bad = {k: e for k, e in errs.items() if not e <= tol}
     assert not bad, (name, model, dtype, errs)
+
+
+def test_f32_wide_rows():
+    """fp32 rows of 256 in the backward's per-source reduction (d_in = 256, and HGT with
+    reordering off at d_out = 128: [dK | dV] rows of 2 d_out)."""
+    g = config_graph("tiny", seed=6, scale=0.3)
+    run_case("rgcn", g, 256, 64, "f32")
+    run_case("hgt", g, 256, 64, "f32")
+    run_case("hgt", g, 128, 128, "f32", reorder=False)
+    run_case("rgat", g, 128, 128, "f32")
+
+
+def test_binding_rejects_bad_shapes():
+    """The C-ABI takes raw pointers; the binding checks shapes, dtypes and alignment first."""
+    from paper_2412_04747_b200 import Graph, Layer
+    g = config_graph("tiny", seed=1, scale=0.2)
+    G = Graph.from_hetero(g)
+    layer = Layer(G, "hgt", 32, 32, dtype="f32")
+    inp = to_device(layer_inputs("hgt", g, 32, 32), "f32")
+    X = inp.pop("X")
+    with pytest.raises(ValueError, match="shape"):
+        layer.forward(X[:, :16].contiguous(), inp)
+    bad = dict(inp, Watt=inp["Watt"][:, :16].contiguous())
+    with pytest.raises(ValueError, match="Watt"):
+        layer.forward(X, bad)
+    with pytest.raises(ValueError, match="needs weight"):
+        layer.forward(X, {k: v for k, v in inp.items() if k != "Wq"})
+    with pytest.raises(ValueError, match="aligned"):
+        flat = torch.empty(X.numel() + 1, dtype=torch.float32, device="cuda")
+        layer.forward(flat[1:].view(X.shape), inp)
+    out = layer.forward(X, inp)
+    with pytest.raises(ValueError, match="dout"):
+        layer.backward(X, inp, out, torch.zeros(g.num_nodes, 16, device="cuda"))

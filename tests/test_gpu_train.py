@@ -124,8 +124,13 @@ def test_two_layer_step(model, graph, scale, dtype):
     torch.cuda.synchronize()
     tols = {}
     if dtype == "bf16":
+        # gradients that are ill-conditioned under one bf16 rounding of the inputs (DESIGN.md b16:
+        # the oracle's own relative change S under a 2^-9 perturbation exceeds 1e-2, e.g. S = 0.11
+        # for layer 2's da on the BGS shape) get max(2e-2, 2 S) in layer 2 and max(2e-2, 3 S) in
+        # layer 1 (whose input gradient has passed through layer 2's backward and a ReLU mask);
+        # the loss and every gradient with S <= 1e-2 are held to the flat 2e-2
         S = bf16_sensitivity(model, g, X, ps, y, trained)
-        tols = {k: max(TOL[dtype], 3 * v) for k, v in S.items()}
+        tols = {k: max(TOL[dtype], (3 if k.startswith("L0.") else 2) * v) for k, v in S.items() if k != "loss"}
     tol_of = lambda k: tols.get(k, TOL[dtype])  # noqa: E731
     assert abs(loss - ref_loss) <= tol_of("loss") * abs(ref_loss), (loss, ref_loss)
     errs = {}

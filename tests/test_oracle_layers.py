@@ -303,3 +303,67 @@ def test_tail_identity_weights():
 def test_fd_hgt_tail(heads, seed):
     g = random_small_graph(500 + seed, allow_multi=True)
     _fd_check("hgt", g, 8, 8, seed=seed, opts={"heads": heads, "tail": True})
+
+
+# ----------------------------------------------------------------- RGCN normaliser c_{v,r} (reading g1)
+def _golden(name):
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", name)))
+
+
+def _frac(s):
+    from fractions import Fraction
+    import math
+    if s.startswith("1/sqrt("):
+        return 1.0 / math.sqrt(int(s[len("1/sqrt("):-1]))
+    return float(Fraction(s))
+
+
+@pytest.mark.parametrize("kind", ["mean", "sym"])
+def test_rgcn_norm_g7_hand_values(kind):
+    """Eq. 3.1's 1/c_{v,r} on G7, values worked by hand (tests/golden/g7_rgcn_norm.json)."""
+    gold = _golden("g7_rgcn_norm.json")
+    want = np.array([_frac(s) for s in gold[f"{kind}_by_eid"]])
+    got = L.rgcn_edge_norm(g7(), kind)
+    assert np.allclose(got, want, rtol=0, atol=1e-15)
+
+
+def test_rgcn_mean_identity_ones_g7():
+    """mean norm, X = 1, W_r = I, W_0 = 0: out_v = #relations with an in-edge into v (hand value)."""
+    g = g7()
+    gold = _golden("g7_rgcn_norm.json")["rgcn_mean_identity_ones"]["out"]
+    I = np.eye(3)
+    out, _ = L.rgcn_forward(g, np.ones((5, 3)), np.stack([I, I]), np.zeros((3, 3)), L.rgcn_edge_norm(g, "mean"))
+    assert np.allclose(out, np.array(gold, float)[:, None] * np.ones((1, 3)), atol=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_rgcn_mean_is_row_normalised_relation_adjacency(seed):
+    """'mean' == sum_r D_r^-1 A_r X W_r + X W_0 with A_r the dense per-relation adjacency (edge
+    multiplicities counted) and D_r its row sums, built here from the edge list, not from
+    rgcn_edge_norm; a norm over the total in-degree (a plausible slip) fails this."""
+    g = random_small_graph(seed, allow_multi=seed % 2 == 1)
+    rng = np.random.default_rng(100 + seed)
+    n, R = g.num_nodes, g.num_rels
+    X = rng.normal(size=(n, 4))
+    W = rng.normal(size=(R, 4, 3))
+    W0 = rng.normal(size=(4, 3))
+    ref = X @ W0
+    for r in range(R):
+        A = np.zeros((n, n))
+        for s_, d_, r_ in zip(g.src, g.dst, g.rel):
+            if r_ == r:
+                A[d_, s_] += 1.0
+        rows = A.sum(axis=1)
+        Dinv = np.divide(1.0, rows, out=np.zeros(n), where=rows > 0)
+        ref = ref + (Dinv[:, None] * A) @ X @ W[r]
+    out, _ = L.rgcn_forward(g, X, W, W0, L.rgcn_edge_norm(g, "mean"))
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+    # and the per-(v, r) weights sum to one
+    norm = L.rgcn_edge_norm(g, "mean")
+    tot = {}
+    for e in range(g.num_edges):
+        k = (int(g.dst[e]), int(g.rel[e]))
+        tot[k] = tot.get(k, 0.0) + norm[e]
+    assert all(abs(v - 1.0) < 1e-12 for v in tot.values())
