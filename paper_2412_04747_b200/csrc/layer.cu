@@ -216,6 +216,7 @@ struct BwdScratch {
   void* GQ = nullptr;     // HGT [N][2D] = [G_v | Q_v] layer dtype
   void* Gt = nullptr;     // RGCN bf16 path: the upstream gradient in bf16 [N][D]
   float4* nst = nullptr;  // HGT [N] (m, 1/sum, G.out, 0)
+  float2* wts = nullptr;  // HGT [E][H] (alpha_e, dl_e) per CSR entry (weighted pair SpMM)
   float* dKV32 = nullptr;  // HGT reordering off: per-node [dK|dV] [N][2D] fp32
   void* dKVdt = nullptr;   //   the same in the layer dtype (bf16 path; = dKV32 on the fp32 path)
   float* dXkv = nullptr;   //   dKV [Wk|Wv]^T  [N][Din]
@@ -232,6 +233,19 @@ struct BwdScratch {
   float* csr_norm = nullptr;
   float* csc_norm = nullptr;
 };
+
+// RGNN_PAIRW=1: the destination-major pass writes (alpha_e, dl_e) per CSR entry and the pair pass is a
+// weighted SpMM (k_pair_spmm); default: the pair-major backward recomputes them per edge from the pair
+// rows and a per-node record.  Measured on mag HGT (B200): SpMM 1.03 ms + 0.05 ms of extra destination-pass
+// writes vs 1.15 ms recomputing, but the per-edge weight gather is a random 8-byte read (+1 GB of DRAM
+// sectors), so the recomputing kernels stay the default.
+bool pair_spmm() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_PAIRW");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 
 // elements of the largest K-major weight image any GEMM of the layer builds (tcgen05 path)
 int64_t bt_elems(const Ctx& c) {
@@ -309,7 +323,8 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
       o.Gdt = ar.take<char>(N * c.D * c.esz);
     }
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
-    o.nst = ar.take<float4>(N * c.H);
+    if (pair_spmm()) o.wts = ar.take<float2>(E * c.H);
+    else o.nst = ar.take<float4>(N * c.H);
     need(seg_node_type(g), (int64_t)c.Din * c.D);
     if (hgt_nr(c.d)) {
       o.dXp = ar.take<char>(U * 2 * c.D * c.esz);  // per-pair [dK|dV] rows
@@ -715,8 +730,8 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
   } else {
     const bool single = single_in_dst(g);
     hgt_bwd_dst(g, c.dt, c.D, c.H, sv.P, sv.Q, sv.stats, G, out, sc.dQ, sc.GQ, sc.nst,
-                single ? g->csr_single : nullptr, sc.dP, sc.pt, c.s);
-    hgt_bwd_pair(g, c.dt, c.D, c.H, sv.P, sc.GQ, sc.nst, sc.dP, single, sc.pt, c.s);
+                single ? g->csr_single : nullptr, sc.dP, sc.wts, sc.pt, c.s);
+    hgt_bwd_pair(g, c.dt, c.D, c.H, sv.P, sc.GQ, sc.nst, sc.wts, sc.dP, single, sc.pt, c.s);
     if (hgt_nr(c.d)) {
       hgt_backward_nr(c, X, w, sv, dX, dW, sc);
       return;

@@ -52,11 +52,10 @@ constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and 
 #else
 #define RGNN_RGAT_DST_LB __launch_bounds__(256)
 #endif
-#ifdef RGNN_DST_MINB
-#define RGNN_DST_LB __launch_bounds__(256, RGNN_DST_MINB)
-#else
-#define RGNN_DST_LB __launch_bounds__(256)
+#ifndef RGNN_DST_MINB
+#define RGNN_DST_MINB 3
 #endif
+#define RGNN_DST_LB __launch_bounds__(256, RGNN_DST_MINB)
 #ifndef RGNN_PAIR_MINB
 #define RGNN_PAIR_MINB 4
 #endif
@@ -527,14 +526,15 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
 // ------------------------------------------------------------------ HGT backward, dst-major (A6)
 // alpha_e = exp(l_e - m_v)/sum_v ; dalpha_e = G_v . M_p ; dl_e = alpha_e (dalpha_e - G_v . out_v)
 // dQ_v = sum_e dl_e K~_p   (layer dtype; heavy rows: fp32 partials merged by k_merge_sum)
-template <class TP, int D, bool GROUP, int H, bool SGL>
+template <class TP, int D, bool GROUP, int H, bool SGL, bool WT>
 __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                      const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                      const float2* __restrict__ stats, const float* __restrict__ Gr,
                                                      const float* __restrict__ out, TP* __restrict__ dQ,
                                                      TP* __restrict__ GQ, float4* __restrict__ nst,
-                                                     const uint8_t* __restrict__ single, TP* __restrict__ dKM) {
+                                                     const uint8_t* __restrict__ single, TP* __restrict__ dKM,
+                                                     float2* __restrict__ wts) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   Work<GROUP, LPR> w;
@@ -559,7 +559,7 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
     if (slot < 0 && e > b && w.writer()) {  // node record for the pair-major pass (heavy rows: k_hgt_node_prep)
       st_tp<V>(GQ + v * 2 * D + c * V, gv);
       st_tp<V>(GQ + v * 2 * D + D + c * V, q);
-      if (w.writer() && c % LH == 0) nst[v * H + hd] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
+      if (nst && c % LH == 0) nst[v * H + hd] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
     }
     for (int t = 0; t < w.span; t += w.step * UNR) {
       const int i0 = b + t + w.first;
@@ -592,6 +592,8 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
         l = gsum<LH>(l, w.mask);
         da = gsum<LH>(da, w.mask);
         float dl = (i < e) ? __expf(l - st.x) * inv * (da - go) : 0.f;
+        if (WT && i < e && c % LH == 0)  // for k_pair_spmm
+          wts[(int64_t)i * H + hd] = make_float2(__expf(l - st.x) * inv, dl);
 #pragma unroll
         for (int k = 0; k < V; ++k) dq[k] = fmaf(dl, kx[k], dq[k]);
         if (SGL && pid[u] >= 0) {  // single-edge pair: dKM_p = [dl q_v | alpha G_v]
@@ -614,14 +616,15 @@ __global__ void RGNN_DST_LB k_hgt_bwd_dst(int64_t n, const int4* __restrict__ it
 }
 
 // Short rows (<= SHORT_MAX in-edges, incl. empty rows), KI per lane group; also the node records.
-template <class TP, int D, int H, int KI, bool SGL>
+template <class TP, int D, int H, int KI, bool SGL, bool WT>
 __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __restrict__ items,
                                                        const int32_t* __restrict__ csr_pair,
                                                        const TP* __restrict__ KM, const TP* __restrict__ Q,
                                                        const float2* __restrict__ stats, const float* __restrict__ Gr,
                                                        const float* __restrict__ out, TP* __restrict__ dQ,
                                                        TP* __restrict__ GQ, float4* __restrict__ nst,
-                                                       const uint8_t* __restrict__ single, TP* __restrict__ dKM) {
+                                                       const uint8_t* __restrict__ single, TP* __restrict__ dKM,
+                                                       float2* __restrict__ wts) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR, LH = LPR / H;
   __shared__ uint4 sg[KI][256];  // G_v chunk (table dtype) of each item, lane-private
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       }
     }
     go[k] = gsum<LH>(go[k], w.mask);
-    if (has && c % LH == 0) nst[v * H + hd] = make_float4(lse[k], go[k], 0.f, 0.f);
+    if (nst && has && c % LH == 0) nst[v * H + hd] = make_float4(lse[k], go[k], 0.f, 0.f);
   }
   for (int t = 0; t < w.span; ++t) {
     uint4 rk[KI], rm[KI];
@@ -696,6 +699,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
       l = gsum<LH>(l, w.mask);
       da = gsum<LH>(da, w.mask);
       const float dl = (w.it[k].y + t < w.it[k].z) ? __expf(l - lse[k]) * (da - go[k]) : 0.f;
+      if (WT && w.it[k].y + t < w.it[k].z && c % LH == 0)
+        wts[(int64_t)(w.it[k].y + t) * H + hd] = make_float2(__expf(l - lse[k]), dl);
 #pragma unroll
       for (int j = 0; j < V; ++j) dq[k][j] = fmaf(dl, kx[j], dq[k][j]);
       if (SGL && pid[k] >= 0) {  // single-edge pair: dKM_p = [dl q_v | alpha G_v]
@@ -1221,7 +1226,7 @@ __global__ void __launch_bounds__(256) k_hgt_node_prep(int64_t n, const int4* __
   go = gsum<LH>(go, group_mask<LPR>(g));
   st_tp<V>(GQ + v * 2 * D + c * V, gv);
   st_tp<V>(GQ + v * 2 * D + D + c * V, qv);
-  if (c % LH == 0) {
+  if (nst && c % LH == 0) {
     float2 st = stats[v * H + c / LH];
     nst[v * H + c / LH] = make_float4(st.y > 0.f ? st.x + logf(st.y) : CUDART_INF_F, go, 0.f, 0.f);
   }
@@ -1625,6 +1630,148 @@ __global__ void __launch_bounds__(RING_TB) k_hgt_bwd_pair_ring(int64_t nch, cons
   cp_async_wait<0>();
 }
 
+// ------------------------------------------------------------------ weighted pair SpMM (A7)
+// The pair-major backward as a two-weight SpMM over the src-CSC: per compact pair p
+//   outA_p = sum_{e in p} wA_e A_{d_e},   outB_p = sum_{e in p} wB_e B_{d_e}   (+ wsum_p = sum wB_e),
+// with the destination record rec_v = [A_v | B_v] (2D wide, table dtype) and the per-edge weights
+// (wA, wB) written by the destination-major pass in CSR order (gathered through csc2csr).  HGT:
+// rec = [G_v | Q_v], w = (alpha_e, dl_e) -> [dM_p | dK~_p]; RGAT: rec = [G_v | X_v], w = (alpha_e, dz_e)
+// -> [dP_p - (sum dz) a_r | bx_p].  No logits, softmax or pair rows are recomputed here: per edge one
+// record gather, one 8-byte weight gather, and 2 x V fused multiply-adds per lane (packed f32x2).
+// One lane group walks one stream chunk (a contiguous CSC run of whole pairs, WorkPlan::chunks) U
+// edges per step; the ids of the next LPR edges arrive as one coalesced load per group and are
+// shuffled to their step; a pair's rows are written when the stream leaves it (split chunks of heavy
+// pairs: the fp32 partial into the chunk's slot, merged by k_merge_sum).
+// acc[0..V/2) += s * (16-byte vector v of the table dtype), packed f32x2 FMAs
+#ifndef RGNN_FFMA2
+#define RGNN_FFMA2 1
+#endif
+template <class TP>
+__device__ __forceinline__ void acc16(float2* acc, uint4 v, float s) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#if !RGNN_FFMA2
+  float x[Vec<TP>::N];
+  cvt16<TP>(v, x);
+#pragma unroll
+  for (int i = 0; i < Vec<TP>::N / 2; ++i) {
+    acc[i].x = fmaf(x[2 * i], s, acc[i].x);
+    acc[i].y = fmaf(x[2 * i + 1], s, acc[i].y);
+  }
+  return;
+#endif
+  const float2 ss = make_float2(s, s);
+  if constexpr (sizeof(TP) == 2) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      acc[i] = __ffma2_rn(make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u)), ss, acc[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      acc[i] = __ffma2_rn(make_float2(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1])), ss, acc[i]);
+  }
+}
+
+#ifndef RGNN_SPMM_U
+#define RGNN_SPMM_U 2
+#endif
+
+#ifndef RGNN_SPMM_MINB
+#define RGNN_SPMM_MINB 3
+#endif
+
+template <class TP, int D, int H, int U, bool WSUM>
+__global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
+    int64_t nch, const int4* __restrict__ chunks, float* __restrict__ pacc, float2* __restrict__ pstat,
+    const int32_t* __restrict__ csc_dst, const int32_t* __restrict__ csc2csr, const int32_t* __restrict__ csc_pair,
+    const TP* __restrict__ rec, const float2* __restrict__ wts, TP* __restrict__ outA, TP* __restrict__ outB,
+    int64_t ostride, float* __restrict__ wsum, int poffA, int poffB) {
+  using G = Geo<TP, D>;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H, V2 = V / 2;
+  static_assert(LPR % U == 0, "U must divide the lanes per row");
+  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR, hd = c / LH;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wid * EG >= nch) return;  // whole warp idle
+  const int64_t gid = wid * EG + g;
+  const int4 ch = gid < nch ? chunks[gid] : make_int4(0, 0, -1, 0);
+  const int a = ch.x, L = ch.y - ch.x, slot = ch.z;
+  const int span = __reduce_max_sync(0xffffffffu, L);
+  const int src0 = g * LPR;
+  // ids of the stream's edges [t, t + LPR): lane c holds edge t + c (past the end: row 0, weight 0, pair -1)
+  int d_cur, x_cur, p_cur, d_nxt, x_nxt, p_nxt;
+  auto ld_ids = [&](int t, int& dd, int& xx, int& pp) {
+    const int i = t + c;
+    const bool ok = i < L;
+    const int j = a + (ok ? i : 0);
+    dd = ok ? __ldg(csc_dst + j) : 0;
+    xx = __ldg(csc2csr + j);
+    pp = ok ? __ldg(csc_pair + j) : -1;
+  };
+  ld_ids(0, d_cur, x_cur, p_cur);
+  ld_ids(LPR, d_nxt, x_nxt, p_nxt);
+  float2 accA[V2], accB[V2];
+  float ws = 0.f;
+#pragma unroll
+  for (int k = 0; k < V2; ++k) accA[k] = accB[k] = make_float2(0.f, 0.f);
+  int cp = -1;  // the pair being accumulated (group-uniform)
+  auto flush = [&]() {
+    float fa[V], fb[V];
+#pragma unroll
+    for (int k = 0; k < V2; ++k) {
+      fa[2 * k] = accA[k].x;
+      fa[2 * k + 1] = accA[k].y;
+      fb[2 * k] = accB[k].x;
+      fb[2 * k + 1] = accB[k].y;
+    }
+    if (slot >= 0) {  // split chunk of a heavy pair: fp32 partial row (A at poffA, B at poffB) + (wsum, 0)
+      float* o = pacc + (int64_t)slot * 2 * D;
+      st_f32<V>(o + poffA + c * V, fa);
+      st_f32<V>(o + poffB + c * V, fb);
+      if (WSUM && c == 0) pstat[slot] = make_float2(ws, 0.f);
+    } else {
+      st_tp<V>(outA + (int64_t)cp * ostride + c * V, fa);
+      st_tp<V>(outB + (int64_t)cp * ostride + c * V, fb);
+      if (WSUM && c == 0) wsum[cp] = ws;
+    }
+  };
+  for (int t0 = 0; t0 < span; t0 += U) {
+    if (t0 > 0 && t0 % LPR == 0) {  // warp-uniform: the prefetched batch becomes current
+      d_cur = d_nxt;
+      x_cur = x_nxt;
+      p_cur = p_nxt;
+      ld_ids(t0 + LPR, d_nxt, x_nxt, p_nxt);
+    }
+    uint4 ra[U], rb[U];
+    float2 ww[U];
+    int pp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int sl = src0 + (t0 + u) % LPR;
+      const int d = __shfl_sync(0xffffffffu, d_cur, sl);
+      const int x = __shfl_sync(0xffffffffu, x_cur, sl);
+      pp[u] = __shfl_sync(0xffffffffu, p_cur, sl);
+      const TP* r = rec + (int64_t)d * 2 * D + c * V;
+      ra[u] = ldg16(r);
+      rb[u] = ldg16(r + D);
+      ww[u] = __ldg(wts + (int64_t)x * H + hd);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (pp[u] != cp) {  // the stream enters a new pair (or leaves its last one)
+        if (cp >= 0) flush();
+#pragma unroll
+        for (int k = 0; k < V2; ++k) accA[k] = accB[k] = make_float2(0.f, 0.f);
+        ws = 0.f;
+        cp = pp[u];
+      }
+      const float wa = pp[u] >= 0 ? ww[u].x : 0.f, wb = pp[u] >= 0 ? ww[u].y : 0.f;
+      acc16<TP>(accA, ra[u], wa);
+      acc16<TP>(accB, rb[u], wb);
+      if (WSUM) ws += wb;
+    }
+  }
+  if (cp >= 0) flush();
+}
+
 // ------------------------------------------------------------------ heavy-id merges
 // One CTA per heavy id: warp w folds chunks w, w+8, ... of the id (lane c owns columns 4c..4c+3
 // of a W-wide row, looping over W in steps of 128); the 8 warp results are then combined in warp
@@ -1899,26 +2046,31 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
 
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const uint8_t* single, void* dKM,
-                 const Partial& pt, cudaStream_t s) {
+                 float2* wts, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       by_heads<Geo<TP, DD>::LPR>(H, [&](auto hc) {
         constexpr int HH = decltype(hc)::value;
-        auto go = [&](auto sc) {
-          constexpr bool SG = decltype(sc)::value;
-          launch_plan_short<2>("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH, SG>,
-                             k_hgt_bwd_dst<TP, DD, true, HH, SG>, k_hgt_bwd_dst_k<TP, DD, HH, 2, SG>,
+        auto go = [&](auto sc, auto wc) {
+          constexpr bool SG = decltype(sc)::value, WT = decltype(wc)::value;
+          launch_plan_short<2>("hgt_bwd_dst", g->rows, Geo<TP, DD>::LPR, k_hgt_bwd_dst<TP, DD, false, HH, SG, WT>,
+                             k_hgt_bwd_dst<TP, DD, true, HH, SG, WT>, k_hgt_bwd_dst_k<TP, DD, HH, 2, SG, WT>,
                              std::make_tuple((const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
                                              static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
-                                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM)),
+                                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM), wts),
                              s, pt.acc, (const int32_t*)g->csr_pair, static_cast<const TP*>(KM),
                              static_cast<const TP*>(Q), stats, G, out, static_cast<TP*>(dQ),
-                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM));
+                             static_cast<TP*>(GQ), nst, single, static_cast<TP*>(dKM), wts);
         };
-        if (single) go(std::true_type());
-        else go(std::false_type());
+        if (single) {
+          if (wts) go(std::true_type(), std::true_type());
+          else go(std::true_type(), std::false_type());
+        } else {
+          if (wts) go(std::false_type(), std::true_type());
+          else go(std::false_type(), std::false_type());
+        }
         launch("hgt_node_prep", k_hgt_node_prep<TP, DD, HH>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256),
                0, s, g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(Q), out, stats,
                static_cast<TP*>(GQ), nst);
@@ -2007,13 +2159,36 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
 inline bool use_ring() {
   static const bool on = [] {
     const char* v = getenv("RGNN_RING");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }
 
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
-                  void* dKM, bool skip_single, const Partial& pt, cudaStream_t s) {
+                  const float2* wts, void* dKM, bool skip_single, const Partial& pt, cudaStream_t s) {
+  if (wts) {  // weighted SpMM: [dM | dK~] = sum_e [alpha_e G_d | dl_e Q_d] (weights from hgt_bwd_dst)
+    const int64_t nch = skip_single ? g->pairs.n_chunks_multi : g->pairs.n_chunks;
+    const int4* ch = skip_single ? g->pairs.chunks_multi : g->pairs.chunks;
+    by_width(D, [&](auto Dc) {
+      constexpr int DD = decltype(Dc)::value;
+      by_dtype(dtype, [&](auto* tp) {
+        using TP = std::remove_pointer_t<decltype(tp)>;
+        constexpr int LPR = Geo<TP, DD>::LPR;
+        constexpr int UU = RGNN_SPMM_U < LPR ? RGNN_SPMM_U : LPR;
+        by_heads<LPR>(H, [&](auto hc) {
+          constexpr int HH = decltype(hc)::value;
+          TP* o = static_cast<TP*>(dKM);
+          launch("hgt_bwd_pair", k_pair_spmm<TP, DD, HH, UU, false>, groups(nch, LPR), dim3(256), 0, s, nch, ch,
+                 pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc2csr,
+                 (const int32_t*)g->csc_pair, static_cast<const TP*>(GQ), wts, o + DD, o, (int64_t)2 * DD,
+                 (float*)nullptr, DD, 0);
+        });
+        launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
+               g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
+      });
+    });
+    return;
+  }
   if (use_ring()) {
     const int64_t nch = skip_single ? g->pairs.n_chunks_multi : g->pairs.n_chunks;
     const int4* ch = skip_single ? g->pairs.chunks_multi : g->pairs.chunks;

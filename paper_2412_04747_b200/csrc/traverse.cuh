@@ -18,13 +18,14 @@ void hgt_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, int H, const void
 void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                        const float* y, const float* te, float slope, float* out, float2* stats, const Partial& pt,
                        cudaStream_t s);
-// also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) of every
-// destination with in-edges (read by hgt_bwd_pair)
+// also writes the per-node record GQ_v = [G_v | Q_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0) (nst may be
+// NULL) of every destination with in-edges, and, when wts != NULL, (alpha_e, dl_e) per CSR entry and
+// head (read by hgt_bwd_pair)
 // single != NULL: the dKM rows of single-edge pairs (graph csr_single) are written here, and
 // hgt_bwd_pair then runs with skip_single (its pair-major pass covers pairs with >= 2 edges)
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const uint8_t* single, void* dKM,
-                 const Partial& pt, cudaStream_t s);
+                 float2* wts, const Partial& pt, cudaStream_t s);
 // also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
 // te != NULL (reordering off): t_e read from te, dz_e written per CSR entry into dz, dX untouched.
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
@@ -38,6 +39,8 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
                    const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
                    float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s);
+// wts != NULL: the weighted SpMM k_pair_spmm over the per-CSR-entry (alpha_e, dl_e) [E][H] that
+// hgt_bwd_dst wrote (nst unused); else the recomputing pair kernels (alpha, dl from K~ / M and nst)
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
-                  void* dKM, bool skip_single, const Partial& pt, cudaStream_t s);
+                  const float2* wts, void* dKM, bool skip_single, const Partial& pt, cudaStream_t s);
 }  // namespace rgnn
