@@ -1402,6 +1402,79 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_s(int64_t 
   }
 }
 
+// Mixed-precision helpers: bf16 x bf16 products are exact in fp32 (fma.rn.f32.bf16, no unpacking of the
+// packed halves); accumulations of a bf16 vector scaled by an fp32 weight as packed f32x2 FMAs.
+__device__ __forceinline__ float bdot4(uint2 a, uint2 b, float acc) {  // acc + sum_k a_k b_k over 4 bf16 pairs
+  asm("{\n.reg .b16 a0, a1, a2, a3, b0, b1, b2, b3;\n"
+      "mov.b32 {a0, a1}, %1;\nmov.b32 {a2, a3}, %2;\nmov.b32 {b0, b1}, %3;\nmov.b32 {b2, b3}, %4;\n"
+      "fma.rn.f32.bf16 %0, a0, b0, %0;\nfma.rn.f32.bf16 %0, a1, b1, %0;\n"
+      "fma.rn.f32.bf16 %0, a2, b2, %0;\nfma.rn.f32.bf16 %0, a3, b3, %0;\n}"
+      : "+f"(acc)
+      : "r"(a.x), "r"(a.y), "r"(b.x), "r"(b.y));
+  return acc;
+}
+
+// Group mode of the HGT pair pass for bf16 tables, split halves: a group of LPR = D / 4 lanes per pair,
+// lanes [0, D/8) own the G half of the destination record and the M half of the pair row, lanes
+// [D/8, D/4) the Q half and K~; each lane does ONE 8-column dot (G.M or K~.Q, mixed-precision bf16
+// FMAs on the packed halves), a reduction over its half, one exchange with its partner lane in the
+// other half, and 8 accumulations (dM or dK~).  One 16-byte gather per lane per edge, ~28 registers:
+// full occupancy with half the per-edge instructions of 4-column lanes.
+__device__ __forceinline__ float bdot8(uint4 a, uint4 b, float acc) {
+  return bdot4(make_uint2(a.z, a.w), make_uint2(b.z, b.w), bdot4(make_uint2(a.x, a.y), make_uint2(b.x, b.y), acc));
+}
+template <int D, int H, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_hgt_bwd_pair_sp(int64_t n, const int4* __restrict__ items,
+                                                               float* __restrict__ pacc,
+                                                               const int32_t* __restrict__ csc_dst,
+                                                               const bf16* __restrict__ KM,
+                                                               const bf16* __restrict__ GQ,
+                                                               const float4* __restrict__ nst,
+                                                               bf16* __restrict__ dKM) {
+  constexpr int HL = D / 8, LPR = 2 * HL, LHH = HL / H;  // lanes per half, per group, per head and half
+  static_assert(LHH >= 1, "a head must own at least one lane of each half");
+  Work<true, LPR> w;
+  if (!w.init(n, items)) return;
+  const int64_t p = w.item.x;
+  const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
+  const int h = c / HL, cc = c % HL, hd = cc / LHH;  // h = 0: G / M / dM,  h = 1: Q / K~ / dK~
+  const uint4 pk = w.has ? ldg16(KM + p * 2 * D + (1 - h) * D + 8 * cc) : make_uint4(0, 0, 0, 0);
+  float2 acc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = make_float2(0.f, 0.f);
+  int dn = b < e ? csc_dst[b] : 0;
+  for (int t = 0; t < w.span; ++t) {
+    const int i = b + t;
+    const int64_t d = dn;
+    const uint4 x = ldg16(GQ + d * 2 * D + h * D + 8 * cc);
+    const float2 ns = i < e ? __ldg(reinterpret_cast<const float2*>(nst + d * H + hd)) : make_float2(CUDART_INF_F, 0.f);
+    dn = i + 1 < e ? csc_dst[i + 1] : 0;
+    float part = gsum<LHH>(bdot8(pk, x, 0.f), w.mask);
+    const float other = __shfl_xor_sync(0xffffffffu, part, HL);
+    const float l = h ? part : other, da = h ? other : part;
+    const float alpha = __expf(l - ns.x);  // 0 past the end (lse = +inf)
+    const float dl = alpha * (da - ns.y);
+    // past the end the gathered row is node 0's, which may never have been written: no accumulation
+    const float s = i < e ? (h ? dl : alpha) : 0.f;
+    const uint4 xv = i < e ? x : make_uint4(0, 0, 0, 0);
+    const float2 ss = make_float2(s, s);
+    acc[0] = __ffma2_rn(make_float2(__uint_as_float(xv.x << 16), __uint_as_float(xv.x & 0xffff0000u)), ss, acc[0]);
+    acc[1] = __ffma2_rn(make_float2(__uint_as_float(xv.y << 16), __uint_as_float(xv.y & 0xffff0000u)), ss, acc[1]);
+    acc[2] = __ffma2_rn(make_float2(__uint_as_float(xv.z << 16), __uint_as_float(xv.z & 0xffff0000u)), ss, acc[2]);
+    acc[3] = __ffma2_rn(make_float2(__uint_as_float(xv.w << 16), __uint_as_float(xv.w & 0xffff0000u)), ss, acc[3]);
+  }
+  if (!w.writer()) return;
+  const int col = (1 - h) * D + 8 * cc;  // dKM row = [dK~ | dM]: h = 1 (dK~) at 0, h = 0 (dM) at D
+  if (slot >= 0) {
+    float* o = pacc + (int64_t)slot * 2 * D + col;
+    *reinterpret_cast<float4*>(o) = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
+    *reinterpret_cast<float4*>(o + 4) = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
+  } else {
+    float f[8] = {acc[0].x, acc[0].y, acc[1].x, acc[1].y, acc[2].x, acc[2].y, acc[3].x, acc[3].y};
+    store16(dKM + p * 2 * D + col, f);
+  }
+}
+
 // Short pairs (<= SHORT_MAX edges), KI per lane group; K~_p / M_p of each item staged in shared memory.
 template <class TP, int D, int H, int KI>
 __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t n, const int4* __restrict__ items,
@@ -1473,161 +1546,6 @@ __global__ void __launch_bounds__(256, RGNN_PAIR_MINB) k_hgt_bwd_pair_k(int64_t 
     st_tp<V>(o + c * V, ak[k]);
     st_tp<V>(o + D + c * V, am[k]);
   }
-}
-
-// ------------------------------------------------------------------ gather-ring pair pass (HGT A7)
-// The pair-major pass as an edge stream: one lane group walks a chunk of the src-CSC (a contiguous
-// run of whole pairs, WorkPlan::chunks) edge by edge, and every gathered node record ([G_d | Q_d]
-// and the (lse_d, G_d . out_d) record) travels global -> shared memory by cp.async into a
-// lane-private S-stage ring, issued S-1 edges ahead of its use.  Only the issuing lane reads a slot
-// (wait_group, no barrier), so the in-flight gathers cost no registers: S-1 edges per group are
-// outstanding at all times, across pair boundaries (short pairs no longer drain the pipeline).  The
-// destination and pair ids of the next LPR edges arrive as one coalesced load per group (lane c holds
-// edge base + c) and are shuffled to the issuing step; the pair's K~_p / M_p ride in the stage of its
-// first edge.  Per pair: dM_p = sum alpha_e G_d, dK~_p = sum dl_e Q_d (as k_hgt_bwd_pair), written
-// when the stream leaves the pair (heavy pairs: their split chunk's fp32 partial into its slot).
-__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-__device__ __forceinline__ float2 lds8(const float2* p) {
-  float2 v;
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-  return v;
-}
-
-struct RingStage {  // one lane's slice of one gathered edge (80 B)
-  uint4 g, q, k, m;
-  float2 ns, pad;
-};
-
-#ifndef RGNN_RING_S
-#define RGNN_RING_S 4
-#endif
-constexpr int RING_TB = 128;
-
-template <class TP, int D, int H, int S>
-__global__ void __launch_bounds__(RING_TB) k_hgt_bwd_pair_ring(int64_t nch, const int4* __restrict__ chunks,
-                                                               float* __restrict__ pacc,
-                                                               const int32_t* __restrict__ csc_dst,
-                                                               const int32_t* __restrict__ csc_pair,
-                                                               const TP* __restrict__ KM, const TP* __restrict__ GQ,
-                                                               const float4* __restrict__ nst, TP* __restrict__ dKM) {
-  using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H;
-  __shared__ RingStage ring[S][RING_TB];
-  const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR, hd = c / LH;
-  const int64_t gid = ((blockIdx.x * (int64_t)RING_TB + threadIdx.x) >> 5) * EG + g;
-  if (((blockIdx.x * (int64_t)RING_TB + threadIdx.x) >> 5) * EG >= nch) return;  // whole warp idle
-  const int4 ch = gid < nch ? chunks[gid] : make_int4(0, 0, -1, 0);
-  const int a = ch.x, L = ch.y - ch.x, slot = ch.z;
-  const int span = __reduce_max_sync(0xffffffffu, L);
-  const int src0 = g * LPR;  // first lane of this group
-  // ids of the edges [base, base + LPR) of the stream: lane c holds edge base + c
-  int d_cur, p_cur, d_nxt, p_nxt;
-  auto ld_ids = [&](int base, int& dd, int& pp) {
-    const int i = base + c;
-    dd = i < L ? __ldg(csc_dst + a + i) : 0;
-    pp = i < L ? __ldg(csc_pair + a + i) : -1;
-  };
-  ld_ids(0, d_cur, p_cur);
-  ld_ids(LPR, d_nxt, p_nxt);
-  int last_issued = -1;
-  int rp[S];      // pair id of the edge in each stage (-2: past the end)
-  bool rf[S];     // the edge is its pair's first in this stream
-#pragma unroll
-  for (int i = 0; i < S; ++i) rp[i] = -2, rf[i] = false;
-  RingStage* const my = &ring[0][threadIdx.x];
-  // issue edge q of the stream into stage st
-  auto issue = [&](int q, int st) {
-    if (q > 0 && q % LPR == 0) {  // warp-uniform: next id batch
-      d_cur = d_nxt;
-      p_cur = p_nxt;
-      ld_ids(q + LPR, d_nxt, p_nxt);
-    }
-    const int d = __shfl_sync(0xffffffffu, d_cur, src0 + q % LPR);
-    const int pp = __shfl_sync(0xffffffffu, p_cur, src0 + q % LPR);
-    const bool valid = q < L;
-    const bool first = valid && pp != last_issued;
-    RingStage* sl = my + st * RING_TB;
-    if (valid) {
-      const TP* gq = GQ + (int64_t)d * 2 * D + c * V;
-      cp_async16_ca(&sl->g, gq);
-      cp_async16_ca(&sl->q, gq + D);
-      cp_async8_ca(&sl->ns, nst + (int64_t)d * H + hd);
-      if (first) {
-        const TP* km = KM + (int64_t)pp * 2 * D + c * V;
-        cp_async16_ca(&sl->k, km);
-        cp_async16_ca(&sl->m, km + D);
-      }
-      last_issued = pp;
-    }
-    cp_async_commit();
-    rp[st] = valid ? pp : -2;
-    rf[st] = first;
-  };
-#pragma unroll
-  for (int q = 0; q < S - 1; ++q) issue(q, q);
-  uint4 kpk = make_uint4(0, 0, 0, 0), mpk = kpk;
-  float ak[V], am[V];
-#pragma unroll
-  for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-  for (int q0 = 0; q0 < span; q0 += S) {
-#pragma unroll
-    for (int st = 0; st < S; ++st) {
-      const int q = q0 + st;
-      issue(q + S - 1, (st + S - 1) % S);
-      cp_async_wait<S - 1>();  // stage st (edge q) has landed for this lane
-      const RingStage* sl = my + st * RING_TB;
-      const bool valid = rp[st] != -2;
-      if (rf[st]) {
-        kpk = lds16(&sl->k);
-        mpk = lds16(&sl->m);
-      }
-      float gr[V], qv[V], x[V];
-      cvt16<TP>(valid ? lds16(&sl->g) : make_uint4(0, 0, 0, 0), gr);
-      cvt16<TP>(valid ? lds16(&sl->q) : make_uint4(0, 0, 0, 0), qv);
-      const float2 ns = valid ? lds8(&sl->ns) : make_float2(CUDART_INF_F, 0.f);
-      float l = 0.f, da = 0.f;
-      cvt16<TP>(kpk, x);
-#pragma unroll
-      for (int k = 0; k < V; ++k) l = fmaf(x[k], qv[k], l);
-      cvt16<TP>(mpk, x);
-#pragma unroll
-      for (int k = 0; k < V; ++k) da = fmaf(gr[k], x[k], da);
-      l = gsum<LH>(l, 0xffffffffu);
-      da = gsum<LH>(da, 0xffffffffu);
-      const float alpha = __expf(l - ns.x);  // 0 past the end (lse = +inf)
-      const float dl = alpha * (da - ns.y);
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        ak[k] = fmaf(dl, qv[k], ak[k]);
-        am[k] = fmaf(alpha, gr[k], am[k]);
-      }
-      if (valid && rp[(st + 1) % S] != rp[st]) {  // the stream leaves pair rp[st]: write its rows
-        if (slot >= 0) {
-          float* o = pacc + (int64_t)slot * 2 * D;
-          st_f32<V>(o + c * V, ak);
-          st_f32<V>(o + D + c * V, am);
-        } else {
-          TP* o = dKM + (int64_t)rp[st] * 2 * D;
-          st_tp<V>(o + c * V, ak);
-          st_tp<V>(o + D + c * V, am);
-        }
-#pragma unroll
-        for (int k = 0; k < V; ++k) ak[k] = am[k] = 0.f;
-      }
-    }
-  }
-  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ weighted pair SpMM (A7)
@@ -1916,6 +1834,16 @@ inline bool stage_pair_rows() {
   return on;
 }
 
+// RGNN_SPLIT=0: the staged group-mode HGT pair kernel (8 columns per lane, 60 registers) instead of the
+// split-halves one on bf16 tables (measured equal on mag HGT: 0.833 vs 0.836 ms for the group half)
+inline bool pair_split() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_SPLIT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 inline dim3 warps(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
 inline dim3 groups(int64_t n, int lpr) { return dim3(ceil_div(ceil_div(n, 32 / lpr) * (int64_t)32, 256)); }
 
@@ -1949,6 +1877,9 @@ inline bool use_short() {
 template <int KI, class KW, class KG, class KS, class... Args, class... SArgs>
 void launch_plan_short(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, KS ks,
                        std::tuple<SArgs...> sargs, cudaStream_t s, Args... args) {
+  // lpr: lanes per item of the group kernel (low 8 bits) and of the short kernel (bits 8..15, 0 = same)
+  const int lpr_s = (lpr >> 8) ? (lpr >> 8) : lpr;
+  lpr &= 0xff;
   if (!use_short()) {
     launch_plan(name, wp, lpr, kw, kg, s, args...);
     return;
@@ -1962,7 +1893,7 @@ void launch_plan_short(const char* name, const WorkPlan& wp, int lpr, KW kw, KG 
   launch(intern(std::string(name) + "/warp"), kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp,
          (const int4*)wp.items, args...);
   std::apply([&](auto... a) {
-    launch(intern(std::string(name) + "/short"), ks, groups(ceil_div(ns, KI), lpr), dim3(256), 0, s, ns,
+    launch(intern(std::string(name) + "/short"), ks, groups(ceil_div(ns, KI), lpr_s), dim3(256), 0, s, ns,
            (const int4*)(wp.items + wp.n_short), a...);
   }, sargs);
   join_side(s);
@@ -2155,15 +2086,6 @@ void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const
   });
 }
 
-// RGNN_RING=0 selects the work-plan pair kernels (warp / staged group / short) instead of the gather ring
-inline bool use_ring() {
-  static const bool on = [] {
-    const char* v = getenv("RGNN_RING");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
                   const float2* wts, void* dKM, bool skip_single, const Partial& pt, cudaStream_t s) {
   if (wts) {  // weighted SpMM: [dM | dK~] = sum_e [alpha_e G_d | dl_e Q_d] (weights from hgt_bwd_dst)
@@ -2182,27 +2104,6 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
                  pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc2csr,
                  (const int32_t*)g->csc_pair, static_cast<const TP*>(GQ), wts, o + DD, o, (int64_t)2 * DD,
                  (float*)nullptr, DD, 0);
-        });
-        launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
-               g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
-      });
-    });
-    return;
-  }
-  if (use_ring()) {
-    const int64_t nch = skip_single ? g->pairs.n_chunks_multi : g->pairs.n_chunks;
-    const int4* ch = skip_single ? g->pairs.chunks_multi : g->pairs.chunks;
-    by_width(D, [&](auto Dc) {
-      constexpr int DD = decltype(Dc)::value;
-      by_dtype(dtype, [&](auto* tp) {
-        using TP = std::remove_pointer_t<decltype(tp)>;
-        constexpr int LPR = Geo<TP, DD>::LPR;
-        by_heads<LPR>(H, [&](auto hc) {
-          constexpr int HH = decltype(hc)::value;
-          launch("hgt_bwd_pair", k_hgt_bwd_pair_ring<TP, DD, HH, RGNN_RING_S>,
-                 dim3(ceil_div(ceil_div(nch, 32 / LPR) * (int64_t)32, RING_TB)), dim3(RING_TB), 0, s, nch, ch,
-                 pt.acc, (const int32_t*)g->csc_dst, (const int32_t*)g->csc_pair, static_cast<const TP*>(KM),
-                 static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
         });
         launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
                g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);
@@ -2229,6 +2130,18 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
                                s, pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
                                static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
         };
+        if constexpr (std::is_same_v<TP, bf16> && DD / 4 <= 32 && (DD / 8) % HH == 0) {
+          if (pair_split()) {  // group mode: split halves, D / 4 lanes per pair; warp and short halves as before
+            launch_plan_short<2>("hgt_bwd_pair", wp, DD / 4 | Geo<TP, DD>::LPR << 8,
+                                 k_hgt_bwd_pair<TP, DD, false, HH>, k_hgt_bwd_pair_sp<DD, HH, 8>,
+                                 k_hgt_bwd_pair_k<TP, DD, HH, 2>,
+                                 std::make_tuple((const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
+                                                 static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM)),
+                                 s, pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM),
+                                 static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
+            return;
+          }
+        }
         if (stage_pair_rows()) go(k_hgt_bwd_pair_s<TP, DD, HH, RGNN_UNR_S>);
         else go(k_hgt_bwd_pair<TP, DD, true, HH>);
       });
