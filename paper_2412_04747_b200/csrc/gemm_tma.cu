@@ -1,0 +1,318 @@
+// A1 / A8 node and pair GEMMs on tcgen05 with TMA tile movement (bf16 operands, fp32 accumulation):
+// the typed segment GEMM Y[row] = X[gather(row)] x W_w of the GEMM template Y[S] = X[G] x W[T]
+// (§3.3.3; compact rows P:764-776), persistent and warp-specialized.
+//
+//   warp 4  (one elected lane) producer: per 64-wide K block of an item (128-row tile x NT columns of
+//           one weight segment) it arms the stage's mbarrier with the stage's byte count and issues
+//           the TMA loads -- A as one 2D box of 128 rows (contiguous A) or as 32 tile::gather4 loads
+//           of 4 rows each (A = X[pair_src], the row indices shuffled to the issuing lane), B as one
+//           2D box of the K-major weight image -- all 128B-swizzled by the TMA unit into the canonical
+//           UMMA K-major layout.  No thread touches operand bytes.
+//   warp 5  MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M = 128, N = NT, K = 16) into one of two
+//           TMEM accumulators; tcgen05.commit frees the stage and publishes the accumulator.
+//   warps 0-3 epilogue (TMEM lane quarters): tcgen05.ld, optional per-row dot (RGAT s_p = P_p . a_r,
+//           P:962), pack to the output dtype into a 128B-swizzled staging box and one TMA 2D store
+//           per 32 rows x 128 bytes (rows that end a segment mid-warp are stored by the lanes).
+// The previous generation (gemm_tc.cu k_gemm_ws / k_gemm_tc) moves the same tiles with per-thread
+// cp.async; this kernel replaces them for every GEMM without the fused per-source row reduction.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "ops.cuh"
+#include "tc_ptx.cuh"
+
+namespace rgnn {
+namespace {
+using namespace tc;
+
+// ---------------------------------------------------------------- host: tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// row-major [rows][cols] tensor of `esz`-byte elements, box {bcols, brows}, 128-byte swizzle
+CUtensorMap make_map(const void* base, int esz, int64_t cols, int64_t rows, int bcols, int brows, bool l2_256) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)bcols, (cuuint32_t)brows}, es[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                 const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B,
+                                 l2_256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RGNN_CHECK(r == CUDA_SUCCESS, RGNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// ---------------------------------------------------------------- kernel
+template <int NT, class TY>
+struct TmaCfg {
+  static constexpr int NCOLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+  static constexpr uint32_t A_BYTES = 128 * 128;
+  static constexpr uint32_t B_BYTES = NT * 128;
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr int RB = NT * (int)sizeof(TY);   // output row bytes of an item
+  static constexpr int CB = RB < 128 ? RB : 128;    // staged row-chunk bytes
+  static constexpr int CC = CB / (int)sizeof(TY);   // columns per chunk
+  static constexpr int PC = CB / 16;                // 16-byte pieces per chunk row
+  static constexpr bool TMA_Y = CB == 128;          // TMA store needs a full 128B-swizzle row
+  static constexpr uint32_t STG = 32 * 128;         // one staging buffer of a warp (32 rows)
+  static constexpr uint32_t STAGING = 4 * 2 * STG;  // 4 epilogue warps, double-buffered
+  static constexpr int S_FIT = (int)((220 * 1024 - STAGING) / STAGE);
+  static constexpr int S = S_FIT < 8 ? S_FIT : 8;
+  static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + STAGING + 256;
+};
+
+template <class TY, int NT, bool GATHER>
+__global__ void __launch_bounds__(192, 1) k_gemm_tma(const __grid_constant__ CUtensorMap tmA,
+                                                     const __grid_constant__ CUtensorMap tmB,
+                                                     const __grid_constant__ CUtensorMap tmY,
+                                                     const Tile* __restrict__ tiles, int ntiles, int nblk,
+                                                     const int32_t* __restrict__ gather, int K, int ntot,
+                                                     TY* __restrict__ Y, const float* __restrict__ dotvec,
+                                                     float* __restrict__ dotout) {
+  using C = TmaCfg<NT, TY>;
+  constexpr int S = C::S;
+  static_assert(S >= 2, "not enough shared memory for two stages");
+  const int KB = K >> 6, nitems = ntiles * nblk;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* staging = smem + S * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t s_base = smem_u32(smem);
+
+  if (warp == 5) tmem_alloc<2 * C::NCOLS>(tslot);
+  if (tid == 128) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (C::TMA_Y) tma_prefetch_desc(&tmY);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 4) {
+    // ------------------------------------------------ TMA producer
+    int st = 0;
+    uint32_t ph = 0;
+    int ridx[4] = {0, 0, 0, 0};  // GATHER: A row indices of tile rows lane + 32 m (clamped to the tile)
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int ti = it / nblk, nb = it - ti * nblk;
+      const Tile t = tiles[ti];
+      if (GATHER) {
+        const int nrows = t.row1 - t.row0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int r = lane + 32 * m;
+          ridx[m] = __ldg(gather + t.row0 + (r < nrows ? r : nrows - 1));
+        }
+      }
+      const int yb = t.w * ntot + nb * NT;
+      for (int kb = 0; kb < KB; ++kb) {
+        if (lane == 0) {
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_expect_tx(&full[st], C::STAGE);
+        }
+        __syncwarp();
+        const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
+        if (GATHER) {
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3: lanes 4(j%8) .. 4(j%8)+3, register j/8
+            const int m = j >> 3, l0 = (j & 7) * 4;
+            const int v = m == 0 ? ridx[0] : m == 1 ? ridx[1] : m == 2 ? ridx[2] : ridx[3];
+            const int y0 = __shfl_sync(0xffffffffu, v, l0), y1 = __shfl_sync(0xffffffffu, v, l0 + 1);
+            const int y2 = __shfl_sync(0xffffffffu, v, l0 + 2), y3 = __shfl_sync(0xffffffffu, v, l0 + 3);
+            if (lane == 0) tma_gather4(sa + j * 512, &tmA, kb * 64, y0, y1, y2, y3, &full[st]);
+          }
+        } else if (lane == 0) {
+          tma_load_2d(sa, &tmA, kb * 64, t.row0, &full[st]);
+        }
+        if (lane == 0) tma_load_2d(sb, &tmB, kb * 64, yb, &full[st]);
+        if (++st == S) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(NT);
+      int st = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);  // the epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d_tmem = tmem + acc * C::NCOLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), idesc, (kb | k) ? 1u : 0u);
+          umma_commit(&empty[st]);  // stage free once these MMAs have read it
+          if (++st == S) { st = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull[acc]);  // accumulator complete
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quarters)
+    constexpr int NV = C::CC < 32 ? C::CC : 32;
+    const int q = warp;
+    uint8_t* stg0 = staging + q * 2 * C::STG;
+    int acc = 0, buf = 0;
+    uint32_t aph = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int ti = it / nblk, nb = it - ti * nblk;
+      const Tile t = tiles[ti];
+      const int nrows = t.row1 - t.row0;
+      const int rows_here = min(32, nrows - q * 32);
+      const int64_t row0 = t.row0 + (int64_t)q * 32;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tb = tmem + acc * C::NCOLS + ((uint32_t)(q * 32) << 16);
+      float dot = 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += C::CC) {
+        uint8_t* stg = stg0 + buf * C::STG;
+        if (C::TMA_Y) {  // the store issued from this buffer two chunks ago has finished reading it
+          if (lane == 0) tma_store_wait_read<1>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int s0 = 0; s0 < C::CC; s0 += 32) {
+          float v[32];
+          tmem_ld32(tb + c0 + s0, v);
+          if (dotvec) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) dot = fmaf(v[i], __ldg(dotvec + (size_t)t.w * ntot + nb * NT + c0 + s0 + i), dot);
+          }
+          stage_vals<TY, NV, C::PC>(stg + lane * C::CB, lane, s0 * (int)sizeof(TY) / 16, v);
+        }
+        if (C::TMA_Y && rows_here == 32) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // staged rows -> async proxy
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, nb * NT + c0, (int)row0, smem_u32(stg));
+            tma_store_commit();
+          }
+        } else {
+          __syncwarp();
+          uint8_t* ybase = reinterpret_cast<uint8_t*>(Y + row0 * ntot + (int64_t)nb * NT + c0);
+          const int64_t ystride = (int64_t)ntot * sizeof(TY);
+#pragma unroll
+          for (int k = lane; k < 32 * C::PC; k += 32) {
+            const int rr = k / C::PC, j = k % C::PC;
+            if (rr < rows_here)
+              *reinterpret_cast<uint4*>(ybase + rr * ystride + j * 16) =
+                  *reinterpret_cast<const uint4*>(stg + rr * C::CB + ((j ^ (rr & (C::PC - 1))) << 4));
+          }
+          __syncwarp();
+        }
+        buf ^= 1;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&tempty[acc]);  // TMEM reads done: the MMA warp may reuse this accumulator
+      if (dotvec && lane < rows_here) dotout[row0 + lane] = dot;
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+    if (C::TMA_Y && lane == 0) tma_store_wait<0>();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<2 * C::NCOLS>(tmem);
+}
+
+template <class TY, int NT>
+void launch_tma(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  using C = TmaCfg<NT, TY>;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    RGNN_CUDA(cudaGetDevice(&dev));
+    RGNN_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    RGNN_CUDA(cudaFuncSetAttribute(k_gemm_tma<TY, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    RGNN_CUDA(cudaFuncSetAttribute(k_gemm_tma<TY, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  }
+  const int nblk = a.N / NT;
+  const int grid = std::min(a.ntiles * nblk, num_sms);
+  // A: gathered rows come one at a time (box {64, 1}); the table's row count only bounds the map
+  const int64_t a_rows = a.gather ? (a.a_rows > 0 ? a.a_rows : ((int64_t)1 << 31) - 1) : a.y_rows;
+  const CUtensorMap tmA = make_map(a.A, 2, a.K, a_rows, 64, a.gather ? 1 : 128, a.gather == nullptr);
+  const CUtensorMap tmB = make_map(Bt, 2, a.K, (int64_t)a.num_w * a.N, 64, NT, true);
+  const CUtensorMap tmY = C::TMA_Y ? make_map(a.Y, (int)sizeof(TY), a.N, a.y_rows, C::CC, 32, true) : tmB;
+  if (a.gather)
+    launch(a.name, k_gemm_tma<TY, NT, true>, dim3(grid), dim3(192), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles, nblk,
+           a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+  else
+    launch(a.name, k_gemm_tma<TY, NT, false>, dim3(grid), dim3(192), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles,
+           nblk, a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+}
+
+template <class TY>
+void tma_by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  switch (a.N < 256 ? a.N : 256) {
+    case 16: launch_tma<TY, 16>(a, Bt, s); break;
+    case 32: launch_tma<TY, 32>(a, Bt, s); break;
+    case 64: launch_tma<TY, 64>(a, Bt, s); break;
+    case 128: launch_tma<TY, 128>(a, Bt, s); break;
+    case 256: launch_tma<TY, 256>(a, Bt, s); break;
+    default: RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "tcgen05 gemm: N");
+  }
+}
+
+}  // namespace
+
+// Contiguous A (node GEMMs, ungathered segment GEMMs) runs here.  Gathered A stays on the cp.async
+// kernels by default: a tile::gather4 moves 4 x 128 B per instruction and one producer thread per SM
+// cannot issue them fast enough (mag pair GEMM at d = 64: 0.74 ms vs 0.24 ms for k_gemm_tc, whose
+// 128 threads per CTA and ~9 CTAs per SM keep more row gathers in flight).
+// RGNN_TMA=0: never (the cp.async generation for every GEMM); RGNN_TMA=2: gathered A as well.
+bool gemm_tma_enabled(const GemmArgs& a) {
+  static const int mode = [] {
+    const char* v = getenv("RGNN_TMA");
+    return v ? atoi(v) : 1;
+  }();
+  if (mode == 0 || encode_fn() == nullptr) return false;
+  if (a.gather != nullptr && mode != 2) return false;
+  if (a.red_ptr != nullptr || a.y_rows <= 0) return false;  // fused row reduction: k_gemm_tc only
+  // TMA: 16-byte aligned bases and row strides
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return al(a.A) && al(a.Y) && (a.K * 2) % 16 == 0;
+}
+
+void gemm_tma(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
+  if (a.y_dtype == BF16) tma_by_n<bf16>(a, Bt, s);
+  else tma_by_n<float>(a, Bt, s);
+}
+
+}  // namespace rgnn

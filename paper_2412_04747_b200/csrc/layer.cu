@@ -396,6 +396,8 @@ bool gemm(const Ctx& c, const Segs& sg, GemmArgs a) {
     const Plan& p = plan(c.g, sg, TC_ROWS, c.s);
     a.tiles = p.tiles;
     a.ntiles = p.count;
+    a.y_rows = sg.ptr.empty() ? 0 : sg.ptr.back();
+    a.a_rows = a.gather ? c.g->N : a.y_rows;
     gemm_tc(a, c.s);
     return true;
   }

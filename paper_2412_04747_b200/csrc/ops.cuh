@@ -33,10 +33,15 @@ struct GemmArgs {
   int red_dtype = F32;
   int num_w = 0;                  // number of weight matrices in B (tcgen05 path: K-major image size)
   void* bt_scratch = nullptr;     // tcgen05 path: device buffer for num_w*K*N bf16 (K-major B image)
+  int64_t y_rows = 0;             // rows of Y (and of A when not gathered); 0: unknown (no TMA path)
+  int64_t a_rows = 0;             // rows of the gathered A table (0: unknown; bounds the TMA map only)
 };
 void gemm_simt(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& a);
 void gemm_tc(const GemmArgs& a, cudaStream_t s);
+// TMA generation of the tcgen05 GEMM (gemm_tma.cu), used by gemm_tc when enabled and applicable
+bool gemm_tma_enabled(const GemmArgs& a);
+void gemm_tma(const GemmArgs& a, const bf16* Bt, cudaStream_t s);
 
 // Segmented weight gradient  out[w] = sum_{rows of w} A[gather(row)]^T Bm[row]   (fp32 out)
 // Deterministic two-level reduction: per-tile partials, then per-segment sums in tile order.

@@ -131,6 +131,7 @@ rgnn_status rgnn_segment_gemm(rgnn_segments_t p, int32_t dtype, const void* X, c
       a.bt_scratch = scratch;
       a.tiles = p->tiles_tc;
       a.ntiles = p->n_tc;
+      a.y_rows = p->rows;
       RGNN_CHECK(gemm_tc_supported(a), RGNN_ERR_UNSUPPORTED,
                  "bf16 segment GEMM: K must be a multiple of 64 (<= 8192), N one of 16/32/64/128 or a multiple of 256");
       gemm_tc(a, s);

@@ -37,12 +37,11 @@ def main():
     plan = SegmentPlan(seg_ptr)
     gen = torch.Generator(device="cuda").manual_seed(2)
     for d in [int(x) for x in args.dims.split(",")]:
-        X = (torch.rand(g.num_nodes, d, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16)
+        # gathered: X has one row per node; ungathered: one row per pair (row r of Y reads row r of X)
+        X = (torch.rand(g.num_nodes if not args.no_gather else U, d, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16)
         W = ((torch.rand(g.num_rels, d, d, device="cuda", generator=gen) * 2 - 1) * (3.0 / d) ** 0.5).to(torch.bfloat16)
         Y = torch.empty(U, d, dtype=torch.bfloat16, device="cuda")
         gather = None if args.no_gather else pair_src
-        if args.no_gather:
-            X = X[:U].contiguous()
         scratch = torch.empty(g.num_rels * d * d * 2, dtype=torch.uint8, device="cuda")
         for _ in range(3):
             segment_gemm(plan, X, W, gather=gather, out=Y, scratch=scratch)
