@@ -359,6 +359,41 @@ def cpu_oracle_sample(g, model, inp, Gh, target_s=15.0, seed=0):
             "seconds": elapsed}
 
 
+def cpu_oracle_grouped(g, model, inp, Gh, max_edges=None, threads=None, seed=0):
+    """Time the fp64 oracle in its grouped mode (oracle/grouped.c: plain C + OpenMP, one product per
+    distinct (relation, node) pair -- exact by P:775 -- cross-checked against the per-edge oracle by
+    tests/test_oracle_grouped.py) on the FULL graph, or, with max_edges, on the in-edge subgraph of
+    random destinations holding about that many edges."""
+    from oracle import grouped as OG
+    from oracle import layers as L
+    from oracle import sample as S
+    threads = int(threads or os.cpu_count() or 1)
+    OG.set_threads(threads)
+    norm_full = L.rgcn_edge_norm(g, "mean") if model == "rgcn" else None
+    if max_edges is None or max_edges >= g.num_edges:
+        sub, loc, Gs, norm = g, inp, Gh, norm_full
+        what = f"full graph ({g.num_nodes} nodes, {g.num_edges} edges)"
+    else:
+        rng = np.random.default_rng(seed)
+        n_dst = max(1, int(g.num_nodes * max_edges / max(1, g.num_edges)))
+        dsts = rng.choice(g.num_nodes, size=min(n_dst, g.num_nodes), replace=False)
+        _, eids = S.in_edge_subgraph(g, dsts)
+        sub, nodes = S.compact_subgraph(g, eids)
+        loc = {k: (v[nodes] if k == "X" else v) for k, v in inp.items()}
+        Gs = Gh[nodes]
+        norm = None if norm_full is None else norm_full[eids]
+        what = f"in-edge subgraph of {len(dsts)} random destinations ({sub.num_edges} edges)"
+    kw = {"norm": norm} if model == "rgcn" else {}
+    t = time.perf_counter()
+    OG.forward_backward(model, sub, loc, Gs, **kw)
+    dt = time.perf_counter() - t
+    return {"value": sub.num_edges / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
+            "sample": f"fp64 grouped oracle (oracle/grouped.c, {threads} OpenMP threads), {model.upper()} fwd+bwd on "
+                      f"the {what} in {dt:.1f} s",
+            "seconds": dt}
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -706,9 +741,16 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.infer:
-        cpu = cpu_oracle_sample(g, model, inp, Gh, target_s=args.cpu_seconds)
-        cpu["single_thread"] = single_thread(lambda t: cpu_oracle_sample(g, model, inp, Gh, target_s=t),
-                                             args.cpu_seconds / 3)
+        if cfg.get("heads", 1) == 1 and not args.no_compact:
+            # D5: nproc threads on the full graph; one thread on an in-edge sample of ~E / nproc edges
+            cpu = cpu_oracle_grouped(g, model, inp, Gh)
+            st = cpu_oracle_grouped(g, model, inp, Gh, max_edges=g.num_edges // max(1, os.cpu_count() or 1),
+                                    threads=1)
+            cpu["single_thread"] = {k: st[k] for k in ("value", "unit", "cores", "sample")}
+        else:  # heads > 1: the per-edge numpy oracle (the grouped C oracle is one-head)
+            cpu = cpu_oracle_sample(g, model, inp, Gh, target_s=args.cpu_seconds)
+            cpu["single_thread"] = single_thread(lambda t: cpu_oracle_sample(g, model, inp, Gh, target_s=t),
+                                                 args.cpu_seconds / 3)
 
     exchange = None
     if world > 1:  # bytes of variant X vs variant P per rank, and the one run
@@ -1021,13 +1063,17 @@ def run_reference(args, cfg, world, rank):
     if cfg["dtype"] == "bf16":
         inp = {k: (round_bf16(v) if k not in ("mu",) else v) for k, v in inp.items()}
     Gh = upstream_grad(g.num_nodes, d)
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    # each step: the grouped oracle on all host cores over an in-edge sample sized to ~per_step seconds
+    # (rate measured on a first small sample); the whole --steps/--warmup run stays within a few minutes
+    per_step = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    probe = cpu_oracle_grouped(g, model, inp, Gh, max_edges=max(1, g.num_edges // 64), seed=999)
+    step_edges = int(min(g.num_edges, probe["value"] * per_step))
     for i in range(args.warmup):
-        cpu_oracle_sample(g, model, inp, Gh, target_s=per_step / 4, seed=100 + i)
+        cpu_oracle_grouped(g, model, inp, Gh, max_edges=max(1, step_edges // 4), seed=100 + i)
     vals, secs, edges = [], 0.0, 0
     last = None
     for i in range(args.steps):
-        r = cpu_oracle_sample(g, model, inp, Gh, target_s=per_step, seed=i)
+        r = cpu_oracle_grouped(g, model, inp, Gh, max_edges=step_edges, seed=i)
         vals.append(r["value"])
         secs += r["seconds"]
         edges += r["value"] * r["seconds"]
