@@ -6,6 +6,7 @@
 // has no fp32 kind (SURVEY.md §0 finding 8), so fp32 GEMMs run on FFMA.  At
 // d = 64 these GEMMs are HBM-bound (arithmetic intensity 16 flop/B fp32), so
 // the kernel is organised for coalesced gathers and stores, not for FLOPs.
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -84,12 +85,159 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const Tile* __restrict__ tile
   }
 }
 
+// fp32 typed segment GEMM for N = 64 / 128 (the layer widths): 128 threads per 64-row tile, thread
+// (tx = tid % 16, ty = tid / 16) owns rows 8 ty .. 8 ty + 7 and columns 4 tx .. 4 tx + 3 (+ 64 for N = 128)
+// as packed f32x2 accumulators; A (gathered rows) and B chunks of KC = 16 k are loaded as float4 into
+// registers one chunk ahead and stored transposed (A) / as is (B) into double-buffered shared memory, so
+// each k step is 2 + N/64 16-byte shared loads for 32 N/64 packed FMAs.  FFMA only (no TF32).
+template <int N>
+__global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles, const float* __restrict__ A, int K,
+                                                  const int32_t* __restrict__ gather, const float* __restrict__ B,
+                                                  bool transB, float* __restrict__ Y, const float* __restrict__ dotvec,
+                                                  float* __restrict__ dotout) {
+  constexpr int NB = N / 64;            // 64-column halves per thread (1 or 2)
+  constexpr int BQ = KC * N / 4 / 128;  // float4 of a B chunk per thread (2 or 4)
+  __shared__ __align__(16) float As[2][KC][BM + 4];
+  __shared__ __align__(16) float Bs[2][KC][N];
+  const Tile t = tiles[blockIdx.x];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int nrows = t.row1 - t.row0;
+  const float* Bw = B + (size_t)t.w * K * N;
+  // A loader: float4 q of the 64 x 16 chunk: row (tid + 128 q) / 4, k quad (tid + 128 q) % 4
+  int64_t arow[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int r = (tid + 128 * q) >> 2;
+    arow[q] = r < nrows ? (gather ? (int64_t)gather[t.row0 + r] : (int64_t)(t.row0 + r)) : -1;
+  }
+  float4 ra[2], rb[BQ];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int kq = (tid + 128 * q) & 3;
+      ra[q] = arow[q] >= 0 ? __ldg(reinterpret_cast<const float4*>(A + arow[q] * K + k0 + 4 * kq))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < BQ; ++q) {
+      const int idx = tid + 128 * q;
+      if (!transB) {  // row kk of the chunk, 4 consecutive n
+        const int kk = idx / (N / 4), n4 = idx % (N / 4);
+        rb[q] = __ldg(reinterpret_cast<const float4*>(Bw + (size_t)(k0 + kk) * N + 4 * n4));
+      } else {  // column n, 4 consecutive k
+        const int n = idx / (KC / 4), k4 = idx % (KC / 4);
+        rb[q] = __ldg(reinterpret_cast<const float4*>(Bw + (size_t)n * K + k0 + 4 * k4));
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = (tid + 128 * q) >> 2, kq = (tid + 128 * q) & 3;
+      As[buf][4 * kq + 0][r] = ra[q].x;
+      As[buf][4 * kq + 1][r] = ra[q].y;
+      As[buf][4 * kq + 2][r] = ra[q].z;
+      As[buf][4 * kq + 3][r] = ra[q].w;
+    }
+#pragma unroll
+    for (int q = 0; q < BQ; ++q) {
+      const int idx = tid + 128 * q;
+      if (!transB) {
+        const int kk = idx / (N / 4), n4 = idx % (N / 4);
+        *reinterpret_cast<float4*>(&Bs[buf][kk][4 * n4]) = rb[q];
+      } else {
+        const int n = idx / (KC / 4), k4 = idx % (KC / 4);
+        Bs[buf][4 * k4 + 0][n] = rb[q].x;
+        Bs[buf][4 * k4 + 1][n] = rb[q].y;
+        Bs[buf][4 * k4 + 2][n] = rb[q].z;
+        Bs[buf][4 * k4 + 3][n] = rb[q].w;
+      }
+    }
+  };
+  float2 acc[8][2 * NB];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 2 * NB; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    if (k0 + KC < K) load(k0 + KC);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][8 * ty]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][8 * ty + 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float2 b[2 * NB];
+#pragma unroll
+      for (int h = 0; h < NB; ++h) {
+        const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 * h + 4 * tx]);
+        b[2 * h] = make_float2(b4.x, b4.y);
+        b[2 * h + 1] = make_float2(b4.z, b4.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 2 * NB; ++j) acc[i][j] = __ffma2_rn(b[j], make_float2(a[i], a[i]), acc[i][j]);
+    }
+    if (k0 + KC < K) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int lrow = 8 * ty + i;
+    const int64_t row = t.row0 + lrow;
+    if (dotvec) {  // per-row scalar epilogue
+      float d = 0.f;
+#pragma unroll
+      for (int h = 0; h < NB; ++h) {
+        const float* dv = dotvec + (size_t)t.w * N + 64 * h + 4 * tx;
+        d = fmaf(acc[i][2 * h].x, dv[0], d);
+        d = fmaf(acc[i][2 * h].y, dv[1], d);
+        d = fmaf(acc[i][2 * h + 1].x, dv[2], d);
+        d = fmaf(acc[i][2 * h + 1].y, dv[3], d);
+      }
+      d = group_sum<16>(d);
+      if (tx == 0 && lrow < nrows) dotout[row] = d;
+    }
+    if (lrow < nrows) {
+#pragma unroll
+      for (int h = 0; h < NB; ++h)
+        *reinterpret_cast<float4*>(Y + row * N + 64 * h + 4 * tx) =
+            make_float4(acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y);
+    }
+  }
+}
+
 template <class TA, class TB, class TY>
 void gemm_dispatch(const GemmArgs& a, cudaStream_t s) {
   const TA* A = static_cast<const TA*>(a.A);
   const TB* B = static_cast<const TB*>(a.B);
   TY* Y = static_cast<TY*>(a.Y);
   dim3 g(a.ntiles), b(256);
+  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TB, float> && std::is_same_v<TY, float>) {
+    // RGNN_F32GEMM=0 keeps the 4 x 4-per-thread kernel for every width (A/B switch)
+    static const bool f32k = [] {
+      const char* v = getenv("RGNN_F32GEMM");
+      return !(v && v[0] == '0');
+    }();
+    const bool al = (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0;
+    if (f32k && al && (a.N == 64 || a.N == 128)) {
+      if (a.N == 64)
+        launch(a.name, k_gemm_f32<64>, g, dim3(128), 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, a.dotvec,
+               a.dotout);
+      else
+        launch(a.name, k_gemm_f32<128>, g, dim3(128), 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, a.dotvec,
+               a.dotout);
+      return;
+    }
+  }
 #define RGNN_GEMM_CASE(NN)                                                                                  \
   case NN:                                                                                                  \
     launch(a.name, k_gemm_simt<TA, TB, TY, NN>, g, b, 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, \
@@ -155,6 +303,79 @@ __global__ void __launch_bounds__(256) k_wgrad(const Tile* __restrict__ tiles, c
       int k2 = k2_0 + tx + 16 * j;
       if (k2 < K2) out[(size_t)k1 * K2 + k2] = acc[i][j];
     }
+  }
+}
+
+// fp32 weight gradient, 64 x 64 output block per CTA (grid as k_wgrad): 128 threads, thread (tx, ty) owns
+// k1 = 8 ty .. 8 ty + 7 and k2 = 4 tx .. 4 tx + 3 as packed f32x2 accumulators; rows stream in chunks of
+// 16 through double-buffered shared memory (float4 loads one chunk ahead, no transposition: both
+// operands are read along their row), 3 16-byte shared loads per 16 packed FMAs.  Requires K1, K2
+// multiples of 64 and 16-byte aligned rows.
+__global__ void __launch_bounds__(128) k_wgrad_f32(const Tile* __restrict__ tiles, const float* __restrict__ A,
+                                                   int K1, const int32_t* __restrict__ gather,
+                                                   const float* __restrict__ Bm, int K2, float* __restrict__ partial) {
+  constexpr int RC = 16;
+  __shared__ __align__(16) float As[2][RC][64 + 4];
+  __shared__ __align__(16) float Bs[2][RC][64 + 4];
+  const Tile t = tiles[blockIdx.x];
+  const int k1_0 = blockIdx.y * 64, k2_0 = blockIdx.z * 64;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float2 acc[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  float4 ra[2], rb[2];
+  // loader: float4 q of a 16 x 64 chunk: row (tid + 128 q) / 16, column quad (tid + 128 q) % 16
+  auto load = [&](int r0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = tid + 128 * q, rr = idx >> 4, c4 = idx & 15;
+      const int r = r0 + rr;
+      const bool ok = r < t.row1;
+      const int64_t ar = ok ? (gather ? (int64_t)gather[r] : (int64_t)r) : 0;
+      ra[q] = ok ? __ldg(reinterpret_cast<const float4*>(A + ar * K1 + k1_0 + 4 * c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      rb[q] = ok ? __ldg(reinterpret_cast<const float4*>(Bm + (int64_t)r * K2 + k2_0 + 4 * c4))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = tid + 128 * q, rr = idx >> 4, c4 = idx & 15;
+      *reinterpret_cast<float4*>(&As[buf][rr][4 * c4]) = ra[q];
+      *reinterpret_cast<float4*>(&Bs[buf][rr][4 * c4]) = rb[q];
+    }
+  };
+  load(t.row0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int r0 = t.row0; r0 < t.row1; r0 += RC) {
+    if (r0 + RC < t.row1) load(r0 + RC);
+#pragma unroll
+    for (int rr = 0; rr < RC; ++rr) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][rr][8 * ty]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][rr][8 * ty + 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][rr][4 * tx]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 b0 = make_float2(b4.x, b4.y), b1 = make_float2(b4.z, b4.w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[i][0] = __ffma2_rn(b0, make_float2(a[i], a[i]), acc[i][0]);
+        acc[i][1] = __ffma2_rn(b1, make_float2(a[i], a[i]), acc[i][1]);
+      }
+    }
+    if (r0 + RC < t.row1) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  float* out = partial + (size_t)blockIdx.x * K1 * K2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k1 = k1_0 + 8 * ty + i;
+    *reinterpret_cast<float4*>(out + (size_t)k1 * K2 + k2_0 + 4 * tx) =
+        make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
   }
 }
 
@@ -542,7 +763,15 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
     launch(a.name, k_wgrad<TA, TB>, g, dim3(256), 0, s, p.tiles, A, a.K1, a.gather, B, a.K2, a.partial);
   };
   const bool a32 = a.a_dtype == F32, b32 = a.b_dtype == F32;
-  if (a32 && b32) go(static_cast<const float*>(a.A), static_cast<const float*>(a.Bm));
+  static const bool f32k = [] {  // RGNN_F32GEMM=0: the 4 x 4-per-thread weight-gradient kernel (A/B switch)
+    const char* v = getenv("RGNN_F32GEMM");
+    return !(v && v[0] == '0');
+  }();
+  const bool al = (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.Bm) & 15) == 0;
+  if (a32 && b32 && f32k && al && a.K1 % 64 == 0 && a.K2 % 64 == 0)
+    launch(a.name, k_wgrad_f32, g, dim3(128), 0, s, p.tiles, static_cast<const float*>(a.A), a.K1, a.gather,
+           static_cast<const float*>(a.Bm), a.K2, a.partial);
+  else if (a32 && b32) go(static_cast<const float*>(a.A), static_cast<const float*>(a.Bm));
   else if (a32) go(static_cast<const float*>(a.A), static_cast<const bf16*>(a.Bm));
   else if (b32) go(static_cast<const bf16*>(a.A), static_cast<const float*>(a.Bm));
   else go(static_cast<const bf16*>(a.A), static_cast<const bf16*>(a.Bm));
