@@ -908,6 +908,38 @@ void dpair_expand(const rgnn_graph_s* g, const float* tdp, float* te, cudaStream
          (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, tdp, te);
 }
 
+// dt[j] = sum of w[i].y over the CSR entries of (rel, dst) run j.  A warp owns 32 consecutive runs: each
+// lane sums its run when it has at most 32 entries; the longer runs of the warp (skewed in-degrees: a mag
+// hub has ~10^5 in-edges per relation) are then summed by the whole warp, one after the other, in lane
+// order with a fixed shuffle tree (deterministic).
+__global__ void k_dpair_sum_w(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
+                              const float2* __restrict__ w, float* __restrict__ dt) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = j < UD ? beg[j] : 0, n = j < UD ? cnt[j] : 0;
+  const bool longrun = n > 32;
+  if (j < UD && !longrun) {
+    float acc = 0.f;
+    for (int i = b; i < b + n; ++i) acc += w[i].y;
+    dt[j] = acc;
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, longrun);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
+    float acc = 0.f;
+    for (int i = lane; i < nn; i += 32) acc += w[bb + i].y;
+    acc = group_sum<32>(acc);
+    if (lane == src) dt[j] = acc;
+  }
+}
+
+void dpair_sum_w(const rgnn_graph_s* g, const float2* w, float* dt, cudaStream_t s) {
+  launch("dpair_sum", k_dpair_sum_w, dim3(ceil_div(g->UD, 256)), dim3(256), 0, s, g->UD,
+         (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, w, dt);
+}
+
 void dpair_sum(const rgnn_graph_s* g, const float* dz, float* dt, cudaStream_t s) {
   launch("dpair_sum", k_dpair_sum, dim3(ceil_div(g->UD * 32, 256)), dim3(256), 0, s, g->UD,
          (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, dz, dt);

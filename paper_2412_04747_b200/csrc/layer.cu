@@ -247,6 +247,23 @@ bool pair_spmm() {
   return on;
 }
 
+// RGAT pair pass, two designs:
+//  * recompute: the pair pass re-derives z_e / alpha_e / dz_e per edge from [G_v | X_v] records (256 B per
+//    edge at d = 64 bf16) and writes per-pair bx rows, summed per relation into B_r;
+//  * weighted SpMM: the destination pass writes (alpha_e, dz_e) per CSR entry, the pair pass gathers only the
+//    G rows (128 B per edge) and B_r is a weighted row sum of X over the (rel, dst) runs of dz.
+// The SpMM wins when the (rel, dst) runs are short (AM, E/UD = 2.4: 2.53 -> 2.39 ms per step); on mag
+// (E/UD = 14.5: long runs, one hub row) the run sums and the weight writes cost more than the gather saves
+// (4.81 -> 4.85 ms), so it is chosen when E <= 8 UD.  RGNN_RGATW=0 / 1 forces either.
+bool rgat_spmm(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
+  static const int mode = [] {
+    const char* v = getenv("RGNN_RGATW");
+    return v ? atoi(v) : -1;
+  }();
+  if (d->model != RGNN_RGAT || d->no_reorder || mode == 0) return false;
+  return mode == 1 || g->E <= 8 * g->UD;
+}
+
 // elements of the largest K-major weight image any GEMM of the layer builds (tcgen05 path)
 int64_t bt_elems(const Ctx& c) {
   const int64_t R = c.g->R, T = c.g->T, Din = c.Din, D = c.D;
@@ -300,7 +317,13 @@ void layout_bwd_scratch(const Ctx& c, Arena& ar, BwdScratch& o) {
     o.dXp = ar.take<char>(U * c.Din * c.esz);
     o.dQ = ar.take<float>(N * c.D);
     o.wsum = ar.take<float>(U);
-    o.bx = ar.take<char>(U * c.D * c.esz);
+    if (rgat_spmm(g, c.d)) {
+      o.wts = ar.take<float2>(E);
+      o.dt = ar.take<float>(std::max<int64_t>(g->UD, 1));
+      width = std::max(width, (int64_t)c.D * count_tiles(seg_dpair_rel(g), WSUM_ROWS));
+    } else {
+      o.bx = ar.take<char>(U * c.D * c.esz);
+    }
     o.Bsum = ar.take<float>(R * c.Din);
     o.GQ = ar.take<char>(N * 2 * c.D * c.esz);
     o.nst = ar.take<float4>(N);
@@ -620,9 +643,9 @@ void rgat_backward_nr(const Ctx& c, const void* X, const rgnn_weights* w, const 
                       const float* G, float* dX, const rgnn_weight_grads* dW, const BwdScratch& sc) {
   rgnn_graph_s* g = c.g;
   rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, nullptr, sv.te, sc.dz, c.d->leaky_slope, sv.stats, G, out, nullptr,
-               sc.GQ, sc.nst, nullptr, nullptr, nullptr, nullptr, nullptr, sc.pt, c.s);
-  rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, nullptr, sv.te, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
-                nullptr, false, sc.pt, c.s);
+               sc.GQ, sc.nst, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sc.pt, c.s);
+  rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, nullptr, sv.te, w->a, c.d->leaky_slope, sc.GQ, sc.nst, nullptr, sc.dP,
+                sc.wsum, nullptr, false, sc.pt, c.s);
   dpair_sum(g, sc.dz, sc.dt, c.s);
   const bool dst_side = dX || dW->dW;
   if (dst_side) dpair_outer(plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s), sc.dt, w->b, c.dt, c.D, sc.dPt, c.s);
@@ -704,9 +727,10 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
     const bool single = single_in_dst(g);
     rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nullptr, nullptr, c.d->leaky_slope, sv.stats, G, out, dXt,
-                 sc.GQ, sc.nst, single ? g->csr_single : nullptr, w->a, sc.dP, sc.bx, sc.wsum, sc.pt, c.s);
-    rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, nullptr, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.dP, sc.wsum,
-                  sc.bx, single, sc.pt, c.s);
+                 sc.GQ, sc.wts ? nullptr : sc.nst, single ? g->csr_single : nullptr, w->a, sc.dP,
+                 sc.wts ? nullptr : sc.bx, sc.wsum, sc.wts, sc.pt, c.s);
+    rgat_bwd_pair(g, c.dt, c.D, sv.P, sv.spair, sv.y, nullptr, w->a, c.d->leaky_slope, sc.GQ, sc.nst, sc.wts, sc.dP,
+                  sc.wsum, sc.bx, single, sc.pt, c.s);
     const bool fused = dX && dW->dW &&
                        fused_pair_bwd(c, seg_pair_rel(g), X, sc.dP, c.D, w->W, sc.dXp, dW->dW, g->R, sc.partial);
     if (dX) {
@@ -718,7 +742,11 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       if (!fused) gemm(c, seg_pair_rel(g), a);
       reduce_pair_rows(c, sc.dXp, c.Din, dX, true);  // owned rows hold the t-path term of the dst pass
     }
-    if (dW->dW || dW->db) {  // B_r = sum_{e in r} dz_e X[d_e] = sum of the per-pair bx rows of relation r
+    if ((dW->dW || dW->db) && sc.wts) {  // B_r = sum_{e in r} dz_e X[d_e]: dz summed per (rel, dst) run, then
+      dpair_sum_w(g, sc.wts, sc.dt, c.s);  // a weighted row sum of X[dpair_dst] per relation
+      const Plan& pp = plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s);
+      seg_wsum(&pp, sc.dt, X, c.dt, c.D, g->dpair_dst, sc.Bsum, g->R, sc.partial, c.s);
+    } else if (dW->dW || dW->db) {  // B_r = the sum of the per-pair bx rows of relation r
       const Plan& pp = plan(g, seg_pair_rel(g), WSUM_ROWS, c.s);
       seg_wsum(&pp, nullptr, sc.bx, c.dt, c.D, nullptr, sc.Bsum, g->R, sc.partial, c.s);
     }

@@ -52,6 +52,9 @@ constexpr int UNR = RGNN_UNR_D;  // edges per group loaded ahead (dst-major and 
 #else
 #define RGNN_RGAT_DST_LB __launch_bounds__(256)
 #endif
+#ifndef RGNN_UNR_WT
+#define RGNN_UNR_WT 2
+#endif
 #ifndef RGNN_DST_MINB
 #define RGNN_DST_MINB 3
 #endif
@@ -728,7 +731,9 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
 // pair pass (alpha_e = exp(l_e - lse_v); 8 bytes per edge gathered instead of 16).
 // TE (reordering off): t_e from te[], no dX t-path here; dz_e is written per CSR entry (dz_out)
 // for the explicit destination-side GEMMs.
-template <class TP, int D, bool GROUP, bool TE, bool SGL>
+// WT: (alpha_e, dz_e) written per CSR entry into wts for the weighted-SpMM pair pass, the node record is
+// the G row alone (GX [N][D]), no bx rows and no nst.
+template <class TP, int D, bool GROUP, bool TE, bool SGL, bool WT>
 __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
@@ -740,10 +745,12 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
                                                       float* __restrict__ dX, TP* __restrict__ GX,
                                                       float4* __restrict__ nst, const uint8_t* __restrict__ single,
                                                       const TP* __restrict__ avec, TP* __restrict__ dP,
-                                                      TP* __restrict__ bx, float* __restrict__ wsum) {
+                                                      TP* __restrict__ bx, float* __restrict__ wsum,
+                                                      float2* __restrict__ wts) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
-  constexpr int UN = SGL ? RGNN_UNR_SGL : UNR;  // the single-edge stores need registers: fewer edges per step
+  // the single-edge stores and the weight writes need registers: fewer edges per step
+  constexpr int UN = SGL ? RGNN_UNR_SGL : WT ? RGNN_UNR_WT : UNR;
   Work<GROUP, LPR> w;
   if (!w.init(n, items)) return;
   const int64_t v = w.item.x;
@@ -764,9 +771,13 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
     const float2 st = stats[v];
     const float inv = 1.f / st.y;
     if (slot < 0 && e > b && w.writer()) {  // node record (heavy rows: k_rgat_node_prep)
-      st_tp<V>(GX + v * 2 * D + c * V, gv);
-      st_tp<V>(GX + v * 2 * D + D + c * V, x);
-      if (w.leader()) nst[v] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
+      if (WT) {
+        st_tp<V>(GX + v * D + c * V, gv);
+      } else {
+        st_tp<V>(GX + v * 2 * D + c * V, gv);
+        st_tp<V>(GX + v * 2 * D + D + c * V, x);
+        if (w.leader()) nst[v] = make_float4(st.x + logf(st.y), go, 0.f, 0.f);
+      }
     }
     for (int t = 0; t < w.span; t += w.step * UN) {
       const int i0 = b + t + w.first;
@@ -816,6 +827,7 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
         float alpha = __expf(l - st.x) * inv;
         float dz = alpha * (da - go) * (z > 0.f ? 1.f : slope);
         if (i < e) {
+          if (WT && c == 0) wts[i] = make_float2(alpha, dz);
           if (TE) {
             if (c == 0) dz_out[i] = dz;
           } else {
@@ -827,9 +839,11 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
 #pragma unroll
               for (int k = 0; k < V; ++k) o[k] = fmaf(dz, av[k], alpha * gv[k]);
               st_tp<V>(dP + (int64_t)pid[u] * D + c * V, o);
+              if (!WT) {
 #pragma unroll
-              for (int k = 0; k < V; ++k) o[k] = dz * x[k];
-              st_tp<V>(bx + (int64_t)pid[u] * D + c * V, o);
+                for (int k = 0; k < V; ++k) o[k] = dz * x[k];
+                st_tp<V>(bx + (int64_t)pid[u] * D + c * V, o);
+              }
               if (c == 0) wsum[pid[u]] = dz;
             }
           }
@@ -958,6 +972,10 @@ __global__ void __launch_bounds__(256) k_rgat_node_prep(int64_t n, const int4* _
 #pragma unroll
   for (int k = 0; k < V; ++k) go = fmaf(gv[k], ov[k], go);
   go = gsum<LPR>(go, group_mask<LPR>(g));
+  if (!nst) {  // weighted-SpMM pair pass: the record is the G row alone ([N][D])
+    st_tp<V>(GX + v * D + c * V, gv);
+    return;
+  }
   st_tp<V>(GX + v * 2 * D + c * V, gv);
   st_tp<V>(GX + v * 2 * D + D + c * V, xv);
   if (c == 0) {
@@ -1597,14 +1615,19 @@ __device__ __forceinline__ void acc16(float2* acc, uint4 v, float s) {
 #define RGNN_SPMM_MINB 3
 #endif
 
-template <class TP, int D, int H, int U, bool WSUM>
+// TWO: the record has two halves [A_v | B_v] (2D wide) and two weights; else one half (D wide) weighted
+// by w.x, with w.y summed per pair (RGAT: rec = G_v, w = (alpha_e, dz_e): dP_p = sum alpha_e G_d +
+// (sum dz_e) a_r, wsum_p = sum dz_e -- AVEC adds the a_r term when the pair's row is written).
+template <class TP, int D, int H, int U, bool TWO, bool AVEC>
 __global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
     int64_t nch, const int4* __restrict__ chunks, float* __restrict__ pacc, float2* __restrict__ pstat,
     const int32_t* __restrict__ csc_dst, const int32_t* __restrict__ csc2csr, const int32_t* __restrict__ csc_pair,
     const TP* __restrict__ rec, const float2* __restrict__ wts, TP* __restrict__ outA, TP* __restrict__ outB,
-    int64_t ostride, float* __restrict__ wsum, int poffA, int poffB) {
+    int64_t ostride, float* __restrict__ wsum, int poffA, int poffB, const int32_t* __restrict__ csc_rel,
+    const TP* __restrict__ avec) {
   using G = Geo<TP, D>;
-  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H, V2 = V / 2;
+  constexpr int V = G::V, LPR = G::LPR, EG = G::EG, LH = LPR / H, V2 = V / 2, RW = TWO ? 2 * D : D;
+  constexpr bool WSUM = !TWO;
   static_assert(LPR % U == 0, "U must divide the lanes per row");
   const int lane = threadIdx.x & 31, g = lane / LPR, c = lane % LPR, hd = c / LH;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1630,7 +1653,7 @@ __global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
   float ws = 0.f;
 #pragma unroll
   for (int k = 0; k < V2; ++k) accA[k] = accB[k] = make_float2(0.f, 0.f);
-  int cp = -1;  // the pair being accumulated (group-uniform)
+  int cp = -1, cbeg = 0;  // the pair being accumulated (group-uniform) and its first stream position
   auto flush = [&]() {
     float fa[V], fb[V];
 #pragma unroll
@@ -1643,11 +1666,17 @@ __global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
     if (slot >= 0) {  // split chunk of a heavy pair: fp32 partial row (A at poffA, B at poffB) + (wsum, 0)
       float* o = pacc + (int64_t)slot * 2 * D;
       st_f32<V>(o + poffA + c * V, fa);
-      st_f32<V>(o + poffB + c * V, fb);
+      if (TWO) st_f32<V>(o + poffB + c * V, fb);
       if (WSUM && c == 0) pstat[slot] = make_float2(ws, 0.f);
     } else {
+      if (AVEC) {  // + (sum dz) a_r
+        float av[V];
+        cvt16<TP>(ldg16(avec + (int64_t)__ldg(csc_rel + a + cbeg) * D + c * V), av);
+#pragma unroll
+        for (int k = 0; k < V; ++k) fa[k] = fmaf(ws, av[k], fa[k]);
+      }
       st_tp<V>(outA + (int64_t)cp * ostride + c * V, fa);
-      st_tp<V>(outB + (int64_t)cp * ostride + c * V, fb);
+      if (TWO) st_tp<V>(outB + (int64_t)cp * ostride + c * V, fb);
       if (WSUM && c == 0) wsum[cp] = ws;
     }
   };
@@ -1667,9 +1696,9 @@ __global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
       const int d = __shfl_sync(0xffffffffu, d_cur, sl);
       const int x = __shfl_sync(0xffffffffu, x_cur, sl);
       pp[u] = __shfl_sync(0xffffffffu, p_cur, sl);
-      const TP* r = rec + (int64_t)d * 2 * D + c * V;
+      const TP* r = rec + (int64_t)d * RW + c * V;
       ra[u] = ldg16(r);
-      rb[u] = ldg16(r + D);
+      if (TWO) rb[u] = ldg16(r + D);
       ww[u] = __ldg(wts + (int64_t)x * H + hd);
     }
 #pragma unroll
@@ -1680,10 +1709,11 @@ __global__ void __launch_bounds__(256, RGNN_SPMM_MINB) k_pair_spmm(
         for (int k = 0; k < V2; ++k) accA[k] = accB[k] = make_float2(0.f, 0.f);
         ws = 0.f;
         cp = pp[u];
+        cbeg = t0 + u;
       }
       const float wa = pp[u] >= 0 ? ww[u].x : 0.f, wb = pp[u] >= 0 ? ww[u].y : 0.f;
       acc16<TP>(accA, ra[u], wa);
-      acc16<TP>(accB, rb[u], wb);
+      if (TWO) acc16<TP>(accB, rb[u], wb);
       if (WSUM) ws += wb;
     }
   }
@@ -2015,7 +2045,7 @@ void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM,
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
                   const float* out, float* dX, void* GX, float4* nst, const uint8_t* single, const void* a, void* dP,
-                  void* bx, float* wsum, const Partial& pt, cudaStream_t s) {
+                  void* bx, float* wsum, float2* wts, const Partial& pt, cudaStream_t s) {
   by_width(D, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
@@ -2024,11 +2054,15 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
         launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, (const int32_t*)g->csr_pair,
                     (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te,
                     dz, slope, stats, G, out, dX, static_cast<TP*>(GX), nst, single, static_cast<const TP*>(a),
-                    static_cast<TP*>(dP), static_cast<TP*>(bx), wsum);
+                    static_cast<TP*>(dP), static_cast<TP*>(bx), wsum, wts);
       };
-      if (te) go(k_rgat_bwd_dst<TP, DD, false, true, false>, k_rgat_bwd_dst<TP, DD, true, true, false>);
-      else if (single) go(k_rgat_bwd_dst<TP, DD, false, false, true>, k_rgat_bwd_dst<TP, DD, true, false, true>);
-      else go(k_rgat_bwd_dst<TP, DD, false, false, false>, k_rgat_bwd_dst<TP, DD, true, false, false>);
+      if (te) go(k_rgat_bwd_dst<TP, DD, false, true, false, false>, k_rgat_bwd_dst<TP, DD, true, true, false, false>);
+      else if (wts && single)
+        go(k_rgat_bwd_dst<TP, DD, false, false, true, true>, k_rgat_bwd_dst<TP, DD, true, false, true, true>);
+      else if (wts) go(k_rgat_bwd_dst<TP, DD, false, false, false, true>, k_rgat_bwd_dst<TP, DD, true, false, false, true>);
+      else if (single)
+        go(k_rgat_bwd_dst<TP, DD, false, false, true, false>, k_rgat_bwd_dst<TP, DD, true, false, true, false>);
+      else go(k_rgat_bwd_dst<TP, DD, false, false, false, false>, k_rgat_bwd_dst<TP, DD, true, false, false, false>);
       launch("rgat_node_prep", k_rgat_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
              g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(X), out, stats,
              static_cast<TP*>(GX), nst);
@@ -2058,8 +2092,29 @@ void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_nor
 }
 
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
-                   const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s) {
+                   const float* te, const void* a, float slope, const void* GX, const float4* nst, const float2* wts,
+                   void* dP, float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s) {
+  if (wts) {  // weighted SpMM: dP_p = sum alpha_e G_d + (sum dz_e) a_r, wsum_p = sum dz_e (GX = G_v rows, [N][D])
+    const int64_t nch = skip_single ? g->pairs.n_chunks_multi : g->pairs.n_chunks;
+    const int4* ch = skip_single ? g->pairs.chunks_multi : g->pairs.chunks;
+    by_width(D, [&](auto Dc) {
+      constexpr int DD = decltype(Dc)::value;
+      by_dtype(dtype, [&](auto* tp) {
+        using TP = std::remove_pointer_t<decltype(tp)>;
+        constexpr int LPR = Geo<TP, DD>::LPR;
+        constexpr int UU = RGNN_SPMM_U < LPR ? RGNN_SPMM_U : LPR;
+        launch("rgat_bwd_pair", k_pair_spmm<TP, DD, 1, UU, false, true>, groups(nch, LPR), dim3(256), 0, s, nch, ch,
+               pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc2csr, (const int32_t*)g->csc_pair,
+               static_cast<const TP*>(GX), wts, static_cast<TP*>(dP), (TP*)nullptr, (int64_t)DD, wsum, 0, DD,
+               (const int32_t*)g->csc_rel, static_cast<const TP*>(a));
+        launch("merge_heavy_pairs", k_merge_rgat_pair<TP, DD>, warps(g->pairs.n_split), dim3(256), 0, s,
+               g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, (const float2*)pt.stat,
+               (const int32_t*)g->pair_csc_beg, (const int32_t*)g->csc_rel, static_cast<const TP*>(a),
+               static_cast<TP*>(dP), wsum, (TP*)nullptr);
+      });
+    });
+    return;
+  }
   WorkPlan wp = g->pairs;  // single-edge pairs resolved by the destination-major pass (reordered path)
   if (skip_single && !te) {
     wp.n_items = wp.n_multi;
@@ -2100,10 +2155,10 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
         by_heads<LPR>(H, [&](auto hc) {
           constexpr int HH = decltype(hc)::value;
           TP* o = static_cast<TP*>(dKM);
-          launch("hgt_bwd_pair", k_pair_spmm<TP, DD, HH, UU, false>, groups(nch, LPR), dim3(256), 0, s, nch, ch,
-                 pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc2csr,
+          launch("hgt_bwd_pair", k_pair_spmm<TP, DD, HH, UU, true, false>, groups(nch, LPR), dim3(256), 0, s, nch,
+                 ch, pt.acc, pt.stat, (const int32_t*)g->csc_dst, (const int32_t*)g->csc2csr,
                  (const int32_t*)g->csc_pair, static_cast<const TP*>(GQ), wts, o + DD, o, (int64_t)2 * DD,
-                 (float*)nullptr, DD, 0);
+                 (float*)nullptr, DD, 0, (const int32_t*)nullptr, (const TP*)nullptr);
         });
         launch("merge_heavy_pairs", k_merge_sum<2 * DD, TP>, dim3(g->pairs.n_split), dim3(256), 0, s,
                g->pairs.n_split, (const int4*)g->pairs.splits, (const float*)pt.acc, static_cast<TP*>(dKM), false);

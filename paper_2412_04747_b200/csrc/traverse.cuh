@@ -26,19 +26,22 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
 void hgt_bwd_dst(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* Q, const float2* stats,
                  const float* G, const float* out, void* dQ, void* GQ, float4* nst, const uint8_t* single, void* dKM,
                  float2* wts, const Partial& pt, cudaStream_t s);
-// also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0).
+// also writes the per-node record GX_v = [G_v | X_v], nst_v = (m_v, 1/sum_v, G_v . out_v, 0); with wts
+// (weighted-SpMM pair pass) instead (alpha_e, dz_e) per CSR entry and GX_v = G_v ([N][D]), no bx, no nst.
 // te != NULL (reordering off): t_e read from te, dz_e written per CSR entry into dz, dX untouched.
 void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const void* X,
                   const float* y, const float* te, float* dz, float slope, const float2* stats, const float* G,
                   const float* out, float* dX, void* GX, float4* nst, const uint8_t* single, const void* a, void* dP,
-                  void* bx, float* wsum, const Partial& pt, cudaStream_t s);
+                  void* bx, float* wsum, float2* wts, const Partial& pt, cudaStream_t s);
 // G: upstream gradient rows in the layer dtype (bf16 copy on the bf16 path)
 void rgcn_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const float* csc_norm, const void* G, void* dP,
                    const Partial& pt, cudaStream_t s);
 // te != NULL (reordering off): t_e = te[csc2csr[i]], bx not computed
+// wts != NULL: weighted SpMM over the per-CSR-entry (alpha_e, dz_e) that rgat_bwd_dst wrote, GX = [N][D]
+// bf16/fp32 rows of G (no bx); else the recomputing pair kernels over GX = [G_v | X_v] and nst
 void rgat_bwd_pair(const rgnn_graph_s* g, int dtype, int D, const void* P, const float* spair, const float* y,
-                   const float* te, const void* a, float slope, const void* GX, const float4* nst, void* dP,
-                   float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s);
+                   const float* te, const void* a, float slope, const void* GX, const float4* nst, const float2* wts,
+                   void* dP, float* wsum, void* bx, bool skip_single, const Partial& pt, cudaStream_t s);
 // wts != NULL: the weighted SpMM k_pair_spmm over the per-CSR-entry (alpha_e, dl_e) [E][H] that
 // hgt_bwd_dst wrote (nst unused); else the recomputing pair kernels (alpha, dl from K~ / M and nst)
 void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM, const void* GQ, const float4* nst,
