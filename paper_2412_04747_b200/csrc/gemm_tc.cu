@@ -755,7 +755,8 @@ void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s) {
   RGNN_CHECK(pair_bwd_tc_supported(a.K1, a.K2), RGNN_ERR_UNSUPPORTED, "fused pair backward: K1 = 64, K2 = 64 / 128");
   RGNN_CUDA(cudaMemsetAsync(a.out, 0, (size_t)a.num_w * a.K1 * a.K2 * sizeof(float), s));
   if (a.plan->count == 0) return;
-  if (a.K2 == 64) launch_pair_bwd_tc<64, 64>(a, s);
+  if (pair_bwd_ws_enabled(a)) pair_bwd_ws(a, s);
+  else if (a.K2 == 64) launch_pair_bwd_tc<64, 64>(a, s);
   else launch_pair_bwd_tc<64, 128>(a, s);
   const Plan& p = *a.plan;
   const int64_t width = (int64_t)a.K1 * a.K2;

@@ -290,6 +290,226 @@ void tma_by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   }
 }
 
+// ---------------------------------------------------------------- fused pair-side backward (A8), warp-specialized
+// The fused kernel of gemm_tc.cu (k_pair_bwd_tc: one pass over a 2048-row weight-gradient tile of the pair
+// gradient rows dP computes both Y = dP W_w^T and the tile's X[src]^T dP partial) with the roles split:
+//   warps 4-7  producers: the sub-tile's gathered X[src] rows by cp.async (zero-filled past the tile end, so
+//              the rows a box reads beyond it contribute nothing to the weight gradient), completion signalled
+//              per thread on the stage's mbarrier (cp.async.mbarrier.arrive.noinc); lane 0 of warp 4 adds the
+//              dP sub-tile as TMA 2D boxes (expect_tx).
+//   warp 8     MMA issuer: D_w += dP^T X (both MN-major) and D_x[s % 2] = dP W^T (both K-major) per sub-tile.
+//   warps 0-3  epilogue: D_x[b] -> bf16 -> 128B-swizzled staging -> one TMA 2D store per 32 rows; at the end the
+//              tile's D_w partial.
+// S stages of (dP | X) sub-tiles (48 KB for K2 = 128) are in flight instead of two.
+template <int K1, int K2>
+struct PbCfg {
+  static constexpr int KB1 = K1 / 64, KB2 = K2 / 64;
+  static constexpr uint32_t BLK = 128 * 128;                 // one 64-wide block of 128 rows
+  static constexpr uint32_t STAGE = (KB1 + KB2) * BLK;       // [dP blocks | X blocks]
+  static constexpr uint32_t WBLK = K1 * 128;                 // one 64-wide K block of the K1 weight rows
+  static constexpr uint32_t WBYTES = KB2 * WBLK;
+  static constexpr uint32_t STAGING = 4 * 32 * 128;          // 4 epilogue warps x 32 rows x 128 B
+  static constexpr int S_FIT = (int)((222 * 1024 - WBYTES - STAGING) / STAGE);
+  static constexpr int S = S_FIT < 6 ? S_FIT : 6;
+  static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + WBYTES + STAGING + 256;
+  static constexpr int NCOLS = 256;                          // D_w (K1) + 2 x D_x (K1)
+};
+
+template <int K1, int K2>
+__global__ void __launch_bounds__(288, 1) k_pair_bwd_ws(const __grid_constant__ CUtensorMap tmP,
+                                                        const __grid_constant__ CUtensorMap tmY,
+                                                        const Tile* __restrict__ tiles, const bf16* __restrict__ A,
+                                                        const int32_t* __restrict__ gather,
+                                                        const bf16* __restrict__ Wm, bf16* __restrict__ Y,
+                                                        float* __restrict__ partial) {
+  using C = PbCfg<K1, K2>;
+  constexpr int S = C::S, KB1 = C::KB1, KB2 = C::KB2;
+  constexpr uint32_t BLK = C::BLK, STAGE = C::STAGE, WBLK = C::WBLK;
+  static_assert(S >= 2 && K1 == 64, "fused pair backward: K1 = 64");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t s_w = s_base + S * STAGE;
+  uint8_t* staging = smem + S * STAGE + C::WBYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
+  uint64_t* empty = full + S;
+  uint64_t* xready = empty + S;  // [2]
+  uint64_t* xempty = xready + 2; // [2]
+  uint64_t* wdone = xempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wdone + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Tile t = tiles[blockIdx.x];
+  const int nsub = (t.row1 - t.row0 + 127) / 128;
+
+  if (warp == 8) tmem_alloc<C::NCOLS>(tslot);
+  if (tid == 0) {
+    tma_prefetch_desc(&tmP);
+    tma_prefetch_desc(&tmY);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 129);  // 128 producer threads' cp.async + the TMA expect_tx arrival
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&xready[i], 1);
+      mbar_init(&xempty[i], 128);
+    }
+    mbar_init(wdone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // the segment's weight W_w (K1 rows of K2) into KB2 swizzled K blocks, by all threads, once
+  for (int idx = tid; idx < K1 * 8 * KB2; idx += blockDim.x) {
+    const int kb = idx / (K1 * 8), rem = idx % (K1 * 8), n = rem >> 3, c = rem & 7;
+    cp_async16(s_w + kb * WBLK + n * 128 + ((c ^ (n & 7)) << 4), Wm + ((int64_t)t.w * K1 + n) * K2 + kb * 64 + c * 8);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------ producers
+    // one cp.async group per sub-tile, up to S - 1 in flight: when a group has landed, the thread fences it
+    // for the async proxy and arrives on its stage's full barrier (128 producer arrivals + the TMA's)
+    const int ptid = tid - 128, c = ptid & 7, r0 = ptid >> 3;  // rows r0 + 16 i, 16-byte chunk c
+    int pend = 0, old = 0;
+    for (int sub = 0; sub < nsub; ++sub) {
+      const int st = sub % S;
+      mbar_wait(&empty[st], ((sub / S) & 1) ^ 1);
+      const uint32_t sb = s_base + st * STAGE;
+      if (ptid == 0) {
+        mbar_expect_tx(&full[st], KB2 * BLK);
+#pragma unroll
+        for (int j = 0; j < KB2; ++j) tma_load_2d(sb + j * BLK, &tmP, j * 64, t.row0 + sub * 128, &full[st]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 16 * i, row = t.row0 + sub * 128 + r;
+        const bool ok = row < t.row1;
+        const int64_t xa = ok ? (int64_t)__ldg(gather + row) : 0;
+        const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+#pragma unroll
+        for (int j = 0; j < KB1; ++j) cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      if (++pend == S - 1) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(&full[old]);
+        if (++old == S) old = 0;
+        --pend;
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (; pend > 0; --pend) {
+      mbar_arrive(&full[old]);
+      if (++old == S) old = 0;
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc_w = umma_idesc_bf16_mn(K1), idesc_x = umma_idesc_bf16(K1);
+      for (int sub = 0; sub < nsub; ++sub) {
+        const int st = sub % S, b = sub & 1;
+        mbar_wait(&full[st], (sub / S) & 1);
+        if (sub >= 2) mbar_wait(&xempty[b], ((sub >> 1) - 1) & 1);  // the epilogue drained D_x[b]
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t sb = s_base + st * STAGE;
+#pragma unroll
+        for (int k = 0; k < 128 / 16; ++k) {  // weight gradient: D_w += dP^T X (both MN-major)
+          const uint64_t da = umma_desc_mn_sw128(sb + k * 2048, KB2 == 2 ? BLK : 0);
+          const uint64_t db = umma_desc_mn_sw128(sb + KB2 * BLK + k * 2048, BLK);
+          umma_bf16(tmem, da, db, idesc_w, (sub | k) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kb = 0; kb < KB2; ++kb)  // dX rows: D_x[b] = dP W^T (both K-major)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + K1 + b * K1, umma_desc_sw128(sb + kb * BLK + k * 32),
+                      umma_desc_sw128(s_w + kb * WBLK + k * 32), idesc_x, (kb | k) ? 1u : 0u);
+        umma_commit(&empty[st]);
+        umma_commit(&xready[b]);
+      }
+      umma_commit(wdone);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quarters)
+    uint8_t* stg = staging + warp * 32 * 128;
+    for (int sub = 0; sub < nsub; ++sub) {
+      const int b = sub & 1;
+      mbar_wait(&xready[b], (sub >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (lane == 0) tma_store_wait_read<0>();  // the staging buffer's previous store has read it
+      __syncwarp();
+      const int64_t row0 = (int64_t)t.row0 + sub * 128 + warp * 32;
+      const int rows_here = min(32, (int)(t.row1 - row0));
+#pragma unroll
+      for (int c0 = 0; c0 < K1; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + K1 + b * K1 + c0, v);
+        stage_vals<bf16, 32, 8>(stg + lane * 128, lane, c0 * 2 / 16, v);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&xempty[b]);
+      if (rows_here == 32) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmY, 0, (int)row0, smem_u32(stg));
+          tma_store_commit();
+        }
+      } else {
+        __syncwarp();
+        uint8_t* ybase = reinterpret_cast<uint8_t*>(Y + row0 * K1);
+#pragma unroll
+        for (int k = lane; k < 32 * 8; k += 32) {
+          const int rr = k / 8, j = k % 8;
+          if (rr < rows_here)
+            *reinterpret_cast<uint4*>(ybase + rr * 128 + j * 16) =
+                *reinterpret_cast<const uint4*>(stg + rr * 128 + ((j ^ (rr & 7)) << 4));
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) tma_store_wait<0>();
+    // the tile's weight-gradient partial: lane m = k2 (rows 0..K2-1 of D_w), columns n = k1
+    mbar_wait(wdone, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    float* out = partial + (size_t)blockIdx.x * K1 * K2;
+    if (warp * 32 < K2) {
+#pragma unroll
+      for (int c0 = 0; c0 < K1; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+        const int m = warp * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) out[(size_t)(c0 + i) * K2 + m] = v[i];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 8) tmem_dealloc<C::NCOLS>(tmem);
+}
+
+template <int K1, int K2>
+void launch_pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s) {
+  using C = PbCfg<K1, K2>;
+  auto k = k_pair_bwd_ws<K1, K2>;
+  static bool attr = false;
+  if (!attr) {
+    RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const CUtensorMap tmP = make_map(a.dP, 2, K2, a.rows, 64, 128, true);
+  const CUtensorMap tmY = make_map(a.Y, 2, K1, a.rows, 64, 32, true);
+  launch(a.name, k, dim3(a.plan->count), dim3(288), C::SMEM, s, tmP, tmY, a.plan->tiles, static_cast<const bf16*>(a.X),
+         a.gather, static_cast<const bf16*>(a.W), static_cast<bf16*>(a.Y), a.partial);
+}
+
 }  // namespace
 
 // Contiguous A (node GEMMs, ungathered segment GEMMs) runs here.  Gathered A stays on the cp.async
@@ -308,6 +528,21 @@ bool gemm_tma_enabled(const GemmArgs& a) {
   // TMA: 16-byte aligned bases and row strides
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   return al(a.A) && al(a.Y) && (a.K * 2) % 16 == 0;
+}
+
+// RGNN_PAIR_WS=0: the two-role fused pair backward of gemm_tc.cu instead of the warp-specialized TMA one
+bool pair_bwd_ws_enabled(const PairBwdArgs& a) {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_PAIR_WS");
+    return !(v && v[0] == '0');
+  }();
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return on && encode_fn() != nullptr && a.rows > 0 && al(a.dP) && al(a.Y) && a.K1 == 64 && (a.K2 == 64 || a.K2 == 128);
+}
+
+void pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s) {
+  if (a.K2 == 64) launch_pair_bwd_ws<64, 64>(a, s);
+  else launch_pair_bwd_ws<64, 128>(a, s);
 }
 
 void gemm_tma(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {

@@ -393,6 +393,7 @@ bool fused_pair_bwd(const Ctx& c, const Segs& sg, const void* X, const void* dP,
   a.X = X; a.gather = c.g->pair_src; a.K1 = c.Din;
   a.dP = dP; a.K2 = K2; a.W = W; a.Y = dXp;
   a.out = dWout; a.num_w = num_w; a.partial = partial;
+  a.rows = sg.ptr.empty() ? 0 : sg.ptr.back();
   a.name = "pair_bwd_fused";
   pair_bwd_tc(a, c.s);
   return true;

@@ -80,9 +80,13 @@ struct PairBwdArgs {
   int num_w = 0;
   float* partial = nullptr;  // scratch [ntiles][K1][K2]
   const char* name = "pair_bwd";
+  int64_t rows = 0;          // rows of dP and Y (0: unknown, no TMA kernel)
 };
 bool pair_bwd_tc_supported(int K1, int K2);
 void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s);
+// warp-specialized TMA version (gemm_tma.cu), used by pair_bwd_tc when enabled and applicable
+bool pair_bwd_ws_enabled(const PairBwdArgs& a);
+void pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s);
 // the second level of the deterministic weight-gradient reduction (dense_ops.cu)
 using SegPartialReduceFn = void (*)(int, const int32_t*, const int32_t*, const float*, int64_t, float*);
 SegPartialReduceFn seg_partial_reduce_kernel();
