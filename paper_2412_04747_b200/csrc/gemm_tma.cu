@@ -292,15 +292,17 @@ void tma_by_n(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
 
 // ---------------------------------------------------------------- fused pair-side backward (A8), warp-specialized
 // The fused kernel of gemm_tc.cu (k_pair_bwd_tc: one pass over a 2048-row weight-gradient tile of the pair
-// gradient rows dP computes both Y = dP W_w^T and the tile's X[src]^T dP partial) with the roles split:
-//   warps 4-7  producers: the sub-tile's gathered X[src] rows by cp.async (zero-filled past the tile end, so
-//              the rows a box reads beyond it contribute nothing to the weight gradient), completion signalled
-//              per thread on the stage's mbarrier (cp.async.mbarrier.arrive.noinc); lane 0 of warp 4 adds the
-//              dP sub-tile as TMA 2D boxes (expect_tx).
-//   warp 8     MMA issuer: D_w += dP^T X (both MN-major) and D_x[s % 2] = dP W^T (both K-major) per sub-tile.
-//   warps 0-3  epilogue: D_x[b] -> bf16 -> 128B-swizzled staging -> one TMA 2D store per 32 rows; at the end the
-//              tile's D_w partial.
-// S stages of (dP | X) sub-tiles (48 KB for K2 = 128) are in flight instead of two.
+// gradient rows dP computes both Y = dP W_w^T and the tile's X[src]^T dP partial), persistent (one CTA per SM
+// walks tiles blockIdx.x, + gridDim.x, ...) with the roles split:
+//   warps 4-7  producers: per 128-row sub-tile the gathered X[src] rows by cp.async (zero-filled past the
+//              tile end, so the rows a dP box reads beyond it contribute nothing to the weight gradient),
+//              the next sub-tile's row indices loaded while this one is issued; lane 0 of warp 4 adds the
+//              dP sub-tile as TMA 2D boxes (expect_tx) and, per tile, the K-major weight W_w into one of
+//              two buffers (freed when the tile two back finished its MMAs).
+//   warp 8     MMA issuer: D_w[j % 2] += dP^T X (both MN-major) and D_x[s % 2] = dP W^T (both K-major).
+//   warps 0-3  epilogue: D_x[b] -> bf16 -> 128B-swizzled staging (two buffers) -> TMA 2D store per 32 rows;
+//              at each tile end the D_w partial of that tile.
+// S stages of (dP | X) sub-tiles are in flight; TMEM = 2 D_w + 2 D_x accumulators (256 columns).
 template <int K1, int K2>
 struct PbCfg {
   static constexpr int KB1 = K1 / 64, KB2 = K2 / 64;
@@ -308,20 +310,21 @@ struct PbCfg {
   static constexpr uint32_t STAGE = (KB1 + KB2) * BLK;       // [dP blocks | X blocks]
   static constexpr uint32_t WBLK = K1 * 128;                 // one 64-wide K block of the K1 weight rows
   static constexpr uint32_t WBYTES = KB2 * WBLK;
-  static constexpr uint32_t STAGING = 4 * 32 * 128;          // 4 epilogue warps x 32 rows x 128 B
-  static constexpr int S_FIT = (int)((222 * 1024 - WBYTES - STAGING) / STAGE);
+  static constexpr uint32_t STG = 32 * 128;                  // one staging buffer of an epilogue warp
+  static constexpr uint32_t STAGING = 4 * 2 * STG;
+  static constexpr int S_FIT = (int)((222 * 1024 - 2 * WBYTES - STAGING) / STAGE);
   static constexpr int S = S_FIT < 6 ? S_FIT : 6;
-  static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + WBYTES + STAGING + 256;
-  static constexpr int NCOLS = 256;                          // D_w (K1) + 2 x D_x (K1)
+  static constexpr size_t SMEM = 1024 + (size_t)S * STAGE + 2 * WBYTES + STAGING + 512;
+  static constexpr int NCOLS = 256;                          // 2 x D_w (K1) + 2 x D_x (K1)
 };
 
 template <int K1, int K2>
 __global__ void __launch_bounds__(288, 1) k_pair_bwd_ws(const __grid_constant__ CUtensorMap tmP,
+                                                        const __grid_constant__ CUtensorMap tmW,
                                                         const __grid_constant__ CUtensorMap tmY,
-                                                        const Tile* __restrict__ tiles, const bf16* __restrict__ A,
-                                                        const int32_t* __restrict__ gather,
-                                                        const bf16* __restrict__ Wm, bf16* __restrict__ Y,
-                                                        float* __restrict__ partial) {
+                                                        const Tile* __restrict__ tiles, int ntiles,
+                                                        const bf16* __restrict__ A, const int32_t* __restrict__ gather,
+                                                        bf16* __restrict__ Y, float* __restrict__ partial) {
   using C = PbCfg<K1, K2>;
   constexpr int S = C::S, KB1 = C::KB1, KB2 = C::KB2;
   constexpr uint32_t BLK = C::BLK, STAGE = C::STAGE, WBLK = C::WBLK;
@@ -329,40 +332,38 @@ __global__ void __launch_bounds__(288, 1) k_pair_bwd_ws(const __grid_constant__ 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t s_base = smem_u32(smem);
-  const uint32_t s_w = s_base + S * STAGE;
-  uint8_t* staging = smem + S * STAGE + C::WBYTES;
+  const uint32_t s_w0 = s_base + S * STAGE;  // two weight buffers of WBYTES
+  uint8_t* staging = smem + S * STAGE + 2 * C::WBYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + C::STAGING);
   uint64_t* empty = full + S;
-  uint64_t* xready = empty + S;  // [2]
-  uint64_t* xempty = xready + 2; // [2]
-  uint64_t* wdone = xempty + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(wdone + 1);
+  uint64_t* xready = empty + S;  // [2] D_x[b] written
+  uint64_t* xempty = xready + 2; // [2] D_x[b] drained
+  uint64_t* wready = xempty + 2; // [2] weight buffer b loaded
+  uint64_t* wfree = wready + 2;  // [2] weight buffer b no longer read
+  uint64_t* dready = wfree + 2;  // [2] D_w[b] complete
+  uint64_t* dfree = dready + 2;  // [2] D_w[b] drained
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfree + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const Tile t = tiles[blockIdx.x];
-  const int nsub = (t.row1 - t.row0 + 127) / 128;
 
   if (warp == 8) tmem_alloc<C::NCOLS>(tslot);
   if (tid == 0) {
     tma_prefetch_desc(&tmP);
+    tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmY);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 129);  // 128 producer threads' cp.async + the TMA expect_tx arrival
+      mbar_init(&full[i], 129);  // 128 producer threads + the TMA expect_tx arrival
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&xready[i], 1);
       mbar_init(&xempty[i], 128);
+      mbar_init(&wready[i], 1);
+      mbar_init(&wfree[i], 1);
+      mbar_init(&dready[i], 1);
+      mbar_init(&dfree[i], 128);
     }
-    mbar_init(wdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // the segment's weight W_w (K1 rows of K2) into KB2 swizzled K blocks, by all threads, once
-  for (int idx = tid; idx < K1 * 8 * KB2; idx += blockDim.x) {
-    const int kb = idx / (K1 * 8), rem = idx % (K1 * 8), n = rem >> 3, c = rem & 7;
-    cp_async16(s_w + kb * WBLK + n * 128 + ((c ^ (n & 7)) << 4), Wm + ((int64_t)t.w * K1 + n) * K2 + kb * 64 + c * 8);
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -370,125 +371,172 @@ __global__ void __launch_bounds__(288, 1) k_pair_bwd_ws(const __grid_constant__ 
 
   if (warp >= 4 && warp < 8) {
     // ------------------------------------------------ producers
-    // one cp.async group per sub-tile, up to S - 1 in flight: when a group has landed, the thread fences it
-    // for the async proxy and arrives on its stage's full barrier (128 producer arrivals + the TMA's)
     const int ptid = tid - 128, c = ptid & 7, r0 = ptid >> 3;  // rows r0 + 16 i, 16-byte chunk c
-    int pend = 0, old = 0;
-    for (int sub = 0; sub < nsub; ++sub) {
-      const int st = sub % S;
-      mbar_wait(&empty[st], ((sub / S) & 1) ^ 1);
-      const uint32_t sb = s_base + st * STAGE;
-      if (ptid == 0) {
-        mbar_expect_tx(&full[st], KB2 * BLK);
-#pragma unroll
-        for (int j = 0; j < KB2; ++j) tma_load_2d(sb + j * BLK, &tmP, j * 64, t.row0 + sub * 128, &full[st]);
-      }
+    int pend = 0, old = 0, g = 0;  // g: global sub-tile counter
+    int nidx[8];
+    auto load_idx = [&](const Tile& t, int sub) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int r = r0 + 16 * i, row = t.row0 + sub * 128 + r;
-        const bool ok = row < t.row1;
-        const int64_t xa = ok ? (int64_t)__ldg(gather + row) : 0;
-        const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
-#pragma unroll
-        for (int j = 0; j < KB1; ++j) cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + xa * K1 + j * 64 + c * 8, ok);
+        const int row = t.row0 + sub * 128 + r0 + 16 * i;
+        nidx[i] = row < t.row1 ? __ldg(gather + row) : -1;
       }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      if (++pend == S - 1) {
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    };
+    auto drain = [&] {  // every issued group landed and released (nothing of an earlier tile left pending)
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      for (; pend > 0; --pend) {
         mbar_arrive(&full[old]);
         if (++old == S) old = 0;
-        --pend;
+      }
+    };
+    int jt = 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++jt) {
+      const Tile t = tiles[ti];
+      const int nsub = (t.row1 - t.row0 + 127) / 128;
+      // the weight buffer of tile jt is freed by the MMAs of tile jt - 2, which need this thread's pending
+      // groups of earlier tiles: release them before anyone waits on it (short tiles at segment ends)
+      if (jt >= 2) drain();
+      if (ptid == 0) {  // this tile's weight into buffer jt % 2 once the tile two back stopped reading it
+        const int wb = jt & 1;
+        mbar_wait(&wfree[wb], ((jt >> 1) & 1) ^ 1);
+        mbar_expect_tx(&wready[wb], C::WBYTES);
+#pragma unroll
+        for (int kb = 0; kb < KB2; ++kb) tma_load_2d(s_w0 + wb * C::WBYTES + kb * WBLK, &tmW, kb * 64, t.w * K1, &wready[wb]);
+      }
+      load_idx(t, 0);
+      for (int sub = 0; sub < nsub; ++sub, ++g) {
+        const int st = g % S;
+        int cur[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cur[i] = nidx[i];
+        if (sub + 1 < nsub) load_idx(t, sub + 1);
+        mbar_wait(&empty[st], ((g / S) & 1) ^ 1);
+        const uint32_t sb = s_base + st * STAGE;
+        if (ptid == 0) {
+          mbar_expect_tx(&full[st], KB2 * BLK);
+#pragma unroll
+          for (int j = 0; j < KB2; ++j) tma_load_2d(sb + j * BLK, &tmP, j * 64, t.row0 + sub * 128, &full[st]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          const bool ok = cur[i] >= 0;
+          const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+#pragma unroll
+          for (int j = 0; j < KB1; ++j)
+            cp_async16_zfill(sb + (KB2 + j) * BLK + off, A + (int64_t)(ok ? cur[i] : 0) * K1 + j * 64 + c * 8, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (++pend == S - 1) {  // the oldest group landed: fence it for the async proxy, release its stage
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_arrive(&full[old]);
+          if (++old == S) old = 0;
+          --pend;
+        }
       }
     }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    for (; pend > 0; --pend) {
-      mbar_arrive(&full[old]);
-      if (++old == S) old = 0;
-    }
+    drain();
   } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc_w = umma_idesc_bf16_mn(K1), idesc_x = umma_idesc_bf16(K1);
-      for (int sub = 0; sub < nsub; ++sub) {
-        const int st = sub % S, b = sub & 1;
-        mbar_wait(&full[st], (sub / S) & 1);
-        if (sub >= 2) mbar_wait(&xempty[b], ((sub >> 1) - 1) & 1);  // the epilogue drained D_x[b]
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t sb = s_base + st * STAGE;
+      int g = 0, jt = 0;
+      for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++jt) {
+        const Tile t = tiles[ti];
+        const int nsub = (t.row1 - t.row0 + 127) / 128, wb = jt & 1;
+        const uint32_t s_w = s_w0 + wb * C::WBYTES;
+        const uint32_t dw = tmem + wb * K1;  // D_w[jt % 2] at columns 0 / 64, D_x[b] at 128 / 192
+        mbar_wait(&wready[wb], (jt >> 1) & 1);
+        if (jt >= 2) mbar_wait(&dfree[wb], ((jt >> 1) - 1) & 1);  // the epilogue drained D_w[wb]
+        for (int sub = 0; sub < nsub; ++sub, ++g) {
+          const int st = g % S, b = g & 1;
+          mbar_wait(&full[st], (g / S) & 1);
+          if (g >= 2) mbar_wait(&xempty[b], ((g >> 1) - 1) & 1);  // the epilogue drained D_x[b]
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t sb = s_base + st * STAGE;
 #pragma unroll
-        for (int k = 0; k < 128 / 16; ++k) {  // weight gradient: D_w += dP^T X (both MN-major)
-          const uint64_t da = umma_desc_mn_sw128(sb + k * 2048, KB2 == 2 ? BLK : 0);
-          const uint64_t db = umma_desc_mn_sw128(sb + KB2 * BLK + k * 2048, BLK);
-          umma_bf16(tmem, da, db, idesc_w, (sub | k) ? 1u : 0u);
+          for (int k = 0; k < 128 / 16; ++k) {
+            const uint64_t da = umma_desc_mn_sw128(sb + k * 2048, KB2 == 2 ? BLK : 0);
+            const uint64_t db = umma_desc_mn_sw128(sb + KB2 * BLK + k * 2048, BLK);
+            umma_bf16(dw, da, db, idesc_w, (sub | k) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kb = 0; kb < KB2; ++kb)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tmem + 2 * K1 + b * K1, umma_desc_sw128(sb + kb * BLK + k * 32),
+                        umma_desc_sw128(s_w + kb * WBLK + k * 32), idesc_x, (kb | k) ? 1u : 0u);
+          umma_commit(&empty[st]);
+          umma_commit(&xready[b]);
         }
-#pragma unroll
-        for (int kb = 0; kb < KB2; ++kb)  // dX rows: D_x[b] = dP W^T (both K-major)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + K1 + b * K1, umma_desc_sw128(sb + kb * BLK + k * 32),
-                      umma_desc_sw128(s_w + kb * WBLK + k * 32), idesc_x, (kb | k) ? 1u : 0u);
-        umma_commit(&empty[st]);
-        umma_commit(&xready[b]);
+        umma_commit(&dready[wb]);
+        umma_commit(&wfree[wb]);
       }
-      umma_commit(wdone);
     }
     __syncwarp();
   } else {
     // ------------------------------------------------ epilogue (warps 0-3 = TMEM lane quarters)
-    uint8_t* stg = staging + warp * 32 * 128;
-    for (int sub = 0; sub < nsub; ++sub) {
-      const int b = sub & 1;
-      mbar_wait(&xready[b], (sub >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (lane == 0) tma_store_wait_read<0>();  // the staging buffer's previous store has read it
-      __syncwarp();
-      const int64_t row0 = (int64_t)t.row0 + sub * 128 + warp * 32;
-      const int rows_here = min(32, (int)(t.row1 - row0));
+    int g = 0, jt = 0, buf = 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++jt) {
+      const Tile t = tiles[ti];
+      const int nsub = (t.row1 - t.row0 + 127) / 128, wb = jt & 1;
+      for (int sub = 0; sub < nsub; ++sub, ++g) {
+        const int b = g & 1;
+        uint8_t* stg = staging + (warp * 2 + buf) * C::STG;
+        mbar_wait(&xready[b], (g >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (lane == 0) tma_store_wait_read<1>();  // the store issued from this buffer two rounds ago has read it
+        __syncwarp();
+        const int64_t row0 = (int64_t)t.row0 + sub * 128 + warp * 32;
+        const int rows_here = min(32, (int)(t.row1 - row0));
 #pragma unroll
-      for (int c0 = 0; c0 < K1; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + K1 + b * K1 + c0, v);
-        stage_vals<bf16, 32, 8>(stg + lane * 128, lane, c0 * 2 / 16, v);
+        for (int c0 = 0; c0 < K1; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 2 * K1 + b * K1 + c0, v);
+          stage_vals<bf16, 32, 8>(stg + lane * 128, lane, c0 * 2 / 16, v);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        mbar_arrive(&xempty[b]);
+        if (rows_here == 32) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, 0, (int)row0, smem_u32(stg));
+            tma_store_commit();
+          }
+        } else {
+          __syncwarp();
+          uint8_t* ybase = reinterpret_cast<uint8_t*>(Y + row0 * K1);
+#pragma unroll
+          for (int k = lane; k < 32 * 8; k += 32) {
+            const int rr = k / 8, j = k % 8;
+            if (rr < rows_here)
+              *reinterpret_cast<uint4*>(ybase + rr * 128 + j * 16) =
+                  *reinterpret_cast<const uint4*>(stg + rr * 128 + ((j ^ (rr & 7)) << 4));
+          }
+          __syncwarp();
+        }
+        buf ^= 1;
+      }
+      // the tile's weight-gradient partial: lane m = k2 (rows 0..K2-1 of D_w), columns n = k1
+      mbar_wait(&dready[wb], (jt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      float* out = partial + (size_t)ti * K1 * K2;
+      if (warp * 32 < K2) {
+#pragma unroll
+        for (int c0 = 0; c0 < K1; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + wb * K1 + c0, v);
+          const int m = warp * 32 + lane;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) out[(size_t)(c0 + i) * K2 + m] = v[i];
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      mbar_arrive(&xempty[b]);
-      if (rows_here == 32) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmY, 0, (int)row0, smem_u32(stg));
-          tma_store_commit();
-        }
-      } else {
-        __syncwarp();
-        uint8_t* ybase = reinterpret_cast<uint8_t*>(Y + row0 * K1);
-#pragma unroll
-        for (int k = lane; k < 32 * 8; k += 32) {
-          const int rr = k / 8, j = k % 8;
-          if (rr < rows_here)
-            *reinterpret_cast<uint4*>(ybase + rr * 128 + j * 16) =
-                *reinterpret_cast<const uint4*>(stg + rr * 128 + ((j ^ (rr & 7)) << 4));
-        }
-        __syncwarp();
-      }
+      mbar_arrive(&dfree[wb]);
     }
     if (lane == 0) tma_store_wait<0>();
-    // the tile's weight-gradient partial: lane m = k2 (rows 0..K2-1 of D_w), columns n = k1
-    mbar_wait(wdone, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    float* out = partial + (size_t)blockIdx.x * K1 * K2;
-    if (warp * 32 < K2) {
-#pragma unroll
-      for (int c0 = 0; c0 < K1; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-        const int m = warp * 32 + lane;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) out[(size_t)(c0 + i) * K2 + m] = v[i];
-      }
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -499,15 +547,19 @@ template <int K1, int K2>
 void launch_pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s) {
   using C = PbCfg<K1, K2>;
   auto k = k_pair_bwd_ws<K1, K2>;
-  static bool attr = false;
-  if (!attr) {
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    RGNN_CUDA(cudaGetDevice(&dev));
+    RGNN_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     RGNN_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
   }
   const CUtensorMap tmP = make_map(a.dP, 2, K2, a.rows, 64, 128, true);
+  const CUtensorMap tmW = make_map(a.W, 2, K2, (int64_t)a.num_w * K1, 64, K1, true);  // W_w rows = K-major B of dX
   const CUtensorMap tmY = make_map(a.Y, 2, K1, a.rows, 64, 32, true);
-  launch(a.name, k, dim3(a.plan->count), dim3(288), C::SMEM, s, tmP, tmY, a.plan->tiles, static_cast<const bf16*>(a.X),
-         a.gather, static_cast<const bf16*>(a.W), static_cast<bf16*>(a.Y), a.partial);
+  const int ntiles = a.plan->count;
+  launch(a.name, k, dim3(std::min(ntiles, num_sms)), dim3(288), C::SMEM, s, tmP, tmW, tmY, a.plan->tiles, ntiles,
+         static_cast<const bf16*>(a.X), a.gather, static_cast<bf16*>(a.Y), a.partial);
 }
 
 }  // namespace
