@@ -2,13 +2,14 @@
 // the typed segment GEMM Y[row] = X[gather(row)] x W_w of the GEMM template Y[S] = X[G] x W[T]
 // (§3.3.3; compact rows P:764-776), persistent and warp-specialized.
 //
-//   warp 4  (one elected lane) producer: per 64-wide K block of an item (128-row tile x NT columns of
-//           one weight segment) it arms the stage's mbarrier with the stage's byte count and issues
-//           the TMA loads -- A as one 2D box of 128 rows (contiguous A) or as 32 tile::gather4 loads
-//           of 4 rows each (A = X[pair_src], the row indices shuffled to the issuing lane), B as one
-//           2D box of the K-major weight image -- all 128B-swizzled by the TMA unit into the canonical
-//           UMMA K-major layout.  No thread touches operand bytes.
-//   warp 5  MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M = 128, N = NT, K = 16) into one of two
+//   warps 4-7 producers: per 64-wide K block of an item (128-row tile x NT columns of one weight
+//           segment) lane 0 of warp 4 arms the stage's mbarrier and issues the TMA loads -- B as one 2D box
+//           of the K-major weight image and, for contiguous A, A as one 2D box of 128 rows -- 128B-swizzled
+//           by the TMA unit into the canonical UMMA K-major layout; gathered A (X[pair_src]) is copied by
+//           the 128 producer threads with cp.async into the same layout (a tile::gather4 TMA moves 4 x 128 B
+//           per instruction from one thread: measured 3x slower for 128-byte rows), the next item's row
+//           indices loaded while the current one is issued.
+//   warp 8  MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M = 128, N = NT, K = 16) into one of two
 //           TMEM accumulators; tcgen05.commit frees the stage and publishes the accumulator.
 //   warps 0-3 epilogue (TMEM lane quarters): tcgen05.ld, optional per-row dot (RGAT s_p = P_p . a_r,
 //           P:962), pack to the output dtype into a 128B-swizzled staging box and one TMA 2D store
@@ -77,13 +78,13 @@ struct TmaCfg {
 };
 
 template <class TY, int NT, bool GATHER>
-__global__ void __launch_bounds__(192, 1) k_gemm_tma(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(288, 1) k_gemm_tma(const __grid_constant__ CUtensorMap tmA,
                                                      const __grid_constant__ CUtensorMap tmB,
                                                      const __grid_constant__ CUtensorMap tmY,
                                                      const Tile* __restrict__ tiles, int ntiles, int nblk,
-                                                     const int32_t* __restrict__ gather, int K, int ntot,
-                                                     TY* __restrict__ Y, const float* __restrict__ dotvec,
-                                                     float* __restrict__ dotout) {
+                                                     const bf16* __restrict__ A, const int32_t* __restrict__ gather,
+                                                     int K, int ntot, TY* __restrict__ Y,
+                                                     const float* __restrict__ dotvec, float* __restrict__ dotout) {
   using C = TmaCfg<NT, TY>;
   constexpr int S = C::S;
   static_assert(S >= 2, "not enough shared memory for two stages");
@@ -99,13 +100,13 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tma(const __grid_constant__ CUt
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t s_base = smem_u32(smem);
 
-  if (warp == 5) tmem_alloc<2 * C::NCOLS>(tslot);
+  if (warp == 8) tmem_alloc<2 * C::NCOLS>(tslot);
   if (tid == 128) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (C::TMA_Y) tma_prefetch_desc(&tmY);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], GATHER ? 129 : 1);  // gathered: 128 producer threads + the TMA expect_tx arrival
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -119,47 +120,69 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tma(const __grid_constant__ CUt
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
 
-  if (warp == 4) {
-    // ------------------------------------------------ TMA producer
-    int st = 0;
+  if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------ producers
+    // B (and A when contiguous) by TMA from lane 0 of warp 4; gathered A rows by the 128 producer threads
+    // with cp.async (one group per stage, up to S - 1 in flight, released on the stage's full barrier once
+    // landed and fenced for the async proxy), the next item's row indices loaded while this one is issued
+    const int ptid = tid - 128, c = ptid & 7, r0 = ptid >> 3;  // rows r0 + 16 i, 16-byte chunk c
+    int st = 0, pend = 0, old = 0;
     uint32_t ph = 0;
-    int ridx[4] = {0, 0, 0, 0};  // GATHER: A row indices of tile rows lane + 32 m (clamped to the tile)
+    int nidx[8], cur[8];
+    auto load_idx = [&](int it) {
+      const Tile t = tiles[it / nblk];
+      const int nrows = t.row1 - t.row0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 16 * i;
+        nidx[i] = __ldg(gather + t.row0 + (r < nrows ? r : nrows - 1));
+      }
+    };
+    if (GATHER && blockIdx.x < nitems) load_idx(blockIdx.x);
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       const int ti = it / nblk, nb = it - ti * nblk;
       const Tile t = tiles[ti];
       if (GATHER) {
-        const int nrows = t.row1 - t.row0;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int r = lane + 32 * m;
-          ridx[m] = __ldg(gather + t.row0 + (r < nrows ? r : nrows - 1));
-        }
+        for (int i = 0; i < 8; ++i) cur[i] = nidx[i];
+        if (it + (int)gridDim.x < nitems) load_idx(it + gridDim.x);
       }
       const int yb = t.w * ntot + nb * NT;
       for (int kb = 0; kb < KB; ++kb) {
-        if (lane == 0) {
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_expect_tx(&full[st], C::STAGE);
-        }
-        __syncwarp();
+        mbar_wait(&empty[st], ph ^ 1);
         const uint32_t sa = s_base + st * C::STAGE, sb = sa + C::A_BYTES;
-        if (GATHER) {
-#pragma unroll 4
-          for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3: lanes 4(j%8) .. 4(j%8)+3, register j/8
-            const int m = j >> 3, l0 = (j & 7) * 4;
-            const int v = m == 0 ? ridx[0] : m == 1 ? ridx[1] : m == 2 ? ridx[2] : ridx[3];
-            const int y0 = __shfl_sync(0xffffffffu, v, l0), y1 = __shfl_sync(0xffffffffu, v, l0 + 1);
-            const int y2 = __shfl_sync(0xffffffffu, v, l0 + 2), y3 = __shfl_sync(0xffffffffu, v, l0 + 3);
-            if (lane == 0) tma_gather4(sa + j * 512, &tmA, kb * 64, y0, y1, y2, y3, &full[st]);
-          }
-        } else if (lane == 0) {
-          tma_load_2d(sa, &tmA, kb * 64, t.row0, &full[st]);
+        if (ptid == 0) {
+          mbar_expect_tx(&full[st], GATHER ? C::B_BYTES : C::STAGE);
+          if (!GATHER) tma_load_2d(sa, &tmA, kb * 64, t.row0, &full[st]);
+          tma_load_2d(sb, &tmB, kb * 64, yb, &full[st]);
         }
-        if (lane == 0) tma_load_2d(sb, &tmB, kb * 64, yb, &full[st]);
+        if (GATHER) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = r0 + 16 * i;
+            cp_async16(sa + r * 128 + ((c ^ (r & 7)) << 4), A + (int64_t)cur[i] * K + kb * 64 + c * 8);
+          }
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          if (++pend == S - 1) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_arrive(&full[old]);
+            if (++old == S) old = 0;
+            --pend;
+          }
+        }
         if (++st == S) { st = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 5) {
+    if (GATHER) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      for (; pend > 0; --pend) {
+        mbar_arrive(&full[old]);
+        if (++old == S) old = 0;
+      }
+    }
+  } else if (warp == 8) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(NT);
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tma(const __grid_constant__ CUt
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 5) tmem_dealloc<2 * C::NCOLS>(tmem);
+  if (warp == 8) tmem_dealloc<2 * C::NCOLS>(tmem);
 }
 
 template <class TY, int NT>
@@ -271,11 +294,11 @@ void launch_tma(const GemmArgs& a, const bf16* Bt, cudaStream_t s) {
   const CUtensorMap tmB = make_map(Bt, 2, a.K, (int64_t)a.num_w * a.N, 64, NT, true);
   const CUtensorMap tmY = C::TMA_Y ? make_map(a.Y, (int)sizeof(TY), a.N, a.y_rows, C::CC, 32, true) : tmB;
   if (a.gather)
-    launch(a.name, k_gemm_tma<TY, NT, true>, dim3(grid), dim3(192), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles, nblk,
-           a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+    launch(a.name, k_gemm_tma<TY, NT, true>, dim3(grid), dim3(288), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles, nblk,
+           static_cast<const bf16*>(a.A), a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
   else
-    launch(a.name, k_gemm_tma<TY, NT, false>, dim3(grid), dim3(192), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles,
-           nblk, a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
+    launch(a.name, k_gemm_tma<TY, NT, false>, dim3(grid), dim3(288), C::SMEM, s, tmA, tmB, tmY, a.tiles, a.ntiles,
+           nblk, static_cast<const bf16*>(a.A), a.gather, a.K, a.N, static_cast<TY*>(a.Y), a.dotvec, a.dotout);
 }
 
 template <class TY>
@@ -564,18 +587,18 @@ void launch_pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-// Contiguous A (node GEMMs, ungathered segment GEMMs) runs here.  Gathered A stays on the cp.async
-// kernels by default: a tile::gather4 moves 4 x 128 B per instruction and one producer thread per SM
-// cannot issue them fast enough (mag pair GEMM at d = 64: 0.74 ms vs 0.24 ms for k_gemm_tc, whose
-// 128 threads per CTA and ~9 CTAs per SM keep more row gathers in flight).
-// RGNN_TMA=0: never (the cp.async generation for every GEMM); RGNN_TMA=2: gathered A as well.
+// GEMMs without the fused per-source row reduction run here: contiguous A (TMA) always, gathered A (the
+// producer warps' cp.async) when K > 128 -- at d = 64 the one-tile-per-CTA k_gemm_tc with ~9 CTAs per SM
+// keeps more independent row gathers in flight (mag pair GEMM 0.242 vs 0.324 ms, wikikg2 0.849 vs 1.228 ms),
+// from d = 512 this persistent pipeline is faster (D3 sweep, d = 1024: 962 vs 890 TFLOP/s).
+// RGNN_TMA=0: never (cp.async generation for every GEMM); 2: contiguous A only; 3: every GEMM.
 bool gemm_tma_enabled(const GemmArgs& a) {
   static const int mode = [] {
     const char* v = getenv("RGNN_TMA");
     return v ? atoi(v) : 1;
   }();
   if (mode == 0 || encode_fn() == nullptr) return false;
-  if (a.gather != nullptr && mode != 2) return false;
+  if (a.gather != nullptr && (mode == 2 || (mode == 1 && a.K <= 128))) return false;
   if (a.red_ptr != nullptr || a.y_rows <= 0) return false;  // fused row reduction: k_gemm_tc only
   // TMA: 16-byte aligned bases and row strides
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
