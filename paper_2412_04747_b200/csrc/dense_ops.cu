@@ -458,13 +458,18 @@ __global__ void __launch_bounds__(256) k_seg_reduce_rows(int64_t n, const int32_
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  int li[UN];  // row indices of the next batch, loaded one batch ahead (the list -> row chain is dependent)
+#pragma unroll
+  for (int q = 0; q < UN; ++q) li[q] = b + q < e ? list[b + q] : -1;
   for (int t = 0; t < span; t += UN) {
     uint4 raw[UN];
 #pragma unroll
     for (int q = 0; q < UN; ++q) {
       raw[q] = make_uint4(0, 0, 0, 0);
-      if (b + t + q < e) raw[q] = ldg16(Y + (int64_t)list[b + t + q] * ld + c * V);
+      if (li[q] >= 0) raw[q] = ldg16(Y + (int64_t)li[q] * ld + c * V);
     }
+#pragma unroll
+    for (int q = 0; q < UN; ++q) li[q] = b + t + UN + q < e ? list[b + t + UN + q] : -1;
 #pragma unroll
     for (int q = 0; q < UN; ++q) {
       float x[V];
