@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Summarise the F1 ablation runs (scripts/gpu_ablation.sh -> gpurun_out/abl/*.json) as the shape
+"""Summarise the F1 ablation runs (scripts/gpu_run.sh ablation -> gpurun_out/ablation/*.json) as the shape
 of the paper's tab:optimizations: speed-up of C (compact, reordering off), R (vanilla, reordered)
 and C+R over the unoptimized U (vanilla, reordering off), training and inference, plus the
 memory footprint (saved + scratch + graph index bytes, and the peak allocated)."""
