@@ -85,42 +85,47 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const Tile* __restrict__ tile
   }
 }
 
-// fp32 typed segment GEMM for N = 64 / 128 (the layer widths): 128 threads per 64-row tile, thread
-// (tx = tid % 16, ty = tid / 16) owns rows 8 ty .. 8 ty + 7 and columns 4 tx .. 4 tx + 3 (+ 64 for N = 128)
-// as packed f32x2 accumulators; A (gathered rows) and B chunks of KC = 16 k are loaded as float4 into
+// fp32 typed segment GEMM for N = 64 / 128 (the layer widths): N threads per 64-row tile, thread
+// (tx = tid % (N/8), ty = tid / (N/8)) owns rows 8 ty .. 8 ty + 7 and columns 4 tx .. 4 tx + 3 and
+// N/2 + 4 tx .. N/2 + 4 tx + 3 as packed f32x2 accumulators (8 x 8 per thread: half the shared-memory reads
+// per FMA of a 8 x 4 tile -- the 64-wide kernel was bound by the shared-memory pipe at 8 x 4); A (gathered rows) and B chunks of KC = 16 k are loaded as float4 into
 // registers one chunk ahead and stored transposed (A) / as is (B) into double-buffered shared memory, so
 // each k step is 2 + N/64 16-byte shared loads for 32 N/64 packed FMAs.  FFMA only (no TF32).
+// NTH threads per 64-row tile, each owning 8 rows x 8 columns (N = NTH): (tx = tid % 8, ty = tid / 8).
 template <int N>
-__global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles, const float* __restrict__ A, int K,
-                                                  const int32_t* __restrict__ gather, const float* __restrict__ B,
-                                                  bool transB, float* __restrict__ Y, const float* __restrict__ dotvec,
-                                                  float* __restrict__ dotout) {
-  constexpr int NB = N / 64;            // 64-column halves per thread (1 or 2)
-  constexpr int BQ = KC * N / 4 / 128;  // float4 of a B chunk per thread (2 or 4)
+__global__ void __launch_bounds__(N) k_gemm_f32(const Tile* __restrict__ tiles, const float* __restrict__ A, int K,
+                                                const int32_t* __restrict__ gather, const float* __restrict__ B,
+                                                bool transB, float* __restrict__ Y, const float* __restrict__ dotvec,
+                                                float* __restrict__ dotout) {
+  constexpr int NTH = N;                // threads: 8 x 8 outputs each over the 64 x N tile
+  constexpr int NB = 2;                 // 4-column groups per thread (8 columns: 4 tx and 4 (tx + 8 .. ) strided)
+  constexpr int AQ = BM * KC / 4 / NTH; // float4 of an A chunk per thread
+  constexpr int BQ = KC * N / 4 / NTH;  // float4 of a B chunk per thread
+  constexpr int TX = N / 8;             // threads along the columns
   __shared__ __align__(16) float As[2][KC][BM + 4];
   __shared__ __align__(16) float Bs[2][KC][N];
   const Tile t = tiles[blockIdx.x];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   const int nrows = t.row1 - t.row0;
   const float* Bw = B + (size_t)t.w * K * N;
-  // A loader: float4 q of the 64 x 16 chunk: row (tid + 128 q) / 4, k quad (tid + 128 q) % 4
-  int64_t arow[2];
+  // A loader: float4 q of the 64 x 16 chunk: row (tid + NTH q) / 4, k quad (tid + NTH q) % 4
+  int64_t arow[AQ];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int r = (tid + 128 * q) >> 2;
+  for (int q = 0; q < AQ; ++q) {
+    const int r = (tid + NTH * q) >> 2;
     arow[q] = r < nrows ? (gather ? (int64_t)gather[t.row0 + r] : (int64_t)(t.row0 + r)) : -1;
   }
-  float4 ra[2], rb[BQ];
+  float4 ra[AQ], rb[BQ];
   auto load = [&](int k0) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int kq = (tid + 128 * q) & 3;
+    for (int q = 0; q < AQ; ++q) {
+      const int kq = (tid + NTH * q) & 3;
       ra[q] = arow[q] >= 0 ? __ldg(reinterpret_cast<const float4*>(A + arow[q] * K + k0 + 4 * kq))
                            : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int q = 0; q < BQ; ++q) {
-      const int idx = tid + 128 * q;
+      const int idx = tid + NTH * q;
       if (!transB) {  // row kk of the chunk, 4 consecutive n
         const int kk = idx / (N / 4), n4 = idx % (N / 4);
         rb[q] = __ldg(reinterpret_cast<const float4*>(Bw + (size_t)(k0 + kk) * N + 4 * n4));
@@ -132,8 +137,8 @@ __global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int r = (tid + 128 * q) >> 2, kq = (tid + 128 * q) & 3;
+    for (int q = 0; q < AQ; ++q) {
+      const int r = (tid + NTH * q) >> 2, kq = (tid + NTH * q) & 3;
       As[buf][4 * kq + 0][r] = ra[q].x;
       As[buf][4 * kq + 1][r] = ra[q].y;
       As[buf][4 * kq + 2][r] = ra[q].z;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles
     }
 #pragma unroll
     for (int q = 0; q < BQ; ++q) {
-      const int idx = tid + 128 * q;
+      const int idx = tid + NTH * q;
       if (!transB) {
         const int kk = idx / (N / 4), n4 = idx % (N / 4);
         *reinterpret_cast<float4*>(&Bs[buf][kk][4 * n4]) = rb[q];
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles
       float2 b[2 * NB];
 #pragma unroll
       for (int h = 0; h < NB; ++h) {
-        const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 * h + 4 * tx]);
+        const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][(N / 2) * h + 4 * tx]);
         b[2 * h] = make_float2(b4.x, b4.y);
         b[2 * h + 1] = make_float2(b4.z, b4.w);
       }
@@ -196,19 +201,19 @@ __global__ void __launch_bounds__(128) k_gemm_f32(const Tile* __restrict__ tiles
       float d = 0.f;
 #pragma unroll
       for (int h = 0; h < NB; ++h) {
-        const float* dv = dotvec + (size_t)t.w * N + 64 * h + 4 * tx;
+        const float* dv = dotvec + (size_t)t.w * N + (N / 2) * h + 4 * tx;
         d = fmaf(acc[i][2 * h].x, dv[0], d);
         d = fmaf(acc[i][2 * h].y, dv[1], d);
         d = fmaf(acc[i][2 * h + 1].x, dv[2], d);
         d = fmaf(acc[i][2 * h + 1].y, dv[3], d);
       }
-      d = group_sum<16>(d);
+      d = group_sum<TX>(d);
       if (tx == 0 && lrow < nrows) dotout[row] = d;
     }
     if (lrow < nrows) {
 #pragma unroll
       for (int h = 0; h < NB; ++h)
-        *reinterpret_cast<float4*>(Y + row * N + 64 * h + 4 * tx) =
+        *reinterpret_cast<float4*>(Y + row * N + (N / 2) * h + 4 * tx) =
             make_float4(acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y);
     }
   }
@@ -230,7 +235,7 @@ void gemm_dispatch(const GemmArgs& a, cudaStream_t s) {
                     (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0;
     if (f32k && al && (a.N == 64 || a.N == 128)) {
       if (a.N == 64)
-        launch(a.name, k_gemm_f32<64>, g, dim3(128), 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, a.dotvec,
+        launch(a.name, k_gemm_f32<64>, g, dim3(64), 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, a.dotvec,
                a.dotout);
       else
         launch(a.name, k_gemm_f32<128>, g, dim3(128), 0, s, a.tiles, A, a.K, a.gather, B, a.transB, Y, a.dotvec,
