@@ -919,16 +919,18 @@ void dpair_expand(const rgnn_graph_s* g, const float* tdp, float* te, cudaStream
 }
 
 // dt[j] = sum of w[i].y over the CSR entries of (rel, dst) run j.  A warp owns 32 consecutive runs: each
-// lane sums its run when it has at most 32 entries; the longer runs of the warp (skewed in-degrees: a mag
-// hub has ~10^5 in-edges per relation) are then summed by the whole warp, one after the other, in lane
-// order with a fixed shuffle tree (deterministic).
+// lane sums its run when it has at most 32 entries; the warp's runs of 33 .. SPLIT_THRESH entries are then
+// summed by the whole warp, one after the other, in lane order with a fixed shuffle tree.  Longer runs (the
+// skewed in-degrees of a mag hub: ~10^5 in-edges per relation) are cut into SPLIT_CHUNK-entry chunks
+// (graph dpair_chunks), one warp each (k_dpair_chunk_sum), and their partials added in chunk order
+// (k_dpair_merge).  Deterministic throughout.
 __global__ void k_dpair_sum_w(int64_t UD, const int32_t* __restrict__ beg, const int32_t* __restrict__ cnt,
                               const float2* __restrict__ w, float* __restrict__ dt) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int b = j < UD ? beg[j] : 0, n = j < UD ? cnt[j] : 0;
-  const bool longrun = n > 32;
-  if (j < UD && !longrun) {
+  const bool longrun = n > 32 && n <= SPLIT_THRESH;
+  if (j < UD && n <= 32) {
     float acc = 0.f;
     for (int i = b; i < b + n; ++i) acc += w[i].y;
     dt[j] = acc;
@@ -945,9 +947,42 @@ __global__ void k_dpair_sum_w(int64_t UD, const int32_t* __restrict__ beg, const
   }
 }
 
-void dpair_sum_w(const rgnn_graph_s* g, const float2* w, float* dt, cudaStream_t s) {
+__global__ void k_dpair_chunk_sum(int64_t n, const int4* __restrict__ chunks, const float2* __restrict__ w,
+                                  float* __restrict__ part) {
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (k >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int4 c = chunks[k];
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // four independent loads in flight per lane
+  int i = c.y + lane;
+  for (; i + 96 < c.z; i += 128) {
+    a0 += w[i].y;
+    a1 += w[i + 32].y;
+    a2 += w[i + 64].y;
+    a3 += w[i + 96].y;
+  }
+  for (; i < c.z; i += 32) a0 += w[i].y;
+  float acc = group_sum<32>((a0 + a1) + (a2 + a3));
+  if (lane == 0) part[c.w] = acc;
+}
+
+__global__ void k_dpair_merge(int64_t n, const int4* __restrict__ splits, const float* __restrict__ part,
+                              float* __restrict__ dt) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int4 sp = splits[k];
+  float acc = 0.f;
+  for (int q = 0; q < sp.z; ++q) acc += part[sp.y + q];
+  dt[sp.x] = acc;
+}
+
+void dpair_sum_w(const rgnn_graph_s* g, const float2* w, float* dt, float* part, cudaStream_t s) {
   launch("dpair_sum", k_dpair_sum_w, dim3(ceil_div(g->UD, 256)), dim3(256), 0, s, g->UD,
          (const int32_t*)g->dpair_csr_beg, (const int32_t*)g->dpair_cnt, w, dt);
+  launch("dpair_sum/chunks", k_dpair_chunk_sum, dim3(ceil_div(g->n_dpair_chunks * 32, 256)), dim3(256), 0, s,
+         g->n_dpair_chunks, (const int4*)g->dpair_chunks, w, part);
+  launch("dpair_sum/merge", k_dpair_merge, dim3(ceil_div(g->n_dpair_splits, 256)), dim3(256), 0, s,
+         g->n_dpair_splits, (const int4*)g->dpair_splits, (const float*)part, dt);
 }
 
 void dpair_sum(const rgnn_graph_s* g, const float* dz, float* dt, cudaStream_t s) {

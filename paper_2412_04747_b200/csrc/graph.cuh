@@ -108,6 +108,12 @@ struct rgnn_graph_s {
   int32_t* dpair_dst = nullptr;      // [UD] (rel,dst) pairs ordered by (rel, dst)
   int32_t* dpair_csr_beg = nullptr;  // [UD]
   int32_t* dpair_cnt = nullptr;      // [UD]
+  // (rel, dst) runs longer than SPLIT_THRESH entries, for the deterministic two-level run sums (dpair_sum_w):
+  // SPLIT_CHUNK-entry chunks (run, begin, end, slot) and per run (run, first slot, number of slots, 0)
+  int4* dpair_chunks = nullptr;
+  int64_t n_dpair_chunks = 0;
+  int4* dpair_splits = nullptr;
+  int64_t n_dpair_splits = 0;
   int32_t* dst_dpair_ptr = nullptr;  // [N+1] lazily (ensure_dst_dpairs): dpairs grouped by destination
   int32_t* dst_dpairs = nullptr;     // [UD]
 

@@ -330,6 +330,35 @@ void build_stream_chunks(rgnn_graph_s* g, const std::vector<int32_t>& pb, const 
   }
 }
 
+// Chunks of the long (rel, dst) runs (graph.cuh dpair_chunks / dpair_splits); one-off host pass.
+void build_dpair_splits(rgnn_graph_s* g, cudaStream_t s) {
+  const int64_t UD = g->UD;
+  std::vector<int32_t> db(UD), dc(UD);
+  if (UD) {
+    RGNN_CUDA(cudaMemcpyAsync(db.data(), g->dpair_csr_beg, UD * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RGNN_CUDA(cudaMemcpyAsync(dc.data(), g->dpair_cnt, UD * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RGNN_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<int4> chunks, splits;
+  for (int64_t j = 0; j < UD; ++j) {
+    if (dc[j] <= SPLIT_THRESH) continue;
+    const int32_t b = db[j], e = db[j] + dc[j];
+    int32_t n = 0;
+    for (int32_t c = b; c < e; c += SPLIT_CHUNK, ++n)
+      chunks.push_back(make_int4((int)j, c, std::min(e, c + SPLIT_CHUNK), (int)chunks.size()));
+    splits.push_back(make_int4((int)j, (int)(chunks.size() - n), n, 0));
+  }
+  g->n_dpair_chunks = (int64_t)chunks.size();
+  g->n_dpair_splits = (int64_t)splits.size();
+  g->dpair_chunks = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<size_t>(chunks.size(), 1), s));
+  g->dpair_splits = reinterpret_cast<int4*>(g->dev_i32(4 * std::max<size_t>(splits.size(), 1), s));
+  if (!chunks.empty())
+    RGNN_CUDA(cudaMemcpyAsync(g->dpair_chunks, chunks.data(), chunks.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  if (!splits.empty())
+    RGNN_CUDA(cudaMemcpyAsync(g->dpair_splits, splits.data(), splits.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  RGNN_CUDA(cudaStreamSynchronize(s));
+}
+
 void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
   const int64_t N = g->N, U = g->U;
   std::vector<int32_t> rp(N + 1), pb(U), pd(U);
@@ -349,6 +378,7 @@ void build_work_plans(rgnn_graph_s* g, cudaStream_t s) {
   }
   build_work_plan(g, rb, rd, g->rows, s, lo, hi);
   build_work_plan(g, pb, pd, g->pairs, s);
+  build_dpair_splits(g, s);
   build_stream_chunks(g, pb, pd, g->pairs, s);
   // short items carry their first edge's gather index (rows: csr_pair, pairs: csc_dst) as
   // w = -2 - index (negative: never a partial slot), saving the short kernels one dependent load

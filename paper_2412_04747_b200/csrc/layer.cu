@@ -252,16 +252,17 @@ bool pair_spmm() {
 //    edge at d = 64 bf16) and writes per-pair bx rows, summed per relation into B_r;
 //  * weighted SpMM: the destination pass writes (alpha_e, dz_e) per CSR entry, the pair pass gathers only the
 //    G rows (128 B per edge) and B_r is a weighted row sum of X over the (rel, dst) runs of dz.
-// The SpMM wins when the (rel, dst) runs are short (AM, E/UD = 2.4: 2.53 -> 2.39 ms per step); on mag
-// (E/UD = 14.5: long runs, one hub row) the run sums and the weight writes cost more than the gather saves
-// (4.81 -> 4.85 ms), so it is chosen when E <= 8 UD.  RGNN_RGATW=0 / 1 forces either.
+// The SpMM is the default: AM (E/UD = 2.4) 2.53 -> 2.39 ms per step; mag (E/UD = 14.5, one hub row) 4.35 ->
+// 4.02 ms once the long (rel, dst) runs are summed in chunks (dpair_sum 0.38 -> 0.08 ms; before that the
+// recompute design was the faster one on mag, 4.81 vs 4.85 ms).  RGNN_RGATW=0 selects the recompute design.
 bool rgat_spmm(const rgnn_graph_s* g, const rgnn_layer_desc* d) {
   static const int mode = [] {
     const char* v = getenv("RGNN_RGATW");
     return v ? atoi(v) : -1;
   }();
+  (void)g;
   if (d->model != RGNN_RGAT || d->no_reorder || mode == 0) return false;
-  return mode == 1 || g->E <= 8 * g->UD;
+  return true;
 }
 
 // elements of the largest K-major weight image any GEMM of the layer builds (tcgen05 path)
@@ -275,7 +276,7 @@ int64_t bt_elems(const Ctx& c) {
 void layout_partial(const Ctx& c, Arena& ar, Partial& pt) {
   const int64_t rows = c.g->rows.n_slots * c.D;
   const int64_t pairs = c.g->pairs.n_slots * (c.d->model == RGNN_RGCN ? c.D : 2 * c.D);
-  pt.acc = ar.take<float>(std::max<int64_t>(std::max(rows, pairs), 1));
+  pt.acc = ar.take<float>(std::max<int64_t>({rows, pairs, c.g->n_dpair_chunks, 1}));  // also dpair_sum_w's partials
   pt.stat = ar.take<float2>(std::max<int64_t>(std::max(c.g->rows.n_slots * c.H, c.g->pairs.n_slots), 1));
 }
 
@@ -744,7 +745,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
       reduce_pair_rows(c, sc.dXp, c.Din, dX, true);  // owned rows hold the t-path term of the dst pass
     }
     if ((dW->dW || dW->db) && sc.wts) {  // B_r = sum_{e in r} dz_e X[d_e]: dz summed per (rel, dst) run, then
-      dpair_sum_w(g, sc.wts, sc.dt, c.s);  // a weighted row sum of X[dpair_dst] per relation
+      dpair_sum_w(g, sc.wts, sc.dt, sc.pt.acc, c.s);  // a weighted row sum of X[dpair_dst] per relation
       const Plan& pp = plan(g, seg_dpair_rel(g), WSUM_ROWS, c.s);
       seg_wsum(&pp, sc.dt, X, c.dt, c.D, g->dpair_dst, sc.Bsum, g->R, sc.partial, c.s);
     } else if (dW->dW || dW->db) {  // B_r = the sum of the per-pair bx rows of relation r

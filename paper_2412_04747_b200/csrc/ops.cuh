@@ -126,7 +126,8 @@ void add_dt(int64_t n, const void* x, int dtype, float* y, cudaStream_t s);
 // and the rank-1 rows dPt[j] = dt[j] b_rel(j) over a dpair_rel plan.
 void dpair_expand(const rgnn_graph_s* g, const float* tdp, float* te, cudaStream_t s);
 void dpair_sum(const rgnn_graph_s* g, const float* dz, float* dt, cudaStream_t s);
-void dpair_sum_w(const rgnn_graph_s* g, const float2* w, float* dt, cudaStream_t s);  // sums w[i].y
+// sums w[i].y; part: g->n_dpair_chunks floats of scratch
+void dpair_sum_w(const rgnn_graph_s* g, const float2* w, float* dt, float* part, cudaStream_t s);
 void dpair_outer(const Plan& p, const float* dt, const void* b, int dtype, int D, void* dPt, cudaStream_t s);
 void convert_f32(int64_t n, const void* in, int dtype, float* out, cudaStream_t s);
 void convert_dt(int64_t n, const float* in, void* out, int dtype, cudaStream_t s);

@@ -184,10 +184,13 @@ struct Work {
   bool has;
   int4 item;
   __device__ __forceinline__ bool init(int64_t n, const int4* __restrict__ items) {
+    return init(n, items, (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  }
+  // warp w of the launch (persistent kernels stride w over the grid)
+  __device__ __forceinline__ bool init(int64_t n, const int4* __restrict__ items, int64_t w) {
     lane = threadIdx.x & 31;
     g = lane / LPR;
     c = lane % LPR;
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     first = GROUP ? 0 : g;
     step = GROUP ? 1 : EG;
     if (GROUP) {
@@ -438,22 +441,53 @@ __global__ void __launch_bounds__(256) k_hgt_fwd_k(int64_t n, const int4* __rest
   }
 }
 
+// ------------------------------------------------------------------ staged relation vectors
+// The RGAT t-path reads y_r = W_r b_r (fp32, R x D) once per edge.  SY kernels stage all of y in
+// shared memory once per (persistent) block and read the row of an edge's relation when it is used,
+// instead of prefetching D floats per edge into registers through L1 (north_star: "shared-memory
+// staging of relation weights").  Used when R * D * 4 <= kStageYMax bytes.
+constexpr int kStageYMax = 48 * 1024;
+// The warp half (heavy chunks, medium rows: few items) is staged and persistent only when y is small:
+// measured on mag (R = 4, 1 KB: bwd warp half 0.70 -> 0.53 ms) and AM (R = 130, 33 KB: slower, the
+// staging is not amortised over the few warp items per block).
+constexpr int kStageYWarpMax = 8 * 1024;
+__device__ __forceinline__ const float* stage_y(const float* __restrict__ y, int ny) {
+  extern __shared__ float4 y_smem[];
+  for (int i = threadIdx.x; i < ny / 4; i += blockDim.x) y_smem[i] = __ldg(reinterpret_cast<const float4*>(y) + i);
+  __syncthreads();
+  return reinterpret_cast<const float*>(y_smem);
+}
+// V floats of a staged row (volatile: read where it is used, not hoisted into the prefetch registers)
+template <int V>
+__device__ __forceinline__ void lds_f32(const float* p, float* o) {
+#pragma unroll
+  for (int i = 0; i < V; i += 4) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p + i));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(o[i]), "=f"(o[i + 1]), "=f"(o[i + 2]), "=f"(o[i + 3]) : "r"(a));
+  }
+}
+
 // ------------------------------------------------------------------ RGAT forward (A3+A4+A5)
 // z_e = s_p + x_v . y_r (reordered t-path), l = LeakyReLU(z), out_v = sum softmax(l)_e P_p.
 // Requires d_in == d_out == D (the x_v chunk lives in the same lanes as the row chunk).
 // TE (reordering off, F1 ablation): the destination term t_e = (X_v W_r) . b_r is read per CSR
 // entry from te[] (computed by the dst-pair GEMM) instead of x_v . y_r.
-template <class TP, int D, bool GROUP, bool TE>
-__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
-                                                  float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
-                                                  const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
-                                                  const float* __restrict__ spair, const TP* __restrict__ X,
-                                                  const float* __restrict__ y, const float* __restrict__ te,
-                                                  float slope, float* __restrict__ out, float2* __restrict__ stats) {
+// SY: y staged in shared memory (persistent grid, stage_y); the edge's relation id is prefetched
+// instead of its y row.
+template <class TP, int D, bool GROUP, bool TE, bool SY>
+__device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4* __restrict__ items,
+                                              float* __restrict__ pacc, float2* __restrict__ pstat,
+                                              const int32_t* __restrict__ csr_pair, const int32_t* __restrict__ csr_rel,
+                                              const TP* __restrict__ P, const float* __restrict__ spair,
+                                              const TP* __restrict__ X, const float* __restrict__ y,
+                                              const float* __restrict__ te, float slope, float* __restrict__ out,
+                                              float2* __restrict__ stats) {
   using G = Geo<TP, D>;
   constexpr int V = G::V, LPR = G::LPR;
+  constexpr int VY = SY ? 1 : V;  // prefetched y columns per edge
   Work<GROUP, LPR> w;
-  if (!w.init(n, items)) return;
+  if (!w.init(n, items, wid)) return false;
   const int64_t v = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float x[V];
@@ -464,7 +498,8 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
   for (int t = 0; t < w.span; t += w.step * UNR) {
     const int i0 = b + t + w.first;
     uint4 rp[UNR];
-    float sp[UNR], yv[UNR][V];
+    float sp[UNR], yv[UNR][VY];
+    int rel[UNR];
     bool ok[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -472,13 +507,15 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
       ok[u] = i < e;
       rp[u] = make_uint4(0, 0, 0, 0);
       sp[u] = 0.f;
+      rel[u] = 0;
 #pragma unroll
-      for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
+      for (int k = 0; k < VY; ++k) yv[u][k] = 0.f;
       if (ok[u]) {
         int64_t p = csr_pair[i];
         rp[u] = ldg16(P + p * D + c * V);
         sp[u] = spair[p];
         if (TE) yv[u][0] = te[i];
+        else if (SY) rel[u] = csr_rel[i];
         else ld_f32<V>(y + (int64_t)csr_rel[i] * D + c * V, yv[u]);
       }
     }
@@ -489,8 +526,14 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
       if (TE) {
         t = yv[u][0];
       } else {
+        float yr[V];
+        if constexpr (SY) lds_f32<V>(y + rel[u] * D + c * V, yr);
+        else {
 #pragma unroll
-        for (int k = 0; k < V; ++k) t = fmaf(x[k], yv[u][k], t);
+          for (int k = 0; k < V; ++k) yr[k] = yv[u][k % VY];
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) t = fmaf(x[k], yr[k], t);
         t = gsum<LPR>(t, w.mask);
       }
       float z = sp[u] + t;
@@ -517,13 +560,44 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
   if (slot >= 0) {
     if (w.writer()) st_f32<V>(pacc + (int64_t)slot * D + c * V, acc);
     if (w.leader()) pstat[slot] = make_float2(m, s);
-    return;
+    return true;
   }
   float inv = s > 0.f ? 1.f / s : 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] *= inv;
   if (w.writer()) st_f32<V>(out + v * D + c * V, acc);
   if (w.leader()) stats[v] = make_float2(m, s);
+  return true;
+}
+
+#ifndef RGNN_SY_MINB
+#define RGNN_SY_MINB 4
+#endif
+template <class TP, int D, bool GROUP, bool TE>
+__global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
+                                                  float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
+                                                  const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+                                                  const float* __restrict__ spair, const TP* __restrict__ X,
+                                                  const float* __restrict__ y, const float* __restrict__ te,
+                                                  float slope, float* __restrict__ out, float2* __restrict__ stats,
+                                                  int ny) {
+  rgat_fwd_item<TP, D, GROUP, TE, false>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, n, items, pacc, pstat,
+                                         csr_pair, csr_rel, P, spair, X, y, te, slope, out, stats);
+}
+// persistent, y staged in shared memory
+template <class TP, int D, bool GROUP>
+__global__ void __launch_bounds__(256, RGNN_SY_MINB) k_rgat_fwd_sy(
+    int64_t n, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
+    const int32_t* __restrict__ csr_pair, const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+    const float* __restrict__ spair, const TP* __restrict__ X, const float* __restrict__ y,
+    const float* __restrict__ te, float slope, float* __restrict__ out, float2* __restrict__ stats, int ny) {
+  const float* ys = stage_y(y, ny);
+  const int64_t stride = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+       rgat_fwd_item<TP, D, GROUP, false, true>(wid, n, items, pacc, pstat, csr_pair, csr_rel, P, spair, X, ys, te, slope,
+                                               out, stats);
+       wid += stride) {
+  }
 }
 
 // ------------------------------------------------------------------ HGT backward, dst-major (A6)
@@ -733,8 +807,8 @@ __global__ void __launch_bounds__(256) k_hgt_bwd_dst_k(int64_t n, const int4* __
 // for the explicit destination-side GEMMs.
 // WT: (alpha_e, dz_e) written per CSR entry into wts for the weighted-SpMM pair pass, the node record is
 // the G row alone (GX [N][D]), no bx rows and no nst.
-template <class TP, int D, bool GROUP, bool TE, bool SGL, bool WT>
-__global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
+template <class TP, int D, bool GROUP, bool TE, bool SGL, bool WT, bool SY>
+__device__ __forceinline__ bool rgat_bwd_dst_item(int64_t wid, int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
@@ -751,8 +825,9 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
   constexpr int V = G::V, LPR = G::LPR;
   // the single-edge stores and the weight writes need registers: fewer edges per step
   constexpr int UN = SGL ? RGNN_UNR_SGL : WT ? RGNN_UNR_WT : UNR;
+  constexpr int VY = SY ? 1 : V;  // prefetched y columns per edge (SY: y staged, read when used)
   Work<GROUP, LPR> w;
-  if (!w.init(n, items)) return;
+  if (!w.init(n, items, wid)) return false;
   const int64_t v = w.item.x;
   const int b = w.item.y, e = w.item.z, slot = w.item.w, c = w.c;
   float dx[V];
@@ -782,8 +857,8 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
     for (int t = 0; t < w.span; t += w.step * UN) {
       const int i0 = b + t + w.first;
       uint4 rp[UN];
-      float sp[UN], yv[UN][V];
-      int pid[UN], rel[UN];  // SGL: single-edge pair id (else -1) and its relation
+      float sp[UN], yv[UN][VY];
+      int pid[UN], rel[UN], ry[UN];  // SGL: single-edge pair id (else -1) and its relation; SY: relation
 #pragma unroll
       for (int u = 0; u < UN; ++u) {
         int i = i0 + u * w.step;
@@ -791,8 +866,9 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
         sp[u] = 0.f;
         pid[u] = -1;
         rel[u] = 0;
+        ry[u] = 0;
 #pragma unroll
-        for (int k = 0; k < V; ++k) yv[u][k] = 0.f;
+        for (int k = 0; k < VY; ++k) yv[u][k] = 0.f;
         if (i < e) {
           int64_t p = csr_pair[i];
           rp[u] = ldg16(P + p * D + c * V);
@@ -801,7 +877,8 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
             yv[u][0] = te[i];
           } else {
             const int r = csr_rel[i];
-            ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
+            if (SY) ry[u] = r;
+            else ld_f32<V>(y + (int64_t)r * D + c * V, yv[u]);
             if (SGL && single[i]) {
               pid[u] = (int)p;
               rel[u] = r;
@@ -812,12 +889,17 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
 #pragma unroll
       for (int u = 0; u < UN; ++u) {
         int i = i0 + u * w.step;
-        float pv[V];
+        float pv[V], yr[V];
         cvt16<TP>(rp[u], pv);
+        if constexpr (SY) lds_f32<V>(y + ry[u] * D + c * V, yr);
+        else {
+#pragma unroll
+          for (int k = 0; k < V; ++k) yr[k] = yv[u][k % VY];
+        }
         float t = 0.f, da = 0.f;
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          if (!TE) t = fmaf(x[k], yv[u][k], t);
+          if (!TE) t = fmaf(x[k], yr[k], t);
           da = fmaf(gv[k], pv[k], da);
         }
         t = TE ? yv[u][0] : gsum<LPR>(t, w.mask);
@@ -832,7 +914,7 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
             if (c == 0) dz_out[i] = dz;
           } else {
 #pragma unroll
-            for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yv[u][k], dx[k]);
+            for (int k = 0; k < V; ++k) dx[k] = fmaf(dz, yr[k], dx[k]);
             if (SGL && pid[u] >= 0) {  // single-edge pair: dP_p = alpha G_v + dz a_r, bx_p = dz X_v, wsum_p = dz
               float av[V], o[V];
               cvt16<TP>(ldg16(avec + (int64_t)rel[u] * D + c * V), av);
@@ -851,10 +933,55 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
       }
     }
   }
-  if (TE) return;
+  if (TE) return true;
   if (!GROUP) sum_groups<LPR, V>(dx);
-  if (!w.writer()) return;
+  if (!w.writer()) return true;
   st_f32<V>((slot >= 0 ? pacc + (int64_t)slot * D : dX + v * D) + c * V, dx);
+  return true;
+}
+
+
+template <class TP, int D, bool GROUP, bool TE, bool SGL, bool WT>
+__global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restrict__ items,
+                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
+                                                      const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+                                                      const float* __restrict__ spair, const TP* __restrict__ X,
+                                                      const float* __restrict__ y, const float* __restrict__ te,
+                                                      float* __restrict__ dz_out, float slope,
+                                                      const float2* __restrict__ stats,
+                                                      const float* __restrict__ Gr, const float* __restrict__ out,
+                                                      float* __restrict__ dX, TP* __restrict__ GX,
+                                                      float4* __restrict__ nst, const uint8_t* __restrict__ single,
+                                                      const TP* __restrict__ avec, TP* __restrict__ dP,
+                                                      TP* __restrict__ bx, float* __restrict__ wsum,
+                                                      float2* __restrict__ wts, int ny) {
+  rgat_bwd_dst_item<TP, D, GROUP, TE, SGL, WT, false>((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, n, items,
+                                                      pacc, csr_pair, csr_rel, P, spair, X, y, te, dz_out, slope,
+                                                      stats, Gr, out, dX, GX, nst, single, avec, dP, bx, wsum, wts);
+}
+// persistent, y staged in shared memory
+template <class TP, int D, bool GROUP, bool SGL, bool WT>
+__global__ void __launch_bounds__(256, RGNN_SY_MINB) k_rgat_bwd_dst_sy(int64_t n, const int4* __restrict__ items,
+                                                      float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
+                                                      const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
+                                                      const float* __restrict__ spair, const TP* __restrict__ X,
+                                                      const float* __restrict__ y, const float* __restrict__ te,
+                                                      float* __restrict__ dz_out, float slope,
+                                                      const float2* __restrict__ stats,
+                                                      const float* __restrict__ Gr, const float* __restrict__ out,
+                                                      float* __restrict__ dX, TP* __restrict__ GX,
+                                                      float4* __restrict__ nst, const uint8_t* __restrict__ single,
+                                                      const TP* __restrict__ avec, TP* __restrict__ dP,
+                                                      TP* __restrict__ bx, float* __restrict__ wsum,
+                                                      float2* __restrict__ wts, int ny) {
+  const float* ys = stage_y(y, ny);
+  const int64_t stride = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+       rgat_bwd_dst_item<TP, D, GROUP, false, SGL, WT, true>(wid, n, items, pacc, csr_pair, csr_rel, P, spair, X, ys, te,
+                                                           dz_out, slope, stats, Gr, out, dX, GX, nst, single, avec,
+                                                           dP, bx, wsum, wts);
+       wid += stride) {
+  }
 }
 
 // ------------------------------------------------------------------ pair-major backward (A7)
@@ -1893,6 +2020,52 @@ void launch_plan(const char* name, const WorkPlan& wp, int lpr, KW kw, KG kg, cu
   profile_end(slot, s);
 }
 
+// RGNN_STAGE_Y=0 keeps the RGAT t-path rows of y in registers via L1 (A/B switch for stage_y)
+inline bool stage_y_on() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_STAGE_Y");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// Grid of a persistent kernel: the blocks that are resident at once (occupancy with `smem` bytes of
+// dynamic shared memory) times the SM count, at most `need`.
+template <class K>
+dim3 resident_grid(K k, size_t smem, unsigned need) {
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  const unsigned cap = (unsigned)std::max(1, per_sm) * (unsigned)std::max(1, sms);
+  return dim3(std::min(need, cap));
+}
+
+// launch_plan with persistent kernels that stage `smem` bytes per block (grid-stride over the items);
+// a warp-half kernel without staging (no dynamic shared memory in its signature) is launched plainly.
+template <class KW, class KG, class... Args>
+void launch_plan_staged(const char* name, const WorkPlan& wp, int lpr, size_t smem, bool warp_staged, KW kw, KG kg,
+                        cudaStream_t s, Args... args) {
+  const int64_t nl = wp.n_items - wp.n_warp;
+  int slot = -1;
+  profile_begin(name, s, &slot);
+  cudaStream_t side = fork_side(s);
+  if (warp_staged)
+    launch(intern(std::string(name) + "/warp"), kw, resident_grid(kw, smem, warps(wp.n_warp).x), dim3(256), smem, s,
+           wp.n_warp, (const int4*)wp.items, args...);
+  else
+    launch(intern(std::string(name) + "/warp"), kw, warps(wp.n_warp), dim3(256), 0, s, wp.n_warp,
+           (const int4*)wp.items, args...);
+  launch(intern(std::string(name) + "/group"), kg, resident_grid(kg, smem, groups(nl, lpr).x), dim3(256), smem, side,
+         nl, (const int4*)(wp.items + wp.n_warp), args...);
+  join_side(s);
+  profile_end(slot, s);
+}
+
 // RGNN_SHORT=0 turns the short-item kernels off (A/B switch)
 inline bool use_short() {
   static const bool on = [] {
@@ -1992,12 +2165,23 @@ void rgat_fwd_traverse(const rgnn_graph_s* g, int dtype, int D, const void* P, c
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
+      const int ny = g->R * DD;
+      const bool sy = !te && stage_y_on() && (size_t)ny * sizeof(float) <= (size_t)kStageYMax;
+      const bool sy_warp = (size_t)ny * sizeof(float) <= (size_t)kStageYWarpMax;
       auto go = [&](auto kw, auto kg) {
-        launch_plan("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
-                    (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair,
-                    static_cast<const TP*>(X), y, te, slope, out, stats);
+        if (sy)
+          launch_plan_staged("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, (size_t)ny * sizeof(float), sy_warp, kw,
+                             kg, s,
+                             pt.acc, pt.stat, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
+                             static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te, slope, out, stats, ny);
+        else
+          launch_plan("rgat_fwd_traverse", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, pt.stat,
+                      (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair,
+                      static_cast<const TP*>(X), y, te, slope, out, stats, ny);
       };
       if (te) go(k_rgat_fwd<TP, DD, false, true>, k_rgat_fwd<TP, DD, true, true>);
+      else if (sy && sy_warp) go(k_rgat_fwd_sy<TP, DD, false>, k_rgat_fwd_sy<TP, DD, true>);
+      else if (sy) go(k_rgat_fwd<TP, DD, false, false>, k_rgat_fwd_sy<TP, DD, true>);
       else go(k_rgat_fwd<TP, DD, false, false>, k_rgat_fwd<TP, DD, true, false>);
     });
     launch("merge_heavy_rows", k_merge_softmax<DD, 1>, dim3(g->rows.n_split), dim3(256), 0, s, g->rows.n_split,
@@ -2050,19 +2234,34 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
     constexpr int DD = decltype(Dc)::value;
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
+      const int ny = g->R * DD;
+      // not with the single-edge-pair stores (SGL): capped at 64 registers they spill (AM RGAT, measured slower)
+      const bool sy = !te && y && !single && stage_y_on() && (size_t)ny * sizeof(float) <= (size_t)kStageYMax;
+      const bool sy_warp = (size_t)ny * sizeof(float) <= (size_t)kStageYWarpMax;
       auto go = [&](auto kw, auto kg) {
-        launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, kw, kg, s, pt.acc, (const int32_t*)g->csr_pair,
-                    (const int32_t*)g->csr_rel, static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te,
-                    dz, slope, stats, G, out, dX, static_cast<TP*>(GX), nst, single, static_cast<const TP*>(a),
-                    static_cast<TP*>(dP), static_cast<TP*>(bx), wsum, wts);
+        auto args = std::make_tuple(pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
+                                    static_cast<const TP*>(P), spair, static_cast<const TP*>(X), y, te, dz, slope,
+                                    stats, G, out, dX, static_cast<TP*>(GX), nst, single, static_cast<const TP*>(a),
+                                    static_cast<TP*>(dP), static_cast<TP*>(bx), wsum, wts, ny);
+        std::apply([&](auto... ar) {
+          if (sy)
+            launch_plan_staged("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, (size_t)ny * sizeof(float), sy_warp, kw,
+                               kg, s, ar...);
+          else
+            launch_plan("rgat_bwd_dst", g->rows, Geo<TP, DD>::LPR, kw, kg, s, ar...);
+        }, args);
+      };
+      auto pick = [&](auto sc, auto wc) {
+        constexpr bool SG = decltype(sc)::value, WT = decltype(wc)::value;
+        if (sy && sy_warp) go(k_rgat_bwd_dst_sy<TP, DD, false, SG, WT>, k_rgat_bwd_dst_sy<TP, DD, true, SG, WT>);
+        else if (sy) go(k_rgat_bwd_dst<TP, DD, false, false, SG, WT>, k_rgat_bwd_dst_sy<TP, DD, true, SG, WT>);
+        else go(k_rgat_bwd_dst<TP, DD, false, false, SG, WT>, k_rgat_bwd_dst<TP, DD, true, false, SG, WT>);
       };
       if (te) go(k_rgat_bwd_dst<TP, DD, false, true, false, false>, k_rgat_bwd_dst<TP, DD, true, true, false, false>);
-      else if (wts && single)
-        go(k_rgat_bwd_dst<TP, DD, false, false, true, true>, k_rgat_bwd_dst<TP, DD, true, false, true, true>);
-      else if (wts) go(k_rgat_bwd_dst<TP, DD, false, false, false, true>, k_rgat_bwd_dst<TP, DD, true, false, false, true>);
-      else if (single)
-        go(k_rgat_bwd_dst<TP, DD, false, false, true, false>, k_rgat_bwd_dst<TP, DD, true, false, true, false>);
-      else go(k_rgat_bwd_dst<TP, DD, false, false, false, false>, k_rgat_bwd_dst<TP, DD, true, false, false, false>);
+      else if (wts && single) pick(std::true_type(), std::true_type());
+      else if (wts) pick(std::false_type(), std::true_type());
+      else if (single) pick(std::true_type(), std::false_type());
+      else pick(std::false_type(), std::false_type());
       launch("rgat_node_prep", k_rgat_node_prep<TP, DD>, groups(g->rows.n_split, Geo<TP, DD>::LPR), dim3(256), 0, s,
              g->rows.n_split, (const int4*)g->rows.splits, G, static_cast<const TP*>(X), out, stats,
              static_cast<TP*>(GX), nst);

@@ -7,6 +7,8 @@
 #                                             launch list of the default bench, compute-sanitizer memcheck
 #   bash scripts/gpu_run.sh ablation          F1 C/R ablation runs (scripts/ablation_table.py summarises them)
 #   bash scripts/gpu_run.sh ncu KERNEL_REGEX [CONFIG]   ncu --set full of the matching kernels of one step
+#   bash scripts/gpu_run.sh abhead CONFIG...  HEAD (a clean checkout in ab_head/, made by scripts/mk_ab_head.sh)
+#                                             against the working tree, interleaved, twice per config
 # Outputs go to gpurun_out/$TAG/ (TAG defaults to the task name).
 set -u
 task=${1:-verify}; shift || true
@@ -68,6 +70,18 @@ case "$task" in
         python bench.py --config $c $mode --no-reorder --no-cpu-baseline --no-e2e 2>&1 | tail -1 > "$out/${tag}_C.json"
         python bench.py --config $c $mode --no-compact --no-cpu-baseline --no-e2e 2>&1 | tail -1 > "$out/${tag}_R.json"
         python bench.py --config $c $mode --no-compact --no-reorder --no-cpu-baseline --no-e2e 2>&1 | tail -1 > "$out/${tag}_U.json"
+      done
+    done
+    ;;
+  abhead)
+    build
+    (cd ab_head && python -c "import __graft_entry__ as g; g.build()" > "../$out/build_head.log" 2>&1) || { tail -30 "$out/build_head.log"; exit 1; }
+    for cfg in "$@"; do
+      for i in 1 2; do
+        (cd ab_head && timeout 300 python bench.py --config "$cfg" --no-cpu-baseline --no-ncu --no-e2e --steps 20 \
+          > "../$out/${cfg}_head$i.json" 2>&1); summ "$out/${cfg}_head$i.json" "$cfg HEAD"
+        timeout 300 python bench.py --config "$cfg" --no-cpu-baseline --no-ncu --no-e2e --steps 20 \
+          > "$out/${cfg}_new$i.json" 2>&1; summ "$out/${cfg}_new$i.json" "$cfg NEW "
       done
     done
     ;;

@@ -160,6 +160,8 @@ def test_split_heavy_rows(model, dtype):
                           a_src=0.3, a_dst=1.3, seed=5, name="hubs")
     deg = np.bincount(g.dst, minlength=g.num_nodes)
     assert deg.max() > 1024  # graph.cuh SPLIT_THRESH
+    # a (rel, dst) run > 1024 as well: RGAT's chunked run sums (dpair_chunks, k_dpair_chunk_sum / merge)
+    assert np.bincount(g.rel.astype(np.int64) * g.num_nodes + g.dst).max() > 1024
     run_case(model, g, 64, 64, dtype)
 
 
