@@ -573,6 +573,9 @@ __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4
 #ifndef RGNN_SY_MINB
 #define RGNN_SY_MINB 4
 #endif
+#ifndef RGNN_SY_MINB_SGL
+#define RGNN_SY_MINB_SGL 3  // the single-edge-pair stores need more registers (64 spill)
+#endif
 template <class TP, int D, bool GROUP, bool TE>
 __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restrict__ items, float* __restrict__ pacc,
                                                   float2* __restrict__ pstat, const int32_t* __restrict__ csr_pair,
@@ -961,7 +964,7 @@ __global__ void RGNN_RGAT_DST_LB k_rgat_bwd_dst(int64_t n, const int4* __restric
 }
 // persistent, y staged in shared memory
 template <class TP, int D, bool GROUP, bool SGL, bool WT>
-__global__ void __launch_bounds__(256, RGNN_SY_MINB) k_rgat_bwd_dst_sy(int64_t n, const int4* __restrict__ items,
+__global__ void __launch_bounds__(256, SGL ? RGNN_SY_MINB_SGL : RGNN_SY_MINB) k_rgat_bwd_dst_sy(int64_t n, const int4* __restrict__ items,
                                                       float* __restrict__ pacc, const int32_t* __restrict__ csr_pair,
                                                       const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
                                                       const float* __restrict__ spair, const TP* __restrict__ X,
@@ -2029,6 +2032,15 @@ inline bool stage_y_on() {
   return on;
 }
 
+// RGNN_STAGE_Y_SGL=1: staged y also for the destination pass that resolves single-edge pairs (AM)
+inline bool stage_y_sgl() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_STAGE_Y_SGL");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 // Grid of a persistent kernel: the blocks that are resident at once (occupancy with `smem` bytes of
 // dynamic shared memory) times the SM count, at most `need`.
 template <class K>
@@ -2235,8 +2247,8 @@ void rgat_bwd_dst(const rgnn_graph_s* g, int dtype, int D, const void* P, const 
     by_dtype(dtype, [&](auto* tp) {
       using TP = std::remove_pointer_t<decltype(tp)>;
       const int ny = g->R * DD;
-      // not with the single-edge-pair stores (SGL): capped at 64 registers they spill (AM RGAT, measured slower)
-      const bool sy = !te && y && !single && stage_y_on() && (size_t)ny * sizeof(float) <= (size_t)kStageYMax;
+      const bool sy = !te && y && (!single || stage_y_sgl()) && stage_y_on() &&
+                      (size_t)ny * sizeof(float) <= (size_t)kStageYMax;
       const bool sy_warp = (size_t)ny * sizeof(float) <= (size_t)kStageYWarpMax;
       auto go = [&](auto kw, auto kg) {
         auto args = std::make_tuple(pt.acc, (const int32_t*)g->csr_pair, (const int32_t*)g->csr_rel,
