@@ -403,12 +403,16 @@ bool fused_pair_bwd(const Ctx& c, const Segs& sg, const void* X, const void* dP,
 // Single-edge pairs get their pair-gradient rows from the destination-major pass (which holds
 // alpha_e, dl_e, q_v and G_v of the edge) instead of a gather in the pair-major pass; used when
 // they are >= 30 % of the pairs (AM 71 %, wikikg2 91 %, mag 14 %).  RGNN_SINGLE=0 / 1 forces it.
-bool single_in_dst(const rgnn_graph_s* g) {
+// Not by default for RGAT's weighted-SpMM pair pass (spmm = true): its destination pass then stays at
+// the register count that admits the staged-y kernel, and the pair pass handles the single-edge pairs
+// with one gathered G row each (AM RGAT 2.296 -> 2.276 ms, measured).
+bool single_in_dst(const rgnn_graph_s* g, bool spmm = false) {
   static const int mode = [] {
     const char* v = getenv("RGNN_SINGLE");
     return v ? atoi(v) : -1;
   }();
   if (mode >= 0) return mode == 1;
+  if (spmm) return false;
   const int64_t n_single = g->pairs.n_items - g->pairs.n_multi;
   return 10 * n_single >= 3 * g->U;
 }
@@ -727,7 +731,7 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     rgat_backward_nr(c, X, w, out, sv, G, dX, dW, sc);
   } else if (model == RGNN_RGAT) {
     float* dXt = dX ? dX : static_cast<float*>(sc.dQ);
-    const bool single = single_in_dst(g);
+    const bool single = single_in_dst(g, sc.wts != nullptr);
     rgat_bwd_dst(g, c.dt, c.D, sv.P, sv.spair, X, sv.y, nullptr, nullptr, c.d->leaky_slope, sv.stats, G, out, dXt,
                  sc.GQ, sc.wts ? nullptr : sc.nst, single ? g->csr_single : nullptr, w->a, sc.dP,
                  sc.wts ? nullptr : sc.bx, sc.wsum, sc.wts, sc.pt, c.s);

@@ -88,6 +88,11 @@ case "$task" in
     timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$1" -o "$out/ncu" \
       python bench.py --config "${2:-mag_hgt}" --no-cpu-baseline --no-ncu --no-e2e --steps 1 --warmup 1 > "$out/ncu.log" 2>&1
     tail -2 "$out/ncu.log"
+    ncu -i "$out/ncu.ncu-rep" --page details --csv > "$out/details.csv" 2>/dev/null
+    python scripts/ncu_summary.py "$out/details.csv" > "$out/summary.txt"; head -60 "$out/summary.txt"
+    ncu -i "$out/ncu.ncu-rep" --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct,smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct,smsp__warp_issue_stalled_mio_throttle_per_warp_active.pct,l1tex__t_bytes_pipe_lsu_mem_global_op_ld.sum,sm__warps_active.avg.pct_of_peak_sustained_active > "$out/raw.csv" 2>/dev/null
+    # the report itself only when small enough to travel back (gpurun copies <= 64 MiB)
+    [ "$(stat -c %s "$out/ncu.ncu-rep")" -gt 40000000 ] && rm -f "$out/ncu.ncu-rep"
     ;;
   *) echo "unknown task $task"; exit 2 ;;
 esac

@@ -1,6 +1,8 @@
 """Parity of the non-default kernel designs that the library selects by environment switch (read once per
-process, so each case runs in a subprocess): the RGAT recompute pair pass (RGNN_RGATW=0) and the
-register-resident t-path rows (RGNN_STAGE_Y=0, also what graphs with R * d * 4 > 48 KB run).
+process, so each case runs in a subprocess): the RGAT recompute pair pass (RGNN_RGATW=0), the
+register-resident t-path rows (RGNN_STAGE_Y=0, also what graphs with R * d * 4 > 48 KB run) and the
+single-edge pairs resolved in the destination pass of the weighted-SpMM design (RGNN_SINGLE=1, with and
+without staged y).
 Same oracle and tolerances as tests/test_gpu_layers.py.
 """
 import os
@@ -26,7 +28,8 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"RGNN_RGATW": "0"}, {"RGNN_STAGE_Y": "0"}, {"RGNN_RGATW": "0", "RGNN_STAGE_Y": "0"}])
+@pytest.mark.parametrize("env", [{"RGNN_RGATW": "0"}, {"RGNN_STAGE_Y": "0"}, {"RGNN_RGATW": "0", "RGNN_STAGE_Y": "0"},
+                                 {"RGNN_SINGLE": "1"}, {"RGNN_SINGLE": "1", "RGNN_STAGE_Y_SGL": "1"}])
 def test_rgat_switches(env):
     r = subprocess.run([sys.executable, "-c", CASE], cwd=ROOT, env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=600)
