@@ -2004,6 +2004,17 @@ inline bool pair_split() {
   return on;
 }
 
+// RGNN_SHORT_PAIR=1: the HGT pair pass keeps its KI = 2 short-item kernel beside the split-halves group
+// kernel; default: the split-halves kernel (32 registers, full occupancy) takes the short pairs as well
+// (mag HGT pair pass 1.175 -> 1.162 ms; the short kernel spills at 64 registers)
+inline bool short_pairs_split() {
+  static const bool on = [] {
+    const char* v = getenv("RGNN_SHORT_PAIR");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 inline dim3 warps(int64_t n) { return dim3(ceil_div(n * 32, 256)); }
 inline dim3 groups(int64_t n, int lpr) { return dim3(ceil_div(ceil_div(n, 32 / lpr) * (int64_t)32, 256)); }
 
@@ -2397,6 +2408,12 @@ void hgt_bwd_pair(const rgnn_graph_s* g, int dtype, int D, int H, const void* KM
                                static_cast<const TP*>(GQ), nst, static_cast<TP*>(dKM));
         };
         if constexpr (std::is_same_v<TP, bf16> && DD / 4 <= 32 && (DD / 8) % HH == 0) {
+          if (pair_split() && !short_pairs_split()) {  // the split-halves kernel also takes the short pairs
+            launch_plan("hgt_bwd_pair", wp, DD / 4, k_hgt_bwd_pair<TP, DD, false, HH>, k_hgt_bwd_pair_sp<DD, HH, 8>, s,
+                        pt.acc, (const int32_t*)g->csc_dst, static_cast<const TP*>(KM), static_cast<const TP*>(GQ),
+                        nst, static_cast<TP*>(dKM));
+            return;
+          }
           if (pair_split()) {  // group mode: split halves, D / 4 lanes per pair; warp and short halves as before
             launch_plan_short<2>("hgt_bwd_pair", wp, DD / 4 | Geo<TP, DD>::LPR << 8,
                                  k_hgt_bwd_pair<TP, DD, false, HH>, k_hgt_bwd_pair_sp<DD, HH, 8>,
