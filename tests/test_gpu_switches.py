@@ -34,3 +34,22 @@ def test_rgat_switches(env):
     r = subprocess.run([sys.executable, "-c", CASE], cwd=ROOT, env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (env, r.stdout[-2000:], r.stderr[-4000:])
+
+
+CASE_HGT = """
+from synth import config_graph
+from tests.test_gpu_layers import run_case
+for dtype in ("f32", "bf16"):
+    run_case("hgt", config_graph("aifb", seed=1), 64, 64, dtype)
+    run_case("hgt", config_graph("tiny", seed=1), 64, 64, dtype)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"RGNN_SHORT_PAIR": "1"}, {"RGNN_SPLIT": "0"}, {"RGNN_SHORT": "0"}])
+def test_hgt_switches(env):
+    """The HGT pair pass with its KI = 2 short-item kernel (RGNN_SHORT_PAIR=1), the staged group kernel
+    instead of the split-halves one (RGNN_SPLIT=0), and no short-item kernels anywhere (RGNN_SHORT=0)."""
+    r = subprocess.run([sys.executable, "-c", CASE_HGT], cwd=ROOT, env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (env, r.stdout[-2000:], r.stderr[-4000:])
