@@ -56,7 +56,7 @@ case "$task" in
     done
     timeout 900 python bench.py --impl reference > "$out/bench_reference.json" 2>&1; tail -c 300 "$out/bench_reference.json"; echo
     timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-      --log-file "$out/launches_mag_hgt.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-ncu --no-e2e > /dev/null 2>&1
+      --log-file "$out/launches_mag_hgt.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-ncu --no-e2e > /dev/null 2>&1  # 5 launches per step kernel (launch_summary.py CSV 5)
     # compute-sanitizer is closed on the GPU pool (round 2); the last memcheck log is profiles/r02_memcheck_gpu_suite.log
     ;;
   ablation)

@@ -30,7 +30,7 @@ for r in rows[hi + 1:]:
 step = {k: v for k, v in tot.items() if cnt[k] % per == 0}
 T = sum(step.values())
 print(f"# {path}: ncu gpu__time_duration.sum per launch (--clock-control none; cold-cache, serialised launches:")
-print(f"# compare SHARES, not absolutes).  Per-step kernels = launched a multiple of {per} times (steps + warmup).")
+print(f"# compare SHARES, not absolutes).  Per-step kernels = launched a multiple of {per} times (warm-up + timed steps + the per-kernel profiling pass of bench.py).")
 print(f"{'share':>7} {'launches':>8} {'mean us':>10} {'total us':>11} {'DRAM GB/launch':>14} {'DRAM TB/s':>9}  kernel")
 for k, v in sorted(step.items(), key=lambda x: -x[1]):
     gb = dram[k] / cnt[k] / 1e9 if k in dram else float("nan")
