@@ -409,6 +409,44 @@ __global__ void __launch_bounds__(256) k_seg_partial_reduce(int nseg, const int3
   }
 }
 
+// The same sum for widths that are a multiple of 128: block = (segment, 128 consecutive elements), lane l of
+// every warp owns elements 4l .. 4l+3 (16-byte loads), the 8 warps take interleaved tiles (two loads in
+// flight per lane), warp sums added in warp order: fixed order, deterministic.  A quarter of the blocks of
+// k_seg_partial_reduce (wikikg2: 535 segments x 4096-wide weight gradients).
+__global__ void __launch_bounds__(256) k_seg_partial_reduce4(int nseg, const int32_t* __restrict__ seg_tile_ptr,
+                                                             const int32_t* __restrict__ seg_w,
+                                                             const float* __restrict__ partial, int64_t width,
+                                                             float* __restrict__ out) {
+  __shared__ float4 red[8][32];
+  const int sidx = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = seg_tile_ptr[sidx], t1 = seg_tile_ptr[sidx + 1];
+  if (t0 == t1) return;
+  const int64_t i = blockIdx.x * (int64_t)128 + 4 * lane;
+  auto ld = [&](int t) { return __ldg(reinterpret_cast<const float4*>(partial + (size_t)t * width + i)); };
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  int t = t0 + warp;
+  for (; t + 8 < t1; t += 16) {
+    const float4 x = ld(t), y = ld(t + 8);
+    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+    b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+  }
+  if (t < t1) {
+    const float4 x = ld(t);
+    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+  }
+  red[warp][lane] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  __syncthreads();
+  if (warp == 0) {
+    float4 s = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      const float4 x = red[k][lane];
+      s.x += x.x; s.y += x.y; s.z += x.z; s.w += x.w;
+    }
+    *reinterpret_cast<float4*>(out + (size_t)seg_w[sidx] * width + i) = s;
+  }
+}
+
 // per tile: partial[tile][k] = sum_rows wt[row] * A[gather(row)][k] (wt == NULL: weight 1).
 // Lanes move 16-byte vectors: LPR = K / V lanes per row, RG = 256 / LPR row groups striding over
 // the tile's rows; the groups' sums are combined in group order in shared memory (deterministic).
@@ -753,7 +791,17 @@ void gemm_simt(const GemmArgs& a, cudaStream_t s) {
   else RGNN_FAIL(RGNN_ERR_UNSUPPORTED, "gemm: unsupported dtype combination");
 }
 
-SegPartialReduceFn seg_partial_reduce_kernel() { return k_seg_partial_reduce; }
+void seg_partial_reduce(const Plan& p, const float* partial, int64_t width, float* out, cudaStream_t s) {
+  const bool al = (reinterpret_cast<uintptr_t>(partial) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  // few long segments (mag: 4 relations x ~400 tiles) keep the 32-element blocks: 4x the blocks to spread
+  // the long tile loops over the SMs (measured: the 128-element blocks cost mag HGT 0.033 -> 0.050 ms)
+  if (width % 128 == 0 && al && (width / 128) * p.nseg >= 2 * 148)
+    launch("wgrad_reduce", k_seg_partial_reduce4, dim3((unsigned)(width / 128), p.nseg), dim3(256), 0, s, p.nseg,
+           p.seg_tile_ptr, p.seg_w, partial, width, out);
+  else
+    launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
+           p.seg_tile_ptr, p.seg_w, partial, width, out);
+}
 
 void wgrad(const WgradArgs& a, cudaStream_t s) {
   const Plan& p = *a.plan;
@@ -762,9 +810,7 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   dim3 g(p.count, ceil_div(a.K1, 64), ceil_div(a.K2, 64));
   if (a.allow_tc && wgrad_tc_supported(a)) {
     wgrad_tc(a, s);
-    int64_t width = (int64_t)a.K1 * a.K2;
-    launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
-           p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
+    seg_partial_reduce(p, a.partial, (int64_t)a.K1 * a.K2, a.out, s);
     return;
   }
   auto go = [&](auto* A, auto* B) {
@@ -785,9 +831,7 @@ void wgrad(const WgradArgs& a, cudaStream_t s) {
   else if (a32) go(static_cast<const float*>(a.A), static_cast<const bf16*>(a.Bm));
   else if (b32) go(static_cast<const bf16*>(a.A), static_cast<const float*>(a.Bm));
   else go(static_cast<const bf16*>(a.A), static_cast<const bf16*>(a.Bm));
-  int64_t width = (int64_t)a.K1 * a.K2;
-  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
-         p.seg_tile_ptr, p.seg_w, a.partial, width, a.out);
+  seg_partial_reduce(p, a.partial, (int64_t)a.K1 * a.K2, a.out, s);
 }
 
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather, float* out,
@@ -803,8 +847,7 @@ void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int
   else
     launch("seg_wsum", k_seg_wsum<bf16>, dim3(p.count), dim3(256), 0, s, p.tiles, wt,
            static_cast<const bf16*>(A), K, gather, partial);
-  launch("wgrad_reduce", k_seg_partial_reduce, dim3(ceil_div(K, 32), p.nseg), dim3(256), 0, s, p.nseg,
-         p.seg_tile_ptr, p.seg_w, partial, (int64_t)K, out);
+  seg_partial_reduce(p, partial, (int64_t)K, out, s);
 }
 
 void seg_reduce_rows(int64_t n, const int32_t* ptr, const int32_t* list, const void* Y, int y_dtype, int K, float* out,

@@ -758,10 +758,7 @@ void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s) {
   if (pair_bwd_ws_enabled(a)) pair_bwd_ws(a, s);
   else if (a.K2 == 64) launch_pair_bwd_tc<64, 64>(a, s);
   else launch_pair_bwd_tc<64, 128>(a, s);
-  const Plan& p = *a.plan;
-  const int64_t width = (int64_t)a.K1 * a.K2;
-  launch("wgrad_reduce", seg_partial_reduce_kernel(), dim3(ceil_div(width, 32), p.nseg), dim3(256), 0, s, p.nseg,
-         p.seg_tile_ptr, p.seg_w, (const float*)a.partial, width, a.out);
+  seg_partial_reduce(*a.plan, (const float*)a.partial, (int64_t)a.K1 * a.K2, a.out, s);
 }
 
 bool wgrad_tc_supported(const WgradArgs& a) {

@@ -88,8 +88,8 @@ void pair_bwd_tc(const PairBwdArgs& a, cudaStream_t s);
 bool pair_bwd_ws_enabled(const PairBwdArgs& a);
 void pair_bwd_ws(const PairBwdArgs& a, cudaStream_t s);
 // the second level of the deterministic weight-gradient reduction (dense_ops.cu)
-using SegPartialReduceFn = void (*)(int, const int32_t*, const int32_t*, const float*, int64_t, float*);
-SegPartialReduceFn seg_partial_reduce_kernel();
+// out[seg_w[s]] = sum over the tiles of segment s of partial[tile] (width floats each), in tile order
+void seg_partial_reduce(const Plan& p, const float* partial, int64_t width, float* out, cudaStream_t s);
 
 // out[w][k] = sum_{rows of w} wt[row] * A[gather(row)][k]  (fp32 out; same two-level scheme)
 void seg_wsum(const Plan* plan, const float* wt, const void* A, int a_dtype, int K, const int32_t* gather,
