@@ -475,7 +475,7 @@ __device__ __forceinline__ void lds_f32(const float* p, float* o) {
 // entry from te[] (computed by the dst-pair GEMM) instead of x_v . y_r.
 // SY: y staged in shared memory (persistent grid, stage_y); the edge's relation id is prefetched
 // instead of its y row.
-template <class TP, int D, bool GROUP, bool TE, bool SY>
+template <class TP, int D, bool GROUP, bool TE, bool SY, int UF = UNR>
 __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4* __restrict__ items,
                                               float* __restrict__ pacc, float2* __restrict__ pstat,
                                               const int32_t* __restrict__ csr_pair, const int32_t* __restrict__ csr_rel,
@@ -495,14 +495,14 @@ __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4
   float m = -CUDART_INF_F, s = 0.f, acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
-  for (int t = 0; t < w.span; t += w.step * UNR) {
+  for (int t = 0; t < w.span; t += w.step * UF) {
     const int i0 = b + t + w.first;
-    uint4 rp[UNR];
-    float sp[UNR], yv[UNR][VY];
-    int rel[UNR];
-    bool ok[UNR];
+    uint4 rp[UF];
+    float sp[UF], yv[UF][VY];
+    int rel[UF];
+    bool ok[UF];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+    for (int u = 0; u < UF; ++u) {
       int i = i0 + u * w.step;
       ok[u] = i < e;
       rp[u] = make_uint4(0, 0, 0, 0);
@@ -519,9 +519,9 @@ __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4
         else ld_f32<V>(y + (int64_t)csr_rel[i] * D + c * V, yv[u]);
       }
     }
-    float l[UNR], mx = m;
+    float l[UF], mx = m;
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+    for (int u = 0; u < UF; ++u) {
       float t = 0.f;
       if (TE) {
         t = yv[u][0];
@@ -546,7 +546,7 @@ __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4
 #pragma unroll
     for (int k = 0; k < V; ++k) acc[k] *= sc;
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
+    for (int u = 0; u < UF; ++u) {
       float wt = safe_exp_diff(l[u], mx);
       s += wt;
       float pv[V];
@@ -573,6 +573,12 @@ __device__ __forceinline__ bool rgat_fwd_item(int64_t wid, int64_t n, const int4
 #ifndef RGNN_SY_MINB
 #define RGNN_SY_MINB 4
 #endif
+#ifndef RGNN_SY_MINB_FWD
+#define RGNN_SY_MINB_FWD RGNN_SY_MINB
+#endif
+#ifndef RGNN_SY_UNR
+#define RGNN_SY_UNR 4  // edges per lane group in flight in the staged forward kernel
+#endif
 #ifndef RGNN_SY_MINB_SGL
 #define RGNN_SY_MINB_SGL 3  // the single-edge-pair stores need more registers (64 spill)
 #endif
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(256) k_rgat_fwd(int64_t n, const int4* __restr
 }
 // persistent, y staged in shared memory
 template <class TP, int D, bool GROUP>
-__global__ void __launch_bounds__(256, RGNN_SY_MINB) k_rgat_fwd_sy(
+__global__ void __launch_bounds__(256, RGNN_SY_MINB_FWD) k_rgat_fwd_sy(
     int64_t n, const int4* __restrict__ items, float* __restrict__ pacc, float2* __restrict__ pstat,
     const int32_t* __restrict__ csr_pair, const int32_t* __restrict__ csr_rel, const TP* __restrict__ P,
     const float* __restrict__ spair, const TP* __restrict__ X, const float* __restrict__ y,
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(256, RGNN_SY_MINB) k_rgat_fwd_sy(
   const float* ys = stage_y(y, ny);
   const int64_t stride = (gridDim.x * (int64_t)blockDim.x) >> 5;
   for (int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-       rgat_fwd_item<TP, D, GROUP, false, true>(wid, n, items, pacc, pstat, csr_pair, csr_rel, P, spair, X, ys, te, slope,
+       rgat_fwd_item<TP, D, GROUP, false, true, RGNN_SY_UNR>(wid, n, items, pacc, pstat, csr_pair, csr_rel, P, spair, X, ys, te, slope,
                                                out, stats);
        wid += stride) {
   }

@@ -73,7 +73,8 @@ case "$task" in
     ;;
   abhead)
     build
-    (cd ab_head && python -c "import __graft_entry__ as g; g.build()" > "../$out/build_head.log" 2>&1) || { tail -30 "$out/build_head.log"; exit 1; }
+    # HEAD_DEFINES: RGNN_DEFINES of the ab_head build (a build-time variant instead of another commit)
+    (cd ab_head && RGNN_DEFINES="${HEAD_DEFINES:-}" python -c "import __graft_entry__ as g; g.build()" > "../$out/build_head.log" 2>&1) || { tail -30 "$out/build_head.log"; exit 1; }
     for cfg in "$@"; do
       for i in 1 2; do
         (cd ab_head && timeout 300 python bench.py --config "$cfg" --no-cpu-baseline --no-ncu --no-e2e --steps 20 \
