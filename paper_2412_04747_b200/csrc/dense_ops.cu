@@ -793,9 +793,10 @@ void gemm_simt(const GemmArgs& a, cudaStream_t s) {
 
 void seg_partial_reduce(const Plan& p, const float* partial, int64_t width, float* out, cudaStream_t s) {
   const bool al = (reinterpret_cast<uintptr_t>(partial) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  // few long segments (mag: 4 relations x ~400 tiles) keep the 32-element blocks: 4x the blocks to spread
-  // the long tile loops over the SMs (measured: the 128-element blocks cost mag HGT 0.033 -> 0.050 ms)
-  if (width % 128 == 0 && al && (width / 128) * p.nseg >= 2 * 148)
+  // few long segments (mag: a handful of relation / type segments x ~400 tiles) keep the 32-element blocks:
+  // 4x the blocks to spread the long tile loops over the SMs (measured: the 128-element blocks cost mag HGT
+  // 0.033 -> 0.050 ms); many short ones (wikikg2: 535 x ~13 tiles, AM: 130 x ~14) take the float4 blocks
+  if (width % 128 == 0 && al && p.count <= 64 * (int64_t)p.nseg)
     launch("wgrad_reduce", k_seg_partial_reduce4, dim3((unsigned)(width / 128), p.nseg), dim3(256), 0, s, p.nseg,
            p.seg_tile_ptr, p.seg_w, partial, width, out);
   else
