@@ -78,9 +78,11 @@ def load_peaks():
 
 
 # ----------------------------------------------------------------- algorithmic bytes per launch
-def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
+def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d, rgat_spmm=True):
     """Bytes each kernel must move, per launch.
-    Each gathered row counts once per use even if L2 serves it; int32 indices; grads fp32."""
+    Each gathered row counts once per use even if L2 serves it; int32 indices; grads fp32.
+    rgat_spmm: RGAT's weighted-SpMM backward (the library default, layer.cu rgat_spmm) instead of the
+    recompute design (RGNN_RGATW=0)."""
     b = 2 if dtype == "bf16" else 4
     out = {}
     if model == "hgt":
@@ -102,14 +104,25 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
     elif model == "rgat":
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b + 4)
         out["rgat_fwd_traverse"] = E * (4 + 4 + d * b + 4) + N * (16 + d_in * b + 4 * d + 8)
-        # A6 also writes the node record [G_v | X_v] (2d*b) + 16 B
-        out["rgat_bwd_dst"] = E * (8 + d * b + 4) + N * (16 + d_in * b + 12 * d + 8 + 2 * d * b + 16)
-        # A7 per edge: CSC dst, the destination's [G|X] row and 16-B record; per pair: P row, s, dP, wsum, bx
-        out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + d * b)
+        if rgat_spmm:
+            # A6 per edge: pair + relation index, P row, s_p, and the (alpha, dz) record written; per node:
+            # X row, G and out (fp32), stats, the G-only node record written, the t-path dX row written
+            out["rgat_bwd_dst"] = E * (4 + 4 + d * b + 4 + 8) + N * (d_in * b + 4 * d + 4 * d + 8 + d * b + 4 * d)
+            # A7 weighted SpMM per edge: CSC dst, CSR position, (alpha, dz), the destination's G row; per pair:
+            # the work item, dP row and wsum written
+            out["rgat_bwd_pair"] = E * (4 + 4 + 8 + d * b) + U * (16 + d * b + 4)
+            # B_r: dz summed per (rel, dst) run, then a weighted row sum of X[dst] per relation; da: wsum-weighted P
+            out["dpair_sum"] = E * 8 + UD * (4 + 4 + 4)
+            out["seg_wsum"] = UD * (4 + 4 + d_in * b) + U * (4 + d * b)
+        else:
+            # A6 also writes the node record [G_v | X_v] (2d*b) + 16 B
+            out["rgat_bwd_dst"] = E * (8 + d * b + 4) + N * (16 + d_in * b + 12 * d + 8 + 2 * d * b + 16)
+            # A7 per edge: CSC dst, the destination's [G|X] row and 16-B record; per pair: P row, s, dP, wsum, bx
+            out["rgat_bwd_pair"] = E * (4 + 2 * d * b + 16) + U * (16 + 4 + d * b + 4 + d * b + 4 + d * b)
+            out["seg_wsum"] = U * (d * b) + U * (4 + d * b)
         out["gemm_pairs_dx"] = U * (d * b + d_in * b)
         out["seg_reduce_rows"] = U * (4 + d_in * b) + N * (4 + 8 * d_in)
         out["wgrad_pairs"] = U * (4 + d_in * b + d * b)
-        out["seg_wsum"] = U * (d * b) + U * (4 + d * b)
     else:
         out["gemm_pairs_fwd"] = U * (4 + d_in * b + d * b)
         out["gemm_selfloop_fwd"] = N * (d_in * b + 4 * d)
@@ -128,6 +141,16 @@ def algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d_in, d):
     return out
 
 
+def dst_rel_pairs(g):
+    """Number of distinct (rel, dst) pairs (UD: the (rel, dst) runs of the dst-CSR)."""
+    return int(np.unique(g.rel.astype(np.int64) * g.num_nodes + g.dst).size)
+
+
+def rgat_spmm_on(args):
+    """Mirror of layer.cu rgat_spmm: the weighted-SpMM RGAT backward unless reordering is off or RGNN_RGATW=0."""
+    return not getattr(args, "no_reorder", False) and os.environ.get("RGNN_RGATW") != "0"
+
+
 def single_edge_pairs(g):
     """Number of (rel, src) pairs with exactly one edge (host count; the library resolves them in
     the destination-major backward pass when they are >= 30 % of the pairs, layer.cu single_in_dst)."""
@@ -136,13 +159,30 @@ def single_edge_pairs(g):
     return int((cnt == 1).sum())
 
 
-def adjust_for_single(alg, model, E, U, U1, d, b):
+def single_in_dst(model, E, U, U1, rgat_spmm=True, env=None):
+    """Mirror of layer.cu single_in_dst: RGNN_SINGLE forces it; RGAT's weighted-SpMM design leaves the
+    single-edge pairs to the pair pass; otherwise on when they are >= 30 % of the pairs."""
+    env = os.environ if env is None else env
+    if model not in ("hgt", "rgat"):
+        return False
+    if env.get("RGNN_SINGLE") in ("0", "1"):
+        return env["RGNN_SINGLE"] == "1"
+    if model == "rgat" and rgat_spmm:
+        return False
+    return 10 * U1 >= 3 * U
+
+
+def adjust_for_single(alg, model, E, U, U1, d, b, rgat_spmm=True, env=None):
     """Move the single-edge pairs' bytes from the pair-major label to the destination-major one:
     the pair pass no longer gathers their node records; the dst pass reads a 1-byte flag per edge
     and writes their gradient rows (HGT [dK~ | dM]; RGAT dP, bx, wsum and reads a_r)."""
-    if model not in ("hgt", "rgat") or 10 * U1 < 3 * U:
+    if not single_in_dst(model, E, U, U1, rgat_spmm, env):
         return alg
     alg = dict(alg)
+    if model == "rgat" and rgat_spmm:  # dst pass writes their dP row + wsum; the pair pass skips them
+        alg["rgat_bwd_pair"] -= U1 * (4 + 4 + 8 + d * b) + U1 * (16 + d * b + 4)
+        alg["rgat_bwd_dst"] += E * 1 + U1 * (d * b + 4)
+        return alg
     if model == "hgt":
         alg["hgt_bwd_pair"] -= U1 * (4 + 2 * d * b + 16) + U1 * (16 + 2 * d * b + 2 * d * b)
         alg["hgt_bwd_dst"] += E * 1 + U1 * (2 * d * b)
@@ -187,9 +227,9 @@ def d4_bytes(model, dtype, N, E, U, d):
 
 # kernel-name regex of each traversal label (every launch of the label: warp, group and short halves)
 LABEL_KERNELS = {"hgt_bwd_pair": "k_hgt_bwd_pair", "hgt_bwd_dst": "k_hgt_bwd_dst", "hgt_fwd_traverse": "k_hgt_fwd",
-                 "rgat_bwd_pair": "k_rgat_bwd_pair", "rgat_bwd_dst": "k_rgat_bwd_dst",
+                 "rgat_bwd_pair": "k_rgat_bwd_pair|k_pair_spmm", "rgat_bwd_dst": "k_rgat_bwd_dst",
                  "rgat_fwd_traverse": "k_rgat_fwd", "rgcn_bwd_pair": "k_rgcn_bwd_pair",
-                 "rgcn_fwd_traverse": "k_rgcn_fwd", "pair_bwd_fused": "k_pair_bwd_tc"}
+                 "rgcn_fwd_traverse": "k_rgcn_fwd", "pair_bwd_fused": "k_pair_bwd_tc|k_pair_bwd_ws"}
 
 
 def source_hash() -> str:
@@ -730,10 +770,12 @@ def main():
     gi = G.info()
     U, E = gi["num_pairs"], gi["num_edges"]
     bsz = 2 if dtype == "bf16" else 4
-    alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, 0, g.num_rels, g.num_node_types, d, d)
+    spmm = rgat_spmm_on(args)
+    UD = dst_rel_pairs(g) if model == "rgat" else 0
+    alg = algorithmic_bytes(model, dtype, g.num_nodes, E, U, UD, g.num_rels, g.num_node_types, d, d, spmm)
     alg = adjust_for_fusions(alg, prof, U, g.num_nodes, d, bsz)
     if world == 1 and not args.no_compact and model in ("hgt", "rgat"):
-        alg = adjust_for_single(alg, model, E, U, single_edge_pairs(g), d, bsz)
+        alg = adjust_for_single(alg, model, E, U, single_edge_pairs(g), d, bsz, spmm)
     roofline = roofline_block(alg, prof, args.steps, ms_per_step, peaks, model, dtype, g.num_nodes, E, U, d,
                               t_fwd, t_bwd, args.infer)
     kernels = roofline.pop("_kernels")
@@ -818,11 +860,11 @@ TRAIN_LR = 1e-3
 LABEL_SEED, LABELLED_FRAC = 5, 1.0
 
 
-def train_bytes(model, dtype, N, E, U, R, T, d, layers, num_params):
+def train_bytes(model, dtype, N, E, U, R, T, d, layers, num_params, UD=0, rgat_spmm=True):
     """Algorithmic bytes per training step: every layer kernel once per layer (the dX kernels of
     layer 1 are pruned: its input is data), plus the F4 kernels."""
     b = 2 if dtype == "bf16" else 4
-    per = algorithmic_bytes(model, dtype, N, E, U, 0, R, T, d, d)
+    per = algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d, d, rgat_spmm)
     dx = {"gemm_pairs_dx", "gemm_nodes_dx", "seg_reduce_rows", "gemm_selfloop_dx", "pair_bwd_fused"}
     out = {k: v * (layers - 1 if k in dx else layers) for k, v in per.items()}
     out["relu_fwd"] = (layers - 1) * N * d * (4 + b)
@@ -1003,11 +1045,13 @@ def run_train(args, cfg, world, rank, local_rank):
     peaks = load_peaks()
     U, E = info["num_pairs"], info["num_edges"]
     nparams = sum(m.numel() for ms_ in st.master for m in ms_.values())
-    alg = train_bytes(model, dtype, g.num_nodes, E, U, g.num_rels, g.num_node_types, d, layers, nparams)
+    spmm = rgat_spmm_on(args)
+    UD = dst_rel_pairs(g) if model == "rgat" else 0
+    alg = train_bytes(model, dtype, g.num_nodes, E, U, g.num_rels, g.num_node_types, d, layers, nparams, UD, spmm)
     alg = adjust_for_fusions(alg, prof, U * (layers - 1), g.num_nodes * (layers - 1), d, 2 if dtype == "bf16" else 4)
     if not args.no_compact and model in ("hgt", "rgat"):
         one = adjust_for_single({k: 0 for k in alg}, model, E, U, single_edge_pairs(g), d,
-                                2 if dtype == "bf16" else 4)
+                                2 if dtype == "bf16" else 4, spmm)
         alg = {k: v + layers * one.get(k, 0) for k, v in alg.items()}
     tot_ms = sum(x["ms"] for x in prof.values())
     kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,

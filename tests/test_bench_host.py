@@ -111,3 +111,27 @@ def test_parse_ncu_dram():
     ])
     tot, n = bench.parse_ncu_dram(csv, "k_hgt_bwd_pair")
     assert n == 2 and abs(tot - (1000.5e6 + 500e3 + 1e9)) < 1
+
+
+def test_rgat_spmm_bytes_hand_counted():
+    # one edge, one pair, one (rel, dst) run, one node, d = 8, bf16: the weighted-SpMM design (default)
+    b = bench.algorithmic_bytes("rgat", "bf16", N=1, E=1, U=1, UD=1, R=1, T=1, d_in=8, d=8)
+    # A6: pair + rel index, P row, s_p, (alpha, dz) written; node: X row, G + out fp32, stats, G record, dX
+    assert b["rgat_bwd_dst"] == (4 + 4 + 16 + 4 + 8) + (16 + 32 + 32 + 8 + 16 + 32)
+    # A7 SpMM: CSC dst, CSR position, (alpha, dz), G row; pair: item, dP row, wsum
+    assert b["rgat_bwd_pair"] == (4 + 4 + 8 + 16) + (16 + 16 + 4)
+    assert b["dpair_sum"] == 8 + 12
+    # the recompute design moves the [G | X] record and its 16-byte (lse, G.out) per edge instead
+    r = bench.algorithmic_bytes("rgat", "bf16", N=1, E=1, U=1, UD=1, R=1, T=1, d_in=8, d=8, rgat_spmm=False)
+    assert r["rgat_bwd_pair"] > b["rgat_bwd_pair"] and "dpair_sum" not in r
+
+
+def test_single_in_dst_mirror():
+    """bench.single_in_dst mirrors layer.cu: RGNN_SINGLE forces; RGAT's SpMM design leaves single-edge
+    pairs to the pair pass; otherwise the 30 % threshold."""
+    assert bench.single_in_dst("hgt", 1000, 700, 300, env={})
+    assert not bench.single_in_dst("hgt", 1000, 700, 100, env={})
+    assert not bench.single_in_dst("rgat", 1000, 700, 600, rgat_spmm=True, env={})
+    assert bench.single_in_dst("rgat", 1000, 700, 600, rgat_spmm=False, env={})
+    assert bench.single_in_dst("rgat", 1000, 700, 0, rgat_spmm=True, env={"RGNN_SINGLE": "1"})
+    assert not bench.single_in_dst("rgcn", 1000, 700, 600, env={"RGNN_SINGLE": "1"})
