@@ -867,6 +867,8 @@ def train_bytes(model, dtype, N, E, U, R, T, d, layers, num_params, UD=0, rgat_s
     per = algorithmic_bytes(model, dtype, N, E, U, UD, R, T, d, d, rgat_spmm)
     dx = {"gemm_pairs_dx", "gemm_nodes_dx", "seg_reduce_rows", "gemm_selfloop_dx", "pair_bwd_fused"}
     out = {k: v * (layers - 1 if k in dx else layers) for k, v in per.items()}
+    if b == 2:  # bf16: layers 2.. run the fused A8 kernel (dX rows + dW); only layer 1 (no dX) runs wgrad_pairs
+        out["wgrad_pairs"] = per["wgrad_pairs"]
     out["relu_fwd"] = (layers - 1) * N * d * (4 + b)
     out["relu_bwd"] = (layers - 1) * N * d * 12
     out["nll_loss"] = N * d * 8 + N * 4

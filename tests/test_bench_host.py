@@ -54,6 +54,8 @@ def test_train_bytes_layers():
     # layer kernels twice, except the dX kernels (layer 1's input is data)
     assert two["rgat_fwd_traverse"] == 2 * one["rgat_fwd_traverse"]
     assert two["gemm_pairs_dx"] == one["gemm_pairs_dx"]
+    # bf16: layer 2 computes dW in the fused A8 kernel, so the separate weight gradient runs once (layer 1)
+    assert two["wgrad_pairs"] == one["wgrad_pairs"] and two["pair_bwd_fused"] == one["pair_bwd_fused"]
     assert two["nll_loss"] == 50 * 64 * 8 + 50 * 4
     assert two["relu_fwd"] == 50 * 64 * (4 + 2)
     assert two["sgd_update"] == 1000 * (12 + 2)
