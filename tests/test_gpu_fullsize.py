@@ -65,6 +65,7 @@ CASES = [
     ("mag", "hgt", "bf16"),
     ("mag", "hgt", "f32"),
     ("mag", "rgat", "bf16"),
+    ("am", "rgat", "bf16"),  # BASELINE configs[2]: 130 relations (33 KB of staged y), 71 % single-edge pairs
     ("wikikg2", "rgcn", "bf16"),
 ]
 
