@@ -1880,14 +1880,29 @@ __global__ void __launch_bounds__(256) k_merge_softmax(int64_t n_split, const in
 #pragma unroll
   for (int k = 1; k < 8; ++k) m = fmaxf(m, sm_m[k][lane]);
   float s = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int i = warp; i < sp.z; i += 8) {
-    float2 st = pstat[(int64_t)(sp.y + i) * H + hh];
-    float wt = safe_exp_diff(st.x, m);
-    s = fmaf(st.y, wt, s);
-    if (act) {
-      float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
-      acc[0] = fmaf(wt, a.x, acc[0]); acc[1] = fmaf(wt, a.y, acc[1]);
-      acc[2] = fmaf(wt, a.z, acc[2]); acc[3] = fmaf(wt, a.w, acc[3]);
+  // slots warp, warp + 8, ... in order (as one slot per step), four loaded before they are used
+  for (int i0 = warp; i0 < sp.z; i0 += 32) {
+    float2 st[4];
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + 8 * u;
+      st[u] = make_float2(-CUDART_INF_F, 0.f);
+      a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < sp.z) {
+        st[u] = pstat[(int64_t)(sp.y + i) * H + hh];
+        if (act) a[u] = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * D + lane * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + 8 * u >= sp.z) break;
+      const float wt = safe_exp_diff(st[u].x, m);
+      s = fmaf(st[u].y, wt, s);
+      if (act) {
+        acc[0] = fmaf(wt, a[u].x, acc[0]); acc[1] = fmaf(wt, a[u].y, acc[1]);
+        acc[2] = fmaf(wt, a[u].z, acc[2]); acc[3] = fmaf(wt, a[u].w, acc[3]);
+      }
     }
   }
   sm_s[warp][lane] = s;
@@ -1920,9 +1935,17 @@ __global__ void __launch_bounds__(256) k_merge_sum(int64_t n_split, const int4* 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = lane * 4; col < W; col += 128) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int i = warp; i < sp.z; i += 8) {
-      float4 a = *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i) * W + col);
-      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    for (int i0 = warp; i0 < sp.z; i0 += 32) {  // slots in order, four loaded before they are added
+      float4 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        a[u] = i0 + 8 * u < sp.z ? *reinterpret_cast<const float4*>(pacc + (int64_t)(sp.y + i0 + 8 * u) * W + col)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + 8 * u >= sp.z) break;
+        acc[0] += a[u].x; acc[1] += a[u].y; acc[2] += a[u].z; acc[3] += a[u].w;
+      }
     }
     *reinterpret_cast<float4*>(&sm_acc[warp][col]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
