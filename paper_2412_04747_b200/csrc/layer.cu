@@ -776,6 +776,12 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     const bool fused = dX && needF &&
                        fused_pair_bwd(c, seg_pair_rt(g), X, sc.dP, 2 * c.D, sv.Fdt, sc.dXp, sc.dF,
                                       std::max(g->n_act, 1), sc.partial);
+    // the small unfold kernels (dF -> dWk, dWv, dWatt, dWmsg) only need dF: on the side stream, overlapped
+    // with the node dX GEMM and the node weight gradient (joined before the layer returns)
+    const bool unfold_side = needF && fused;
+    if (unfold_side)
+      hgt_unfold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sc.dF, sc.dFu, dW->dWk, dW->dWv,
+                 dW->dWatt, dW->dWmsg, fork_side(c.s));
     if (dX) {
       // per-pair rows first, then the node GEMM whose epilogue adds them per source (tcgen05 path)
       GemmArgs a;
@@ -801,7 +807,9 @@ void backward(const Ctx& c, const void* X, const rgnn_weights* w, const float* o
     if (dW->dWq)
       do_wgrad(c, seg_node_type_own(g), X, c.dt, c.Din, nullptr, sc.dQ, c.dt, c.D, dW->dWq, g->T, sc.partial,
                "wgrad_nodes");
-    if (needF) {
+    if (unfold_side) {
+      join_side(c.s);
+    } else if (needF) {
       if (!fused)
         do_wgrad(c, seg_pair_rt(g), X, c.dt, c.Din, g->pair_src, sc.dP, c.dt, 2 * c.D, sc.dF, std::max(g->n_act, 1),
                  sc.partial, "wgrad_pairs");
