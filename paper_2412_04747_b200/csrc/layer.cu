@@ -554,7 +554,8 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
       a.name = "gemm_pairs_fwd";
       gemm(c, seg_pair_rel(g), a);
     } else {
-      hgt_fold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, c.s);
+      // the weight fold (A2) runs on the side stream while the Q GEMM (independent of it) runs here
+      hgt_fold(g, c.Din, c.D, c.D / c.H, w->Wk, w->Wv, w->Watt, w->Wmsg, w->mu, c.dt, sv.F32, sv.Fdt, fork_side(c.s));
       GemmArgs a;
       a.A = X; a.a_dtype = c.dt; a.K = c.Din; a.gather = g->pair_src;
       a.B = c.dt == F32 ? (const void*)sv.F32 : sv.Fdt; a.b_dtype = c.dt;
@@ -566,6 +567,7 @@ void forward(const Ctx& c, const void* X, const rgnn_weights* w, float* out, con
       q.num_w = g->T; q.bt_scratch = sc.bt;
       q.name = "gemm_nodes_fwd";
       gemm(c, seg_node_type_own(g), q);
+      join_side(c.s);
       pair_gemm(c, seg_pair_rt(g), a);
     }
     if (hgt_nr(c.d)) {
